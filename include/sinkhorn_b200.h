@@ -1,0 +1,166 @@
+/*
+ * sinkhorn_b200.h -- C ABI of the B200-native batched log-domain Sinkhorn loss.
+ *
+ * Drop-in boundary for the reference's FFI (`/root/reference/pkg/frontend/src/ffi.ts`).
+ * Plain C types only: no torch, no C++ in the signatures.  The library is
+ * `paper_1907_01729_b200/_lib/libsinkhorn_b200.so` (built by __graft_entry__.build()).
+ *
+ * Two layers:
+ *
+ *  1. Host-buffer entry points with the reference's exact semantics
+ *     (row-major float64 views, outputs written in place, integer status,
+ *     nothing thrown).  `sinkhorn_forward_v1` replaces ffi.ts:80-134 and
+ *     `sinkhorn_backward_v1` replaces ffi.ts:143-191.  They copy the views to
+ *     the GPU, run the fp32 device pipeline below and copy results back.
+ *
+ *  2. Device entry points (`*_device_v1`) over float32 device pointers,
+ *     stream-ordered on a caller-supplied cudaStream_t, with caller-owned
+ *     workspace.  These are what the PyTorch layer binds (ctypes) and what
+ *     extends the reference: per-sample costs, on-the-fly grid costs,
+ *     iteration count / residual outputs, partial (max, sum-exp) outputs for
+ *     row-sharded multi-GPU solves, and the transport-plan gradient dC.
+ *
+ * Status codes: ffi.ts:21-25 (0, 10-13) plus extensions 14-21 (the reference
+ * raises exceptions for these).
+ */
+#ifndef SINKHORN_B200_H
+#define SINKHORN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define SINKHORN_STATUS_OK 0                /* ffi.ts:21 STATUS_OK */
+#define SINKHORN_STATUS_SHAPE_MISMATCH 10   /* ffi.ts:22 */
+#define SINKHORN_STATUS_INVALID_HISTOGRAM 11/* ffi.ts:23 (core.py:143-160 rules) */
+#define SINKHORN_STATUS_NON_FINITE_OUTPUT 12/* ffi.ts:24; also NaN state (batch.py:326-327) */
+#define SINKHORN_STATUS_ZERO_MASS_LANE 13   /* ffi.ts:25; batch.py:366-370 */
+#define SINKHORN_STATUS_INVALID_CONFIG 14   /* core.py:88-96 ValueError */
+#define SINKHORN_STATUS_INVALID_COST 15     /* core.py:53-63 ValueError */
+#define SINKHORN_STATUS_BAD_ARGUMENT 16     /* null pointer / unsupported descriptor */
+#define SINKHORN_STATUS_WORKSPACE 17        /* workspace too small */
+#define SINKHORN_STATUS_CUDA_ERROR 20       /* CUDA runtime error (message: sinkhorn_last_error) */
+
+/* ---- layer 1: host float64 views (ffi.ts:14-19 TensorView) ------------- */
+
+/* Row-major contiguous view. `length` is the number of elements available at
+ * `data` (ffi.ts:33-38 checks offset + size <= data.length; fold any offset
+ * into `data`). */
+typedef struct sinkhorn_view_v1 {
+  double* data;
+  int32_t ndim;
+  int64_t shape[2];
+  int64_t length;
+} sinkhorn_view_v1;
+
+/* Replaces ffi.ts:80-134 sinkhorn_forward_v1.  Shapes: mu (B,d1), nu (B,d2),
+ * cost (d1,d2), out_cost (B,), out_log_u (B,d1), out_log_v (B,d2).
+ * check_interval is 10, the CLI default the reference's runner inherits
+ * (runner.ts:48-55, cli.py:50).  B == 0 is a successful no-op. */
+int32_t sinkhorn_forward_v1(const sinkhorn_view_v1* mu, const sinkhorn_view_v1* nu,
+                            const sinkhorn_view_v1* cost, double lambda, int32_t max_iters,
+                            double tolerance, const sinkhorn_view_v1* out_cost,
+                            const sinkhorn_view_v1* out_log_u, const sinkhorn_view_v1* out_log_v);
+
+/* Replaces ffi.ts:143-191 sinkhorn_backward_v1.  Shapes: log_u (B,d1),
+ * log_v (B,d2), upstream (B,), out_grad_mu (B,d1), out_grad_nu (B,d2).
+ * Any -inf potential returns 13 (ffi.ts:177-179). */
+int32_t sinkhorn_backward_v1(const sinkhorn_view_v1* log_u, const sinkhorn_view_v1* log_v,
+                             double lambda, const sinkhorn_view_v1* upstream,
+                             const sinkhorn_view_v1* out_grad_mu,
+                             const sinkhorn_view_v1* out_grad_nu);
+
+/* ---- layer 2: device float32 pipeline ----------------------------------- */
+
+#define SINKHORN_COST_SHARED 0     /* one stored (d1,d2) cost for all lanes (the reference's case) */
+#define SINKHORN_COST_PER_SAMPLE 1 /* stored (B,d1,d2), one cost per lane (BASELINE config 4) */
+#define SINKHORN_COST_GRID2D 2     /* squared Euclidean on an nx*ny grid, never materialised
+                                      (BASELINE config 3); d1 = d2 = nx*ny,
+                                      point k at ((k % nx)*hx, (k / nx)*hy) */
+
+typedef struct sinkhorn_problem_v1 {
+  int64_t B, d1, d2;
+  int32_t cost_kind;     /* SINKHORN_COST_* */
+  int32_t grid_nx, grid_ny;
+  float grid_hx, grid_hy;
+} sinkhorn_problem_v1;
+
+#define SINKHORN_FLAG_SKIP_VALIDATION 1u /* trust mu/nu/cost (caller validated) */
+#define SINKHORN_FLAG_PARTIAL_ROWS 2u    /* reserved: row-sharded solves use the half-sweep API */
+
+typedef struct sinkhorn_options_v1 {
+  double lambda;          /* > 0, finite */
+  int32_t max_iters;      /* >= 1 */
+  int32_t check_interval; /* >= 1 (reference default 10) */
+  double tolerance;       /* >= 0; 0 runs exactly max_iters iterations */
+  uint32_t flags;
+} sinkhorn_options_v1;
+
+/* Bytes of device workspace sinkhorn_forward_device_v1 needs for `prob`. */
+size_t sinkhorn_workspace_bytes_v1(const sinkhorn_problem_v1* prob);
+
+/* batch_forward (batch.py:264-349) on the GPU.  All pointers are device
+ * pointers; mu (B,d1), nu (B,d2) row-major; cost (d1,d2) for SHARED,
+ * (B,d1,d2) for PER_SAMPLE, ignored for GRID2D.  Outputs: out_cost (B,),
+ * out_log_u (B,d1), out_log_v (B,d2) natural-log potentials; optional
+ * out_iterations (1 int32, host or device memory: host) and out_residuals (B,)
+ * may be NULL.  `stream` is a cudaStream_t (NULL = legacy default stream).
+ * Synchronises `stream` once at the end (and at every convergence check when
+ * tolerance > 0) to report the status. */
+int32_t sinkhorn_forward_device_v1(const sinkhorn_problem_v1* prob,
+                                   const sinkhorn_options_v1* opt, const float* mu,
+                                   const float* nu, const float* cost, float* out_cost,
+                                   float* out_log_u, float* out_log_v, int32_t* out_iterations,
+                                   float* out_residuals, void* workspace,
+                                   size_t workspace_bytes, void* stream);
+
+/* batch_backward (batch.py:352-375): grad = upstream[b]*lambda*(x - mean_i x).
+ * Any -inf in a lane returns 13; `out_zero_mass_lane` (host, may be NULL)
+ * receives the first such lane.  No workspace beyond 64 bytes (passed). */
+int32_t sinkhorn_backward_device_v1(int64_t B, int64_t d1, int64_t d2, double lambda,
+                                    const float* log_u, const float* log_v,
+                                    const float* upstream, float* out_grad_mu,
+                                    float* out_grad_nu, int32_t* out_zero_mass_lane,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* One half-sweep, fused_log_reduction (batch.py:208-230):
+ * out[b,j] = target[b,j] - logsumexp_i(-cost[i,j]/lambda + log_x[b,i]),
+ * shapes log_x (B,d1), cost (d1,d2), target (B,d2), out (B,d2), natural log.
+ * With out_max/out_sum non-NULL the (max, sum) accumulator pairs of the
+ * reduction are emitted instead (log base 2: lse = max + log2(sum)), which is
+ * the partial state a row-sharded solve merges across GPUs
+ * (OnlineLseAccumulator.merge, batch.py:116-130); `out` may then be NULL.
+ * Workspace: sinkhorn_half_sweep_workspace_bytes_v1. */
+size_t sinkhorn_half_sweep_workspace_bytes_v1(int64_t B, int64_t d1, int64_t d2);
+int32_t sinkhorn_half_sweep_device_v1(int64_t B, int64_t d1, int64_t d2, double lambda,
+                                      const float* log_x, const float* cost,
+                                      const float* target, float* out, float* out_max,
+                                      float* out_sum, void* workspace, size_t workspace_bytes,
+                                      void* stream);
+
+/* Transport-plan gradient w.r.t. the cost (north-star item 4, core.py:363-368):
+ * SHARED:     dC[i,j]   = sum_b upstream[b] * P_b[i,j]
+ * PER_SAMPLE: dC[b,i,j] = upstream[b] * P_b[i,j]
+ * with P_b[i,j] = exp(log_u[b,i] - c[i,j]/lambda + log_v[b,j]): the envelope
+ * gradient dE^lambda/dC = P, the same multiplier convention as the histogram
+ * gradient (pkg/docs/KNOWN-FAILURES.md:14-22); see DESIGN.md.
+ * GRID2D is rejected (no materialised cost to differentiate). */
+int32_t sinkhorn_plan_grad_device_v1(const sinkhorn_problem_v1* prob, double lambda,
+                                     const float* log_u, const float* log_v, const float* cost,
+                                     const float* upstream, float* out_grad_cost, void* stream);
+
+/* Human-readable detail for the last non-zero status on this thread. */
+const char* sinkhorn_last_error(void);
+
+/* Library version string ("paper_1907_01729_b200 <semver> sm_100a"). */
+const char* sinkhorn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SINKHORN_B200_H */

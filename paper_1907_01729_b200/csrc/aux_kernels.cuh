@@ -1,0 +1,331 @@
+// aux_kernels.cuh -- setup / validation / finalisation / backward kernels.
+//
+// None of these is on the per-iteration path; together they touch
+// O(B*(d1+d2)) values (plus one pass over a shared cost) per solve.
+#pragma once
+
+#include "common.cuh"
+
+namespace skb {
+
+// Status word: first error wins, in stream order, which reproduces the
+// reference's check order (shapes on the host, then histograms ffi.ts:111-115,
+// then the cost the CLI validates, core.py:53-63).
+__device__ __forceinline__ void set_status(int* status, int code) { atomicCAS(status, 0, code); }
+
+__global__ void fill_kernel(float* __restrict__ x, size_t n, float v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    x[i] = v;
+}
+
+// Per-row histogram validation (core.py:143-160, ffi.ts:53-63): finite,
+// non-negative, |sum - 1| <= 1e-6 with the sum in fp64 and a fixed-order tree.
+// One block per row; `bad_row` receives the first offending row (atomicMin).
+template <typename T>
+__global__ void __launch_bounds__(256) validate_rows_kernel(const T* __restrict__ m, int d,
+                                                            int* status, int* bad_row) {
+  __shared__ double s_sum[256];
+  __shared__ int s_bad[256];
+  const int b = blockIdx.x;
+  const T* row = m + (size_t)b * d;
+  double acc = 0.0;
+  int bad = 0;
+  for (int i = threadIdx.x; i < d; i += 256) {
+    const double v = (double)row[i];
+    if (!(v >= 0.0) || isinf(v)) bad = 1;   // NaN, -x, +-inf
+    acc += v;
+  }
+  s_sum[threadIdx.x] = acc;
+  s_bad[threadIdx.x] = bad;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      s_sum[threadIdx.x] += s_sum[threadIdx.x + w];
+      s_bad[threadIdx.x] |= s_bad[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (s_bad[0] || !(fabs(s_sum[0] - 1.0) <= 1e-6)) {
+      set_status(status, 11);
+      atomicMin(bad_row, b);
+    }
+  }
+}
+
+// Marginal setup (batch.py:291-296): log2 marginal, linear marginal and the
+// initial potential (0 on the support / -inf off it, or all -inf), written
+// in the solver layout x[b*sb + i*si] with padding rows/lanes = (-inf, 0, -inf).
+// Reads the (B, d) row-major input through a 32x32 shared tile so both the
+// read and the (possibly transposed) write are coalesced.
+__global__ void __launch_bounds__(256) prep_marginal_kernel(const float* __restrict__ m, int B,
+                                                            int d, int Bp, int Dp, long long sb,
+                                                            long long si, float* __restrict__ l2m,
+                                                            float* __restrict__ lin,
+                                                            float* __restrict__ pot0,
+                                                            int pot_on_support) {
+  __shared__ float tile[32][33];
+  const int i0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int b = b0 + r, i = i0 + tx;
+    tile[r][tx] = (b < B && i < d) ? m[(size_t)b * d + i] : 0.f;
+  }
+  __syncthreads();
+  const bool dim_major = (si != 1);
+  for (int r = ty; r < 32; r += 8) {
+    // dim-major: consecutive threads walk lanes; lane-major: walk dims
+    const int b = dim_major ? (b0 + tx) : (b0 + r);
+    const int i = dim_major ? (i0 + r) : (i0 + tx);
+    if (b >= Bp || i >= Dp) continue;
+    const float v = dim_major ? tile[tx][r] : tile[r][tx];
+    const bool valid = (b < B && i < d);
+    const size_t o = (size_t)b * sb + (size_t)i * si;
+    const float mv = valid ? v : 0.f;
+    l2m[o] = (valid && mv > 0.f) ? log2f(mv) : neg_inf();
+    lin[o] = mv;
+    pot0[o] = (valid && pot_on_support && mv > 0.f) ? 0.f : neg_inf();
+  }
+}
+
+// Shared cost setup: A2 = c * k (k = -log2e/lambda) into [D1p][D2p] and its
+// transpose into [D2p][D1p], -inf padding, plus CostMatrix validation
+// (finite, >= 0; core.py:53-63) -> status 15.
+__global__ void __launch_bounds__(256) prep_cost_kernel(const float* __restrict__ c, int d1,
+                                                        int d2, int D1p, int D2p, float k,
+                                                        float* __restrict__ a2,
+                                                        float* __restrict__ a2t, int* status) {
+  __shared__ float tile[32][33];
+  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  bool bad = false;
+  for (int r = ty; r < 32; r += 8) {
+    const int i = i0 + r, j = j0 + tx;
+    float v = neg_inf();
+    if (i < d1 && j < d2) {
+      const float cv = c[(size_t)i * d2 + j];
+      if (!(cv >= 0.f) || isinf(cv)) bad = true;
+      v = cv * k;
+    }
+    tile[r][tx] = v;
+    if (i < D1p && j < D2p) a2[(size_t)i * D2p + j] = v;
+  }
+  if (bad) set_status(status, 15);
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int j = j0 + r, i = i0 + tx;
+    if (j < D2p && i < D1p) a2t[(size_t)j * D1p + i] = tile[tx][r];
+  }
+}
+
+// Per-sample cost validation (optional pass over B*d1*d2 values).
+__global__ void validate_cost_kernel(const float* __restrict__ c, size_t n, int* status) {
+  bool bad = false;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const float v = c[i];
+    if (!(v >= 0.f) || isinf(v)) bad = true;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) set_status(status, 15);
+}
+
+// Max over lanes of the residual vector (NaN wins), for the host's stopping test
+// (batch.py:318-322).
+__global__ void reduce_max_kernel(const float* __restrict__ res, int B, float* out) {
+  __shared__ float s[256];
+  float v = 0.f;
+  for (int b = threadIdx.x; b < B; b += 256) {
+    const float r = res[b];
+    v = (r != r || v != v) ? __int_as_float(0x7fc00000) : fmaxf(v, r);
+  }
+  s[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const float a = s[threadIdx.x], bb = s[threadIdx.x + w];
+      s[threadIdx.x] = (a != a || bb != bb) ? __int_as_float(0x7fc00000) : fmaxf(a, bb);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+// E0 per lane (batch.py:334-337): cost_e0[b] = 2^(log2 sum_j 2^e0[j,b]).
+// Block = 256 threads = 8 warps over 32 lanes; warps split j and merge their
+// (max, sum) pairs in fixed order.
+__global__ void __launch_bounds__(256) e0_finalize_kernel(const float* __restrict__ e0, int B,
+                                                          int d2, long long sb, long long sj,
+                                                          float* __restrict__ out_cost,
+                                                          int* status) {
+  __shared__ float sm[8][32], ss[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.x * 32 + lane;
+  float m = kNegBig, s = 0.f;
+  if (b < B) {
+    for (int j = warp; j < d2; j += 8) {
+      const float v = e0[(size_t)b * sb + (size_t)j * sj];
+      if (v > m + kLazy) {
+        s *= ex2(m - v);
+        m = v;
+      }
+      s += ex2(v - m);
+    }
+  }
+  sm[warp][lane] = m;
+  ss[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && b < B) {
+    for (int w = 1; w < 8; ++w) lse_merge(m, s, sm[w][lane], ss[w][lane]);
+    const float cost = exp2f(lse_final(m, s));
+    out_cost[b] = cost;
+    if (!isfinite(cost)) set_status(status, 12);
+  }
+}
+
+// Solver layout (log2) -> caller layout (B, d) row-major natural log; NaN in
+// the state is status 12 (batch.py:326-327 NaNProduced, ffi.ts:124-128).
+__global__ void __launch_bounds__(256) export_potential_kernel(const float* __restrict__ x,
+                                                               int B, int d, long long sb,
+                                                               long long si,
+                                                               float* __restrict__ out,
+                                                               int* status, float scale) {
+  __shared__ float tile[32][33];
+  const int i0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const bool dim_major = (si != 1);
+  bool nan = false;
+  for (int r = ty; r < 32; r += 8) {
+    const int b = dim_major ? (b0 + tx) : (b0 + r);
+    const int i = dim_major ? (i0 + r) : (i0 + tx);
+    float v = 0.f;
+    if (b < B && i < d) v = x[(size_t)b * sb + (size_t)i * si];
+    if (dim_major) tile[tx][r] = v; else tile[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int b = b0 + r, i = i0 + tx;
+    if (b < B && i < d) {
+      const float v = tile[r][tx];
+      if (v != v) nan = true;
+      out[(size_t)b * d + i] = v * scale;
+    }
+  }
+  if (__any_sync(0xffffffffu, nan) && tx == 0) set_status(status, 12);
+}
+
+// Analytic backward (batch.py:352-375, ffi.ts:171-189): per lane row,
+// grad = up[b] * lambda * (x - mean x), mean in fp64 with a fixed-order tree;
+// any -inf -> status 13 and the first such lane.  grid (B, 2 sides).
+template <typename T>
+__global__ void __launch_bounds__(256) backward_kernel(const T* __restrict__ log_u,
+                                                       const T* __restrict__ log_v, int d1,
+                                                       int d2, double lam,
+                                                       const T* __restrict__ up,
+                                                       T* __restrict__ g_mu,
+                                                       T* __restrict__ g_nu, int* status,
+                                                       int* bad_lane) {
+  __shared__ double s_sum[256];
+  __shared__ int s_dead[256];
+  const int b = blockIdx.x;
+  const bool side_u = (blockIdx.y == 0);
+  const int d = side_u ? d1 : d2;
+  const T* x = (side_u ? log_u : log_v) + (size_t)b * d;
+  T* g = (side_u ? g_mu : g_nu) + (size_t)b * d;
+  double acc = 0.0;
+  int dead = 0;
+  for (int i = threadIdx.x; i < d; i += 256) {
+    const double v = (double)x[i];
+    if (isinf(v) && v < 0) dead = 1;
+    acc += v;
+  }
+  s_sum[threadIdx.x] = acc;
+  s_dead[threadIdx.x] = dead;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      s_sum[threadIdx.x] += s_sum[threadIdx.x + w];
+      s_dead[threadIdx.x] |= s_dead[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (s_dead[0]) {
+    if (threadIdx.x == 0) {
+      set_status(status, 13);
+      atomicMin(bad_lane, b);
+    }
+    return;
+  }
+  const double mean = s_sum[0] / (double)d;
+  const double scale = (double)up[b] * lam;
+  for (int i = threadIdx.x; i < d; i += 256) g[i] = (T)(scale * ((double)x[i] - mean));
+}
+
+// Caller layout (B, d) row-major natural log -> solver layout (log2), -inf padding.
+__global__ void __launch_bounds__(256) import_potential_kernel(const float* __restrict__ in,
+                                                               int B, int d, int Bp, int Dp,
+                                                               long long sb, long long si,
+                                                               float* __restrict__ x) {
+  __shared__ float tile[32][33];
+  const int i0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int b = b0 + r, i = i0 + tx;
+    tile[r][tx] = (b < B && i < d) ? in[(size_t)b * d + i] * kLog2e : neg_inf();
+  }
+  __syncthreads();
+  const bool dim_major = (si != 1);
+  for (int r = ty; r < 32; r += 8) {
+    const int b = dim_major ? (b0 + tx) : (b0 + r);
+    const int i = dim_major ? (i0 + r) : (i0 + tx);
+    if (b >= Bp || i >= Dp) continue;
+    x[(size_t)b * sb + (size_t)i * si] = dim_major ? tile[tx][r] : tile[r][tx];
+  }
+}
+
+// double <-> float conversions for the host-buffer (float64) ABI layer.
+__global__ void f64_to_f32_kernel(const double* __restrict__ a, float* __restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    b[i] = (float)a[i];
+}
+__global__ void f32_to_f64_kernel(const float* __restrict__ a, double* __restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    b[i] = (double)a[i];
+}
+
+// Transport-plan gradient dC (core.py:363-368): for a shared cost
+// dC[i,j] = sum_b up[b] * 2^(f2[b,i] + A2[i,j] + g2[b,j]) with natural-log
+// inputs log_u/log_v (B, d) row-major; each plan entry is <= 1, so the sum is
+// formed directly in the linear domain.  One thread per (i, j); lanes looped.
+__global__ void __launch_bounds__(256) plan_grad_shared_kernel(
+    const float* __restrict__ log_u, const float* __restrict__ log_v,
+    const float* __restrict__ c, const float* __restrict__ up, int B, int d1, int d2, float k,
+    float* __restrict__ dc) {
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int i = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (i >= d1 || j >= d2) return;
+  const float a = c[(size_t)i * d2 + j] * k;
+  float acc = 0.f;
+  for (int b = 0; b < B; ++b) {
+    const float t = (log_u[(size_t)b * d1 + i] + log_v[(size_t)b * d2 + j]) * kLog2e + a;
+    acc = fmaf(up[b], exp2f(t), acc);
+  }
+  dc[(size_t)i * d2 + j] = acc;
+}
+
+__global__ void __launch_bounds__(256) plan_grad_per_sample_kernel(
+    const float* __restrict__ log_u, const float* __restrict__ log_v,
+    const float* __restrict__ c, const float* __restrict__ up, int d1, int d2, float k,
+    float* __restrict__ dc) {
+  const int b = blockIdx.z;
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int i = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (i >= d1 || j >= d2) return;
+  const size_t o = ((size_t)b * d1 + i) * d2 + j;
+  const float t = (log_u[(size_t)b * d1 + i] + log_v[(size_t)b * d2 + j]) * kLog2e + c[o] * k;
+  dc[o] = up[b] * exp2f(t);
+}
+
+}  // namespace skb

@@ -1,0 +1,123 @@
+// common.cuh -- sm_100a helpers shared by the Sinkhorn kernels.
+//
+// Everything the iteration computes lives in log base 2: potentials
+// f2 = log_u * log2(e), costs A2 = -c * log2(e) / lambda, so every exponential
+// is one MUFU.EX2 (ex2.approx.ftz.f32) and every log one MUFU.LG2.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace skb {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+// Finite "minus infinity" for running maxima: keeps (m - m') finite so the
+// online rescale never evaluates exp(-inf - -inf) = NaN (batch.py:106-110
+// guards the same case with its _maybe_dead mask).
+constexpr float kNegBig = -1.0e30f;
+// Lazy rescale threshold (log2 units): the running max is only raised when a
+// chunk exceeds it by more than this, so terms stay <= 2^8 and the sum of up
+// to 2^20 of them cannot overflow fp32.
+constexpr float kLazy = 8.0f;
+
+// Half-sweep epilogues (see sweep_tiled.cuh) and fused residual terms.
+enum SweepMode : int { kModeUpdate = 0, kModePartial = 1, kModeTail = 2 };
+enum ResKind : int { kResNone = 0, kResRow = 1, kResCol = 2 };
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float neg_inf() { return __int_as_float(0xff800000); }
+
+// (m, s) -> log2-sum-exp; an empty accumulator (s == 0) is -inf (batch.py:132-138).
+__device__ __forceinline__ float lse_final(float m, float s) {
+  return s > 0.0f ? m + log2f(s) : neg_inf();
+}
+
+// OnlineLseAccumulator.merge (batch.py:116-130) on (max, sum) pairs; both
+// maxima are finite (>= kNegBig) by construction so no NaN guard is needed.
+__device__ __forceinline__ void lse_merge(float& m, float& s, float m2, float s2) {
+  float mn = fmaxf(m, m2);
+  s = s * ex2(m - mn) + s2 * ex2(m2 - mn);
+  m = mn;
+}
+
+// target - lse with the reference's zero-mass rule: a -inf target stays -inf
+// (test_reduction.py:207-216) even where the reduction is also empty.
+__device__ __forceinline__ float sweep_out(float target, float lse) {
+  return target == neg_inf() ? neg_inf() : target - lse;
+}
+
+// Non-negative float max via integer atomics (order-independent, deterministic).
+__device__ __forceinline__ void atomic_max_nonneg(float* addr, float v) {
+  atomicMax(reinterpret_cast<unsigned int*>(addr), __float_as_uint(v));
+}
+
+// ---- programmatic dependent launch (griddepcontrol) ----------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---- mbarrier + TMA ------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+
+// 2-D tiled TMA load: box at (c0 = inner coordinate, c1 = outer) into smem,
+// completing `bytes` on the mbarrier.
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+}  // namespace skb

@@ -1,0 +1,876 @@
+// sinkhorn_abi.cu -- host runtime + C ABI of the B200 Sinkhorn loss.
+//
+// The iteration loop (batch.py:314-324) runs here in C++: it enqueues the
+// half-sweep kernels on the caller's stream with programmatic dependent
+// launch, keeps every intermediate in the caller-provided workspace, and only
+// synchronises when the reference's semantics need a host decision (the
+// convergence test every check_interval iterations when tolerance > 0) and once
+// at the end to report the status word.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/sinkhorn_b200.h"
+#include "aux_kernels.cuh"
+#include "common.cuh"
+#include "sweep_lane.cuh"
+#include "sweep_tiled.cuh"
+
+using namespace skb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CK(expr)                                                                           \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(SINKHORN_STATUS_CUDA_ERROR,                                              \
+                  std::string(#expr) + ": " + cudaGetErrorString(_e));                     \
+  } while (0)
+
+// ---- tiled-sweep configuration ---------------------------------------------
+constexpr int BT = 64, PT = 64, QC = 32, RB = 4, RP = 4, NSTAGE = 4;
+constexpr int KC_UPD = 8, KC_TAIL = 4;
+constexpr int TILE_PAD = 64;  // dims padded so both q (QC) and p (PT) tiles divide them
+constexpr int MAX_OCC = 2;
+
+template <bool kGrid, int kMode>
+struct TiledK {
+  static constexpr int KC = (kMode == kModeTail) ? KC_TAIL : KC_UPD;
+  using S = TiledSweep<BT, PT, QC, RB, RP, KC, NSTAGE, kGrid, kMode>;
+  static void* fn() {
+    return reinterpret_cast<void*>(
+        &tiled_sweep_kernel<BT, PT, QC, RB, RP, KC, NSTAGE, kGrid, kMode>);
+  }
+};
+
+struct DeviceInfo {
+  int dev = -1;
+  int sms = 148;
+};
+
+DeviceInfo device_info() {
+  DeviceInfo di;
+  cudaGetDevice(&di.dev);
+  cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, di.dev);
+  return di;
+}
+
+size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+
+inline float neg_inf_host() { return -INFINITY; }
+
+// ---- TMA descriptor encoding through the driver entry point ----------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D fp32 row-major [rows][cols] tensor, box {box_cols, box_rows}.
+bool make_tmap(CUtensorMap* m, const float* base, size_t rows, size_t cols, int box_rows,
+               int box_cols) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// ---- launch helpers ----------------------------------------------------------
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+int grid_for(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 16); }
+
+// ---- workspace layout --------------------------------------------------------
+struct Carver {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    size_t o = off;
+    off = round_up(off + bytes, 256);
+    return o;
+  }
+};
+
+struct Layout {
+  bool tiled = true;
+  int64_t B = 0, d1 = 0, d2 = 0;
+  int Bp = 0, D1p = 0, D2p = 0;   // padded extents (tiled) / leading dims (lane)
+  long long sb1 = 0, si1 = 0, sb2 = 0, si2 = 0;  // element (b,i) at b*sb + i*si
+  size_t a2 = 0, a2t = 0, f2 = 0, g2[2] = {0, 0}, l2mu = 0, l2nu = 0, mu = 0, nu = 0, e0 = 0;
+  size_t res = 0, scratch = 0, part = 0, counters = 0, status = 0, badrow = 0, total = 0;
+  size_t part_bytes = 0, counter_count = 0;
+  int lane_nsplit = 1, lane_nj = 1, lane_vec = 4;
+};
+
+Layout make_layout(const sinkhorn_problem_v1& pr, int sms) {
+  Layout L;
+  L.B = pr.B;
+  L.d1 = pr.d1;
+  L.d2 = pr.d2;
+  L.tiled = (pr.cost_kind != SINKHORN_COST_PER_SAMPLE);
+  Carver c;
+  if (L.tiled) {
+    L.Bp = (int)round_up(pr.B, BT);
+    L.D1p = (int)round_up(pr.d1, TILE_PAD);
+    L.D2p = (int)round_up(pr.d2, TILE_PAD);
+    L.sb1 = L.sb2 = 1;
+    L.si1 = L.si2 = L.Bp;
+    if (pr.cost_kind == SINKHORN_COST_SHARED) {
+      L.a2 = c.take((size_t)L.D1p * L.D2p * 4);
+      L.a2t = c.take((size_t)L.D2p * L.D1p * 4);
+    }
+    const size_t n1 = (size_t)L.D1p * L.Bp * 4, n2 = (size_t)L.D2p * L.Bp * 4;
+    L.f2 = c.take(n1);
+    L.g2[0] = c.take(n2);
+    L.g2[1] = c.take(n2);
+    L.l2mu = c.take(n1);
+    L.l2nu = c.take(n2);
+    L.mu = c.take(n1);
+    L.nu = c.take(n2);
+    L.e0 = c.take(n2);
+    L.part_bytes = (size_t)sms * MAX_OCC * 2 * 3 * BT * PT * 4;
+    L.part = c.take(L.part_bytes);
+    L.counter_count = (size_t)(L.Bp / BT) * (std::max(L.D1p, L.D2p) / PT);
+  } else {
+    L.lane_vec = (pr.d2 % 4 == 0 && pr.d1 % 4 == 0) ? 4 : 1;
+    L.Bp = (int)pr.B;
+    L.D1p = (int)round_up(pr.d1, 4);
+    L.D2p = (int)round_up(pr.d2, 4);
+    L.sb1 = L.D1p;
+    L.si1 = 1;
+    L.sb2 = L.D2p;
+    L.si2 = 1;
+    const size_t n1 = (size_t)L.B * L.D1p * 4, n2 = (size_t)L.B * L.D2p * 4;
+    L.f2 = c.take(n1);
+    L.g2[0] = c.take(n2);
+    L.g2[1] = c.take(n2);
+    L.l2mu = c.take(n1);
+    L.l2nu = c.take(n2);
+    L.mu = c.take(n1);
+    L.nu = c.take(n2);
+    L.e0 = c.take(n2);
+    L.lane_nj = (int)((pr.d2 + 256 * L.lane_vec - 1) / (256 * L.lane_vec));
+    const long long ctas = (long long)pr.B * L.lane_nj;
+    const long long want = 4LL * sms * 8;   // a few waves of resident CTAs
+    int ns = (int)std::min<long long>(std::max<long long>(1, want / std::max(1LL, ctas)), 16);
+    ns = (int)std::min<long long>(ns, std::max<long long>(1, pr.d1 / 64));
+    L.lane_nsplit = ns;
+    L.part_bytes = ns > 1 ? (size_t)pr.B * L.lane_nj * ns * 3 * 256 * L.lane_vec * 4 : 256;
+    L.part = c.take(L.part_bytes);
+    L.counter_count = (size_t)pr.B * L.lane_nj;
+  }
+  L.res = c.take((size_t)std::max(L.Bp, 1) * 4);
+  L.scratch = c.take(64);
+  L.counters = c.take(std::max<size_t>(L.counter_count, 1) * 4);
+  L.status = c.take(4);
+  L.badrow = c.take(4);
+  L.total = c.off;
+  return L;
+}
+
+template <typename T>
+T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+int occupancy_tiled(void* fn, size_t smem) {
+  static int cache[8] = {0};
+  (void)cache;
+  int occ = 1;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, BT / RB * (PT / RP), smem);
+  return std::max(1, std::min(occ, MAX_OCC));
+}
+
+// One tiled half-sweep launch.
+struct TiledArgs {
+  const CUtensorMap* tg;
+  const CUtensorMap* tx;
+  int Qv, Pv, Qp, Pp;
+  const float* target;
+  const float* marg;
+  float* out;
+  const float* old;
+  float* res;
+  int res_kind;
+  float* e0;
+  float* pmax;
+  float* psum;
+};
+
+template <bool kGrid, int kMode>
+int launch_tiled(const Layout& L, void* ws, const DeviceInfo& di, const TiledArgs& a,
+                 const sinkhorn_problem_v1& pr, float lam, cudaStream_t st) {
+  using K = TiledK<kGrid, kMode>;
+  TiledSweepParams p = {};
+  p.Qv = a.Qv;
+  p.Pv = a.Pv;
+  p.Bp = L.Bp;
+  p.ntile_b = L.Bp / BT;
+  p.ntile_p = a.Pp / PT;
+  p.nq = a.Qp / QC;
+  p.W = (long long)p.ntile_b * p.ntile_p * p.nq;
+  const size_t smem = K::S::SMEM_BYTES;
+  const int occ = occupancy_tiled(K::fn(), smem);
+  p.G = (int)std::min<long long>(p.W, (long long)di.sms * occ);
+  p.target = a.target;
+  p.marg = a.marg;
+  p.out = a.out;
+  p.old = a.old;
+  p.res = a.res;
+  p.res_kind = a.res_kind;
+  p.e0 = a.e0;
+  p.pmax = a.pmax;
+  p.psum = a.psum;
+  p.part = at<float>(ws, L.part);
+  p.counters = at<int>(ws, L.counters);
+  p.cinv = -lam * kLn2;
+  p.gk = -kLog2e / lam;
+  p.gnx = pr.grid_nx;
+  p.ghx2 = pr.grid_hx * pr.grid_hx;
+  p.ghy2 = pr.grid_hy * pr.grid_hy;
+  auto kern = &tiled_sweep_kernel<BT, PT, QC, RB, RP, K::KC, NSTAGE, kGrid, kMode>;
+  CK(launch_pdl(kern, dim3(p.G), dim3(K::S::NT), smem, st, *a.tg, *a.tx, p));
+  return 0;
+}
+
+// ---- the solver --------------------------------------------------------------
+struct Solve {
+  sinkhorn_problem_v1 pr;
+  sinkhorn_options_v1 op;
+  Layout L;
+  DeviceInfo di;
+  void* ws;
+  cudaStream_t st;
+  float lam;
+  CUtensorMap tm_a2, tm_a2t, tm_f2, tm_g2[2];
+  const float* cost;
+
+  float* F(size_t off) const { return at<float>(ws, off); }
+
+  int setup_maps() {
+    if (!L.tiled) return 0;
+    const float* gsrc_col = pr.cost_kind == SINKHORN_COST_SHARED ? F(L.a2) : F(L.f2);
+    const float* gsrc_row = pr.cost_kind == SINKHORN_COST_SHARED ? F(L.a2t) : F(L.f2);
+    bool ok = true;
+    if (pr.cost_kind == SINKHORN_COST_SHARED) {
+      ok &= make_tmap(&tm_a2, gsrc_col, L.D1p, L.D2p, QC, PT);
+      ok &= make_tmap(&tm_a2t, gsrc_row, L.D2p, L.D1p, QC, PT);
+    }
+    ok &= make_tmap(&tm_f2, F(L.f2), L.D1p, L.Bp, QC, BT);
+    ok &= make_tmap(&tm_g2[0], F(L.g2[0]), L.D2p, L.Bp, QC, BT);
+    ok &= make_tmap(&tm_g2[1], F(L.g2[1]), L.D2p, L.Bp, QC, BT);
+    if (pr.cost_kind != SINKHORN_COST_SHARED) {
+      tm_a2 = tm_f2;   // unused by the grid kernel; any valid map
+      tm_a2t = tm_f2;
+    }
+    return ok ? 0 : fail(SINKHORN_STATUS_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
+  }
+
+  // column half-sweep: g2[dst] = l2nu - LSE_i(A2 + f2)
+  int col_sweep(int dst, int src_old, int res_kind) {
+    if (L.tiled) {
+      TiledArgs a = {&tm_a2, &tm_f2, (int)pr.d1, (int)pr.d2, L.D1p, L.D2p, F(L.l2nu), F(L.nu),
+                     F(L.g2[dst]), F(L.g2[src_old]), F(L.res), res_kind, nullptr, nullptr,
+                     nullptr};
+      return pr.cost_kind == SINKHORN_COST_GRID2D
+                 ? launch_tiled<true, kModeUpdate>(L, ws, di, a, pr, lam, st)
+                 : launch_tiled<false, kModeUpdate>(L, ws, di, a, pr, lam, st);
+    }
+    return lane_col(kModeUpdate, F(L.g2[dst]), F(L.g2[src_old]), res_kind);
+  }
+
+  // row half-sweep: f2 = l2mu - LSE_j(A2^T + g2[src])
+  int row_sweep(int src, int res_kind) {
+    if (L.tiled) {
+      TiledArgs a = {&tm_a2t, &tm_g2[src], (int)pr.d2, (int)pr.d1, L.D2p, L.D1p, F(L.l2mu),
+                     F(L.mu), F(L.f2), nullptr, F(L.res), res_kind, nullptr, nullptr, nullptr};
+      return pr.cost_kind == SINKHORN_COST_GRID2D
+                 ? launch_tiled<true, kModeUpdate>(L, ws, di, a, pr, lam, st)
+                 : launch_tiled<false, kModeUpdate>(L, ws, di, a, pr, lam, st);
+    }
+    LaneSweepParams p = lane_params();
+    p.x = F(L.g2[src]);
+    p.ldx = L.D2p;
+    p.ldo = L.D1p;
+    p.target = F(L.l2mu);
+    p.marg = F(L.mu);
+    p.out = F(L.f2);
+    p.res = F(L.res);
+    p.res_kind = res_kind;
+    const int rows = 32;
+    dim3 grid((unsigned)((pr.d1 + rows - 1) / rows), (unsigned)pr.B);
+    if (L.lane_vec == 4)
+      CK(launch_pdl(&lane_row_kernel<4>, grid, dim3(256), 0, st, p, rows));
+    else
+      CK(launch_pdl(&lane_row_kernel<1>, grid, dim3(256), 0, st, p, rows));
+    return 0;
+  }
+
+  // final column pass: E0 terms + column residual against g2[cur]
+  int tail(int cur) {
+    if (L.tiled) {
+      TiledArgs a = {&tm_a2, &tm_f2, (int)pr.d1, (int)pr.d2, L.D1p, L.D2p, F(L.l2nu), F(L.nu),
+                     nullptr, F(L.g2[cur]), F(L.res), kResCol, F(L.e0), nullptr, nullptr};
+      return pr.cost_kind == SINKHORN_COST_GRID2D
+                 ? launch_tiled<true, kModeTail>(L, ws, di, a, pr, lam, st)
+                 : launch_tiled<false, kModeTail>(L, ws, di, a, pr, lam, st);
+    }
+    return lane_col(kModeTail, nullptr, F(L.g2[cur]), kResCol);
+  }
+
+  LaneSweepParams lane_params() {
+    LaneSweepParams p = {};
+    p.d1 = (int)pr.d1;
+    p.d2 = (int)pr.d2;
+    p.cost = cost;
+    p.kscale = -kLog2e / lam;
+    p.part = F(L.part);
+    p.counters = at<int>(ws, L.counters);
+    p.nsplit = L.lane_nsplit;
+    p.status = at<int>(ws, L.status);
+    return p;
+  }
+
+  int lane_col(int mode, float* out, const float* old, int res_kind) {
+    LaneSweepParams p = lane_params();
+    p.x = F(L.f2);
+    p.ldx = L.D1p;
+    p.ldo = L.D2p;
+    p.target = F(L.l2nu);
+    p.marg = F(L.nu);
+    p.out = out;
+    p.old = old;
+    p.res = F(L.res);
+    p.res_kind = res_kind;
+    p.e0 = F(L.e0);
+    dim3 grid((unsigned)L.lane_nsplit, (unsigned)pr.B, (unsigned)L.lane_nj);
+    if (mode == kModeTail) {
+      if (L.lane_vec == 4) CK(launch_pdl(&lane_col_kernel<4, kModeTail>, grid, dim3(256), 0, st, p));
+      else CK(launch_pdl(&lane_col_kernel<1, kModeTail>, grid, dim3(256), 0, st, p));
+    } else {
+      if (L.lane_vec == 4) CK(launch_pdl(&lane_col_kernel<4, kModeUpdate>, grid, dim3(256), 0, st, p));
+      else CK(launch_pdl(&lane_col_kernel<1, kModeUpdate>, grid, dim3(256), 0, st, p));
+    }
+    return 0;
+  }
+
+  int zero_res() {
+    CK(cudaMemsetAsync(F(L.res), 0, (size_t)std::max(L.Bp, 1) * 4, st));
+    return 0;
+  }
+
+  int read_status(int* out) {
+    CK(cudaMemcpyAsync(out, at<int>(ws, L.status), 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return 0;
+  }
+};
+
+int fill(float* p, size_t n, float v, cudaStream_t st) {
+  if (n == 0) return 0;
+  fill_kernel<<<grid_for(n), 256, 0, st>>>(p, n, v);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int check_problem(const sinkhorn_problem_v1* pr) {
+  if (!pr) return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null problem");
+  if (pr->B < 0 || pr->d1 < 0 || pr->d2 < 0)
+    return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "negative extent");
+  if (pr->B > INT32_MAX || pr->d1 > INT32_MAX || pr->d2 > INT32_MAX)
+    return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "extent exceeds int32");
+  if (pr->cost_kind == SINKHORN_COST_GRID2D) {
+    if (pr->grid_nx < 1 || pr->grid_ny < 1 || (int64_t)pr->grid_nx * pr->grid_ny != pr->d1 ||
+        pr->d1 != pr->d2)
+      return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "grid cost needs d1 = d2 = nx*ny");
+    if (!(std::isfinite(pr->grid_hx) && std::isfinite(pr->grid_hy) && pr->grid_hx >= 0 &&
+          pr->grid_hy >= 0))
+      return fail(SINKHORN_STATUS_INVALID_COST, "grid spacing must be finite and >= 0");
+  } else if (pr->cost_kind != SINKHORN_COST_SHARED && pr->cost_kind != SINKHORN_COST_PER_SAMPLE) {
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "unknown cost_kind");
+  }
+  return 0;
+}
+
+int check_options(const sinkhorn_options_v1* op) {
+  if (!op) return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null options");
+  // SinkhornConfig.__post_init__ (core.py:88-96)
+  if (!(std::isfinite(op->lambda) && op->lambda > 0))
+    return fail(SINKHORN_STATUS_INVALID_CONFIG, "lam must be positive and finite");
+  if (op->max_iters < 1) return fail(SINKHORN_STATUS_INVALID_CONFIG, "max_iters must be >= 1");
+  if (!(std::isfinite(op->tolerance) && op->tolerance >= 0))
+    return fail(SINKHORN_STATUS_INVALID_CONFIG, "tolerance must be >= 0");
+  if (op->check_interval < 1)
+    return fail(SINKHORN_STATUS_INVALID_CONFIG, "check_interval must be >= 1");
+  return 0;
+}
+
+int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, const float* mu,
+                 const float* nu, const float* cost, float* out_cost, float* out_log_u,
+                 float* out_log_v, int32_t* out_iterations, float* out_residuals, void* ws,
+                 size_t ws_bytes, cudaStream_t st) {
+  Solve S;
+  S.pr = pr;
+  S.op = op;
+  S.di = device_info();
+  S.L = make_layout(pr, S.di.sms);
+  S.ws = ws;
+  S.st = st;
+  S.lam = (float)op.lambda;
+  S.cost = cost;
+  const Layout& L = S.L;
+  if (ws_bytes < L.total || ws == nullptr)
+    return fail(SINKHORN_STATUS_WORKSPACE, "workspace too small");
+  int* status = at<int>(ws, L.status);
+  int* badrow = at<int>(ws, L.badrow);
+
+  // ---- setup (batch.py:279-296) ----
+  CK(cudaMemsetAsync(status, 0, 4, st));
+  CK(cudaMemsetAsync(badrow, 0x7f, 4, st));
+  CK(cudaMemsetAsync(at<int>(ws, L.counters), 0, std::max<size_t>(L.counter_count, 1) * 4, st));
+  CK(cudaMemsetAsync(S.F(L.res), 0, (size_t)std::max(L.Bp, 1) * 4, st));
+  if (!(op.flags & SINKHORN_FLAG_SKIP_VALIDATION)) {
+    validate_rows_kernel<float><<<(unsigned)pr.B, 256, 0, st>>>(mu, (int)pr.d1, status, badrow);
+    validate_rows_kernel<float><<<(unsigned)pr.B, 256, 0, st>>>(nu, (int)pr.d2, status, badrow);
+    CK(cudaGetLastError());
+  }
+  {
+    dim3 g1((unsigned)((L.D1p + 31) / 32), (unsigned)((L.Bp + 31) / 32));
+    prep_marginal_kernel<<<g1, 256, 0, st>>>(mu, (int)pr.B, (int)pr.d1, L.Bp, L.D1p, L.sb1,
+                                              L.si1, S.F(L.l2mu), S.F(L.mu), S.F(L.f2), 1);
+    dim3 g2((unsigned)((L.D2p + 31) / 32), (unsigned)((L.Bp + 31) / 32));
+    prep_marginal_kernel<<<g2, 256, 0, st>>>(nu, (int)pr.B, (int)pr.d2, L.Bp, L.D2p, L.sb2,
+                                              L.si2, S.F(L.l2nu), S.F(L.nu), S.F(L.g2[0]), 0);
+    CK(cudaGetLastError());
+    if (int e = fill(S.F(L.g2[1]), (size_t)(L.tiled ? (size_t)L.D2p * L.Bp : (size_t)L.B * L.D2p),
+                     neg_inf_host(), st))
+      return e;
+  }
+  if (pr.cost_kind == SINKHORN_COST_SHARED) {
+    dim3 g((unsigned)((L.D2p + 31) / 32), (unsigned)((L.D1p + 31) / 32));
+    prep_cost_kernel<<<g, 256, 0, st>>>(cost, (int)pr.d1, (int)pr.d2, L.D1p, L.D2p,
+                                         (float)(-1.4426950408889634 / op.lambda), S.F(L.a2),
+                                         S.F(L.a2t), status);
+    CK(cudaGetLastError());
+  } else if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE && !(op.flags & SINKHORN_FLAG_SKIP_VALIDATION)) {
+    const size_t n = (size_t)pr.B * pr.d1 * pr.d2;
+    validate_cost_kernel<<<grid_for(n), 256, 0, st>>>(cost, n, status);
+    CK(cudaGetLastError());
+  }
+  if (int e = S.setup_maps()) return e;
+
+  // ---- lockstep iteration (batch.py:314-324) ----
+  const bool checks = op.tolerance > 0;
+  int cur = 0;            // g2[cur] holds log_v_k
+  bool have_next = false; // g2[cur] already advanced by a check sweep
+  int iters = 0;
+  bool converged = false;
+  for (int k = 1; k <= op.max_iters; ++k) {
+    if (!have_next) {
+      if (int e = S.col_sweep(cur ^ 1, cur, kResNone)) return e;
+      cur ^= 1;
+    }
+    have_next = false;
+    const bool last = (k == op.max_iters);
+    const bool check = checks && (k % op.check_interval == 0) && !last;
+    if (check || last) {
+      if (int e = S.zero_res()) return e;
+    }
+    if (int e = S.row_sweep(cur, (check || last) ? kResRow : kResNone)) return e;
+    iters = k;
+    if (check) {
+      // column sweep k+1 doubles as the column residual of iteration k
+      if (int e = S.col_sweep(cur ^ 1, cur, kResCol)) return e;
+      reduce_max_kernel<<<1, 256, 0, st>>>(S.F(L.res), (int)pr.B, S.F(L.scratch));
+      CK(cudaGetLastError());
+      float hmax = 0.f;
+      int hstatus = 0;
+      CK(cudaMemcpyAsync(&hmax, S.F(L.scratch), 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&hstatus, status, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (hstatus != 0) break;
+      if ((double)hmax <= op.tolerance) {
+        converged = true;   // keep g2[cur] = log_v_k; discard the k+1 sweep
+        break;
+      }
+      cur ^= 1;
+      have_next = true;
+    }
+  }
+  (void)converged;
+  // ---- tail: residual + stable E0 in one column pass (batch.py:323-337) ----
+  if (int e = S.tail(cur)) return e;
+  {
+    const int nb = (int)((pr.B + 31) / 32);
+    const long long sb = L.tiled ? 1 : L.D2p, sj = L.tiled ? L.Bp : 1;
+    e0_finalize_kernel<<<nb, 256, 0, st>>>(S.F(L.e0), (int)pr.B, (int)pr.d2, sb, sj, out_cost,
+                                           status);
+    dim3 gu((unsigned)((pr.d1 + 31) / 32), (unsigned)((pr.B + 31) / 32));
+    export_potential_kernel<<<gu, 256, 0, st>>>(S.F(L.f2), (int)pr.B, (int)pr.d1, L.sb1, L.si1,
+                                                out_log_u, status, kLn2);
+    dim3 gv((unsigned)((pr.d2 + 31) / 32), (unsigned)((pr.B + 31) / 32));
+    export_potential_kernel<<<gv, 256, 0, st>>>(S.F(L.g2[cur]), (int)pr.B, (int)pr.d2, L.sb2,
+                                                L.si2, out_log_v, status, kLn2);
+    CK(cudaGetLastError());
+    if (out_residuals)
+      CK(cudaMemcpyAsync(out_residuals, S.F(L.res), (size_t)pr.B * 4, cudaMemcpyDeviceToDevice,
+                         st));
+  }
+  if (out_iterations) *out_iterations = iters;
+  int hstatus = 0;
+  if (int e = S.read_status(&hstatus)) return e;
+  if (hstatus == 11) {
+    int row = 0;
+    cudaMemcpy(&row, badrow, 4, cudaMemcpyDeviceToHost);
+    return fail(11, "invalid histogram in row " + std::to_string(row));
+  }
+  if (hstatus != 0) return fail(hstatus, "device status " + std::to_string(hstatus));
+  return 0;
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI (the only symbols the library exports; built with -fvisibility=hidden)
+// =============================================================================
+#pragma GCC visibility push(default)
+extern "C" {
+
+const char* sinkhorn_last_error(void) { return g_last_error.c_str(); }
+
+const char* sinkhorn_version(void) { return "paper_1907_01729_b200 0.1.0 sm_100a"; }
+
+size_t sinkhorn_workspace_bytes_v1(const sinkhorn_problem_v1* prob) {
+  if (check_problem(prob) != 0) return 0;
+  return make_layout(*prob, device_info().sms).total;
+}
+
+int32_t sinkhorn_forward_device_v1(const sinkhorn_problem_v1* prob,
+                                   const sinkhorn_options_v1* opt, const float* mu,
+                                   const float* nu, const float* cost, float* out_cost,
+                                   float* out_log_u, float* out_log_v, int32_t* out_iterations,
+                                   float* out_residuals, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  if (int e = check_problem(prob)) return e;
+  if (prob->B == 0) {   // ffi.ts:107-109
+    if (out_iterations) *out_iterations = 0;
+    return 0;
+  }
+  if (prob->d1 == 0 || prob->d2 == 0)
+    return fail(SINKHORN_STATUS_INVALID_HISTOGRAM, "empty histogram cannot sum to 1");
+  if (int e = check_options(opt)) return e;
+  if (!mu || !nu || !out_cost || !out_log_u || !out_log_v ||
+      (prob->cost_kind != SINKHORN_COST_GRID2D && !cost))
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
+  return forward_impl(*prob, *opt, mu, nu, cost, out_cost, out_log_u, out_log_v, out_iterations,
+                      out_residuals, workspace, workspace_bytes,
+                      static_cast<cudaStream_t>(stream));
+}
+
+
+int32_t sinkhorn_backward_device_v1(int64_t B, int64_t d1, int64_t d2, double lambda,
+                                    const float* log_u, const float* log_v,
+                                    const float* upstream, float* out_grad_mu,
+                                    float* out_grad_nu, int32_t* out_zero_mass_lane,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  if (B < 0 || d1 < 0 || d2 < 0) return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "negative extent");
+  if (B == 0) return 0;
+  if (!log_u || !log_v || !upstream || !out_grad_mu || !out_grad_nu || !workspace)
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
+  if (workspace_bytes < 8) return fail(SINKHORN_STATUS_WORKSPACE, "backward needs 8 bytes");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int* status = static_cast<int*>(workspace);
+  int* bad = status + 1;
+  CK(cudaMemsetAsync(status, 0, 4, st));
+  CK(cudaMemsetAsync(bad, 0x7f, 4, st));
+  backward_kernel<float><<<dim3((unsigned)B, 2), 256, 0, st>>>(
+      log_u, log_v, (int)d1, (int)d2, lambda, upstream, out_grad_mu, out_grad_nu, status, bad);
+  CK(cudaGetLastError());
+  int h[2] = {0, 0};
+  CK(cudaMemcpyAsync(h, status, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h[0] == SINKHORN_STATUS_ZERO_MASS_LANE) {
+    if (out_zero_mass_lane) *out_zero_mass_lane = h[1];
+    return fail(SINKHORN_STATUS_ZERO_MASS_LANE, "zero-mass bin in lane " + std::to_string(h[1]));
+  }
+  return h[0];
+}
+
+size_t sinkhorn_half_sweep_workspace_bytes_v1(int64_t B, int64_t d1, int64_t d2) {
+  sinkhorn_problem_v1 pr = {B, d1, d2, SINKHORN_COST_SHARED, 0, 0, 0.f, 0.f};
+  if (check_problem(&pr) != 0) return 0;
+  return make_layout(pr, device_info().sms).total;
+}
+
+int32_t sinkhorn_half_sweep_device_v1(int64_t B, int64_t d1, int64_t d2, double lambda,
+                                      const float* log_x, const float* cost,
+                                      const float* target, float* out, float* out_max,
+                                      float* out_sum, void* workspace, size_t workspace_bytes,
+                                      void* stream) {
+  sinkhorn_problem_v1 pr = {B, d1, d2, SINKHORN_COST_SHARED, 0, 0, 0.f, 0.f};
+  if (int e = check_problem(&pr)) return e;
+  if (B == 0 || d2 == 0) return 0;
+  if (!(std::isfinite(lambda) && lambda > 0))
+    return fail(SINKHORN_STATUS_INVALID_CONFIG, "lam must be positive and finite");
+  const bool partial = (out_max != nullptr || out_sum != nullptr);
+  if (!log_x || !cost || (partial ? (!out_max || !out_sum) : (!out || !target)))
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
+  Solve S;
+  S.pr = pr;
+  S.di = device_info();
+  S.L = make_layout(pr, S.di.sms);
+  S.ws = workspace;
+  S.st = static_cast<cudaStream_t>(stream);
+  S.lam = (float)lambda;
+  S.cost = cost;
+  const Layout& L = S.L;
+  if (workspace == nullptr || workspace_bytes < L.total)
+    return fail(SINKHORN_STATUS_WORKSPACE, "workspace too small");
+  cudaStream_t st = S.st;
+  int* status = at<int>(workspace, L.status);
+  CK(cudaMemsetAsync(status, 0, 4, st));
+  CK(cudaMemsetAsync(at<int>(workspace, L.counters), 0,
+                     std::max<size_t>(L.counter_count, 1) * 4, st));
+  {
+    dim3 g((unsigned)((L.D2p + 31) / 32), (unsigned)((L.D1p + 31) / 32));
+    prep_cost_kernel<<<g, 256, 0, st>>>(cost, (int)d1, (int)d2, L.D1p, L.D2p,
+                                         (float)(-1.4426950408889634 / lambda), S.F(L.a2),
+                                         S.F(L.a2t), status);
+    dim3 gx((unsigned)((L.D1p + 31) / 32), (unsigned)((L.Bp + 31) / 32));
+    import_potential_kernel<<<gx, 256, 0, st>>>(log_x, (int)B, (int)d1, L.Bp, L.D1p, L.sb1,
+                                                 L.si1, S.F(L.f2));
+    if (!partial) {
+      dim3 gt((unsigned)((L.D2p + 31) / 32), (unsigned)((L.Bp + 31) / 32));
+      import_potential_kernel<<<gt, 256, 0, st>>>(target, (int)B, (int)d2, L.Bp, L.D2p, L.sb2,
+                                                   L.si2, S.F(L.l2nu));
+    }
+    CK(cudaGetLastError());
+  }
+  if (int e = S.setup_maps()) return e;
+  TiledArgs a = {&S.tm_a2, &S.tm_f2, (int)d1, (int)d2, L.D1p, L.D2p, S.F(L.l2nu), S.F(L.nu),
+                 S.F(L.g2[0]), nullptr, nullptr, kResNone, nullptr, S.F(L.g2[0]), S.F(L.g2[1])};
+  if (partial) {
+    if (int e = launch_tiled<false, kModePartial>(L, workspace, S.di, a, pr, S.lam, st)) return e;
+  } else {
+    if (int e = launch_tiled<false, kModeUpdate>(L, workspace, S.di, a, pr, S.lam, st)) return e;
+  }
+  dim3 gv((unsigned)((d2 + 31) / 32), (unsigned)((B + 31) / 32));
+  if (partial) {
+    export_potential_kernel<<<gv, 256, 0, st>>>(S.F(L.g2[0]), (int)B, (int)d2, L.sb2, L.si2,
+                                                out_max, status, 1.0f);
+    export_potential_kernel<<<gv, 256, 0, st>>>(S.F(L.g2[1]), (int)B, (int)d2, L.sb2, L.si2,
+                                                out_sum, status, 1.0f);
+  } else {
+    export_potential_kernel<<<gv, 256, 0, st>>>(S.F(L.g2[0]), (int)B, (int)d2, L.sb2, L.si2,
+                                                out, status, kLn2);
+  }
+  CK(cudaGetLastError());
+  int h = 0;
+  if (int e = S.read_status(&h)) return e;
+  return h == 0 ? 0 : fail(h, "device status " + std::to_string(h));
+}
+
+int32_t sinkhorn_plan_grad_device_v1(const sinkhorn_problem_v1* prob, double lambda,
+                                     const float* log_u, const float* log_v, const float* cost,
+                                     const float* upstream, float* out_grad_cost, void* stream) {
+  if (int e = check_problem(prob)) return e;
+  if (prob->cost_kind == SINKHORN_COST_GRID2D)
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "grid cost is not materialised");
+  if (!(std::isfinite(lambda) && lambda > 0))
+    return fail(SINKHORN_STATUS_INVALID_CONFIG, "lam must be positive and finite");
+  if (prob->d1 == 0 || prob->d2 == 0) return 0;
+  if (!log_u || !log_v || !cost || !upstream || !out_grad_cost)
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const float k = (float)(-1.4426950408889634 / lambda);
+  dim3 g((unsigned)((prob->d2 + 31) / 32), (unsigned)((prob->d1 + 7) / 8));
+  if (prob->cost_kind == SINKHORN_COST_SHARED) {
+    plan_grad_shared_kernel<<<g, 256, 0, st>>>(log_u, log_v, cost, upstream, (int)prob->B,
+                                                (int)prob->d1, (int)prob->d2, k, out_grad_cost);
+  } else {
+    if (prob->B == 0) return 0;
+    g.z = (unsigned)prob->B;
+    plan_grad_per_sample_kernel<<<g, 256, 0, st>>>(log_u, log_v, cost, upstream, (int)prob->d1,
+                                                    (int)prob->d2, k, out_grad_cost);
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// ---- layer 1: host float64 views, the exact ffi.ts contract -----------------
+static bool view_ok(const sinkhorn_view_v1* v, int ndim, int64_t s0, int64_t s1) {
+  if (!v || v->ndim != ndim) return false;
+  if (v->shape[0] != s0 || (ndim == 2 && v->shape[1] != s1)) return false;
+  const int64_t n = ndim == 2 ? s0 * s1 : s0;
+  return n <= v->length && (n == 0 || v->data != nullptr);   // ffi.ts:33-38
+}
+
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+}  // namespace
+
+int32_t sinkhorn_forward_v1(const sinkhorn_view_v1* mu, const sinkhorn_view_v1* nu,
+                            const sinkhorn_view_v1* cost, double lambda, int32_t max_iters,
+                            double tolerance, const sinkhorn_view_v1* out_cost,
+                            const sinkhorn_view_v1* out_log_u, const sinkhorn_view_v1* out_log_v) {
+  // ffi.ts:91-106 shape checks
+  if (!mu || !nu || !cost || mu->ndim != 2 || nu->ndim != 2 || cost->ndim != 2)
+    return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "mu, nu and cost must be 2-D");
+  const int64_t B = mu->shape[0], d1 = mu->shape[1], d2 = nu->shape[1];
+  if (!view_ok(mu, 2, B, d1) || !view_ok(nu, 2, B, d2) || nu->shape[0] != B ||
+      !view_ok(cost, 2, d1, d2) || !view_ok(out_cost, 1, B, 0) || !view_ok(out_log_u, 2, B, d1) ||
+      !view_ok(out_log_v, 2, B, d2))
+    return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "view shapes disagree");
+  if (B == 0) return 0;   // ffi.ts:107-109
+  if (B > INT32_MAX || d1 > INT32_MAX || d2 > INT32_MAX)
+    return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "extent exceeds int32");
+  if (d1 == 0 || d2 == 0)
+    return fail(SINKHORN_STATUS_INVALID_HISTOGRAM, "empty histogram cannot sum to 1");
+  cudaStream_t st = cudaStreamPerThread;
+  const size_t n_mu = (size_t)B * d1, n_nu = (size_t)B * d2, n_c = (size_t)d1 * d2;
+  sinkhorn_problem_v1 pr = {B, d1, d2, SINKHORN_COST_SHARED, 0, 0, 0.f, 0.f};
+  const size_t ws_bytes = make_layout(pr, device_info().sms).total;
+  // one device allocation: f64 staging + f32 inputs/outputs + solver workspace
+  Carver c;
+  const size_t o_d64 = c.take(std::max(n_mu + n_nu + n_c, n_mu + n_nu + (size_t)B) * 8);
+  const size_t o_f_mu = c.take(n_mu * 4), o_f_nu = c.take(n_nu * 4), o_f_c = c.take(n_c * 4);
+  const size_t o_cost = c.take((size_t)B * 4), o_lu = c.take(n_mu * 4), o_lv = c.take(n_nu * 4);
+  const size_t o_ws = c.take(ws_bytes);
+  DevBuf buf;
+  buf.st = st;
+  CK(cudaMallocAsync(&buf.p, c.off, st));
+  double* d64 = at<double>(buf.p, o_d64);
+  CK(cudaMemcpyAsync(d64, mu->data, n_mu * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d64 + n_mu, nu->data, n_nu * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d64 + n_mu + n_nu, cost->data, n_c * 8, cudaMemcpyHostToDevice, st));
+  // histogram validation in float64, exactly ffi.ts:53-63 (status 11)
+  int* vstat = at<int>(buf.p, o_ws + make_layout(pr, device_info().sms).status);
+  int* vbad = at<int>(buf.p, o_ws + make_layout(pr, device_info().sms).badrow);
+  CK(cudaMemsetAsync(vstat, 0, 4, st));
+  CK(cudaMemsetAsync(vbad, 0x7f, 4, st));
+  validate_rows_kernel<double><<<(unsigned)B, 256, 0, st>>>(d64, (int)d1, vstat, vbad);
+  validate_rows_kernel<double><<<(unsigned)B, 256, 0, st>>>(d64 + n_mu, (int)d2, vstat, vbad);
+  CK(cudaGetLastError());
+  int hs = 0;
+  CK(cudaMemcpyAsync(&hs, vstat, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hs != 0) return fail(hs, "invalid histogram");
+  sinkhorn_options_v1 op = {lambda, max_iters, 10, tolerance, SINKHORN_FLAG_SKIP_VALIDATION};
+  if (int e = check_options(&op)) return e;
+  f64_to_f32_kernel<<<grid_for(n_mu), 256, 0, st>>>(d64, at<float>(buf.p, o_f_mu), n_mu);
+  f64_to_f32_kernel<<<grid_for(n_nu), 256, 0, st>>>(d64 + n_mu, at<float>(buf.p, o_f_nu), n_nu);
+  f64_to_f32_kernel<<<grid_for(n_c), 256, 0, st>>>(d64 + n_mu + n_nu, at<float>(buf.p, o_f_c), n_c);
+  CK(cudaGetLastError());
+  int32_t iters = 0;
+  int e = forward_impl(pr, op, at<float>(buf.p, o_f_mu), at<float>(buf.p, o_f_nu),
+                       at<float>(buf.p, o_f_c), at<float>(buf.p, o_cost), at<float>(buf.p, o_lu),
+                       at<float>(buf.p, o_lv), &iters, nullptr, at<void>(buf.p, o_ws), ws_bytes,
+                       st);
+  if (e != 0) return e;
+  // outputs back as float64 (ffi.ts:123-133 writes in place)
+  f32_to_f64_kernel<<<grid_for(B), 256, 0, st>>>(at<float>(buf.p, o_cost), d64, (size_t)B);
+  f32_to_f64_kernel<<<grid_for(n_mu), 256, 0, st>>>(at<float>(buf.p, o_lu), d64 + B, n_mu);
+  f32_to_f64_kernel<<<grid_for(n_nu), 256, 0, st>>>(at<float>(buf.p, o_lv), d64 + B + n_mu, n_nu);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out_cost->data, d64, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out_log_u->data, d64 + B, n_mu * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out_log_v->data, d64 + B + n_mu, n_nu * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int32_t sinkhorn_backward_v1(const sinkhorn_view_v1* log_u, const sinkhorn_view_v1* log_v,
+                             double lambda, const sinkhorn_view_v1* upstream,
+                             const sinkhorn_view_v1* out_grad_mu,
+                             const sinkhorn_view_v1* out_grad_nu) {
+  // ffi.ts:151-165
+  if (!log_u || !log_v || log_u->ndim != 2 || log_v->ndim != 2)
+    return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "potentials must be 2-D");
+  const int64_t B = log_u->shape[0], d1 = log_u->shape[1], d2 = log_v->shape[1];
+  if (log_v->shape[0] != B || !view_ok(log_u, 2, B, d1) || !view_ok(log_v, 2, B, d2) ||
+      !view_ok(upstream, 1, B, 0) || !view_ok(out_grad_mu, 2, B, d1) ||
+      !view_ok(out_grad_nu, 2, B, d2))
+    return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "view shapes disagree");
+  if (B == 0) return 0;
+  if (B > INT32_MAX || d1 > INT32_MAX || d2 > INT32_MAX)
+    return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "extent exceeds int32");
+  cudaStream_t st = cudaStreamPerThread;
+  const size_t n1 = (size_t)B * d1, n2 = (size_t)B * d2;
+  DevBuf buf;
+  buf.st = st;
+  CK(cudaMallocAsync(&buf.p, (2 * n1 + 2 * n2 + B) * 8 + 16, st));
+  double* u = static_cast<double*>(buf.p);
+  double* v = u + n1;
+  double* up = v + n2;
+  double* gu = up + B;
+  double* gv = gu + n1;
+  int* stat = reinterpret_cast<int*>(gv + n2);
+  CK(cudaMemcpyAsync(u, log_u->data, n1 * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(v, log_v->data, n2 * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(up, upstream->data, (size_t)B * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(stat, 0, 4, st));
+  CK(cudaMemsetAsync(stat + 1, 0x7f, 4, st));
+  backward_kernel<double><<<dim3((unsigned)B, 2), 256, 0, st>>>(u, v, (int)d1, (int)d2, lambda,
+                                                                up, gu, gv, stat, stat + 1);
+  CK(cudaGetLastError());
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, stat, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h != 0) return fail(h, "zero-mass lane");   // ffi.ts:177-179
+  CK(cudaMemcpyAsync(out_grad_mu->data, gu, n1 * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out_grad_nu->data, gv, n2 * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+}  // extern "C"
+#pragma GCC visibility pop

@@ -1,0 +1,249 @@
+"""PyTorch-facing Sinkhorn loss over the sm_100a C ABI.
+
+Mirrors the reference's differentiable node ``sinkhornLoss``
+(pkg/frontend/src/loss.ts:59-131): forward solves every lane through the
+C-ABI forward and saves only the final log potentials (loss.ts:104);
+backward turns them into mean-zero gradients through the C-ABI backward
+without re-running anything (loss.ts:105-128), so autograd memory does not
+depend on the iteration count.
+
+PyTorch supplies device memory (the caching allocator backs the solver
+workspace), the stream, and autograd; every arithmetic operation on the
+path is one of the library's kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .errors import ShapeMismatch, raise_for_status
+
+
+@dataclass(frozen=True)
+class GridCost:
+    """Squared Euclidean cost on an nx x ny grid, recomputed on the fly.
+
+    Point k sits at ((k % nx) * hx, (k // nx) * hy); the default spacing
+    1/(n-1) puts the grid on the unit square (BASELINE config 3).
+    """
+
+    nx: int
+    ny: int
+    hx: float | None = None
+    hy: float | None = None
+
+    @property
+    def d(self) -> int:
+        return self.nx * self.ny
+
+    def spacing(self) -> tuple[float, float]:
+        hx = self.hx if self.hx is not None else 1.0 / max(self.nx - 1, 1)
+        hy = self.hy if self.hy is not None else 1.0 / max(self.ny - 1, 1)
+        return float(hx), float(hy)
+
+    def materialize(self, device=None, dtype=torch.float64) -> torch.Tensor:
+        """The (d, d) matrix this descriptor stands for (tests / dC only)."""
+        hx, hy = self.spacing()
+        k = torch.arange(self.d, device=device)
+        x = (k % self.nx).to(dtype) * hx
+        y = (k // self.nx).to(dtype) * hy
+        return (x[:, None] - x[None, :]) ** 2 + (y[:, None] - y[None, :]) ** 2
+
+
+@dataclass
+class SolveResult:
+    """Per-lane E0 costs plus the complete backward state (batch.py:237-253)."""
+
+    cost_e0: torch.Tensor     # (B,)
+    log_u: torch.Tensor       # (B, d1)
+    log_v: torch.Tensor       # (B, d2)
+    lam: float
+    iterations_run: int
+    residuals: torch.Tensor   # (B,)
+
+
+def _stream_handle(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _as_f32_cuda(x, device=None) -> torch.Tensor:
+    t = torch.as_tensor(x)
+    if device is None:
+        device = t.device if t.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    return t.to(device=device, dtype=torch.float32).contiguous()
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _problem(B: int, d1: int, d2: int, cost) -> _lib.Problem:
+    pr = _lib.Problem()
+    pr.B, pr.d1, pr.d2 = B, d1, d2
+    if isinstance(cost, GridCost):
+        hx, hy = cost.spacing()
+        pr.cost_kind = _lib.COST_GRID2D
+        pr.grid_nx, pr.grid_ny = cost.nx, cost.ny
+        pr.grid_hx, pr.grid_hy = hx, hy
+    elif cost.dim() == 3:
+        pr.cost_kind = _lib.COST_PER_SAMPLE
+    else:
+        pr.cost_kind = _lib.COST_SHARED
+    return pr
+
+
+def _check_shapes(mu: torch.Tensor, nu: torch.Tensor, cost) -> tuple[int, int, int]:
+    if mu.dim() != 2 or nu.dim() != 2:
+        raise ShapeMismatch("mu and nu must be 2-D (batch, dim)")
+    B, d1 = mu.shape
+    if nu.shape[0] != B:
+        raise ShapeMismatch(f"batch sizes differ: mu has {B}, nu has {nu.shape[0]}")
+    d2 = nu.shape[1]
+    if isinstance(cost, GridCost):
+        if cost.d != d1 or cost.d != d2:
+            raise ShapeMismatch(f"grid has {cost.d} points but histograms have d1={d1}, d2={d2}")
+    elif cost.dim() == 2:
+        if tuple(cost.shape) != (d1, d2):
+            raise ShapeMismatch(f"cost is {tuple(cost.shape)} but histograms have d1={d1}, d2={d2}")
+    elif cost.dim() == 3:
+        if tuple(cost.shape) != (B, d1, d2):
+            raise ShapeMismatch(f"per-sample cost is {tuple(cost.shape)}, need ({B}, {d1}, {d2})")
+    else:
+        raise ShapeMismatch("cost must be (d1, d2), (B, d1, d2) or a GridCost")
+    return B, d1, d2
+
+
+def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.0,
+          check_interval: int = 10, validate: bool = True) -> SolveResult:
+    """batch_forward (batch.py:264-349) on the GPU.
+
+    mu (B, d1), nu (B, d2) histograms; cost a (d1, d2) tensor shared by all
+    lanes, a (B, d1, d2) per-sample tensor, or a GridCost.  Inputs are cast
+    to contiguous float32 on the current CUDA device.
+    """
+    mu = _as_f32_cuda(mu)
+    dev = mu.device
+    nu = _as_f32_cuda(nu, dev)
+    if not isinstance(cost, GridCost):
+        cost = _as_f32_cuda(cost, dev)
+    B, d1, d2 = _check_shapes(mu, nu, cost)
+    lib = _lib.load()
+    pr = _problem(B, d1, d2, cost)
+    op = _lib.Options()
+    op.lam, op.max_iters, op.check_interval, op.tolerance = float(lam), int(max_iters), \
+        int(check_interval), float(tolerance)
+    op.flags = 0 if validate else _lib.FLAG_SKIP_VALIDATION
+    out_cost = torch.empty(B, device=dev, dtype=torch.float32)
+    log_u = torch.empty(B, d1, device=dev, dtype=torch.float32)
+    log_v = torch.empty(B, d2, device=dev, dtype=torch.float32)
+    residuals = torch.empty(B, device=dev, dtype=torch.float32)
+    with torch.cuda.device(dev):
+        nbytes = lib.sinkhorn_workspace_bytes_v1(ctypes.byref(pr))
+        ws = torch.empty(max(nbytes, 256), device=dev, dtype=torch.uint8)
+        iters = ctypes.c_int32(0)
+        st = lib.sinkhorn_forward_device_v1(
+            ctypes.byref(pr), ctypes.byref(op), _ptr(mu), _ptr(nu),
+            None if isinstance(cost, GridCost) else _ptr(cost), _ptr(out_cost), _ptr(log_u),
+            _ptr(log_v), ctypes.byref(iters), _ptr(residuals), _ptr(ws), ws.numel(),
+            _stream_handle(dev))
+    raise_for_status(st, "sinkhorn_forward_device_v1")
+    return SolveResult(out_cost, log_u, log_v, float(lam), int(iters.value), residuals)
+
+
+def potentials_backward(log_u: torch.Tensor, log_v: torch.Tensor, lam: float,
+                        upstream: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """batch_backward (batch.py:352-375): up[b] * lam * (x - mean_i x)."""
+    dev = log_u.device
+    log_u = _as_f32_cuda(log_u, dev)
+    log_v = _as_f32_cuda(log_v, dev)
+    up = _as_f32_cuda(upstream, dev).reshape(-1)
+    B, d1 = log_u.shape
+    d2 = log_v.shape[1]
+    if log_v.shape[0] != B or up.numel() != B:
+        raise ShapeMismatch(f"upstream must have shape ({B},), got {tuple(upstream.shape)}")
+    g_mu = torch.empty_like(log_u)
+    g_nu = torch.empty_like(log_v)
+    if B == 0:
+        return g_mu, g_nu
+    lib = _lib.load()
+    ws = torch.empty(64, device=dev, dtype=torch.uint8)
+    lane = ctypes.c_int32(-1)
+    with torch.cuda.device(dev):
+        st = lib.sinkhorn_backward_device_v1(B, d1, d2, float(lam), _ptr(log_u), _ptr(log_v),
+                                             _ptr(up), _ptr(g_mu), _ptr(g_nu),
+                                             ctypes.byref(lane), _ptr(ws), ws.numel(),
+                                             _stream_handle(dev))
+    raise_for_status(st, "sinkhorn_backward_device_v1", lane=lane.value)
+    return g_mu, g_nu
+
+
+def plan_gradient(log_u: torch.Tensor, log_v: torch.Tensor, cost: torch.Tensor, lam: float,
+                  upstream: torch.Tensor) -> torch.Tensor:
+    """dC = sum_b up_b P_b (shared) or up_b P_b (per-sample); P from core.py:363-368."""
+    dev = log_u.device
+    cost = _as_f32_cuda(cost, dev)
+    up = _as_f32_cuda(upstream, dev).reshape(-1)
+    B, d1 = log_u.shape
+    d2 = log_v.shape[1]
+    pr = _problem(B, d1, d2, cost)
+    out = torch.empty_like(cost)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        st = lib.sinkhorn_plan_grad_device_v1(ctypes.byref(pr), float(lam),
+                                              _ptr(log_u.float().contiguous()),
+                                              _ptr(log_v.float().contiguous()), _ptr(cost),
+                                              _ptr(up), _ptr(out), _stream_handle(dev))
+    raise_for_status(st, "sinkhorn_plan_grad_device_v1")
+    return out
+
+
+class SinkhornLossFunction(torch.autograd.Function):
+    """Custom node: forward = C-ABI forward, backward = C-ABI backward (loss.ts:59-131)."""
+
+    @staticmethod
+    def forward(ctx, mu, nu, cost, lam, max_iters, tolerance, check_interval):
+        grid = cost if isinstance(cost, GridCost) else None
+        res = solve(mu.detach(), nu.detach(), grid if grid is not None else cost.detach(), lam,
+                    max_iters, tolerance, check_interval)
+        # the complete backward state: final potentials only (loss.ts:104)
+        if grid is None and ctx.needs_input_grad[2]:
+            ctx.save_for_backward(res.log_u, res.log_v, cost.detach())
+        else:
+            ctx.save_for_backward(res.log_u, res.log_v)
+        ctx.lam = float(lam)
+        ctx.in_dtypes = (mu.dtype, nu.dtype, None if grid is not None else cost.dtype)
+        ctx.iterations_run = res.iterations_run
+        return res.cost_e0.to(mu.dtype)
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        saved = ctx.saved_tensors
+        log_u, log_v = saved[0], saved[1]
+        g_mu = g_nu = g_c = None
+        if ctx.needs_input_grad[0] or ctx.needs_input_grad[1]:
+            gm, gn = potentials_backward(log_u, log_v, ctx.lam, grad_out.detach())
+            g_mu = gm.to(ctx.in_dtypes[0]) if ctx.needs_input_grad[0] else None
+            g_nu = gn.to(ctx.in_dtypes[1]) if ctx.needs_input_grad[1] else None
+        if len(saved) == 3 and ctx.needs_input_grad[2]:
+            g_c = plan_gradient(log_u, log_v, saved[2], ctx.lam, grad_out.detach())
+            g_c = g_c.to(ctx.in_dtypes[2])
+        return g_mu, g_nu, g_c, None, None, None, None
+
+
+def sinkhorn_loss(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.0,
+                  check_interval: int = 10) -> torch.Tensor:
+    """Per-lane E0 transport loss, shape (B,) (loss.ts:59-131).
+
+    Defaults follow the reference node: max_iters 1000, tolerance 0
+    (loss.ts:76-77).  1-D histograms are treated as a batch of one
+    (loss.ts:41-49).  Gradients reach whichever of mu / nu (/ cost) require them.
+    """
+    if mu.dim() == 1:
+        mu = mu.unsqueeze(0)
+    if nu.dim() == 1:
+        nu = nu.unsqueeze(0)
+    return SinkhornLossFunction.apply(mu, nu, cost, lam, max_iters, tolerance, check_interval)
