@@ -1,0 +1,472 @@
+"""Benchmark: B*d1*d2*iters/s of the log-domain Sinkhorn forward + analytic backward.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl ours|reference]
+
+Default workload (N=1) is BASELINE.json configs[1] ("config 2"): 28x28 grid
+histograms (d=784), B=256 lanes per GPU, shared stored squared-Euclidean cost,
+lambda=0.05, 100 iterations (tolerance 0, like the reference's own bench,
+cli.py:293-297), forward + backward.  Synthetic inputs, generated on the device.
+A "step" is one forward (100 iterations + the fused residual/E0 tail) plus the
+analytic backward over the batch.  Multi-GPU (torchrun): the batch is sharded
+(weak scaling, 256 lanes per GPU) with one final NCCL all-gather of the
+per-lane losses per step.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle port
+of the reference (oracle/, kind "port") on the same workload instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "B·d1·d2·iters/sec, log-Sinkhorn fwd+bwd"
+UNIT = "cell*iter/s"
+MUFU_PER_SM_CLK = 16     # ex2 results per SM per clock (sm_100 SFU)
+
+CONFIGS = {
+    1: dict(workload="config1: 1-D histograms d=100, B=32, |i-j|^2/99^2 shared cost, lambda=0.1",
+            B=32, d=100, cost="index", lam=0.1, iters=100),
+    2: dict(workload="config2: 28x28 grid histograms d=784, B=256 per GPU, shared stored "
+                     "squared-Euclidean cost, lambda=0.05",
+            B=256, d=784, cost="grid_stored", nx=28, lam=0.05, iters=100),
+    3: dict(workload="config3: 64x64 grid histograms d=4096, B=512 per GPU, on-the-fly "
+                     "squared-Euclidean cost, lambda=1e-3",
+            B=512, d=4096, cost="grid_fly", nx=64, lam=1e-3, iters=100),
+    4: dict(workload="config4: per-sample U[0,1) costs d1=d2=1024, B=1024 per GPU "
+                     "(streamed from HBM), lambda=0.05",
+            B=1024, d=1024, cost="per_sample", lam=0.05, iters=100),
+    5: dict(workload="config5: d=65536 shared stored |i-j|^2/(d-1)^2 cost, B=64, lambda=0.05",
+            B=64, d=65536, cost="index", lam=0.05, iters=100),
+}
+
+
+def load_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md "clocks" line)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            with open(self.path) as f:
+                for line in f:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) >= 7:
+                        rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        smax = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        load = [s for s in sm if s > 0.5 * smax] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs (on the device)
+
+def make_inputs(cfg: dict, device, seed: int):
+    import torch
+
+    from paper_1907_01729_b200 import GridCost
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    B, d = cfg["B"], cfg["d"]
+
+    def hist(n):
+        m = torch.rand(n, d, generator=g, device=device, dtype=torch.float64) + 0.5
+        return (m / m.sum(dim=1, keepdim=True)).float()
+
+    mu, nu = hist(B), hist(B)
+    kind = cfg["cost"]
+    if kind == "index":
+        i = torch.arange(d, device=device, dtype=torch.float64)
+        cost = ((i[:, None] - i[None, :]).abs() / max(d - 1, 1)) ** 2
+        cost = cost.float()
+    elif kind == "grid_stored":
+        cost = GridCost(cfg["nx"], cfg["nx"]).materialize(device=device).float()
+    elif kind == "grid_fly":
+        cost = GridCost(cfg["nx"], cfg["nx"])
+    elif kind == "per_sample":
+        cost = torch.rand(B, d, d, generator=g, device=device, dtype=torch.float32)
+    else:
+        raise ValueError(kind)
+    return mu, nu, cost
+
+
+def work_units(cfg: dict) -> float:
+    return float(cfg["B"]) * cfg["d"] * cfg["d"] * cfg["iters"]
+
+
+def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic) -> dict:
+    """Dominant kernel = the half-sweep (2*iters launches per step)."""
+    cells = float(cfg["B"]) * cfg["d"] * cfg["d"]          # cells per sweep launch
+    if cfg["cost"] == "per_sample":
+        achieved = cells * 4 / (sweep_ms * 1e-3) / 1e9      # algorithmic bytes: C read once
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "lane_col_kernel / lane_row_kernel (per-sample sweep)",
+                "algorithmic_per_launch": f"{cells * 4:.4g} B (4 B per cell)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+    sms = 148
+    fmax = float(peaks.get("sm_max_mhz", 1965.0))
+    achieved = cells / (sweep_ms * 1e-3) / 1e12            # one ex2 per cell per sweep
+    peak = sms * MUFU_PER_SM_CLK * fmax * 1e6 / 1e12
+    out = {"bound": "mufu", "achieved": achieved, "peak": peak, "unit": "Tex2/s",
+           "frac": achieved / peak, "traffic": traffic,
+           "kernel": "tiled_sweep_kernel (stream-K online-LSE half-sweep)",
+           "algorithmic_per_launch": f"{cells:.4g} ex2 (1 per cell)",
+           "peak_source": f"148 SM x {MUFU_PER_SM_CLK} ex2/clk x sm_max_mhz {fmax:.0f} "
+                          "(MEASURED_PEAKS.json)"}
+    if clocks.get("sm_mhz"):
+        out["frac_at_measured_clock"] = achieved / (sms * MUFU_PER_SM_CLK * clocks["sm_mhz"] * 1e-6)
+    return out
+
+
+def load_traffic(cfg_id: int):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            data = json.load(f)
+        v = data.get(f"config{cfg_id}", {}).get("dram_bytes_per_sweep_launch")
+        return v
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port of the reference (oracle/), bounded sample
+
+def cpu_reference_sample(cfg: dict, seed: int = 0) -> dict:
+    """Time the reference algorithm (oracle port, float64) on host cores.
+
+    Lanes are independent at tolerance 0 and every iteration costs the same
+    (test_batch.py:46-63), so a run of k1 and k2 iterations gives the
+    per-iteration slope and the fixed tail (final residual + E0); the rate is
+    extrapolated to the configured iteration count.
+    """
+    from oracle import sinkhorn_oracle as orc
+
+    rng = np.random.default_rng(seed)
+    B, d, lam, iters = cfg["B"], cfg["d"], cfg["lam"], cfg["iters"]
+    threads = os.cpu_count() or 1
+    kind = cfg["cost"]
+    if kind in ("index", "grid_stored") and d <= 1024:
+        Bs = B
+        mu = orc.random_histogram_batch(Bs, d, rng)
+        nu = orc.random_histogram_batch(Bs, d, rng)
+        c = orc.index_grid_cost(d) if kind == "index" else orc.grid2d_cost(cfg["nx"])
+
+        def run(k):
+            t0 = time.perf_counter()
+            r = orc.batch_forward(mu, nu, c, lam, k, 0.0, workers=threads)
+            orc.batch_backward(r.log_u, r.log_v, lam, np.ones(Bs))
+            return time.perf_counter() - t0
+        k1, k2 = 1, 2
+        sample = f"streaming port (batch.py structure), B={Bs} d={d}, {k1} and {k2} iterations"
+        cores = threads
+    else:
+        # dense single-lane restatement (core.py:305-357) on a lane subset
+        Bs = 1
+        dd = min(d, 4096)
+        mu = orc.random_histogram_batch(1, dd, rng)[0]
+        nu = orc.random_histogram_batch(1, dd, rng)[0]
+        if kind == "per_sample":
+            c = orc.per_sample_cost(1, 0, dd, dd).astype(np.float64)
+        elif kind == "grid_fly" or kind == "grid_stored":
+            c = orc.grid2d_cost(int(math.isqrt(dd)))
+        else:
+            c = orc.index_grid_cost(dd)
+
+        def run(k):
+            t0 = time.perf_counter()
+            r = orc.dense_forward(mu, nu, c, lam, k)
+            orc.batch_backward(r.log_u, r.log_v, lam, np.ones(1))
+            return time.perf_counter() - t0
+        k1, k2 = 1, 2
+        sample = (f"dense single-lane port (core.py:305-357), 1 lane of d={dd}, {k1} and {k2} "
+                  "iterations" + (f"; per-cell rate extrapolated to d={d}" if dd != d else ""))
+        cores = 1
+    t1, t2 = run(k1), run(k2)
+    per_iter = max((t2 - t1) / (k2 - k1), 1e-9)
+    tail = max(t1 - k1 * per_iter, 0.0)
+    cells_sample = float(Bs) * mu.shape[-1] * mu.shape[-1]
+    t_full = tail + iters * per_iter                     # extrapolated full forward+backward
+    rate = cells_sample * iters / t_full
+    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": sample + f"; extrapolated to {iters} iterations (slope + fixed tail)",
+            "seconds": t1 + t2, "ms_per_step_full": t_full * 1e3 * (B / Bs)}
+
+
+# ---------------------------------------------------------------------------
+
+def init_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_reference_sample(dict(cfg, iters=cfg["iters"]), seed=1)
+    vals, ms = [], []
+    for s in range(args.steps):
+        r = cpu_reference_sample(cfg, seed=s)
+        vals.append(r["value"])
+        ms.append(r["ms_per_step_full"])
+    r["value"] = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(ms), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "B": cfg["B"], "d1": cfg["d"], "d2": cfg["d"],
+                   "iters": cfg["iters"], "lambda": cfg["lam"]},
+        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1907_01729_b200 as skb
+    from paper_1907_01729_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+    peaks = load_peaks()
+    mu, nu, cost = make_inputs(cfg, dev, seed=1234 + rank)
+    B, d, lam, iters = cfg["B"], cfg["d"], cfg["lam"], cfg["iters"]
+    up = torch.ones(B, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, device=dev, dtype=torch.float32)
+    gathered = torch.empty(B * world, device=dev) if world > 1 else None
+
+    def step():
+        res = skb.solve(mu, nu, cost, lam, iters, 0.0, 10, validate=True, time_loop=True)
+        gm, gn = skb.potentials_backward(res.log_u, res.log_v, lam, up)
+        if world > 1:   # the single final loss collective of a batch-sharded step
+            dist.all_gather_into_tensor(gathered, res.cost_e0)
+        return res
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    loop_ms = []
+    launches0 = lib.sinkhorn_launch_count_v1()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for s in range(args.steps):
+            flush.zero_()                       # L2 flush between steps (outside the events)
+            starts[s].record()
+            res = step()
+            ends[s].record()
+            loop_ms.append(res.loop_ms)
+        torch.cuda.synchronize()
+    launches = lib.sinkhorn_launch_count_v1() - launches0
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    ms = sum(step_ms) / len(step_ms)
+    sweep_ms = statistics.median(loop_ms) / (2 * iters)
+    t = torch.tensor([ms, sweep_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, sweep_ms = float(t[0]), float(t[1])
+    value = world * work_units(cfg) / (ms * 1e-3)
+
+    # ---- end to end through the public / reference-facing API with host buffers ----
+    e2e = run_e2e(args, cfg, mu, nu, cost, lam, iters, dev)
+    if world > 1:
+        te = torch.tensor([e2e["seconds_per_step"]], device=dev, dtype=torch.float64)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e["seconds_per_step"] = float(te[0])
+    e2e_value = world * work_units(cfg) / e2e["seconds_per_step"]
+
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": cfg["workload"], "B_per_gpu": B, "global_batch": B * world,
+                   "d1": d, "d2": d, "iters": iters, "lambda": lam, "tolerance": 0.0,
+                   "parallelism": f"batch-sharded dp{world}",
+                   "l2": "flushed between steps (256 MiB write outside the timed events)"},
+        "roofline": roofline(cfg, sweep_ms, peaks, clocks, load_traffic(args.config)),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
+                "d2h_bytes_per_step": e2e["d2h"], "path": e2e["path"]},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_reference_sample(cfg)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
+    """Host buffers in, host results out, copies inside the timed region."""
+    import ctypes
+
+    import torch
+
+    import paper_1907_01729_b200 as skb
+    from paper_1907_01729_b200 import _lib
+
+    B, d = cfg["B"], cfg["d"]
+    steps = max(1, min(args.steps, 10))
+    if cfg["cost"] in ("index", "grid_stored"):
+        # the reference-facing C ABI: sinkhorn_forward_v1 / sinkhorn_backward_v1 (ffi.ts:80-191)
+        lib = _lib.load()
+        h_mu = mu.double().cpu().numpy()
+        h_nu = nu.double().cpu().numpy()
+        h_c = cost.double().cpu().numpy()
+        o_cost, o_lu, o_lv = np.empty(B), np.empty((B, d)), np.empty((B, d))
+        up, g_mu, g_nu = np.ones(B), np.empty((B, d)), np.empty((B, d))
+
+        def view(a):
+            v = _lib.View()
+            v.data = a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+            v.ndim = a.ndim
+            v.shape[0] = a.shape[0]
+            v.shape[1] = a.shape[1] if a.ndim == 2 else 0
+            v.length = a.size
+            return v
+        vs = [view(a) for a in (h_mu, h_nu, h_c, o_cost, o_lu, o_lv, up, g_mu, g_nu)]
+
+        def one():
+            st = lib.sinkhorn_forward_v1(ctypes.byref(vs[0]), ctypes.byref(vs[1]),
+                                         ctypes.byref(vs[2]), lam, iters, 0.0,
+                                         ctypes.byref(vs[3]), ctypes.byref(vs[4]),
+                                         ctypes.byref(vs[5]))
+            assert st == 0, (st, _lib.last_error())
+            st = lib.sinkhorn_backward_v1(ctypes.byref(vs[4]), ctypes.byref(vs[5]), lam,
+                                          ctypes.byref(vs[6]), ctypes.byref(vs[7]),
+                                          ctypes.byref(vs[8]))
+            assert st == 0, (st, _lib.last_error())
+        h2d = 8 * (2 * B * d + d * d) + 8 * (2 * B * d + B)
+        d2h = 8 * (B + 2 * B * d) + 8 * (2 * B * d)
+        path = "C ABI sinkhorn_forward_v1 + sinkhorn_backward_v1, host float64 views"
+    else:
+        h_mu = mu.cpu().pin_memory()
+        h_nu = nu.cpu().pin_memory()
+        grid = isinstance(cost, skb.GridCost)
+        h_c = None if grid else cost.cpu().pin_memory()
+        h_loss = torch.empty(B).pin_memory()
+        h_gm = torch.empty(B, d).pin_memory()
+        h_gn = torch.empty(B, d).pin_memory()
+
+        def one():
+            m = h_mu.to(dev, non_blocking=True)
+            n = h_nu.to(dev, non_blocking=True)
+            c = cost if grid else h_c.to(dev, non_blocking=True)
+            res = skb.solve(m, n, c, lam, iters, 0.0)
+            gm, gn = skb.potentials_backward(res.log_u, res.log_v, lam, torch.ones(B, device=dev))
+            h_loss.copy_(res.cost_e0, non_blocking=True)
+            h_gm.copy_(gm, non_blocking=True)
+            h_gn.copy_(gn, non_blocking=True)
+            torch.cuda.synchronize()
+        h2d = 4 * (2 * B * d + (0 if grid else B * d * d))
+        d2h = 4 * (B + 2 * B * d)
+        path = "torch API solve()+potentials_backward() from pinned host tensors"
+    one()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    dt = (time.perf_counter() - t0) / steps
+    return {"seconds_per_step": dt, "h2d": h2d, "d2h": d2h, "path": path}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world, rank, local = init_dist()
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+    else:
+        run_ours(args, cfg, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -91,6 +91,7 @@ typedef struct sinkhorn_problem_v1 {
 
 #define SINKHORN_FLAG_SKIP_VALIDATION 1u /* trust mu/nu/cost (caller validated) */
 #define SINKHORN_FLAG_PARTIAL_ROWS 2u    /* reserved: row-sharded solves use the half-sweep API */
+#define SINKHORN_FLAG_TIME_LOOP 4u       /* record CUDA events around the iteration loop */
 
 typedef struct sinkhorn_options_v1 {
   double lambda;          /* > 0, finite */
@@ -142,6 +143,22 @@ int32_t sinkhorn_half_sweep_device_v1(int64_t B, int64_t d1, int64_t d2, double 
                                       float* out_sum, void* workspace, size_t workspace_bytes,
                                       void* stream);
 
+/* Per-lane log2 of sum_{i,j} P[i,j] * c[i,j] over the given cost rows: the
+ * E0 partial a row-sharded solve merges across GPUs by log-sum-exp
+ * (batch.py:331-337 restricted to a row block).  Natural-log inputs
+ * log_u (B,d1), log_v (B,d2); out_log2 (B,).  Workspace as the half-sweep. */
+int32_t sinkhorn_e0_partial_device_v1(int64_t B, int64_t d1, int64_t d2, double lambda,
+                                      const float* log_u, const float* log_v, const float* cost,
+                                      float* out_log2, void* workspace, size_t workspace_bytes,
+                                      void* stream);
+
+/* Cross-process agreement on the stopping test (batch-sharded lockstep,
+ * batch.py:318-322): when set (per thread), every convergence check calls
+ * fn(local max residual, user) and stops iff the returned global max <= tol.
+ * All ranks call it the same number of times.  NULL restores local checks. */
+typedef double (*sinkhorn_residual_reducer_v1)(double local_max, void* user);
+void sinkhorn_set_residual_reducer_v1(sinkhorn_residual_reducer_v1 fn, void* user);
+
 /* Transport-plan gradient w.r.t. the cost (north-star item 4, core.py:363-368):
  * SHARED:     dC[i,j]   = sum_b upstream[b] * P_b[i,j]
  * PER_SAMPLE: dC[b,i,j] = upstream[b] * P_b[i,j]
@@ -158,6 +175,12 @@ const char* sinkhorn_last_error(void);
 
 /* Library version string ("paper_1907_01729_b200 <semver> sm_100a"). */
 const char* sinkhorn_version(void);
+
+/* Instrumentation (benchmarks): kernels launched by this thread so far, and
+ * the elapsed milliseconds (CUDA events on the caller's stream) of the last
+ * iteration loop run with SINKHORN_FLAG_TIME_LOOP (-1 if none). */
+unsigned long long sinkhorn_launch_count_v1(void);
+float sinkhorn_last_loop_ms_v1(void);
 
 #ifdef __cplusplus
 }

@@ -29,6 +29,7 @@ COST_PER_SAMPLE = 1
 COST_GRID2D = 2
 
 FLAG_SKIP_VALIDATION = 1
+FLAG_TIME_LOOP = 4
 
 # every symbol include/sinkhorn_b200.h declares
 EXPORTED_SYMBOLS = (
@@ -40,8 +41,12 @@ EXPORTED_SYMBOLS = (
     "sinkhorn_half_sweep_workspace_bytes_v1",
     "sinkhorn_half_sweep_device_v1",
     "sinkhorn_plan_grad_device_v1",
+    "sinkhorn_e0_partial_device_v1",
+    "sinkhorn_set_residual_reducer_v1",
     "sinkhorn_last_error",
     "sinkhorn_version",
+    "sinkhorn_launch_count_v1",
+    "sinkhorn_last_loop_ms_v1",
 )
 
 
@@ -79,6 +84,9 @@ class Options(ctypes.Structure):
     ]
 
 
+# double (*)(double local_max, void* user)
+REDUCER = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
+
 _lock = threading.Lock()
 _lib = None
 
@@ -100,8 +108,12 @@ def _declare(lib):
         "sinkhorn_half_sweep_workspace_bytes_v1": (sz, [i64, i64, i64]),
         "sinkhorn_half_sweep_device_v1": (i32, [i64, i64, i64, f64, P, P, P, P, P, P, P, sz, P]),
         "sinkhorn_plan_grad_device_v1": (i32, [ctypes.POINTER(Problem), f64, P, P, P, P, P, P]),
+        "sinkhorn_e0_partial_device_v1": (i32, [i64, i64, i64, f64, P, P, P, P, P, sz, P]),
+        "sinkhorn_set_residual_reducer_v1": (None, [REDUCER, P]),
         "sinkhorn_last_error": (ctypes.c_char_p, []),
         "sinkhorn_version": (ctypes.c_char_p, []),
+        "sinkhorn_launch_count_v1": (ctypes.c_ulonglong, []),
+        "sinkhorn_last_loop_ms_v1": (ctypes.c_float, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

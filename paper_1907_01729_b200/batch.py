@@ -107,6 +107,32 @@ def partial_log_reduction(log_x, c, lam: float) -> tuple[torch.Tensor, torch.Ten
     return m, s
 
 
+def e0_partial_log2(log_u, log_v, c, lam: float) -> torch.Tensor:
+    """Per-lane log2 sum_{i,j} P_ij c_ij over the rows of `c` (a row shard);
+    E0 = 2^(LSE over shards) (batch.py:331-337)."""
+    log_u = _as_f32_cuda(log_u)
+    dev = log_u.device
+    log_v = _as_f32_cuda(log_v, dev)
+    c = _as_f32_cuda(_cost(c), dev)
+    if log_u.dim() != 2 or log_v.dim() != 2 or c.dim() != 2 or \
+            tuple(c.shape) != (log_u.shape[1], log_v.shape[1]) or log_u.shape[0] != log_v.shape[0]:
+        raise ShapeMismatch("e0_partial_log2: log_u (B,d1), log_v (B,d2), cost (d1,d2)")
+    if not (math.isfinite(lam) and lam > 0):
+        raise InvalidConfig(f"lam must be positive and finite, got {lam}")
+    B, d1 = log_u.shape
+    d2 = log_v.shape[1]
+    out = torch.empty(B, device=dev, dtype=torch.float32)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        nbytes = lib.sinkhorn_half_sweep_workspace_bytes_v1(B, d1, d2)
+        ws = torch.empty(max(nbytes, 256), device=dev, dtype=torch.uint8)
+        st = lib.sinkhorn_e0_partial_device_v1(B, d1, d2, float(lam), _ptr(log_u), _ptr(log_v),
+                                               _ptr(c), _ptr(out), _ptr(ws), ws.numel(),
+                                               _stream_handle(dev))
+    raise_for_status(st, "sinkhorn_e0_partial_device_v1")
+    return out
+
+
 def _check_half(log_u, c, log_nu):
     if log_u.dim() != 2 or log_nu.dim() != 2:
         raise ShapeMismatch("log_u and log_nu must be 2-D (batch, dim)")

@@ -157,7 +157,7 @@ __global__ void reduce_max_kernel(const float* __restrict__ res, int B, float* o
 __global__ void __launch_bounds__(256) e0_finalize_kernel(const float* __restrict__ e0, int B,
                                                           int d2, long long sb, long long sj,
                                                           float* __restrict__ out_cost,
-                                                          int* status) {
+                                                          int* status, int out_log2) {
   __shared__ float sm[8][32], ss[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x * 32 + lane;
@@ -177,9 +177,13 @@ __global__ void __launch_bounds__(256) e0_finalize_kernel(const float* __restric
   __syncthreads();
   if (warp == 0 && b < B) {
     for (int w = 1; w < 8; ++w) lse_merge(m, s, sm[w][lane], ss[w][lane]);
-    const float cost = exp2f(lse_final(m, s));
-    out_cost[b] = cost;
-    if (!isfinite(cost)) set_status(status, 12);
+    if (out_log2) {      // partial (row-sharded) E0: log2 of this shard's sum
+      out_cost[b] = lse_final(m, s);
+    } else {
+      const float cost = exp2f(lse_final(m, s));
+      out_cost[b] = cost;
+      if (!isfinite(cost)) set_status(status, 12);
+    }
   }
 }
 

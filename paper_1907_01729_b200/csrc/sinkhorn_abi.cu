@@ -28,6 +28,11 @@ using namespace skb;
 namespace {
 
 thread_local std::string g_last_error;
+thread_local unsigned long long g_launches = 0;   // kernels this thread launched
+thread_local float g_last_loop_ms = -1.f;         // last timed iteration loop (ms)
+// Optional cross-rank agreement on the stopping test (batch-sharded solves).
+thread_local sinkhorn_residual_reducer_v1 g_reducer = nullptr;
+thread_local void* g_reducer_user = nullptr;
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -118,6 +123,7 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++g_launches;
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
@@ -411,6 +417,7 @@ struct Solve {
 
 int fill(float* p, size_t n, float v, cudaStream_t st) {
   if (n == 0) return 0;
+  ++g_launches;
   fill_kernel<<<grid_for(n), 256, 0, st>>>(p, n, v);
   CK(cudaGetLastError());
   return 0;
@@ -473,15 +480,19 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   CK(cudaMemsetAsync(at<int>(ws, L.counters), 0, std::max<size_t>(L.counter_count, 1) * 4, st));
   CK(cudaMemsetAsync(S.F(L.res), 0, (size_t)std::max(L.Bp, 1) * 4, st));
   if (!(op.flags & SINKHORN_FLAG_SKIP_VALIDATION)) {
+    ++g_launches;
     validate_rows_kernel<float><<<(unsigned)pr.B, 256, 0, st>>>(mu, (int)pr.d1, status, badrow);
+    ++g_launches;
     validate_rows_kernel<float><<<(unsigned)pr.B, 256, 0, st>>>(nu, (int)pr.d2, status, badrow);
     CK(cudaGetLastError());
   }
   {
     dim3 g1((unsigned)((L.D1p + 31) / 32), (unsigned)((L.Bp + 31) / 32));
+    ++g_launches;
     prep_marginal_kernel<<<g1, 256, 0, st>>>(mu, (int)pr.B, (int)pr.d1, L.Bp, L.D1p, L.sb1,
                                               L.si1, S.F(L.l2mu), S.F(L.mu), S.F(L.f2), 1);
     dim3 g2((unsigned)((L.D2p + 31) / 32), (unsigned)((L.Bp + 31) / 32));
+    ++g_launches;
     prep_marginal_kernel<<<g2, 256, 0, st>>>(nu, (int)pr.B, (int)pr.d2, L.Bp, L.D2p, L.sb2,
                                               L.si2, S.F(L.l2nu), S.F(L.nu), S.F(L.g2[0]), 0);
     CK(cudaGetLastError());
@@ -491,18 +502,29 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   }
   if (pr.cost_kind == SINKHORN_COST_SHARED) {
     dim3 g((unsigned)((L.D2p + 31) / 32), (unsigned)((L.D1p + 31) / 32));
+    ++g_launches;
     prep_cost_kernel<<<g, 256, 0, st>>>(cost, (int)pr.d1, (int)pr.d2, L.D1p, L.D2p,
                                          (float)(-1.4426950408889634 / op.lambda), S.F(L.a2),
                                          S.F(L.a2t), status);
     CK(cudaGetLastError());
   } else if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE && !(op.flags & SINKHORN_FLAG_SKIP_VALIDATION)) {
     const size_t n = (size_t)pr.B * pr.d1 * pr.d2;
+    ++g_launches;
     validate_cost_kernel<<<grid_for(n), 256, 0, st>>>(cost, n, status);
     CK(cudaGetLastError());
   }
   if (int e = S.setup_maps()) return e;
 
   // ---- lockstep iteration (batch.py:314-324) ----
+  // Optional: CUDA events on the caller's stream around the iteration loop, so
+  // a benchmark can report the sweep kernels' average launch duration.
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  const bool timed = (op.flags & SINKHORN_FLAG_TIME_LOOP) != 0;
+  if (timed) {
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaEventRecord(ev0, st));
+  }
   const bool checks = op.tolerance > 0;
   int cur = 0;            // g2[cur] holds log_v_k
   bool have_next = false; // g2[cur] already advanced by a check sweep
@@ -524,6 +546,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     if (check) {
       // column sweep k+1 doubles as the column residual of iteration k
       if (int e = S.col_sweep(cur ^ 1, cur, kResCol)) return e;
+      ++g_launches;
       reduce_max_kernel<<<1, 256, 0, st>>>(S.F(L.res), (int)pr.B, S.F(L.scratch));
       CK(cudaGetLastError());
       float hmax = 0.f;
@@ -531,8 +554,10 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
       CK(cudaMemcpyAsync(&hmax, S.F(L.scratch), 4, cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(&hstatus, status, 4, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      double gmax = (hstatus != 0) ? NAN : (double)hmax;
+      if (g_reducer) gmax = g_reducer(gmax, g_reducer_user);   // every rank calls it per check
       if (hstatus != 0) break;
-      if ((double)hmax <= op.tolerance) {
+      if (gmax <= op.tolerance) {
         converged = true;   // keep g2[cur] = log_v_k; discard the k+1 sweep
         break;
       }
@@ -541,17 +566,21 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     }
   }
   (void)converged;
+  if (timed) CK(cudaEventRecord(ev1, st));
   // ---- tail: residual + stable E0 in one column pass (batch.py:323-337) ----
   if (int e = S.tail(cur)) return e;
   {
     const int nb = (int)((pr.B + 31) / 32);
     const long long sb = L.tiled ? 1 : L.D2p, sj = L.tiled ? L.Bp : 1;
+    ++g_launches;
     e0_finalize_kernel<<<nb, 256, 0, st>>>(S.F(L.e0), (int)pr.B, (int)pr.d2, sb, sj, out_cost,
-                                           status);
+                                           status, 0);
     dim3 gu((unsigned)((pr.d1 + 31) / 32), (unsigned)((pr.B + 31) / 32));
+    ++g_launches;
     export_potential_kernel<<<gu, 256, 0, st>>>(S.F(L.f2), (int)pr.B, (int)pr.d1, L.sb1, L.si1,
                                                 out_log_u, status, kLn2);
     dim3 gv((unsigned)((pr.d2 + 31) / 32), (unsigned)((pr.B + 31) / 32));
+    ++g_launches;
     export_potential_kernel<<<gv, 256, 0, st>>>(S.F(L.g2[cur]), (int)pr.B, (int)pr.d2, L.sb2,
                                                 L.si2, out_log_v, status, kLn2);
     CK(cudaGetLastError());
@@ -562,6 +591,13 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   if (out_iterations) *out_iterations = iters;
   int hstatus = 0;
   if (int e = S.read_status(&hstatus)) return e;
+  if (timed) {
+    float ms = -1.f;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    g_last_loop_ms = ms;
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+  }
   if (hstatus == 11) {
     int row = 0;
     cudaMemcpy(&row, badrow, 4, cudaMemcpyDeviceToHost);
@@ -582,6 +618,10 @@ extern "C" {
 const char* sinkhorn_last_error(void) { return g_last_error.c_str(); }
 
 const char* sinkhorn_version(void) { return "paper_1907_01729_b200 0.1.0 sm_100a"; }
+
+unsigned long long sinkhorn_launch_count_v1(void) { return g_launches; }
+
+float sinkhorn_last_loop_ms_v1(void) { return g_last_loop_ms; }
 
 size_t sinkhorn_workspace_bytes_v1(const sinkhorn_problem_v1* prob) {
   if (check_problem(prob) != 0) return 0;
@@ -626,6 +666,7 @@ int32_t sinkhorn_backward_device_v1(int64_t B, int64_t d1, int64_t d2, double la
   int* bad = status + 1;
   CK(cudaMemsetAsync(status, 0, 4, st));
   CK(cudaMemsetAsync(bad, 0x7f, 4, st));
+  ++g_launches;
   backward_kernel<float><<<dim3((unsigned)B, 2), 256, 0, st>>>(
       log_u, log_v, (int)d1, (int)d2, lambda, upstream, out_grad_mu, out_grad_nu, status, bad);
   CK(cudaGetLastError());
@@ -676,14 +717,17 @@ int32_t sinkhorn_half_sweep_device_v1(int64_t B, int64_t d1, int64_t d2, double 
                      std::max<size_t>(L.counter_count, 1) * 4, st));
   {
     dim3 g((unsigned)((L.D2p + 31) / 32), (unsigned)((L.D1p + 31) / 32));
+    ++g_launches;
     prep_cost_kernel<<<g, 256, 0, st>>>(cost, (int)d1, (int)d2, L.D1p, L.D2p,
                                          (float)(-1.4426950408889634 / lambda), S.F(L.a2),
                                          S.F(L.a2t), status);
     dim3 gx((unsigned)((L.D1p + 31) / 32), (unsigned)((L.Bp + 31) / 32));
+    ++g_launches;
     import_potential_kernel<<<gx, 256, 0, st>>>(log_x, (int)B, (int)d1, L.Bp, L.D1p, L.sb1,
                                                  L.si1, S.F(L.f2));
     if (!partial) {
       dim3 gt((unsigned)((L.D2p + 31) / 32), (unsigned)((L.Bp + 31) / 32));
+      ++g_launches;
       import_potential_kernel<<<gt, 256, 0, st>>>(target, (int)B, (int)d2, L.Bp, L.D2p, L.sb2,
                                                    L.si2, S.F(L.l2nu));
     }
@@ -699,11 +743,14 @@ int32_t sinkhorn_half_sweep_device_v1(int64_t B, int64_t d1, int64_t d2, double 
   }
   dim3 gv((unsigned)((d2 + 31) / 32), (unsigned)((B + 31) / 32));
   if (partial) {
+    ++g_launches;
     export_potential_kernel<<<gv, 256, 0, st>>>(S.F(L.g2[0]), (int)B, (int)d2, L.sb2, L.si2,
                                                 out_max, status, 1.0f);
+    ++g_launches;
     export_potential_kernel<<<gv, 256, 0, st>>>(S.F(L.g2[1]), (int)B, (int)d2, L.sb2, L.si2,
                                                 out_sum, status, 1.0f);
   } else {
+    ++g_launches;
     export_potential_kernel<<<gv, 256, 0, st>>>(S.F(L.g2[0]), (int)B, (int)d2, L.sb2, L.si2,
                                                 out, status, kLn2);
   }
@@ -728,16 +775,83 @@ int32_t sinkhorn_plan_grad_device_v1(const sinkhorn_problem_v1* prob, double lam
   const float k = (float)(-1.4426950408889634 / lambda);
   dim3 g((unsigned)((prob->d2 + 31) / 32), (unsigned)((prob->d1 + 7) / 8));
   if (prob->cost_kind == SINKHORN_COST_SHARED) {
+    ++g_launches;
     plan_grad_shared_kernel<<<g, 256, 0, st>>>(log_u, log_v, cost, upstream, (int)prob->B,
                                                 (int)prob->d1, (int)prob->d2, k, out_grad_cost);
   } else {
     if (prob->B == 0) return 0;
     g.z = (unsigned)prob->B;
+    ++g_launches;
     plan_grad_per_sample_kernel<<<g, 256, 0, st>>>(log_u, log_v, cost, upstream, (int)prob->d1,
                                                     (int)prob->d2, k, out_grad_cost);
   }
   CK(cudaGetLastError());
   return 0;
+}
+
+void sinkhorn_set_residual_reducer_v1(sinkhorn_residual_reducer_v1 fn, void* user) {
+  g_reducer = fn;
+  g_reducer_user = user;
+}
+
+int32_t sinkhorn_e0_partial_device_v1(int64_t B, int64_t d1, int64_t d2, double lambda,
+                                      const float* log_u, const float* log_v, const float* cost,
+                                      float* out_log2, void* workspace, size_t workspace_bytes,
+                                      void* stream) {
+  sinkhorn_problem_v1 pr = {B, d1, d2, SINKHORN_COST_SHARED, 0, 0, 0.f, 0.f};
+  if (int e = check_problem(&pr)) return e;
+  if (B == 0) return 0;
+  if (!(std::isfinite(lambda) && lambda > 0))
+    return fail(SINKHORN_STATUS_INVALID_CONFIG, "lam must be positive and finite");
+  if (!log_u || !log_v || !cost || !out_log2)
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
+  Solve S;
+  S.pr = pr;
+  S.di = device_info();
+  S.L = make_layout(pr, S.di.sms);
+  S.ws = workspace;
+  S.st = static_cast<cudaStream_t>(stream);
+  S.lam = (float)lambda;
+  S.cost = cost;
+  const Layout& L = S.L;
+  if (workspace == nullptr || workspace_bytes < L.total)
+    return fail(SINKHORN_STATUS_WORKSPACE, "workspace too small");
+  cudaStream_t st = S.st;
+  int* status = at<int>(workspace, L.status);
+  CK(cudaMemsetAsync(status, 0, 4, st));
+  CK(cudaMemsetAsync(at<int>(workspace, L.counters), 0,
+                     std::max<size_t>(L.counter_count, 1) * 4, st));
+  if (d1 == 0 || d2 == 0) {
+    if (int e = fill(out_log2, (size_t)B, neg_inf_host(), st)) return e;
+    return 0;
+  }
+  {
+    dim3 g((unsigned)((L.D2p + 31) / 32), (unsigned)((L.D1p + 31) / 32));
+    ++g_launches;
+    prep_cost_kernel<<<g, 256, 0, st>>>(cost, (int)d1, (int)d2, L.D1p, L.D2p,
+                                         (float)(-1.4426950408889634 / lambda), S.F(L.a2),
+                                         S.F(L.a2t), status);
+    dim3 gx((unsigned)((L.D1p + 31) / 32), (unsigned)((L.Bp + 31) / 32));
+    ++g_launches;
+    import_potential_kernel<<<gx, 256, 0, st>>>(log_u, (int)B, (int)d1, L.Bp, L.D1p, L.sb1,
+                                                 L.si1, S.F(L.f2));
+    dim3 gv((unsigned)((L.D2p + 31) / 32), (unsigned)((L.Bp + 31) / 32));
+    ++g_launches;
+    import_potential_kernel<<<gv, 256, 0, st>>>(log_v, (int)B, (int)d2, L.Bp, L.D2p, L.sb2,
+                                                 L.si2, S.F(L.g2[0]));
+    CK(cudaGetLastError());
+  }
+  if (int e = S.setup_maps()) return e;
+  TiledArgs a = {&S.tm_a2, &S.tm_f2, (int)d1, (int)d2, L.D1p, L.D2p, S.F(L.l2nu), S.F(L.nu),
+                 nullptr, S.F(L.g2[0]), nullptr, kResNone, S.F(L.e0), nullptr, nullptr};
+  if (int e = launch_tiled<false, kModeTail>(L, workspace, S.di, a, pr, S.lam, st)) return e;
+  ++g_launches;
+  e0_finalize_kernel<<<(unsigned)((B + 31) / 32), 256, 0, st>>>(S.F(L.e0), (int)B, (int)d2, 1,
+                                                                 L.Bp, out_log2, status, 1);
+  CK(cudaGetLastError());
+  int h = 0;
+  if (int e = S.read_status(&h)) return e;
+  return h == 0 ? 0 : fail(h, "device status " + std::to_string(h));
 }
 
 // ---- layer 1: host float64 views, the exact ffi.ts contract -----------------
@@ -797,7 +911,9 @@ int32_t sinkhorn_forward_v1(const sinkhorn_view_v1* mu, const sinkhorn_view_v1* 
   int* vbad = at<int>(buf.p, o_ws + make_layout(pr, device_info().sms).badrow);
   CK(cudaMemsetAsync(vstat, 0, 4, st));
   CK(cudaMemsetAsync(vbad, 0x7f, 4, st));
+  ++g_launches;
   validate_rows_kernel<double><<<(unsigned)B, 256, 0, st>>>(d64, (int)d1, vstat, vbad);
+  ++g_launches;
   validate_rows_kernel<double><<<(unsigned)B, 256, 0, st>>>(d64 + n_mu, (int)d2, vstat, vbad);
   CK(cudaGetLastError());
   int hs = 0;
@@ -806,8 +922,11 @@ int32_t sinkhorn_forward_v1(const sinkhorn_view_v1* mu, const sinkhorn_view_v1* 
   if (hs != 0) return fail(hs, "invalid histogram");
   sinkhorn_options_v1 op = {lambda, max_iters, 10, tolerance, SINKHORN_FLAG_SKIP_VALIDATION};
   if (int e = check_options(&op)) return e;
+  ++g_launches;
   f64_to_f32_kernel<<<grid_for(n_mu), 256, 0, st>>>(d64, at<float>(buf.p, o_f_mu), n_mu);
+  ++g_launches;
   f64_to_f32_kernel<<<grid_for(n_nu), 256, 0, st>>>(d64 + n_mu, at<float>(buf.p, o_f_nu), n_nu);
+  ++g_launches;
   f64_to_f32_kernel<<<grid_for(n_c), 256, 0, st>>>(d64 + n_mu + n_nu, at<float>(buf.p, o_f_c), n_c);
   CK(cudaGetLastError());
   int32_t iters = 0;
@@ -817,8 +936,11 @@ int32_t sinkhorn_forward_v1(const sinkhorn_view_v1* mu, const sinkhorn_view_v1* 
                        st);
   if (e != 0) return e;
   // outputs back as float64 (ffi.ts:123-133 writes in place)
+  ++g_launches;
   f32_to_f64_kernel<<<grid_for(B), 256, 0, st>>>(at<float>(buf.p, o_cost), d64, (size_t)B);
+  ++g_launches;
   f32_to_f64_kernel<<<grid_for(n_mu), 256, 0, st>>>(at<float>(buf.p, o_lu), d64 + B, n_mu);
+  ++g_launches;
   f32_to_f64_kernel<<<grid_for(n_nu), 256, 0, st>>>(at<float>(buf.p, o_lv), d64 + B + n_mu, n_nu);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out_cost->data, d64, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
@@ -859,6 +981,7 @@ int32_t sinkhorn_backward_v1(const sinkhorn_view_v1* log_u, const sinkhorn_view_
   CK(cudaMemcpyAsync(up, upstream->data, (size_t)B * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(stat, 0, 4, st));
   CK(cudaMemsetAsync(stat + 1, 0x7f, 4, st));
+  ++g_launches;
   backward_kernel<double><<<dim3((unsigned)B, 2), 256, 0, st>>>(u, v, (int)d1, (int)d2, lambda,
                                                                 up, gu, gv, stat, stat + 1);
   CK(cudaGetLastError());

@@ -64,6 +64,7 @@ class SolveResult:
     lam: float
     iterations_run: int
     residuals: torch.Tensor   # (B,)
+    loop_ms: float = -1.0     # iteration-loop time (CUDA events) when solve(time_loop=True)
 
 
 def _stream_handle(device: torch.device) -> int:
@@ -118,25 +119,29 @@ def _check_shapes(mu: torch.Tensor, nu: torch.Tensor, cost) -> tuple[int, int, i
 
 
 def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.0,
-          check_interval: int = 10, validate: bool = True) -> SolveResult:
+          check_interval: int = 10, validate: bool = True, time_loop: bool = False) -> SolveResult:
     """batch_forward (batch.py:264-349) on the GPU.
 
     mu (B, d1), nu (B, d2) histograms; cost a (d1, d2) tensor shared by all
     lanes, a (B, d1, d2) per-sample tensor, or a GridCost.  Inputs are cast
     to contiguous float32 on the current CUDA device.
     """
+    mu, nu = torch.as_tensor(mu), torch.as_tensor(nu)
+    if not isinstance(cost, GridCost):
+        cost = torch.as_tensor(cost)
+    B, d1, d2 = _check_shapes(mu, nu, cost)   # host-side, before touching the device
     mu = _as_f32_cuda(mu)
     dev = mu.device
     nu = _as_f32_cuda(nu, dev)
     if not isinstance(cost, GridCost):
         cost = _as_f32_cuda(cost, dev)
-    B, d1, d2 = _check_shapes(mu, nu, cost)
     lib = _lib.load()
     pr = _problem(B, d1, d2, cost)
     op = _lib.Options()
     op.lam, op.max_iters, op.check_interval, op.tolerance = float(lam), int(max_iters), \
         int(check_interval), float(tolerance)
-    op.flags = 0 if validate else _lib.FLAG_SKIP_VALIDATION
+    op.flags = (0 if validate else _lib.FLAG_SKIP_VALIDATION) | \
+        (_lib.FLAG_TIME_LOOP if time_loop else 0)
     out_cost = torch.empty(B, device=dev, dtype=torch.float32)
     log_u = torch.empty(B, d1, device=dev, dtype=torch.float32)
     log_v = torch.empty(B, d2, device=dev, dtype=torch.float32)
@@ -151,7 +156,8 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
             _ptr(log_v), ctypes.byref(iters), _ptr(residuals), _ptr(ws), ws.numel(),
             _stream_handle(dev))
     raise_for_status(st, "sinkhorn_forward_device_v1")
-    return SolveResult(out_cost, log_u, log_v, float(lam), int(iters.value), residuals)
+    loop_ms = float(lib.sinkhorn_last_loop_ms_v1()) if time_loop else -1.0
+    return SolveResult(out_cost, log_u, log_v, float(lam), int(iters.value), residuals, loop_ms)
 
 
 def potentials_backward(log_u: torch.Tensor, log_v: torch.Tensor, lam: float,
