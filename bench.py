@@ -66,21 +66,27 @@ def load_peaks() -> dict:
 # clocks during the timed region (B200_PROFILING.md "clocks" line)
 
 class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region.
+
+    Sampling every 100 ms contends with the driver while the solver enqueues
+    its ~200 launches per step, so the interval defaults to 500 ms."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, interval_ms: int = 500):
         self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
         self.proc = None
         self.gpu = gpu_index
+        self.interval_ms = interval_ms
 
     def __enter__(self):
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
             time.sleep(0.3)
         except (OSError, FileNotFoundError):
@@ -324,7 +330,7 @@ def run_ours(args, cfg, world, rank, local):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     loop_ms = []
     launches0 = lib.sinkhorn_launch_count_v1()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, args.clock_interval_ms) as clk:
         torch.cuda.synchronize()
         for s in range(args.steps):
             flush.zero_()                       # L2 flush between steps (outside the events)
@@ -389,7 +395,7 @@ def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
 
     B, d = cfg["B"], cfg["d"]
     steps = max(1, min(args.steps, 10))
-    if cfg["cost"] in ("index", "grid_stored"):
+    if cfg["cost"] in ("index", "grid_stored") and d <= 8192:
         # the reference-facing C ABI: sinkhorn_forward_v1 / sinkhorn_backward_v1 (ffi.ts:80-191)
         lib = _lib.load()
         h_mu = mu.double().cpu().numpy()
@@ -425,7 +431,8 @@ def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
         h_mu = mu.cpu().pin_memory()
         h_nu = nu.cpu().pin_memory()
         grid = isinstance(cost, skb.GridCost)
-        h_c = None if grid else cost.cpu().pin_memory()
+        big = (not grid) and cost.numel() * 4 > (4 << 30)   # > 4 GiB: pageable, not pinned
+        h_c = None if grid else (cost.cpu() if big else cost.cpu().pin_memory())
         h_loss = torch.empty(B).pin_memory()
         h_gm = torch.empty(B, d).pin_memory()
         h_gn = torch.empty(B, d).pin_memory()
@@ -459,6 +466,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--clock-interval-ms", type=int, default=500)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world, rank, local = init_dist()

@@ -16,6 +16,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
+#include <cstdlib>
 
 #include "../../include/sinkhorn_b200.h"
 #include "aux_kernels.cuh"
@@ -48,20 +50,28 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 // ---- tiled-sweep configuration ---------------------------------------------
-constexpr int BT = 64, PT = 64, QC = 32, RB = 4, RP = 4, NSTAGE = 4;
-constexpr int KC_UPD = 8, KC_TAIL = 4;
-constexpr int TILE_PAD = 64;  // dims padded so both q (QC) and p (PT) tiles divide them
+constexpr int QC = 32, RB = 4, RP = 4, NSTAGE = 4;
+constexpr int BT_MAX = 128;   // lane tile: 128 (16 warps, 1 CTA/SM) or 64 (8 warps, 2 CTAs/SM)
+constexpr int PT_MAX = 64;    // output-tile widths: 64 or 56 (picked per sweep, see pick_pt)
+constexpr int TILE_PAD = 64;  // buffer extents padded to 64 (>= every tile / TMA box)
 constexpr int MAX_OCC = 2;
 
-template <bool kGrid, int kMode>
+template <int BT, int PT, bool kGrid, int kMode>
 struct TiledK {
-  static constexpr int KC = (kMode == kModeTail) ? KC_TAIL : KC_UPD;
-  using S = TiledSweep<BT, PT, QC, RB, RP, KC, NSTAGE, kGrid, kMode>;
+  using S = TiledSweep<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>;
   static void* fn() {
-    return reinterpret_cast<void*>(
-        &tiled_sweep_kernel<BT, PT, QC, RB, RP, KC, NSTAGE, kGrid, kMode>);
+    return reinterpret_cast<void*>(&tiled_sweep_kernel<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>);
   }
 };
+
+// Lane tile: 128 lanes (one 16-warp CTA per SM: no inter-CTA warp-priority
+// skew, half as many stream-K pieces per tile) whenever the batch has > 64 lanes.
+int pick_bt(int64_t B) { return B > 64 ? 128 : 64; }
+
+// Output-tile width.  Always 64 (8 warps: an even 4 warps per scheduler at 2
+// CTAs/SM; 7-warp tiles left the 4 SMSPs 4/4/3/3).  A ragged extent is covered
+// by shifting the last tile left (it overlaps its neighbour) so no tile is partial.
+int pick_pt(int /*P*/) { return 64; }
 
 struct DeviceInfo {
   int dev = -1;
@@ -69,9 +79,14 @@ struct DeviceInfo {
 };
 
 DeviceInfo device_info() {
+  static thread_local int cached_dev = -1, cached_sms = 0;
   DeviceInfo di;
   cudaGetDevice(&di.dev);
-  cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, di.dev);
+  if (di.dev != cached_dev) {
+    cudaDeviceGetAttribute(&cached_sms, cudaDevAttrMultiProcessorCount, di.dev);
+    cached_dev = di.dev;
+  }
+  di.sms = cached_sms;
   return di;
 }
 
@@ -158,7 +173,7 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms) {
   L.tiled = (pr.cost_kind != SINKHORN_COST_PER_SAMPLE);
   Carver c;
   if (L.tiled) {
-    L.Bp = (int)round_up(pr.B, BT);
+    L.Bp = (int)round_up(pr.B, pick_bt(pr.B));
     L.D1p = (int)round_up(pr.d1, TILE_PAD);
     L.D2p = (int)round_up(pr.d2, TILE_PAD);
     L.sb1 = L.sb2 = 1;
@@ -176,9 +191,9 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms) {
     L.mu = c.take(n1);
     L.nu = c.take(n2);
     L.e0 = c.take(n2);
-    L.part_bytes = (size_t)sms * MAX_OCC * 2 * 3 * BT * PT * 4;
+    L.part_bytes = (size_t)sms * MAX_OCC * 2 * 3 * 64 * PT_MAX * 4;   // G*BT is constant
     L.part = c.take(L.part_bytes);
-    L.counter_count = (size_t)(L.Bp / BT) * (std::max(L.D1p, L.D2p) / PT);
+    L.counter_count = (size_t)(L.Bp / 64) * (std::max(L.D1p, L.D2p) / 32 + 1);
   } else {
     L.lane_vec = (pr.d2 % 4 == 0 && pr.d1 % 4 == 0) ? 4 : 1;
     L.Bp = (int)pr.B;
@@ -221,13 +236,22 @@ T* at(void* ws, size_t off) {
   return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
 }
 
-int occupancy_tiled(void* fn, size_t smem) {
-  static int cache[8] = {0};
-  (void)cache;
+// Resident CTAs per SM for a kernel; the attribute set + occupancy query cost
+// tens of microseconds, so they run once per (kernel, device) and are cached.
+int occupancy_tiled(void* fn, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<void*, int>, int>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : cache)
+    if (e.first.first == fn && e.first.second == dev) return e.second;
   int occ = 1;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, BT / RB * (PT / RP), smem);
-  return std::max(1, std::min(occ, MAX_OCC));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
+  occ = std::max(1, std::min(occ, MAX_OCC));
+  cache.push_back({{fn, dev}, occ});
+  return occ;
 }
 
 // One tiled half-sweep launch.
@@ -246,21 +270,22 @@ struct TiledArgs {
   float* psum;
 };
 
-template <bool kGrid, int kMode>
-int launch_tiled(const Layout& L, void* ws, const DeviceInfo& di, const TiledArgs& a,
-                 const sinkhorn_problem_v1& pr, float lam, cudaStream_t st) {
-  using K = TiledK<kGrid, kMode>;
+template <int BT, int PT, bool kGrid, int kMode>
+int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const TiledArgs& a,
+                    const sinkhorn_problem_v1& pr, float lam, cudaStream_t st) {
+  using K = TiledK<BT, PT, kGrid, kMode>;
   TiledSweepParams p = {};
   p.Qv = a.Qv;
   p.Pv = a.Pv;
   p.Bp = L.Bp;
   p.ntile_b = L.Bp / BT;
-  p.ntile_p = a.Pp / PT;
-  p.nq = a.Qp / QC;
-  p.W = (long long)p.ntile_b * p.ntile_p * p.nq;
+  p.ntile_p = (a.Pv + PT - 1) / PT;
+  p.nq = (a.Qv + QC - 1) / QC;
+  p.W = (long long)p.ntile_b * p.ntile_p * a.Qv;   // stream-K over reduction rows
+  const long long W = (long long)p.ntile_b * p.ntile_p * p.nq;   // chunks: cap on the grid
   const size_t smem = K::S::SMEM_BYTES;
-  const int occ = occupancy_tiled(K::fn(), smem);
-  p.G = (int)std::min<long long>(p.W, (long long)di.sms * occ);
+  const int occ = std::min(K::S::OCC, occupancy_tiled(K::fn(), K::S::NT, smem));
+  p.G = (int)std::min<long long>(W, (long long)di.sms * occ);
   p.target = a.target;
   p.marg = a.marg;
   p.out = a.out;
@@ -277,9 +302,43 @@ int launch_tiled(const Layout& L, void* ws, const DeviceInfo& di, const TiledArg
   p.gnx = pr.grid_nx;
   p.ghx2 = pr.grid_hx * pr.grid_hx;
   p.ghy2 = pr.grid_hy * pr.grid_hy;
-  auto kern = &tiled_sweep_kernel<BT, PT, QC, RB, RP, K::KC, NSTAGE, kGrid, kMode>;
+  auto kern = &tiled_sweep_kernel<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>;
+  // Diagnostics: SKB_DEBUG_TIMING=<n> dumps per-CTA timing of the n-th tiled launch.
+  static long long dbg_count = 0;
+  static const char* dbg_env = getenv("SKB_DEBUG_TIMING");
+  unsigned long long* dbg = nullptr;
+  const bool dump = dbg_env && (++dbg_count == atoll(dbg_env));
+  if (dump) cudaMallocAsync(reinterpret_cast<void**>(&dbg), (size_t)p.G * 32, st);
+  p.dbg = dbg;
   CK(launch_pdl(kern, dim3(p.G), dim3(K::S::NT), smem, st, *a.tg, *a.tx, p));
+  // merge + epilogue of the tiles the stream-K split cut between CTAs
+  CK(launch_pdl(&tiled_fixup_kernel<BT, PT, QC, RB, RP, kMode>,
+                dim3((unsigned)(p.ntile_b * p.ntile_p * (K::S::NT / 256))), dim3(256), 0, st, p));
+  if (dump) {
+    std::vector<unsigned long long> h((size_t)p.G * 4);
+    cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFreeAsync(dbg, st);
+    unsigned long long t0 = ~0ull;
+    for (int i = 0; i < p.G; ++i) t0 = std::min(t0, h[4 * i]);
+    FILE* f = fopen("gpurun_out/cta_timing.csv", "w");
+    if (f) {
+      fprintf(f, "cta,sm,start_ns,end_ns,chunks,merges,rows,W,G,ntile_b,ntile_p,nq\n");
+      for (int i = 0; i < p.G; ++i)
+        fprintf(f, "%d,%llu,%llu,%llu,%llu,%llu,%llu,%lld,%d,%d,%d,%d\n", i, h[4 * i + 2] & 0xffff,
+                h[4 * i] - t0, h[4 * i + 1] - t0, (h[4 * i + 2] >> 16) & 0xffff,
+                h[4 * i + 2] >> 32, h[4 * i + 3], p.W, p.G, p.ntile_b, p.ntile_p, p.nq);
+      fclose(f);
+    }
+  }
   return 0;
+}
+
+template <bool kGrid, int kMode>
+int launch_tiled(const Layout& L, void* ws, const DeviceInfo& di, const TiledArgs& a,
+                 const sinkhorn_problem_v1& pr, float lam, cudaStream_t st) {
+  return pick_bt(pr.B) == 128 ? launch_tiled_pt<128, 64, kGrid, kMode>(L, ws, di, a, pr, lam, st)
+                               : launch_tiled_pt<64, 64, kGrid, kMode>(L, ws, di, a, pr, lam, st);
 }
 
 // ---- the solver --------------------------------------------------------------
@@ -302,12 +361,14 @@ struct Solve {
     const float* gsrc_row = pr.cost_kind == SINKHORN_COST_SHARED ? F(L.a2t) : F(L.f2);
     bool ok = true;
     if (pr.cost_kind == SINKHORN_COST_SHARED) {
-      ok &= make_tmap(&tm_a2, gsrc_col, L.D1p, L.D2p, QC, PT);
-      ok &= make_tmap(&tm_a2t, gsrc_row, L.D2p, L.D1p, QC, PT);
+      // G boxes are [QC][PT] with PT picked from the sweep's output extent
+      ok &= make_tmap(&tm_a2, gsrc_col, L.D1p, L.D2p, QC, pick_pt((int)pr.d2));
+      ok &= make_tmap(&tm_a2t, gsrc_row, L.D2p, L.D1p, QC, pick_pt((int)pr.d1));
     }
-    ok &= make_tmap(&tm_f2, F(L.f2), L.D1p, L.Bp, QC, BT);
-    ok &= make_tmap(&tm_g2[0], F(L.g2[0]), L.D2p, L.Bp, QC, BT);
-    ok &= make_tmap(&tm_g2[1], F(L.g2[1]), L.D2p, L.Bp, QC, BT);
+    const int bt = pick_bt(pr.B);
+    ok &= make_tmap(&tm_f2, F(L.f2), L.D1p, L.Bp, QC, bt);
+    ok &= make_tmap(&tm_g2[0], F(L.g2[0]), L.D2p, L.Bp, QC, bt);
+    ok &= make_tmap(&tm_g2[1], F(L.g2[1]), L.D2p, L.Bp, QC, bt);
     if (pr.cost_kind != SINKHORN_COST_SHARED) {
       tm_a2 = tm_f2;   // unused by the grid kernel; any valid map
       tm_a2t = tm_f2;

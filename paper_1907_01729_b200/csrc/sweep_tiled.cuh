@@ -37,8 +37,8 @@ struct TiledSweepParams {
   int Qv, Pv;          // valid reduce / output extents (d)
   int Bp;              // padded lane count (row stride of dim-major buffers)
   int ntile_b, ntile_p, nq;
-  long long W;         // atoms = ntile_b * ntile_p * nq
-  int G;               // grid size
+  long long W;         // stream-K units: reduction rows over all tiles = ntiles * Qv
+  int G;               // grid size (<= W / QC, so every CTA owns >= 1 chunk of rows)
   const float* target; // [Pp][Bp] log2 marginal of the output side
   const float* marg;   // [Pp][Bp] linear marginal of the output side (residuals)
   float* out;          // [Pp][Bp] updated potentials (UPDATE)
@@ -54,9 +54,10 @@ struct TiledSweepParams {
   // on-the-fly grid cost: G[q,p] = gk * (hx2*dx^2 + hy2*dy^2), points k -> (k % nx, k / nx)
   int gnx;
   float gk, ghx2, ghy2;
+  unsigned long long* dbg;   // optional per-CTA timing records (diagnostics), nullable
 };
 
-template <int BT, int PT, int QC, int RB, int RP, int KC, int NSTAGE, bool kGrid, int kMode>
+template <int BT, int PT, int QC, int RB, int RP, int NSTAGE, bool kGrid, int kMode>
 struct TiledSweep {
   static constexpr int NT = (BT / RB) * (PT / RP);
   static constexpr int NTB = BT / RB;          // threads along lanes (within a warp)
@@ -66,100 +67,34 @@ struct TiledSweep {
   static constexpr int STAGE_FLOATS = G_FLOATS + X_FLOATS;
   static constexpr uint32_t TMA_BYTES = (kGrid ? 0 : G_FLOATS * 4) + X_FLOATS * 4;
   static constexpr size_t SMEM_BYTES =
-      1024 /*align slack*/ + size_t(NSTAGE) * STAGE_FLOATS * 4 + 64 * 8 /*bars*/ + BT * 4 +
+      size_t(NSTAGE) * STAGE_FLOATS * 4 + 64 * 8 /*bars*/ + BT * 4 +
       (kGrid ? (QC + PT) * 8 : 0);
-  static_assert(NTB == 16, "thread map assumes 16 lane-threads per half warp");
+  static_assert(NTB == 16 || NTB == 32, "lane-threads per (half) warp");
+  static constexpr int OCC = (NT >= 512) ? 1 : 2;   // CTAs per SM the launch bounds target
   static_assert(NT % 32 == 0, "whole warps");
   static_assert(RB == 4 && RP == 4, "float4 tile loads");
-  static_assert(QC % KC == 0, "sub-chunks");
+  static_assert(QC % 4 == 0, "unroll");
 };
 
-__device__ __forceinline__ long long atom_begin(long long c, long long W, long long G) {
-  return (c * W) / G;
+// Even stream-K split over reduction rows: CTA c owns rows [c*W/G, (c+1)*W/G)
+// of the (tile, q) space, so per-CTA work differs by at most one row.
+__device__ __forceinline__ long long atom_begin(const TiledSweepParams& p, long long c) {
+  return (long long)(((unsigned long long)c * (unsigned long long)p.W) / (unsigned long long)p.G);
 }
-// CTA owning atom a: largest c with atom_begin(c) <= a.
-__device__ __forceinline__ long long atom_owner(long long a, long long W, long long G) {
-  return ((a + 1) * G - 1) / W;
+// CTA owning row a: the largest c with atom_begin(c) <= a.
+__device__ __forceinline__ long long atom_owner(const TiledSweepParams& p, long long a) {
+  return (long long)(((unsigned long long)(a + 1) * (unsigned long long)p.G - 1) /
+                     (unsigned long long)p.W);
 }
 
-template <int BT, int PT, int QC, int RB, int RP, int KC, int NSTAGE, bool kGrid, int kMode>
-__global__ void __launch_bounds__((BT / RB) * (PT / RP), 1)
-    tiled_sweep_kernel(const __grid_constant__ CUtensorMap tmap_g,
-                       const __grid_constant__ CUtensorMap tmap_x, const TiledSweepParams p) {
-  using S = TiledSweep<BT, PT, QC, RB, RP, KC, NSTAGE, kGrid, kMode>;
-  constexpr int NT = S::NT;
-  constexpr int NV = S::NV;
-  constexpr int NOUT = RB * RP;
-
-  extern __shared__ uint8_t smem_raw[];
-  float* smem = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * S::STAGE_FLOATS);
-  float* s_res = reinterpret_cast<float*>(bars + 64);
-  int* s_flag = reinterpret_cast<int*>(bars + 60);
-  float* s_gq = s_res + BT;        // grid mode: q coordinates (x, y) [QC][2]
-  float* s_gp = s_gq + 2 * QC;     // grid mode: p coordinates [PT][2]
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int warp = tid >> 5;
-  const int tb = lane & 15;                 // lane-group index (b = tb*RB + rb)
-  const int tp = warp * 2 + (lane >> 4);    // output-group index (p = tp*RP + rp)
-
-  const long long W = p.W;
-  const long long Gc = p.G;
-  const long long c = blockIdx.x;
-  const long long a_begin = atom_begin(c, W, Gc);
-  const long long a_end = atom_begin(c + 1, W, Gc);
-  const int n_local = int(a_end - a_begin);
-  const int nq = p.nq;
-
-  if (tid == 0) {
-    for (int s = 0; s < NSTAGE; ++s) mbar_init(&bars[s], 1);
-    fence_barrier_init();
-    if (!kGrid) prefetch_tmap(&tmap_g);
-    prefetch_tmap(&tmap_x);
-  }
-  __syncthreads();
-  // Everything above overlaps the previous kernel's tail; inputs are read below.
-  pdl_wait();
-
-  auto atom_coords = [&](long long a, int& tile, int& qc, int& b0, int& p0) {
-    tile = int(a / nq);
-    qc = int(a - (long long)tile * nq);
-    const int tb_idx = tile % p.ntile_b;     // lane tiles innermost: consecutive tiles share G
-    const int tp_idx = tile / p.ntile_b;
-    b0 = tb_idx * BT;
-    p0 = tp_idx * PT;
-  };
-
-  auto issue = [&](int l) {
-    const long long a = a_begin + l;
-    int tile, qc, b0, p0;
-    atom_coords(a, tile, qc, b0, p0);
-    const int s = l % NSTAGE;
-    float* st = smem + s * S::STAGE_FLOATS;
-    mbar_arrive_expect_tx(&bars[s], S::TMA_BYTES);
-    if (!kGrid) tma_load_2d(st, &tmap_g, p0, qc * QC, &bars[s]);
-    tma_load_2d(st + S::G_FLOATS, &tmap_x, b0, qc * QC, &bars[s]);
-  };
-
-  if (tid == 0) {
-    for (int l = 0; l < NSTAGE && l < n_local; ++l) issue(l);
-  }
-
-  float M[NOUT], Sm[NOUT], S2[NOUT];
-  auto reset_acc = [&]() {
-#pragma unroll
-    for (int o = 0; o < NOUT; ++o) {
-      M[o] = kNegBig;
-      Sm[o] = 0.f;
-      S2[o] = 0.f;
-    }
-  };
-  reset_acc();
-
-  // finalize one output tile from the accumulators in registers
-  auto epilogue = [&](int b0, int p0) {
+// Finalise one output tile from per-thread accumulators (M, Sm, S2 hold the
+// thread's RB x RP outputs).  Called by every thread of the CTA (it may sync).
+template <int BT, int PT, int RB, int RP, int NT, int kMode>
+__device__ __forceinline__ void tile_epilogue(const TiledSweepParams& p, int tid, int tb, int tp,
+                                              int b0, int p0, int own_lo, const float* M,
+                                              const float* Sm, const float* S2, float* s_res) {
+  // tid/NT here are the block-local thread index and block size (the caller
+  // passes the lane/output groups tb/tp of the sweep's thread map)
     if (p.res != nullptr && (kMode == kModeTail || p.res_kind != kResNone)) {
       for (int i = tid; i < BT; i += NT) s_res[i] = 0.f;
       __syncthreads();
@@ -171,7 +106,7 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), 1)
 #pragma unroll
     for (int rp = 0; rp < RP; ++rp) {
       const int pp = p0 + tp * RP + rp;
-      if (pp >= p.Pv) continue;
+      if (pp >= p.Pv || pp < own_lo) continue;
       const size_t row = size_t(pp) * p.Bp + bb;
       if (kMode == kModePartial) {
         *reinterpret_cast<float4*>(p.pmax + row) =
@@ -229,14 +164,121 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), 1)
         if (b0 + i < p.Bp) atomic_max_nonneg(&p.res[b0 + i], s_res[i]);
       }
     }
+  }
+
+// Thread -> (lane group, output group) map shared by the sweep and the fixup:
+// a warp covers 64 lanes x 8 outputs (16 lane-threads x 2 output-groups), so
+// per row it reads 256 B of X and two 16 B G vectors (3 shared wavefronts);
+// with BT=128 the warps split into two lane halves.
+template <int BT, int RB, int NT>
+__device__ __forceinline__ void thread_map(int tid, int& tb, int& tp) {
+  constexpr int NTB = BT / RB;
+  constexpr int NW = NT / 32;
+  constexpr int WPH = NW / (NTB / 16);
+  const int warp = tid >> 5, lane = tid & 31;
+  tb = (warp / WPH) * 16 + (lane & 15);
+  tp = (warp % WPH) * 2 + (lane >> 4);
+}
+
+template <int BT, int PT, int QC, int RB, int RP, int NSTAGE, bool kGrid, int kMode>
+__global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) >= 512) ? 1 : 2)
+    tiled_sweep_kernel(const __grid_constant__ CUtensorMap tmap_g,
+                       const __grid_constant__ CUtensorMap tmap_x, const TiledSweepParams p) {
+  using S = TiledSweep<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>;
+  constexpr int NT = S::NT;
+  constexpr int NV = S::NV;
+  constexpr int NOUT = RB * RP;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* smem = reinterpret_cast<float*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * S::STAGE_FLOATS);
+  float* s_res = reinterpret_cast<float*>(bars + 64);
+  float* s_gq = s_res + BT;        // grid mode: q coordinates (x, y) [QC][2]
+  float* s_gp = s_gq + 2 * QC;     // grid mode: p coordinates [PT][2]
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  int tb, tp;   // lane group (b = tb*RB + rb), output group (p = tp*RP + rp)
+  thread_map<BT, RB, NT>(tid, tb, tp);
+
+  const long long c = blockIdx.x;
+  const long long a_begin = atom_begin(p, c);     // first row (global row index)
+  const long long a_end = atom_begin(p, c + 1);   // one past the last row
+  const int nq = p.nq;
+  const long long Qv = p.Qv;
+  // global chunk index of a row: tile * nq + (q / QC)
+  auto chunk_of = [&](long long r) {
+    const long long t = r / Qv;
+    return t * nq + (r - t * Qv) / QC;
   };
+  const long long g_first = chunk_of(a_begin);
+  const int n_local = int(chunk_of(a_end - 1) - g_first + 1);
+
+  if (tid == 0) {
+    for (int s = 0; s < NSTAGE; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+    if (!kGrid) prefetch_tmap(&tmap_g);
+    prefetch_tmap(&tmap_x);
+  }
+  __syncthreads();
+  // Everything above overlaps the previous kernel's tail; inputs are read below.
+  pdl_wait();
+  unsigned long long dbg_t0 = 0, dbg_tw = 0, dbg_tm = 0;
+  if (p.dbg != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
+  int dbg_merges = 0;
+
+  // Output tile tp_idx covers [p0, p0 + PT) but owns (writes) [tp_idx*PT, ...):
+  // the last tile is shifted left to end at Pv, so no tile is partial (a
+  // partial tile's few active warps are latency-bound and stretch the tail).
+  auto atom_coords = [&](long long a, int& tile, int& qc, int& b0, int& p0) {
+    tile = int(a / nq);
+    qc = int(a - (long long)tile * nq);
+    const int tb_idx = tile % p.ntile_b;     // lane tiles innermost: consecutive tiles share G
+    const int tp_idx = tile / p.ntile_b;
+    b0 = tb_idx * BT;
+    p0 = (tp_idx == p.ntile_p - 1) ? max(p.Pv - PT, 0) : tp_idx * PT;
+  };
+
+  auto issue = [&](int l) {
+    const long long a = g_first + l;
+    int tile, qc, b0, p0;
+    atom_coords(a, tile, qc, b0, p0);
+    const int s = l % NSTAGE;
+    float* st = smem + s * S::STAGE_FLOATS;
+    mbar_arrive_expect_tx(&bars[s], S::TMA_BYTES);
+    if (!kGrid) tma_load_2d(st, &tmap_g, p0, qc * QC, &bars[s]);
+    tma_load_2d(st + S::G_FLOATS, &tmap_x, b0, qc * QC, &bars[s]);
+  };
+
+  if (tid == 0) {
+    for (int l = 0; l < NSTAGE && l < n_local; ++l) issue(l);
+  }
+
+  float M[NOUT], Sm[NOUT], S2[NOUT];
+  auto reset_acc = [&]() {
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) {
+      M[o] = kNegBig;
+      Sm[o] = 0.f;
+      S2[o] = 0.f;
+    }
+  };
+  reset_acc();
 
   int cur_tile = -1;
   int seg_q0 = 0;
   for (int l = 0; l < n_local; ++l) {
-    const long long a = a_begin + l;
+    const long long a = g_first + l;
     int tile, qc, b0, p0;
     atom_coords(a, tile, qc, b0, p0);
+    // this CTA's rows inside the chunk: [k_lo, k_hi) relative to the chunk start
+    const long long row0 = (long long)tile * Qv + (long long)qc * QC;
+    const int chunk_rows = (int)(Qv - (long long)qc * QC < QC ? Qv - (long long)qc * QC : QC);
+    const int k_lo = (int)(a_begin > row0 ? a_begin - row0 : 0);
+    int k_hi = (int)(a_end - row0 < chunk_rows ? a_end - row0 : chunk_rows);
+    // rows past Qv are -inf padding: round the natural chunk end up to a pair
+    if (k_hi == chunk_rows) k_hi = min(QC, (k_hi + 1) & ~1);
     if (tile != cur_tile) {
       cur_tile = tile;
       seg_q0 = qc;
@@ -272,64 +314,109 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), 1)
     if (kGrid) __syncthreads();
 
     // ---- consume: the hot loop --------------------------------------------
-    const int kvalid = min(QC, p.Qv - qc * QC);
-    const bool active = (p0 + tp * RP) < p.Pv;   // uniform per half-warp
-    if (active) {
-      for (int kk = 0; kk < kvalid; kk += KC) {
-        float g[KC][RP], x[KC][RB];
+    // Rows beyond Qv are -inf in both tiles (padded buffers / recomputed tile),
+    // so the chunk length can be rounded up to the unroll width.
+    // a warp covers 2 output groups; skip it only if both are past Pv (uniform)
+    const bool warp_active = __any_sync(0xffffffffu, (p0 + tp * RP) < p.Pv);
+    if (warp_active) {
+      // Outputs are handled in lane pairs (rb = 2h, 2h+1) so every add is a
+      // packed FADD2 with the cost value broadcast: o = (2h + e) * RP + rp.
+      // phase 1: exact max of this chunk, 2 rows per FMNMX3 (1 instr / cell)
+      float cm[NOUT];
 #pragma unroll
-        for (int k = 0; k < KC; ++k) {
-          const float4 gv = *reinterpret_cast<const float4*>(Gs + (kk + k) * PT + tp * RP);
-          const float4 xv = *reinterpret_cast<const float4*>(Xs + (kk + k) * BT + tb * RB);
-          g[k][0] = gv.x; g[k][1] = gv.y; g[k][2] = gv.z; g[k][3] = gv.w;
-          x[k][0] = xv.x; x[k][1] = xv.y; x[k][2] = xv.z; x[k][3] = xv.w;
+      for (int o = 0; o < NOUT; ++o) cm[o] = kNegBig;
+      const int k_pairs_end = k_lo + ((k_hi - k_lo) & ~1);
+#pragma unroll 2
+      for (int k = k_lo; k < k_pairs_end; k += 2) {
+        const float4 ga = *reinterpret_cast<const float4*>(Gs + k * PT + tp * RP);
+        const float4 gb = *reinterpret_cast<const float4*>(Gs + (k + 1) * PT + tp * RP);
+        const float4 xa = *reinterpret_cast<const float4*>(Xs + k * BT + tb * RB);
+        const float4 xb = *reinterpret_cast<const float4*>(Xs + (k + 1) * BT + tb * RB);
+        const float gav[4] = {ga.x, ga.y, ga.z, ga.w};
+        const float gbv[4] = {gb.x, gb.y, gb.z, gb.w};
+        const uint64_t xa2[2] = {pk2(xa.x, xa.y), pk2(xa.z, xa.w)};
+        const uint64_t xb2[2] = {pk2(xb.x, xb.y), pk2(xb.z, xb.w)};
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int rp = 0; rp < RP; ++rp) {
+            const uint64_t ta = fadd2(xa2[h], pk2(gav[rp], gav[rp]));
+            const uint64_t tb2 = fadd2(xb2[h], pk2(gbv[rp], gbv[rp]));
+            const int o0 = (2 * h) * RP + rp, o1 = (2 * h + 1) * RP + rp;
+            cm[o0] = fmax3(cm[o0], lo2(ta), lo2(tb2));
+            cm[o1] = fmax3(cm[o1], hi2(ta), hi2(tb2));
+          }
+      }
+      if (k_pairs_end < k_hi) {   // odd row at a CTA boundary
+        const int k = k_pairs_end;
+        const float4 ga = *reinterpret_cast<const float4*>(Gs + k * PT + tp * RP);
+        const float4 xa = *reinterpret_cast<const float4*>(Xs + k * BT + tb * RB);
+        const float gav[4] = {ga.x, ga.y, ga.z, ga.w};
+        const float xav[4] = {xa.x, xa.y, xa.z, xa.w};
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+          for (int rp = 0; rp < RP; ++rp)
+            cm[rb * RP + rp] = fmaxf(cm[rb * RP + rp], gav[rp] + xav[rb]);
+      }
+      // phase 2: lazy online rescale (batch.py:98-105), warp-uniform so the
+      // branch never diverges; the running max only moves when a chunk beats
+      // it by more than kLazy, i.e. rarely after the first chunks.
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) {
+        if (__any_sync(0xffffffffu, cm[o] > M[o] + kLazy)) {
+          const float mn = fmaxf(M[o], cm[o]);
+          const float r = ex2(M[o] - mn);
+          Sm[o] *= r;
+          if (kMode == kModeTail) S2[o] *= r;
+          M[o] = mn;
         }
-        float cw[KC][RP];
+      }
+      // phase 3: one ex2 per cell; packed adds for t = g + x, t - M and the
+      // chunk-local sums (which keep the fp32 error ~ sqrt(Q/QC))
+      uint64_t nM[2][RP], acc[2][RP], acc2[2][RP];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int rp = 0; rp < RP; ++rp) {
+          nM[h][rp] = pk2(-M[(2 * h) * RP + rp], -M[(2 * h + 1) * RP + rp]);
+          acc[h][rp] = 0ull;
+          acc2[h][rp] = 0ull;
+        }
+#pragma unroll 4
+      for (int k = k_lo; k < k_hi; ++k) {
+        const float4 gv = *reinterpret_cast<const float4*>(Gs + k * PT + tp * RP);
+        const float4 xv = *reinterpret_cast<const float4*>(Xs + k * BT + tb * RB);
+        const float g[4] = {gv.x, gv.y, gv.z, gv.w};
+        const uint64_t x2[2] = {pk2(xv.x, xv.y), pk2(xv.z, xv.w)};
+        float cw[4];
         if (kMode == kModeTail) {
           // c = G * cinv; padding rows (G = -inf) must weigh 0, not +inf
 #pragma unroll
-          for (int k = 0; k < KC; ++k)
-#pragma unroll
-            for (int rp = 0; rp < RP; ++rp)
-              cw[k][rp] = (g[k][rp] == neg_inf()) ? 0.f : g[k][rp] * p.cinv;
+          for (int rp = 0; rp < RP; ++rp) cw[rp] = (g[rp] == neg_inf()) ? 0.f : g[rp] * p.cinv;
         }
 #pragma unroll
-        for (int rb = 0; rb < RB; ++rb) {
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int rp = 0; rp < RP; ++rp) {
-            const int o = rb * RP + rp;
-            float t[KC];
-            float cm = kNegBig;
+            const uint64_t a = fadd2(fadd2(x2[h], pk2(g[rp], g[rp])), nM[h][rp]);
+            const uint64_t e = pk2(ex2(lo2(a)), ex2(hi2(a)));
+            acc[h][rp] = fadd2(acc[h][rp], e);
+            if (kMode == kModeTail) acc2[h][rp] = ffma2(e, pk2(cw[rp], cw[rp]), acc2[h][rp]);
+          }
+      }
 #pragma unroll
-            for (int k = 0; k < KC; ++k) {
-              t[k] = g[k][rp] + x[k][rb];
-              cm = fmaxf(cm, t[k]);
-            }
-            if (cm > M[o] + kLazy) {   // lazy online rescale (batch.py:98-105)
-              const float r = ex2(M[o] - cm);
-              Sm[o] *= r;
-              if (kMode == kModeTail) S2[o] *= r;
-              M[o] = cm;
-            }
-            float e[KC], e2[KC];
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int k = 0; k < KC; ++k) {
-              e[k] = ex2(t[k] - M[o]);
-              if (kMode == kModeTail) e2[k] = e[k] * cw[k][rp];
-            }
-            // pairwise tree inside the chunk keeps the fp32 error ~ sqrt(Q/KC)
-#pragma unroll
-            for (int w = 1; w < KC; w *= 2)
-#pragma unroll
-              for (int k = 0; k + w < KC; k += 2 * w) {
-                e[k] += e[k + w];
-                if (kMode == kModeTail) e2[k] += e2[k + w];
-              }
-            Sm[o] += e[0];
-            if (kMode == kModeTail) S2[o] += e2[0];
+        for (int rp = 0; rp < RP; ++rp) {
+          const int o0 = (2 * h) * RP + rp, o1 = (2 * h + 1) * RP + rp;
+          Sm[o0] += lo2(acc[h][rp]);
+          Sm[o1] += hi2(acc[h][rp]);
+          if (kMode == kModeTail) {
+            S2[o0] += lo2(acc2[h][rp]);
+            S2[o1] += hi2(acc2[h][rp]);
           }
         }
-      }
     }
     __syncthreads();   // every warp is done with stage s
     if (tid == 0 && l + NSTAGE < n_local) issue(l + NSTAGE);
@@ -337,56 +424,115 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), 1)
     // ---- segment end: finalize or hand over to the stream-K merge ---------
     const bool seg_end = (qc == nq - 1) || (l == n_local - 1);
     if (!seg_end) continue;
-    const long long t_first = (long long)tile * nq;
-    const long long c_lo = atom_owner(t_first, W, Gc);
-    const long long c_hi = atom_owner(t_first + nq - 1, W, Gc);
+    if (p.dbg != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_tw));
+    const long long t_first = (long long)tile * Qv;   // first row of this tile
+    const long long c_lo = atom_owner(p, t_first);
+    const long long c_hi = atom_owner(p, t_first + Qv - 1);
+    const int own_lo = (tile / p.ntile_b) * PT;
     if (c_lo == c_hi) {
-      epilogue(b0, p0);
+      tile_epilogue<BT, PT, RB, RP, NT, kMode>(p, tid, tb, tp, b0, p0, own_lo, M, Sm, S2, s_res);
     } else {
+      // split tile: leave this piece's (max, sum[, E0 sum]) for the fixup kernel
       const int slot = (a_begin >= t_first) ? 0 : 1;
-      float* mine = p.part + ((c * 2 + slot) * NV) * (size_t)(BT * PT);
+      float* mine = p.part + ((c * 2 + slot) * NV) * (size_t)(BT * PT) + tid * NOUT;
 #pragma unroll
       for (int o = 0; o < NOUT; o += 4) {
-        *reinterpret_cast<float4*>(mine + tid * NOUT + o) =
-            make_float4(M[o], M[o + 1], M[o + 2], M[o + 3]);
-        *reinterpret_cast<float4*>(mine + BT * PT + tid * NOUT + o) =
-            make_float4(Sm[o], Sm[o + 1], Sm[o + 2], Sm[o + 3]);
+        __stcg(reinterpret_cast<float4*>(mine + o), make_float4(M[o], M[o + 1], M[o + 2], M[o + 3]));
+        __stcg(reinterpret_cast<float4*>(mine + BT * PT + o),
+               make_float4(Sm[o], Sm[o + 1], Sm[o + 2], Sm[o + 3]));
         if (NV == 3)
-          *reinterpret_cast<float4*>(mine + 2 * BT * PT + tid * NOUT + o) =
-              make_float4(S2[o], S2[o + 1], S2[o + 2], S2[o + 3]);
+          __stcg(reinterpret_cast<float4*>(mine + 2 * BT * PT + o),
+                 make_float4(S2[o], S2[o + 1], S2[o + 2], S2[o + 3]));
       }
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) {
-        const int pieces = int(c_hi - c_lo + 1);
-        const int prev = atomicAdd(&p.counters[tile], 1);
-        *s_flag = (prev == pieces - 1);
-      }
-      __syncthreads();
-      if (*s_flag) {
-        __threadfence();
-        reset_acc();
-        for (long long cc = c_lo; cc <= c_hi; ++cc) {
-          const int sl = (atom_begin(cc, W, Gc) >= t_first) ? 0 : 1;
-          const float* src = p.part + ((cc * 2 + sl) * NV) * (size_t)(BT * PT);
-#pragma unroll
-          for (int o = 0; o < NOUT; ++o) {
-            const float m2 = __ldcg(src + tid * NOUT + o);
-            const float s2v = __ldcg(src + BT * PT + tid * NOUT + o);
-            const float mn = fmaxf(M[o], m2);
-            const float ra = ex2(M[o] - mn), rb2 = ex2(m2 - mn);
-            Sm[o] = Sm[o] * ra + s2v * rb2;
-            if (NV == 3) S2[o] = S2[o] * ra + __ldcg(src + 2 * BT * PT + tid * NOUT + o) * rb2;
-            M[o] = mn;
-          }
-        }
-        epilogue(b0, p0);
-        if (tid == 0) p.counters[tile] = 0;
-      }
+      ++dbg_merges;
     }
     reset_acc();
     (void)seg_q0;
   }
+  if (p.dbg != nullptr && tid == 0) {
+    unsigned long long t1, smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    unsigned int sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    smid = sm;
+    p.dbg[4 * blockIdx.x + 0] = dbg_t0;
+    p.dbg[4 * blockIdx.x + 1] = t1;
+    p.dbg[4 * blockIdx.x + 2] = smid | ((unsigned long long)n_local << 16) |
+                                ((unsigned long long)dbg_merges << 32);
+    p.dbg[4 * blockIdx.x + 3] = ((dbg_tw - dbg_t0) & 0xffffffffull) |
+                                (dbg_tm ? ((dbg_tm - dbg_t0) << 32) : 0ull);
+  }
+  pdl_launch_dependents();
+}
+
+// Merge the stream-K pieces of every split tile in ascending CTA order (the
+// reference's ascending span merge, batch.py:198-201: deterministic) and run
+// the tile epilogue.  One CTA per tile, same thread map as the sweep, so each
+// thread merges exactly the outputs its counterpart accumulated.  Launched
+// right after the sweep with programmatic dependent launch.
+template <int BT, int PT, int QC, int RB, int RP, int kMode>
+__global__ void __launch_bounds__(256) tiled_fixup_kernel(const TiledSweepParams p) {
+  constexpr int NT = (BT / RB) * (PT / RP);   // the sweep's threads per tile
+  constexpr int NB = 256;                     // fixup threads per CTA (NT / NB CTAs per tile)
+  constexpr int NOUT = RB * RP;
+  constexpr int NV = (kMode == kModeTail) ? 3 : 2;
+  constexpr int GRP = 4;                      // pieces whose loads are in flight together
+  __shared__ float s_res[BT];
+  pdl_wait();
+  const int tile = blockIdx.x / (NT / NB);
+  const int vtid = (blockIdx.x % (NT / NB)) * NB + threadIdx.x;   // the sweep thread mirrored
+  const long long Qv = p.Qv;
+  const long long t_first = (long long)tile * Qv;
+  const long long c_lo = atom_owner(p, t_first);
+  const long long c_hi = atom_owner(p, t_first + Qv - 1);
+  if (c_lo == c_hi) return;   // finalised by the sweep itself
+  int tb, tp;
+  thread_map<BT, RB, NT>(vtid, tb, tp);
+  const int tb_idx = tile % p.ntile_b, tp_idx = tile / p.ntile_b;
+  const int b0 = tb_idx * BT;
+  const int p0 = (tp_idx == p.ntile_p - 1) ? max(p.Pv - PT, 0) : tp_idx * PT;
+  const int own_lo = tp_idx * PT;
+  float M[NOUT], Sm[NOUT], S2[NOUT];
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o) {
+    M[o] = kNegBig;
+    Sm[o] = 0.f;
+    S2[o] = 0.f;
+  }
+#pragma unroll 1
+  for (long long c0 = c_lo; c0 <= c_hi; c0 += GRP) {
+    float4 mv[GRP][NOUT / 4], sv[GRP][NOUT / 4], tv[GRP][NOUT / 4];
+#pragma unroll
+    for (int g = 0; g < GRP; ++g) {
+      const long long cc = c0 + g;
+      if (cc > c_hi) break;
+      const int sl = (atom_begin(p, cc) >= t_first) ? 0 : 1;
+      const float* src = p.part + ((cc * 2 + sl) * NV) * (size_t)(BT * PT) + vtid * NOUT;
+#pragma unroll
+      for (int j = 0; j < NOUT / 4; ++j) {
+        mv[g][j] = __ldcg(reinterpret_cast<const float4*>(src) + j);
+        sv[g][j] = __ldcg(reinterpret_cast<const float4*>(src + BT * PT) + j);
+        if (NV == 3) tv[g][j] = __ldcg(reinterpret_cast<const float4*>(src + 2 * BT * PT) + j);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < GRP; ++g) {
+      if (c0 + g > c_hi) break;   // ascending piece order (batch.py:198-201)
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) {
+        const float m2 = reinterpret_cast<const float*>(&mv[g][o / 4])[o % 4];
+        const float s2v = reinterpret_cast<const float*>(&sv[g][o / 4])[o % 4];
+        const float mn = fmaxf(M[o], m2);
+        const float ra = ex2(M[o] - mn), rb2 = ex2(m2 - mn);
+        Sm[o] = Sm[o] * ra + s2v * rb2;
+        if (NV == 3)
+          S2[o] = S2[o] * ra + reinterpret_cast<const float*>(&tv[g][o / 4])[o % 4] * rb2;
+        M[o] = mn;
+      }
+    }
+  }
+  tile_epilogue<BT, PT, RB, RP, NB, kMode>(p, threadIdx.x, tb, tp, b0, p0, own_lo, M, Sm, S2,
+                                           s_res);
   pdl_launch_dependents();
 }
 

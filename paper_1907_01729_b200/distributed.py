@@ -42,18 +42,37 @@ NEG_BIG = -1.0e30
 # batch sharding
 
 
+def global_max(local: float, group=None) -> float:
+    """Max over ranks of a per-rank residual; NaN never converges (batch.py:320)."""
+    v = local if local == local else math.inf
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def gather_lane_values(local: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather per-lane values from ranks holding different lane counts."""
+    ws = dist.get_world_size(group)
+    dev = local.device
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(ws)]
+    dist.all_gather(sizes, torch.tensor([local.numel()], device=dev), group=group)
+    n = max(int(x.item()) for x in sizes)
+    buf = torch.full((n,), float("nan"), device=dev, dtype=local.dtype)
+    buf[: local.numel()] = local
+    parts = [torch.empty_like(buf) for _ in range(ws)]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([p[: int(x.item())] for p, x in zip(parts, sizes)])
+
+
 @contextmanager
 def global_residual_reducer(group=None):
     """Make the library's convergence test use the max residual over all ranks."""
     lib = _lib.load()
 
     def reduce(local: float, _user) -> float:
-        v = local if local == local else math.inf      # NaN never converges (batch.py:320)
-        dev = torch.device("cuda", torch.cuda.current_device()) \
-            if dist.get_backend(group) == "nccl" else torch.device("cpu")
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-        return float(t.item())
+        return global_max(local, group)
 
     cb = _lib.REDUCER(reduce)
     lib.sinkhorn_set_residual_reducer_v1(cb, None)
@@ -72,17 +91,7 @@ def batch_sharded_solve(mu_local, nu_local, cost, lam: float, max_iters: int = 1
             res = solve(mu_local, nu_local, cost, lam, max_iters, tolerance, check_interval)
     else:
         res = solve(mu_local, nu_local, cost, lam, max_iters, tolerance, check_interval)
-    ws = dist.get_world_size(group)
-    sizes = [torch.zeros(1, dtype=torch.int64, device=res.cost_e0.device) for _ in range(ws)]
-    dist.all_gather(sizes, torch.tensor([res.cost_e0.numel()], device=res.cost_e0.device),
-                    group=group)
-    n = max(int(s.item()) for s in sizes)
-    buf = torch.full((n,), float("nan"), device=res.cost_e0.device)
-    buf[: res.cost_e0.numel()] = res.cost_e0
-    parts = [torch.empty_like(buf) for _ in range(ws)]
-    dist.all_gather(parts, buf, group=group)
-    costs = torch.cat([p[: int(s.item())] for p, s in zip(parts, sizes)])
-    return res, costs
+    return res, gather_lane_values(res.cost_e0, group)
 
 
 # ---------------------------------------------------------------------------
@@ -134,9 +143,10 @@ def row_sharded_solve(mu_local, nu, backend, lam: float, max_iters: int,
     nu (B, d2) replicated.  Returns log_u for the local rows, the full log_v,
     global E0 per lane, iterations and residuals (batch.py:264-349 semantics).
     """
-    f32 = torch.float32
-    mu_local = mu_local.to(f32)
-    nu = nu.to(f32)
+    # float32 on the device; float64 when a CPU backend drives the same logic (tests)
+    dt = torch.float64 if mu_local.dtype == torch.float64 else torch.float32
+    mu_local = mu_local.to(dt)
+    nu = nu.to(dt)
     log_mu = torch.log(mu_local)
     log_nu = torch.log(nu)
     log_u = torch.where(mu_local > 0, torch.zeros_like(mu_local),
@@ -205,7 +215,8 @@ def row_sharded_backward(log_u_local, log_v, lam: float, upstream, group=None,
 
 
 __all__ = [
-    "CudaShardBackend", "batch_sharded_solve", "global_residual_reducer",
+    "CudaShardBackend", "batch_sharded_solve", "gather_lane_values", "global_max",
+    "global_residual_reducer",
     "row_sharded_backward", "row_sharded_solve",
 ]
 

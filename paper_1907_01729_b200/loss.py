@@ -71,6 +71,20 @@ def _stream_handle(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+_WS_CACHE: dict = {}
+
+
+def _workspace(dev: torch.device, nbytes: int) -> torch.Tensor:
+    """Per-(device, stream) workspace, grown on demand and reused across calls
+    (stream-ordered reuse is safe; calls on other streams get their own)."""
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    ws = _WS_CACHE.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 256), device=dev, dtype=torch.uint8)
+        _WS_CACHE[key] = ws
+    return ws
+
+
 def _as_f32_cuda(x, device=None) -> torch.Tensor:
     t = torch.as_tensor(x)
     if device is None:
@@ -148,7 +162,7 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
     residuals = torch.empty(B, device=dev, dtype=torch.float32)
     with torch.cuda.device(dev):
         nbytes = lib.sinkhorn_workspace_bytes_v1(ctypes.byref(pr))
-        ws = torch.empty(max(nbytes, 256), device=dev, dtype=torch.uint8)
+        ws = _workspace(dev, nbytes)
         iters = ctypes.c_int32(0)
         st = lib.sinkhorn_forward_device_v1(
             ctypes.byref(pr), ctypes.byref(op), _ptr(mu), _ptr(nu),
