@@ -92,6 +92,7 @@ typedef struct sinkhorn_problem_v1 {
 #define SINKHORN_FLAG_SKIP_VALIDATION 1u /* trust mu/nu/cost (caller validated) */
 #define SINKHORN_FLAG_PARTIAL_ROWS 2u    /* reserved: row-sharded solves use the half-sweep API */
 #define SINKHORN_FLAG_TIME_LOOP 4u       /* record CUDA events around the iteration loop */
+#define SINKHORN_FLAG_EXACT_MAX 8u       /* always two-pass chunks (no previous-lse estimate) */
 
 typedef struct sinkhorn_options_v1 {
   double lambda;          /* > 0, finite */
@@ -180,6 +181,9 @@ const char* sinkhorn_version(void);
  * the elapsed milliseconds (CUDA events on the caller's stream) of the last
  * iteration loop run with SINKHORN_FLAG_TIME_LOOP (-1 if none). */
 unsigned long long sinkhorn_launch_count_v1(void);
+/* Solves this thread redid in exact two-pass mode because a previous-lse
+ * estimate overshot the result (estimate mode). */
+unsigned long long sinkhorn_exact_reruns_v1(void);
 float sinkhorn_last_loop_ms_v1(void);
 
 #ifdef __cplusplus

@@ -30,6 +30,7 @@ COST_GRID2D = 2
 
 FLAG_SKIP_VALIDATION = 1
 FLAG_TIME_LOOP = 4
+FLAG_EXACT_MAX = 8
 
 # every symbol include/sinkhorn_b200.h declares
 EXPORTED_SYMBOLS = (
@@ -46,6 +47,7 @@ EXPORTED_SYMBOLS = (
     "sinkhorn_last_error",
     "sinkhorn_version",
     "sinkhorn_launch_count_v1",
+    "sinkhorn_exact_reruns_v1",
     "sinkhorn_last_loop_ms_v1",
 )
 
@@ -113,6 +115,7 @@ def _declare(lib):
         "sinkhorn_last_error": (ctypes.c_char_p, []),
         "sinkhorn_version": (ctypes.c_char_p, []),
         "sinkhorn_launch_count_v1": (ctypes.c_ulonglong, []),
+        "sinkhorn_exact_reruns_v1": (ctypes.c_ulonglong, []),
         "sinkhorn_last_loop_ms_v1": (ctypes.c_float, []),
     }
     for name, (res, args) in sig.items():

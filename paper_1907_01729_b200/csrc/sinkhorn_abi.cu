@@ -32,6 +32,7 @@ namespace {
 thread_local std::string g_last_error;
 thread_local unsigned long long g_launches = 0;   // kernels this thread launched
 thread_local float g_last_loop_ms = -1.f;         // last timed iteration loop (ms)
+thread_local unsigned long long g_exact_reruns = 0;  // solves redone without estimates
 // Optional cross-rank agreement on the stopping test (batch-sharded solves).
 thread_local sinkhorn_residual_reducer_v1 g_reducer = nullptr;
 thread_local void* g_reducer_user = nullptr;
@@ -55,6 +56,7 @@ constexpr int BT_MAX = 128;   // lane tile: 128 (16 warps, 1 CTA/SM) or 64 (8 wa
 constexpr int PT_MAX = 64;    // output-tile widths: 64 or 56 (picked per sweep, see pick_pt)
 constexpr int TILE_PAD = 64;  // buffer extents padded to 64 (>= every tile / TMA box)
 constexpr int MAX_OCC = 2;
+constexpr int kEstFromIter = 3;   // first iteration whose sweeps start from the previous lse
 
 template <int BT, int PT, bool kGrid, int kMode>
 struct TiledK {
@@ -268,6 +270,9 @@ struct TiledArgs {
   float* e0;
   float* pmax;
   float* psum;
+  const float* est_old = nullptr;   // estimate mode: output-side potentials before the sweep
+  int use_est = 0;
+  int* est_fail = nullptr;
 };
 
 template <int BT, int PT, bool kGrid, int kMode>
@@ -295,6 +300,9 @@ int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const Tiled
   p.e0 = a.e0;
   p.pmax = a.pmax;
   p.psum = a.psum;
+  p.est_old = a.est_old;
+  p.use_est = (a.use_est && a.est_old != nullptr) ? 1 : 0;
+  p.est_fail = a.est_fail;
   p.part = at<float>(ws, L.part);
   p.counters = at<int>(ws, L.counters);
   p.cinv = -lam * kLn2;
@@ -312,8 +320,11 @@ int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const Tiled
   p.dbg = dbg;
   CK(launch_pdl(kern, dim3(p.G), dim3(K::S::NT), smem, st, *a.tg, *a.tx, p));
   // merge + epilogue of the tiles the stream-K split cut between CTAs
+  static const bool no_fixup = getenv("SKB_DIAG_NO_FIXUP") != nullptr;   // timing experiments only
+  if (!no_fixup)
   CK(launch_pdl(&tiled_fixup_kernel<BT, PT, QC, RB, RP, kMode>,
-                dim3((unsigned)(p.ntile_b * p.ntile_p * (K::S::NT / 256))), dim3(256), 0, st, p));
+                dim3((unsigned)(p.ntile_b * p.ntile_p * (K::S::NT * 4 / 256))), dim3(256), 0,
+                st, p));
   if (dump) {
     std::vector<unsigned long long> h((size_t)p.G * 4);
     cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
@@ -352,6 +363,8 @@ struct Solve {
   float lam;
   CUtensorMap tm_a2, tm_a2t, tm_f2, tm_g2[2];
   const float* cost;
+  bool est = false;        // estimate mode for the tiled sweeps (set per iteration)
+  int* est_fail = nullptr;
 
   float* F(size_t off) const { return at<float>(ws, off); }
 
@@ -381,7 +394,7 @@ struct Solve {
     if (L.tiled) {
       TiledArgs a = {&tm_a2, &tm_f2, (int)pr.d1, (int)pr.d2, L.D1p, L.D2p, F(L.l2nu), F(L.nu),
                      F(L.g2[dst]), F(L.g2[src_old]), F(L.res), res_kind, nullptr, nullptr,
-                     nullptr};
+                     nullptr, F(L.g2[src_old]), est ? 1 : 0, est_fail};
       return pr.cost_kind == SINKHORN_COST_GRID2D
                  ? launch_tiled<true, kModeUpdate>(L, ws, di, a, pr, lam, st)
                  : launch_tiled<false, kModeUpdate>(L, ws, di, a, pr, lam, st);
@@ -393,7 +406,8 @@ struct Solve {
   int row_sweep(int src, int res_kind) {
     if (L.tiled) {
       TiledArgs a = {&tm_a2t, &tm_g2[src], (int)pr.d2, (int)pr.d1, L.D2p, L.D1p, F(L.l2mu),
-                     F(L.mu), F(L.f2), nullptr, F(L.res), res_kind, nullptr, nullptr, nullptr};
+                     F(L.mu), F(L.f2), nullptr, F(L.res), res_kind, nullptr, nullptr, nullptr,
+                     F(L.f2), est ? 1 : 0, est_fail};
       return pr.cost_kind == SINKHORN_COST_GRID2D
                  ? launch_tiled<true, kModeUpdate>(L, ws, di, a, pr, lam, st)
                  : launch_tiled<false, kModeUpdate>(L, ws, di, a, pr, lam, st);
@@ -420,7 +434,8 @@ struct Solve {
   int tail(int cur) {
     if (L.tiled) {
       TiledArgs a = {&tm_a2, &tm_f2, (int)pr.d1, (int)pr.d2, L.D1p, L.D2p, F(L.l2nu), F(L.nu),
-                     nullptr, F(L.g2[cur]), F(L.res), kResCol, F(L.e0), nullptr, nullptr};
+                     nullptr, F(L.g2[cur]), F(L.res), kResCol, F(L.e0), nullptr, nullptr,
+                     F(L.g2[cur]), est ? 1 : 0, est_fail};
       return pr.cost_kind == SINKHORN_COST_GRID2D
                  ? launch_tiled<true, kModeTail>(L, ws, di, a, pr, lam, st)
                  : launch_tiled<false, kModeTail>(L, ws, di, a, pr, lam, st);
@@ -519,7 +534,7 @@ int check_options(const sinkhorn_options_v1* op) {
 int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, const float* mu,
                  const float* nu, const float* cost, float* out_cost, float* out_log_u,
                  float* out_log_v, int32_t* out_iterations, float* out_residuals, void* ws,
-                 size_t ws_bytes, cudaStream_t st) {
+                 size_t ws_bytes, cudaStream_t st, bool allow_est = true) {
   Solve S;
   S.pr = pr;
   S.op = op;
@@ -534,9 +549,11 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     return fail(SINKHORN_STATUS_WORKSPACE, "workspace too small");
   int* status = at<int>(ws, L.status);
   int* badrow = at<int>(ws, L.badrow);
+  S.est_fail = at<int>(ws, L.scratch + 16);
 
   // ---- setup (batch.py:279-296) ----
   CK(cudaMemsetAsync(status, 0, 4, st));
+  CK(cudaMemsetAsync(S.est_fail, 0, 4, st));
   CK(cudaMemsetAsync(badrow, 0x7f, 4, st));
   CK(cudaMemsetAsync(at<int>(ws, L.counters), 0, std::max<size_t>(L.counter_count, 1) * 4, st));
   CK(cudaMemsetAsync(S.F(L.res), 0, (size_t)std::max(L.Bp, 1) * 4, st));
@@ -592,6 +609,8 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   int iters = 0;
   bool converged = false;
   for (int k = 1; k <= op.max_iters; ++k) {
+    // estimate mode once the potentials have settled past the first sweeps
+    S.est = allow_est && k >= kEstFromIter;
     if (!have_next) {
       if (int e = S.col_sweep(cur ^ 1, cur, kResNone)) return e;
       cur ^= 1;
@@ -629,6 +648,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   (void)converged;
   if (timed) CK(cudaEventRecord(ev1, st));
   // ---- tail: residual + stable E0 in one column pass (batch.py:323-337) ----
+  S.est = allow_est && iters >= kEstFromIter;
   if (int e = S.tail(cur)) return e;
   {
     const int nb = (int)((pr.B + 31) / 32);
@@ -652,6 +672,19 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   if (out_iterations) *out_iterations = iters;
   int hstatus = 0;
   if (int e = S.read_status(&hstatus)) return e;
+  if (allow_est && L.tiled) {
+    int hfail = 0;
+    CK(cudaMemcpy(&hfail, S.est_fail, 4, cudaMemcpyDeviceToHost));
+    if (hfail) {   // an estimate overshot: recompute the whole solve exactly
+      ++g_exact_reruns;
+      if (timed) {
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+      }
+      return forward_impl(pr, op, mu, nu, cost, out_cost, out_log_u, out_log_v, out_iterations,
+                          out_residuals, ws, ws_bytes, st, false);
+    }
+  }
   if (timed) {
     float ms = -1.f;
     cudaEventElapsedTime(&ms, ev0, ev1);
@@ -682,6 +715,8 @@ const char* sinkhorn_version(void) { return "paper_1907_01729_b200 0.1.0 sm_100a
 
 unsigned long long sinkhorn_launch_count_v1(void) { return g_launches; }
 
+unsigned long long sinkhorn_exact_reruns_v1(void) { return g_exact_reruns; }
+
 float sinkhorn_last_loop_ms_v1(void) { return g_last_loop_ms; }
 
 size_t sinkhorn_workspace_bytes_v1(const sinkhorn_problem_v1* prob) {
@@ -708,7 +743,8 @@ int32_t sinkhorn_forward_device_v1(const sinkhorn_problem_v1* prob,
     return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
   return forward_impl(*prob, *opt, mu, nu, cost, out_cost, out_log_u, out_log_v, out_iterations,
                       out_residuals, workspace, workspace_bytes,
-                      static_cast<cudaStream_t>(stream));
+                      static_cast<cudaStream_t>(stream),
+                      (opt->flags & SINKHORN_FLAG_EXACT_MAX) == 0);
 }
 
 

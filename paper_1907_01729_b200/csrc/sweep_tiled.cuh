@@ -30,6 +30,8 @@
 
 #include "common.cuh"
 
+#include <type_traits>
+
 namespace skb {
 
 
@@ -55,7 +57,20 @@ struct TiledSweepParams {
   int gnx;
   float gk, ghx2, ghy2;
   unsigned long long* dbg;   // optional per-CTA timing records (diagnostics), nullable
+  // Estimate mode: start every output's running max at the previous iteration's
+  // log-sum-exp, target - est_old, and reduce each chunk in one pass.
+  const float* est_old;      // output-side potentials before this sweep (nullable)
+  int use_est;
+  int* est_fail;             // set when an estimate was > kEstSlack above the result
 };
+
+// One-pass chunks tolerate terms up to 2^kRedo above the running max (no fp32
+// overflow for <= 2^20 terms); beyond that the warp redoes the chunk exactly.
+constexpr float kRedo = 100.f;
+// An estimate more than this above the final lse could have flushed
+// significant terms: flag it and the host reruns the solve in exact mode.
+constexpr float kEstSlack = 100.f;
+constexpr float kParked = 1.0e30f;   // running max of outputs whose target is -inf
 
 template <int BT, int PT, int QC, int RB, int RP, int NSTAGE, bool kGrid, int kMode>
 struct TiledSweep {
@@ -121,6 +136,17 @@ __device__ __forceinline__ void tile_epilogue(const TiledSweepParams& p, int tid
       if (kMode == kModeUpdate) {
         const float4 tg = *reinterpret_cast<const float4*>(p.target + row);
         const float tv[4] = {tg.x, tg.y, tg.z, tg.w};
+        if (p.use_est) {
+          const float4 eo = *reinterpret_cast<const float4*>(p.est_old + row);
+          const float ev[4] = {eo.x, eo.y, eo.z, eo.w};
+          bool bad = false;
+#pragma unroll
+          for (int rb = 0; rb < RB; ++rb) {
+            const float est = tv[rb] - ev[rb];
+            if (tv[rb] != neg_inf() && isfinite(est) && !(lse[rb] >= est - kEstSlack)) bad = true;
+          }
+          if (bad) atomicOr(p.est_fail, 1);
+        }
         float ov[4];
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) ov[rb] = sweep_out(tv[rb], lse[rb]);
@@ -319,104 +345,165 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
     // a warp covers 2 output groups; skip it only if both are past Pv (uniform)
     const bool warp_active = __any_sync(0xffffffffu, (p0 + tp * RP) < p.Pv);
     if (warp_active) {
+      if (p.use_est && (l == 0 || qc == 0)) {
+        // segment start: running max := previous lse (target - old); outputs
+        // with a -inf target never need their lse and are parked
+#pragma unroll
+        for (int rp = 0; rp < RP; ++rp) {
+          const int pp = min(p0 + tp * RP + rp, p.Pv - 1);
+          const size_t row = size_t(pp) * p.Bp + b0 + tb * RB;
+          const float4 tg = __ldg(reinterpret_cast<const float4*>(p.target + row));
+          const float4 eo = *reinterpret_cast<const float4*>(p.est_old + row);
+          const float tv[4] = {tg.x, tg.y, tg.z, tg.w};
+          const float ev[4] = {eo.x, eo.y, eo.z, eo.w};
+#pragma unroll
+          for (int rb = 0; rb < RB; ++rb) {
+            const float est = tv[rb] - ev[rb];
+            M[rb * RP + rp] = (tv[rb] == neg_inf()) ? kParked : (isfinite(est) ? est : kNegBig);
+          }
+        }
+      }
       // Outputs are handled in lane pairs (rb = 2h, 2h+1) so every add is a
       // packed FADD2 with the cost value broadcast: o = (2h + e) * RP + rp.
-      // phase 1: exact max of this chunk, 2 rows per FMNMX3 (1 instr / cell)
-      float cm[NOUT];
-#pragma unroll
-      for (int o = 0; o < NOUT; ++o) cm[o] = kNegBig;
-      const int k_pairs_end = k_lo + ((k_hi - k_lo) & ~1);
-#pragma unroll 2
-      for (int k = k_lo; k < k_pairs_end; k += 2) {
-        const float4 ga = *reinterpret_cast<const float4*>(Gs + k * PT + tp * RP);
-        const float4 gb = *reinterpret_cast<const float4*>(Gs + (k + 1) * PT + tp * RP);
-        const float4 xa = *reinterpret_cast<const float4*>(Xs + k * BT + tb * RB);
-        const float4 xb = *reinterpret_cast<const float4*>(Xs + (k + 1) * BT + tb * RB);
-        const float gav[4] = {ga.x, ga.y, ga.z, ga.w};
-        const float gbv[4] = {gb.x, gb.y, gb.z, gb.w};
-        const uint64_t xa2[2] = {pk2(xa.x, xa.y), pk2(xa.z, xa.w)};
-        const uint64_t xb2[2] = {pk2(xb.x, xb.y), pk2(xb.z, xb.w)};
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int rp = 0; rp < RP; ++rp) {
-            const uint64_t ta = fadd2(xa2[h], pk2(gav[rp], gav[rp]));
-            const uint64_t tb2 = fadd2(xb2[h], pk2(gbv[rp], gbv[rp]));
-            const int o0 = (2 * h) * RP + rp, o1 = (2 * h + 1) * RP + rp;
-            cm[o0] = fmax3(cm[o0], lo2(ta), lo2(tb2));
-            cm[o1] = fmax3(cm[o1], hi2(ta), hi2(tb2));
-          }
-      }
-      if (k_pairs_end < k_hi) {   // odd row at a CTA boundary
-        const int k = k_pairs_end;
-        const float4 ga = *reinterpret_cast<const float4*>(Gs + k * PT + tp * RP);
-        const float4 xa = *reinterpret_cast<const float4*>(Xs + k * BT + tb * RB);
-        const float gav[4] = {ga.x, ga.y, ga.z, ga.w};
-        const float xav[4] = {xa.x, xa.y, xa.z, xa.w};
-#pragma unroll
-        for (int rb = 0; rb < RB; ++rb)
-#pragma unroll
-          for (int rp = 0; rp < RP; ++rp)
-            cm[rb * RP + rp] = fmaxf(cm[rb * RP + rp], gav[rp] + xav[rb]);
-      }
-      // phase 2: lazy online rescale (batch.py:98-105), warp-uniform so the
-      // branch never diverges; the running max only moves when a chunk beats
-      // it by more than kLazy, i.e. rarely after the first chunks.
-#pragma unroll
-      for (int o = 0; o < NOUT; ++o) {
-        if (__any_sync(0xffffffffu, cm[o] > M[o] + kLazy)) {
-          const float mn = fmaxf(M[o], cm[o]);
-          const float r = ex2(M[o] - mn);
-          Sm[o] *= r;
-          if (kMode == kModeTail) S2[o] *= r;
-          M[o] = mn;
-        }
-      }
+      uint64_t acc[2][RP], acc2[2][RP];
       // phase 3: one ex2 per cell; packed adds for t = g + x, t - M and the
       // chunk-local sums (which keep the fp32 error ~ sqrt(Q/QC))
-      uint64_t nM[2][RP], acc[2][RP], acc2[2][RP];
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int rp = 0; rp < RP; ++rp) {
-          nM[h][rp] = pk2(-M[(2 * h) * RP + rp], -M[(2 * h + 1) * RP + rp]);
-          acc[h][rp] = 0ull;
-          acc2[h][rp] = 0ull;
-        }
-#pragma unroll 4
-      for (int k = k_lo; k < k_hi; ++k) {
-        const float4 gv = *reinterpret_cast<const float4*>(Gs + k * PT + tp * RP);
-        const float4 xv = *reinterpret_cast<const float4*>(Xs + k * BT + tb * RB);
-        const float g[4] = {gv.x, gv.y, gv.z, gv.w};
-        const uint64_t x2[2] = {pk2(xv.x, xv.y), pk2(xv.z, xv.w)};
-        float cw[4];
-        if (kMode == kModeTail) {
-          // c = G * cinv; padding rows (G = -inf) must weigh 0, not +inf
-#pragma unroll
-          for (int rp = 0; rp < RP; ++rp) cw[rp] = (g[rp] == neg_inf()) ? 0.f : g[rp] * p.cinv;
-        }
+      auto phase3 = [&]() {
+        uint64_t nM[2][RP];
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int rp = 0; rp < RP; ++rp) {
-            const uint64_t a = fadd2(fadd2(x2[h], pk2(g[rp], g[rp])), nM[h][rp]);
-            const uint64_t e = pk2(ex2(lo2(a)), ex2(hi2(a)));
-            acc[h][rp] = fadd2(acc[h][rp], e);
-            if (kMode == kModeTail) acc2[h][rp] = ffma2(e, pk2(cw[rp], cw[rp]), acc2[h][rp]);
+            nM[h][rp] = pk2(-M[(2 * h) * RP + rp], -M[(2 * h + 1) * RP + rp]);
+            acc[h][rp] = 0ull;
+            acc2[h][rp] = 0ull;
           }
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int rp = 0; rp < RP; ++rp) {
-          const int o0 = (2 * h) * RP + rp, o1 = (2 * h + 1) * RP + rp;
-          Sm[o0] += lo2(acc[h][rp]);
-          Sm[o1] += hi2(acc[h][rp]);
+#pragma unroll 4
+        for (int k = k_lo; k < k_hi; ++k) {
+          const float4 gv = *reinterpret_cast<const float4*>(Gs + k * PT + tp * RP);
+          const float4 xv = *reinterpret_cast<const float4*>(Xs + k * BT + tb * RB);
+          const float g[4] = {gv.x, gv.y, gv.z, gv.w};
+          const uint64_t x2[2] = {pk2(xv.x, xv.y), pk2(xv.z, xv.w)};
+          float cw[4];
           if (kMode == kModeTail) {
-            S2[o0] += lo2(acc2[h][rp]);
-            S2[o1] += hi2(acc2[h][rp]);
+            // c = G * cinv; padding rows (G = -inf) must weigh 0, not +inf
+#pragma unroll
+            for (int rp = 0; rp < RP; ++rp) cw[rp] = (g[rp] == neg_inf()) ? 0.f : g[rp] * p.cinv;
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int rp = 0; rp < RP; ++rp) {
+              const uint64_t a = fadd2(fadd2(x2[h], pk2(g[rp], g[rp])), nM[h][rp]);
+              const uint64_t e = pk2(ex2(lo2(a)), ex2(hi2(a)));
+              acc[h][rp] = fadd2(acc[h][rp], e);
+              if (kMode == kModeTail) acc2[h][rp] = ffma2(e, pk2(cw[rp], cw[rp]), acc2[h][rp]);
+            }
+        }
+      };
+      bool exact = !p.use_est;
+      if (!exact) {
+        phase3();
+        // A term above 2^kRedo (or inf/NaN) means the shift was too low for
+        // this chunk: discard it and redo the chunk exactly (warp-uniform).
+        bool ok = true;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int rp = 0; rp < RP; ++rp)
+            ok = ok && (lo2(acc[h][rp]) <= 0x1p100f) && (hi2(acc[h][rp]) <= 0x1p100f);
+        if (!__all_sync(0xffffffffu, ok)) {
+          exact = true;
+        } else {
+          // Fold the chunk in and renormalise the running sum by its own
+          // power-of-two exponent: exact scaling that keeps the shift M at
+          // the running lse (branch-free; no max pass needed).
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int rp = 0; rp < RP; ++rp)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int o = (2 * h + e) * RP + rp;
+                const float tot = Sm[o] + (e ? hi2(acc[h][rp]) : lo2(acc[h][rp]));
+                const int bits = __float_as_int(tot);
+                const int ex = ((bits >> 23) & 0xff);
+                const int sh = (ex == 0) ? 0 : ex - 127;            // 0 or denormal: keep
+                Sm[o] = __int_as_float(bits - (sh << 23));
+                if (kMode == kModeTail) {
+                  const float t2 = S2[o] + (e ? hi2(acc2[h][rp]) : lo2(acc2[h][rp]));
+                  S2[o] = ldexpf(t2, -sh);
+                }
+                M[o] += (float)sh;
+              }
+        }
+      }
+      if (exact) {
+        // phase 1: exact max of this chunk, 2 rows per FMNMX3 (1 instr / cell)
+        float cm[NOUT];
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) cm[o] = kNegBig;
+        const int k_pairs_end = k_lo + ((k_hi - k_lo) & ~1);
+#pragma unroll 2
+        for (int k = k_lo; k < k_pairs_end; k += 2) {
+          const float4 ga = *reinterpret_cast<const float4*>(Gs + k * PT + tp * RP);
+          const float4 gb = *reinterpret_cast<const float4*>(Gs + (k + 1) * PT + tp * RP);
+          const float4 xa = *reinterpret_cast<const float4*>(Xs + k * BT + tb * RB);
+          const float4 xb = *reinterpret_cast<const float4*>(Xs + (k + 1) * BT + tb * RB);
+          const float gav[4] = {ga.x, ga.y, ga.z, ga.w};
+          const float gbv[4] = {gb.x, gb.y, gb.z, gb.w};
+          const uint64_t xa2[2] = {pk2(xa.x, xa.y), pk2(xa.z, xa.w)};
+          const uint64_t xb2[2] = {pk2(xb.x, xb.y), pk2(xb.z, xb.w)};
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int rp = 0; rp < RP; ++rp) {
+              const uint64_t ta = fadd2(xa2[h], pk2(gav[rp], gav[rp]));
+              const uint64_t tb2 = fadd2(xb2[h], pk2(gbv[rp], gbv[rp]));
+              const int o0 = (2 * h) * RP + rp, o1 = (2 * h + 1) * RP + rp;
+              cm[o0] = fmax3(cm[o0], lo2(ta), lo2(tb2));
+              cm[o1] = fmax3(cm[o1], hi2(ta), hi2(tb2));
+            }
+        }
+        if (k_pairs_end < k_hi) {   // odd row at a CTA boundary
+          const int k = k_pairs_end;
+          const float4 ga = *reinterpret_cast<const float4*>(Gs + k * PT + tp * RP);
+          const float4 xa = *reinterpret_cast<const float4*>(Xs + k * BT + tb * RB);
+          const float gav[4] = {ga.x, ga.y, ga.z, ga.w};
+          const float xav[4] = {xa.x, xa.y, xa.z, xa.w};
+#pragma unroll
+          for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+            for (int rp = 0; rp < RP; ++rp)
+              cm[rb * RP + rp] = fmaxf(cm[rb * RP + rp], gav[rp] + xav[rb]);
+        }
+        // phase 2: lazy online rescale (batch.py:98-105), warp-uniform so the
+        // branch never diverges; the running max only moves when a chunk beats
+        // it by more than kLazy, i.e. rarely after the first chunks.
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) {
+          if (__any_sync(0xffffffffu, cm[o] > M[o] + kLazy)) {
+            const float mn = fmaxf(M[o], cm[o]);
+            const float r = ex2(M[o] - mn);
+            Sm[o] *= r;
+            if (kMode == kModeTail) S2[o] *= r;
+            M[o] = mn;
           }
         }
+        phase3();
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int rp = 0; rp < RP; ++rp) {
+            const int o0 = (2 * h) * RP + rp, o1 = (2 * h + 1) * RP + rp;
+            Sm[o0] += lo2(acc[h][rp]);
+            Sm[o1] += hi2(acc[h][rp]);
+            if (kMode == kModeTail) {
+              S2[o0] += lo2(acc2[h][rp]);
+              S2[o1] += hi2(acc2[h][rp]);
+            }
+          }
+      }
     }
     __syncthreads();   // every warp is done with stage s
     if (tid == 0 && l + NSTAGE < n_local) issue(l + NSTAGE);
@@ -473,14 +560,18 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
 template <int BT, int PT, int QC, int RB, int RP, int kMode>
 __global__ void __launch_bounds__(256) tiled_fixup_kernel(const TiledSweepParams p) {
   constexpr int NT = (BT / RB) * (PT / RP);   // the sweep's threads per tile
-  constexpr int NB = 256;                     // fixup threads per CTA (NT / NB CTAs per tile)
   constexpr int NOUT = RB * RP;
+  constexpr int NG = NOUT / 4;                // float4 groups per sweep thread (one per rb)
+  constexpr int NB = 256;                     // fixup threads per CTA
+  constexpr int CPT = NT * NG / NB;           // fixup CTAs per tile
   constexpr int NV = (kMode == kModeTail) ? 3 : 2;
-  constexpr int GRP = 4;                      // pieces whose loads are in flight together
+  constexpr int GRP = 8;                      // pieces whose loads are in flight together
+  static_assert(RP == 4, "one float4 group = the RP outputs of one lane");
   __shared__ float s_res[BT];
   pdl_wait();
-  const int tile = blockIdx.x / (NT / NB);
-  const int vtid = (blockIdx.x % (NT / NB)) * NB + threadIdx.x;   // the sweep thread mirrored
+  const int tile = blockIdx.x / CPT;
+  const int e = (blockIdx.x % CPT) * NB + threadIdx.x;   // float4 group within the tile
+  const int vtid = e / NG, rb = e % NG;                  // mirrored sweep thread, its lane
   const long long Qv = p.Qv;
   const long long t_first = (long long)tile * Qv;
   const long long c_lo = atom_owner(p, t_first);
@@ -489,50 +580,90 @@ __global__ void __launch_bounds__(256) tiled_fixup_kernel(const TiledSweepParams
   int tb, tp;
   thread_map<BT, RB, NT>(vtid, tb, tp);
   const int tb_idx = tile % p.ntile_b, tp_idx = tile / p.ntile_b;
-  const int b0 = tb_idx * BT;
+  const int b = tb_idx * BT + tb * RB + rb;
   const int p0 = (tp_idx == p.ntile_p - 1) ? max(p.Pv - PT, 0) : tp_idx * PT;
   const int own_lo = tp_idx * PT;
-  float M[NOUT], Sm[NOUT], S2[NOUT];
+  float M[4], Sm[4], S2[4];
 #pragma unroll
-  for (int o = 0; o < NOUT; ++o) {
-    M[o] = kNegBig;
-    Sm[o] = 0.f;
-    S2[o] = 0.f;
+  for (int r = 0; r < 4; ++r) {
+    M[r] = kNegBig;
+    Sm[r] = 0.f;
+    S2[r] = 0.f;
   }
 #pragma unroll 1
   for (long long c0 = c_lo; c0 <= c_hi; c0 += GRP) {
-    float4 mv[GRP][NOUT / 4], sv[GRP][NOUT / 4], tv[GRP][NOUT / 4];
+    float4 mv[GRP], sv[GRP], tv[GRP];
 #pragma unroll
     for (int g = 0; g < GRP; ++g) {
       const long long cc = c0 + g;
       if (cc > c_hi) break;
       const int sl = (atom_begin(p, cc) >= t_first) ? 0 : 1;
-      const float* src = p.part + ((cc * 2 + sl) * NV) * (size_t)(BT * PT) + vtid * NOUT;
-#pragma unroll
-      for (int j = 0; j < NOUT / 4; ++j) {
-        mv[g][j] = __ldcg(reinterpret_cast<const float4*>(src) + j);
-        sv[g][j] = __ldcg(reinterpret_cast<const float4*>(src + BT * PT) + j);
-        if (NV == 3) tv[g][j] = __ldcg(reinterpret_cast<const float4*>(src + 2 * BT * PT) + j);
-      }
+      const float* src = p.part + ((cc * 2 + sl) * NV) * (size_t)(BT * PT) + vtid * NOUT + rb * 4;
+      mv[g] = __ldcg(reinterpret_cast<const float4*>(src));
+      sv[g] = __ldcg(reinterpret_cast<const float4*>(src + BT * PT));
+      if (NV == 3) tv[g] = __ldcg(reinterpret_cast<const float4*>(src + 2 * BT * PT));
     }
 #pragma unroll
     for (int g = 0; g < GRP; ++g) {
       if (c0 + g > c_hi) break;   // ascending piece order (batch.py:198-201)
+      const float* m2 = reinterpret_cast<const float*>(&mv[g]);
+      const float* s2 = reinterpret_cast<const float*>(&sv[g]);
+      const float* t2 = reinterpret_cast<const float*>(&tv[g]);
 #pragma unroll
-      for (int o = 0; o < NOUT; ++o) {
-        const float m2 = reinterpret_cast<const float*>(&mv[g][o / 4])[o % 4];
-        const float s2v = reinterpret_cast<const float*>(&sv[g][o / 4])[o % 4];
-        const float mn = fmaxf(M[o], m2);
-        const float ra = ex2(M[o] - mn), rb2 = ex2(m2 - mn);
-        Sm[o] = Sm[o] * ra + s2v * rb2;
-        if (NV == 3)
-          S2[o] = S2[o] * ra + reinterpret_cast<const float*>(&tv[g][o / 4])[o % 4] * rb2;
-        M[o] = mn;
+      for (int r = 0; r < 4; ++r) {
+        const float mn = fmaxf(M[r], m2[r]);
+        const float ra = ex2(M[r] - mn), rb2 = ex2(m2[r] - mn);
+        Sm[r] = Sm[r] * ra + s2[r] * rb2;
+        if (NV == 3) S2[r] = S2[r] * ra + t2[r] * rb2;
+        M[r] = mn;
       }
     }
   }
-  tile_epilogue<BT, PT, RB, RP, NB, kMode>(p, threadIdx.x, tb, tp, b0, p0, own_lo, M, Sm, S2,
-                                           s_res);
+  // epilogue for lane b, outputs p0 + tp*RP + r
+  const bool want_res = p.res != nullptr && (kMode == kModeTail || p.res_kind != kResNone);
+  if (want_res) {
+    for (int i = threadIdx.x; i < BT; i += NB) s_res[i] = 0.f;
+    __syncthreads();
+  }
+  float rmax = 0.f;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int pp = p0 + tp * RP + r;
+    if (pp >= p.Pv || pp < own_lo) continue;
+    const size_t o = size_t(pp) * p.Bp + b;
+    if (kMode == kModePartial) {
+      p.pmax[o] = M[r];
+      p.psum[o] = Sm[r];
+      continue;
+    }
+    const float lse = lse_final(M[r], Sm[r]);
+    if (kMode == kModeUpdate) {
+      const float tg = p.target[o];
+      if (p.use_est) {
+        const float est = tg - p.est_old[o];
+        if (tg != neg_inf() && isfinite(est) && !(lse >= est - kEstSlack)) atomicOr(p.est_fail, 1);
+      }
+      const float ov = sweep_out(tg, lse);
+      p.out[o] = ov;
+      if (want_res) {
+        const float base = (p.res_kind == kResCol) ? p.old[o] : ov;
+        rmax = fmaxf(rmax, fabsf(exp2f(base + lse) - p.marg[o]));
+      }
+    } else {   // TAIL
+      const float od = p.old[o];
+      p.e0[o] = (S2[r] > 0.f) ? (M[r] + log2f(S2[r]) + od) : neg_inf();
+      rmax = fmaxf(rmax, fabsf(exp2f(od + lse) - p.marg[o]));
+    }
+  }
+  if (want_res) {
+    const float v = (rmax != rmax) ? __int_as_float(0x7fc00000) : rmax;
+    atomic_max_nonneg(&s_res[b - tb_idx * BT], v);
+    __syncthreads();
+    for (int i = threadIdx.x; i < BT; i += NB) {
+      const float rv = s_res[i];
+      if (rv != 0.f) atomic_max_nonneg(&p.res[tb_idx * BT + i], rv);
+    }
+  }
   pdl_launch_dependents();
 }
 

@@ -161,3 +161,23 @@ def test_autograd_node_matches_reference_gradients(cuda):
     assert np.abs(nu.grad.double().cpu().numpy() - g["grad_nu"]).max() <= GRAD_ATOL
     # each lane's gradient is mean-zero (loss.test.ts:124-151)
     assert torch.allclose(mu.grad.sum(dim=1), torch.zeros(mu.shape[0], device=cuda), atol=1e-5)
+
+
+@pytest.mark.parametrize("name", ["config2_subset", "stability", "zero_mass"])
+def test_estimate_mode_matches_exact_two_pass(name, cuda):
+    """The one-pass chunks seeded by the previous lse (estimate mode) and the
+    exact two-pass chunks agree to fp32 rounding."""
+    skb = _skb()
+    g = load_golden(name)
+    c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
+    args = (torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
+            float(g["lam"]), int(g["max_iters"]), float(g["tol"]), int(g["check_interval"]))
+    fast = skb.solve(*args)
+    exact = skb.solve(*args, exact_max=True)
+    assert fast.iterations_run == exact.iterations_run
+    rel = (fast.cost_e0.double() - exact.cost_e0.double()).abs() / exact.cost_e0.double().abs()
+    assert float(rel.max()) <= 2e-6
+    fin = torch.isfinite(exact.log_u)
+    assert torch.equal(fin, torch.isfinite(fast.log_u))
+    scale = max(1.0, float(exact.log_u[fin].abs().max()))
+    assert float((fast.log_u[fin] - exact.log_u[fin]).abs().max()) <= 2e-5 * scale
