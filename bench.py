@@ -344,6 +344,7 @@ def run_ours(args, cfg, world, rank, local):
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     ms = sum(step_ms) / len(step_ms)
+    step_stats = {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)}
     sweep_ms = statistics.median(loop_ms) / (2 * iters)
     t = torch.tensor([ms, sweep_ms], device=dev, dtype=torch.float64)
     if world > 1:
@@ -374,6 +375,7 @@ def run_ours(args, cfg, world, rank, local):
                 "d2h_bytes_per_step": e2e["d2h"], "path": e2e["path"]},
         "gpu_launches": int(launches),
         "clocks": clocks,
+        "step_ms_stats": step_stats,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference_sample(cfg)

@@ -31,6 +31,7 @@ COST_GRID2D = 2
 FLAG_SKIP_VALIDATION = 1
 FLAG_TIME_LOOP = 4
 FLAG_EXACT_MAX = 8
+FLAG_MUFU_ONLY = 16
 
 # every symbol include/sinkhorn_b200.h declares
 EXPORTED_SYMBOLS = (
@@ -130,7 +131,7 @@ def load():
     with _lock:
         if _lib is not None:
             return _lib
-        path = lib_path()
+        path = os.environ.get("SINKHORN_B200_LIB") or lib_path()   # override: experiments
         if not os.path.exists(path):
             raise ImportError(
                 f"{path} is missing: the B200 kernels are not built. "

@@ -67,6 +67,36 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
+// 2^a for a pair on the FMA pipe (FADD2/FFMA2 + integer exponent add), so a
+// share of the exponentials bypasses the 16/clk/SM MUFU (FlashAttention-4's
+// trick).  Degree-5 near-minimax polynomial on [-0.5, 0.5]: max relative
+// error 2.1e-7 in fp32, on par with ex2.approx.  Inputs below -126 return a
+// value <= 2^-126 (not exactly 0): only used where such terms are negligible
+// against a running sum near 1 (the solver's sweeps, not the empty-reduction
+// half-sweep API).
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b);
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c);
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t a) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
+  const uint64_t x = pk2(fmaxf(lo, -126.f), fmaxf(hi, -126.f));
+  const uint64_t t = fadd2(x, pk2(12582912.f, 12582912.f));        // 1.5 * 2^23: round
+  const uint64_t j = fadd2(t, pk2(-12582912.f, -12582912.f));      // nearest integer
+  const uint64_t f = ffma2(j, pk2(-1.f, -1.f), x);                  // x - j in [-1/2, 1/2]
+  uint64_t p = ffma2(pk2(1.3276466634124517e-3f, 1.3276466634124517e-3f), f,
+                     pk2(9.675540961325169e-3f, 9.675540961325169e-3f));
+  p = ffma2(p, f, pk2(5.550713464617729e-2f, 5.550713464617729e-2f));
+  p = ffma2(p, f, pk2(2.4022120237350464e-1f, 2.4022120237350464e-1f));
+  p = ffma2(p, f, pk2(6.931469440460205e-1f, 6.931469440460205e-1f));
+  p = ffma2(p, f, pk2(1.0000001192092896f, 1.0000001192092896f));
+  // times 2^j: the integer j sits in t's low mantissa bits, so t << 23 is j << 23
+  float p0, p1, t0, t1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(p0), "=f"(p1) : "l"(p));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(t0), "=f"(t1) : "l"(t));
+  return pk2(__uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23)),
+             __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23)));
+}
+
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));

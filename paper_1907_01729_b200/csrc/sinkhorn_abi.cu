@@ -273,6 +273,7 @@ struct TiledArgs {
   const float* est_old = nullptr;   // estimate mode: output-side potentials before the sweep
   int use_est = 0;
   int* est_fail = nullptr;
+  int use_poly = 0;                 // FMA-pipe exponentials for part of the cells
 };
 
 template <int BT, int PT, bool kGrid, int kMode>
@@ -303,6 +304,7 @@ int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const Tiled
   p.est_old = a.est_old;
   p.use_est = (a.use_est && a.est_old != nullptr) ? 1 : 0;
   p.est_fail = a.est_fail;
+  p.use_poly = a.use_poly;
   p.part = at<float>(ws, L.part);
   p.counters = at<int>(ws, L.counters);
   p.cinv = -lam * kLn2;
@@ -364,6 +366,7 @@ struct Solve {
   CUtensorMap tm_a2, tm_a2t, tm_f2, tm_g2[2];
   const float* cost;
   bool est = false;        // estimate mode for the tiled sweeps (set per iteration)
+  bool poly = true;        // FMA-pipe polynomial exponentials for part of the cells
   int* est_fail = nullptr;
 
   float* F(size_t off) const { return at<float>(ws, off); }
@@ -394,7 +397,7 @@ struct Solve {
     if (L.tiled) {
       TiledArgs a = {&tm_a2, &tm_f2, (int)pr.d1, (int)pr.d2, L.D1p, L.D2p, F(L.l2nu), F(L.nu),
                      F(L.g2[dst]), F(L.g2[src_old]), F(L.res), res_kind, nullptr, nullptr,
-                     nullptr, F(L.g2[src_old]), est ? 1 : 0, est_fail};
+                     nullptr, F(L.g2[src_old]), est ? 1 : 0, est_fail, poly ? 1 : 0};
       return pr.cost_kind == SINKHORN_COST_GRID2D
                  ? launch_tiled<true, kModeUpdate>(L, ws, di, a, pr, lam, st)
                  : launch_tiled<false, kModeUpdate>(L, ws, di, a, pr, lam, st);
@@ -407,7 +410,7 @@ struct Solve {
     if (L.tiled) {
       TiledArgs a = {&tm_a2t, &tm_g2[src], (int)pr.d2, (int)pr.d1, L.D2p, L.D1p, F(L.l2mu),
                      F(L.mu), F(L.f2), nullptr, F(L.res), res_kind, nullptr, nullptr, nullptr,
-                     F(L.f2), est ? 1 : 0, est_fail};
+                     F(L.f2), est ? 1 : 0, est_fail, poly ? 1 : 0};
       return pr.cost_kind == SINKHORN_COST_GRID2D
                  ? launch_tiled<true, kModeUpdate>(L, ws, di, a, pr, lam, st)
                  : launch_tiled<false, kModeUpdate>(L, ws, di, a, pr, lam, st);
@@ -435,7 +438,7 @@ struct Solve {
     if (L.tiled) {
       TiledArgs a = {&tm_a2, &tm_f2, (int)pr.d1, (int)pr.d2, L.D1p, L.D2p, F(L.l2nu), F(L.nu),
                      nullptr, F(L.g2[cur]), F(L.res), kResCol, F(L.e0), nullptr, nullptr,
-                     F(L.g2[cur]), est ? 1 : 0, est_fail};
+                     F(L.g2[cur]), est ? 1 : 0, est_fail, poly ? 1 : 0};
       return pr.cost_kind == SINKHORN_COST_GRID2D
                  ? launch_tiled<true, kModeTail>(L, ws, di, a, pr, lam, st)
                  : launch_tiled<false, kModeTail>(L, ws, di, a, pr, lam, st);
@@ -544,6 +547,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   S.st = st;
   S.lam = (float)op.lambda;
   S.cost = cost;
+  S.poly = (op.flags & SINKHORN_FLAG_MUFU_ONLY) == 0;
   const Layout& L = S.L;
   if (ws_bytes < L.total || ws == nullptr)
     return fail(SINKHORN_STATUS_WORKSPACE, "workspace too small");

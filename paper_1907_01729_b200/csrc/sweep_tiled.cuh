@@ -61,6 +61,7 @@ struct TiledSweepParams {
   // log-sum-exp, target - est_old, and reduce each chunk in one pass.
   const float* est_old;      // output-side potentials before this sweep (nullable)
   int use_est;
+  int use_poly;              // route kPolyPairs of the 8 output pairs through ex2_poly2
   int* est_fail;             // set when an estimate was > kEstSlack above the result
 };
 
@@ -71,6 +72,11 @@ constexpr float kRedo = 100.f;
 // significant terms: flag it and the host reruns the solve in exact mode.
 constexpr float kEstSlack = 100.f;
 constexpr float kParked = 1.0e30f;   // running max of outputs whose target is -inf
+// Output pairs (of 8 per thread) whose exponentials run on the FMA pipe.
+#ifndef SKB_POLY_PAIRS
+#define SKB_POLY_PAIRS 2
+#endif
+constexpr int kPolyPairs = SKB_POLY_PAIRS;
 
 template <int BT, int PT, int QC, int RB, int RP, int NSTAGE, bool kGrid, int kMode>
 struct TiledSweep {
@@ -368,7 +374,8 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
       uint64_t acc[2][RP], acc2[2][RP];
       // phase 3: one ex2 per cell; packed adds for t = g + x, t - M and the
       // chunk-local sums (which keep the fp32 error ~ sqrt(Q/QC))
-      auto phase3 = [&]() {
+      auto phase3 = [&](auto poly) {
+        constexpr bool kPoly = decltype(poly)::value;
         uint64_t nM[2][RP];
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -395,7 +402,9 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
 #pragma unroll
             for (int rp = 0; rp < RP; ++rp) {
               const uint64_t a = fadd2(fadd2(x2[h], pk2(g[rp], g[rp])), nM[h][rp]);
-              const uint64_t e = pk2(ex2(lo2(a)), ex2(hi2(a)));
+              const uint64_t e = (kPoly && h * RP + rp < kPolyPairs)
+                                     ? ex2_poly2(a)
+                                     : pk2(ex2(lo2(a)), ex2(hi2(a)));
               acc[h][rp] = fadd2(acc[h][rp], e);
               if (kMode == kModeTail) acc2[h][rp] = ffma2(e, pk2(cw[rp], cw[rp]), acc2[h][rp]);
             }
@@ -403,7 +412,7 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
       };
       bool exact = !p.use_est;
       if (!exact) {
-        phase3();
+        if (p.use_poly) phase3(std::true_type{}); else phase3(std::false_type{});
         // A term above 2^kRedo (or inf/NaN) means the shift was too low for
         // this chunk: discard it and redo the chunk exactly (warp-uniform).
         bool ok = true;
@@ -490,7 +499,7 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
             M[o] = mn;
           }
         }
-        phase3();
+        if (p.use_poly) phase3(std::true_type{}); else phase3(std::false_type{});
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll

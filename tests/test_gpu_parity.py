@@ -181,3 +181,19 @@ def test_estimate_mode_matches_exact_two_pass(name, cuda):
     assert torch.equal(fin, torch.isfinite(fast.log_u))
     scale = max(1.0, float(exact.log_u[fin].abs().max()))
     assert float((fast.log_u[fin] - exact.log_u[fin]).abs().max()) <= 2e-5 * scale
+
+
+@pytest.mark.parametrize("name", ["config2_subset", "config5_pin4096"])
+def test_polynomial_exp2_share_matches_mufu_only(name, cuda):
+    """Part of the exponentials run as an FMA-pipe polynomial (ex2_poly2); the
+    result must match the all-MUFU path to fp32 rounding."""
+    skb = _skb()
+    g = load_golden(name)
+    c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
+    args = (torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
+            float(g["lam"]), int(g["max_iters"]), float(g["tol"]), int(g["check_interval"]))
+    poly = skb.solve(*args)
+    mufu = skb.solve(*args, mufu_only=True)
+    rel = (poly.cost_e0.double() - mufu.cost_e0.double()).abs() / mufu.cost_e0.double().abs()
+    assert float(rel.max()) <= 2e-6
+    _check_loss_and_grads(g, poly)
