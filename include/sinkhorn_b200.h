@@ -94,6 +94,7 @@ typedef struct sinkhorn_problem_v1 {
 #define SINKHORN_FLAG_TIME_LOOP 4u       /* record CUDA events around the iteration loop */
 #define SINKHORN_FLAG_EXACT_MAX 8u       /* always two-pass chunks (no previous-lse estimate) */
 #define SINKHORN_FLAG_MUFU_ONLY 16u      /* every exponential on MUFU (no FMA-pipe polynomial) */
+#define SINKHORN_FLAG_PERSISTENT 32u     /* shared/grid costs: whole loop in one cooperative kernel */
 
 typedef struct sinkhorn_options_v1 {
   double lambda;          /* > 0, finite */

@@ -32,6 +32,7 @@ FLAG_SKIP_VALIDATION = 1
 FLAG_TIME_LOOP = 4
 FLAG_EXACT_MAX = 8
 FLAG_MUFU_ONLY = 16
+FLAG_PERSISTENT = 32
 
 # every symbol include/sinkhorn_b200.h declares
 EXPORTED_SYMBOLS = (

@@ -24,6 +24,7 @@
 #include "common.cuh"
 #include "sweep_lane.cuh"
 #include "sweep_tiled.cuh"
+#include "persistent.cuh"
 
 using namespace skb;
 
@@ -276,10 +277,9 @@ struct TiledArgs {
   int use_poly = 0;                 // FMA-pipe exponentials for part of the cells
 };
 
-template <int BT, int PT, bool kGrid, int kMode>
-int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const TiledArgs& a,
-                    const sinkhorn_problem_v1& pr, float lam, cudaStream_t st) {
-  using K = TiledK<BT, PT, kGrid, kMode>;
+template <int BT, int PT>
+TiledSweepParams build_tiled_params(const Layout& L, void* ws, const TiledArgs& a,
+                                    const sinkhorn_problem_v1& pr, float lam, int G) {
   TiledSweepParams p = {};
   p.Qv = a.Qv;
   p.Pv = a.Pv;
@@ -288,10 +288,7 @@ int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const Tiled
   p.ntile_p = (a.Pv + PT - 1) / PT;
   p.nq = (a.Qv + QC - 1) / QC;
   p.W = (long long)p.ntile_b * p.ntile_p * a.Qv;   // stream-K over reduction rows
-  const long long W = (long long)p.ntile_b * p.ntile_p * p.nq;   // chunks: cap on the grid
-  const size_t smem = K::S::SMEM_BYTES;
-  const int occ = std::min(K::S::OCC, occupancy_tiled(K::fn(), K::S::NT, smem));
-  p.G = (int)std::min<long long>(W, (long long)di.sms * occ);
+  p.G = G;
   p.target = a.target;
   p.marg = a.marg;
   p.out = a.out;
@@ -301,10 +298,6 @@ int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const Tiled
   p.e0 = a.e0;
   p.pmax = a.pmax;
   p.psum = a.psum;
-  p.est_old = a.est_old;
-  p.use_est = (a.use_est && a.est_old != nullptr) ? 1 : 0;
-  p.est_fail = a.est_fail;
-  p.use_poly = a.use_poly;
   p.part = at<float>(ws, L.part);
   p.counters = at<int>(ws, L.counters);
   p.cinv = -lam * kLn2;
@@ -312,38 +305,34 @@ int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const Tiled
   p.gnx = pr.grid_nx;
   p.ghx2 = pr.grid_hx * pr.grid_hx;
   p.ghy2 = pr.grid_hy * pr.grid_hy;
+  p.est_old = a.est_old;
+  p.use_est = (a.use_est && a.est_old != nullptr) ? 1 : 0;
+  p.est_fail = a.est_fail;
+  p.use_poly = a.use_poly;
+  p.dbg = nullptr;
+  return p;
+}
+
+// chunks of the (tile, q) space: every CTA of a sweep must own >= 1 row
+template <int BT, int PT>
+long long tiled_chunks(const Layout& L, int Pv, int Qv) {
+  return (long long)(L.Bp / BT) * ((Pv + PT - 1) / PT) * ((Qv + QC - 1) / QC);
+}
+
+template <int BT, int PT, bool kGrid, int kMode>
+int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const TiledArgs& a,
+                    const sinkhorn_problem_v1& pr, float lam, cudaStream_t st) {
+  using K = TiledK<BT, PT, kGrid, kMode>;
+  const size_t smem = K::S::SMEM_BYTES;
+  const int occ = std::min(K::S::OCC, occupancy_tiled(K::fn(), K::S::NT, smem));
+  const int G = (int)std::min<long long>(tiled_chunks<BT, PT>(L, a.Pv, a.Qv), (long long)di.sms * occ);
+  TiledSweepParams p = build_tiled_params<BT, PT>(L, ws, a, pr, lam, G);
   auto kern = &tiled_sweep_kernel<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>;
-  // Diagnostics: SKB_DEBUG_TIMING=<n> dumps per-CTA timing of the n-th tiled launch.
-  static long long dbg_count = 0;
-  static const char* dbg_env = getenv("SKB_DEBUG_TIMING");
-  unsigned long long* dbg = nullptr;
-  const bool dump = dbg_env && (++dbg_count == atoll(dbg_env));
-  if (dump) cudaMallocAsync(reinterpret_cast<void**>(&dbg), (size_t)p.G * 32, st);
-  p.dbg = dbg;
   CK(launch_pdl(kern, dim3(p.G), dim3(K::S::NT), smem, st, *a.tg, *a.tx, p));
   // merge + epilogue of the tiles the stream-K split cut between CTAs
-  static const bool no_fixup = getenv("SKB_DIAG_NO_FIXUP") != nullptr;   // timing experiments only
-  if (!no_fixup)
   CK(launch_pdl(&tiled_fixup_kernel<BT, PT, QC, RB, RP, kMode>,
                 dim3((unsigned)(p.ntile_b * p.ntile_p * (K::S::NT * 4 / 256))), dim3(256), 0,
                 st, p));
-  if (dump) {
-    std::vector<unsigned long long> h((size_t)p.G * 4);
-    cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    cudaFreeAsync(dbg, st);
-    unsigned long long t0 = ~0ull;
-    for (int i = 0; i < p.G; ++i) t0 = std::min(t0, h[4 * i]);
-    FILE* f = fopen("gpurun_out/cta_timing.csv", "w");
-    if (f) {
-      fprintf(f, "cta,sm,start_ns,end_ns,chunks,merges,rows,W,G,ntile_b,ntile_p,nq\n");
-      for (int i = 0; i < p.G; ++i)
-        fprintf(f, "%d,%llu,%llu,%llu,%llu,%llu,%llu,%lld,%d,%d,%d,%d\n", i, h[4 * i + 2] & 0xffff,
-                h[4 * i] - t0, h[4 * i + 1] - t0, (h[4 * i + 2] >> 16) & 0xffff,
-                h[4 * i + 2] >> 32, h[4 * i + 3], p.W, p.G, p.ntile_b, p.ntile_p, p.nq);
-      fclose(f);
-    }
-  }
   return 0;
 }
 
@@ -487,6 +476,81 @@ struct Solve {
     return 0;
   }
 
+  template <int BT, bool kGrid>
+  int persistent_loop_bt(const sinkhorn_options_v1& op, bool allow_est, int* iters, int* cur) {
+    constexpr int PT = 64;
+    using K = TiledK<BT, PT, kGrid, kModeUpdate>;
+    auto kern = &persistent_solve_kernel<BT, PT, QC, RB, RP, NSTAGE, kGrid>;
+    const size_t smem = K::S::SMEM_BYTES;
+    static bool attr_set[2] = {false, false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[kGrid ? 1 : 0]) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_set[kGrid ? 1 : 0] = true;
+    }
+    // every CTA must own >= 1 row of both sweep orientations
+    const long long G = std::min<long long>(
+        di.sms, std::min(tiled_chunks<BT, PT>(L, (int)pr.d2, (int)pr.d1),
+                         tiled_chunks<BT, PT>(L, (int)pr.d1, (int)pr.d2)));
+    PersistMaps maps;
+    maps.a2 = tm_a2;
+    maps.a2t = tm_a2t;
+    maps.f2 = tm_f2;
+    maps.g2[0] = tm_g2[0];
+    maps.g2[1] = tm_g2[1];
+    PersistParams P = {};
+    TiledArgs ca = {&tm_a2, &tm_f2, (int)pr.d1, (int)pr.d2, L.D1p, L.D2p, F(L.l2nu), F(L.nu),
+                    nullptr, nullptr, F(L.res), kResNone, nullptr, nullptr, nullptr,
+                    nullptr, 0, est_fail, poly ? 1 : 0};
+    TiledArgs ra = {&tm_a2t, &tm_g2[0], (int)pr.d2, (int)pr.d1, L.D2p, L.D1p, F(L.l2mu),
+                    F(L.mu), F(L.f2), nullptr, F(L.res), kResNone, nullptr, nullptr, nullptr,
+                    nullptr, 0, est_fail, poly ? 1 : 0};
+    P.col = build_tiled_params<BT, PT>(L, ws, ca, pr, lam, (int)G);
+    P.row = build_tiled_params<BT, PT>(L, ws, ra, pr, lam, (int)G);
+    P.g2[0] = F(L.g2[0]);
+    P.g2[1] = F(L.g2[1]);
+    P.f2 = F(L.f2);
+    P.res = F(L.res);
+    P.B = (int)pr.B;
+    P.Bp = L.Bp;
+    P.max_iters = op.max_iters;
+    P.check_interval = op.check_interval;
+    P.est_from = allow_est ? kEstFromIter : (op.max_iters + 1);
+    P.tol = op.tolerance;
+    P.bar = at<unsigned int>(ws, L.scratch + 32);
+    P.result = at<int>(ws, L.scratch + 40);
+    CK(cudaMemsetAsync(P.bar, 0, 4, st));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3(K::S::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident: grid barriers are safe
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ++g_launches;
+    CK(cudaLaunchKernelEx(&cfg, kern, maps, P));
+    int h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, P.result, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *iters = h[0];
+    *cur = h[1];
+    (void)dev;
+    return 0;
+  }
+
+  int persistent_loop(const sinkhorn_options_v1& op, bool allow_est, int* iters, int* cur) {
+    const bool grid = pr.cost_kind == SINKHORN_COST_GRID2D;
+    if (pick_bt(pr.B) == 128)
+      return grid ? persistent_loop_bt<128, true>(op, allow_est, iters, cur)
+                  : persistent_loop_bt<128, false>(op, allow_est, iters, cur);
+    return grid ? persistent_loop_bt<64, true>(op, allow_est, iters, cur)
+                : persistent_loop_bt<64, false>(op, allow_est, iters, cur);
+  }
+
   int read_status(int* out) {
     CK(cudaMemcpyAsync(out, at<int>(ws, L.status), 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -612,7 +676,15 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   bool have_next = false; // g2[cur] already advanced by a check sweep
   int iters = 0;
   bool converged = false;
-  for (int k = 1; k <= op.max_iters; ++k) {
+  // Opt-in: the whole loop in one cooperative kernel (no launches, device-side
+  // stopping test).  Off by default: its grid barriers (~3.5 us each, two per
+  // half-sweep) cost more than the launch gaps they remove.
+  const bool persist = L.tiled && g_reducer == nullptr &&
+                       (op.flags & SINKHORN_FLAG_PERSISTENT) != 0;
+  if (persist) {
+    if (int e = S.persistent_loop(op, allow_est, &iters, &cur)) return e;
+  }
+  for (int k = 1; !persist && k <= op.max_iters; ++k) {
     // estimate mode once the potentials have settled past the first sweeps
     S.est = allow_est && k >= kEstFromIter;
     if (!have_next) {

@@ -65,6 +65,20 @@ struct TiledSweepParams {
   int* est_fail;             // set when an estimate was > kEstSlack above the result
 };
 
+// Per-call fields of a sweep (the rest of TiledSweepParams is static over a
+// solve and stays in constant / kernel-parameter space).
+struct SweepDyn {
+  float* out;
+  const float* old;
+  const float* est_old;
+  int use_est;
+  int res_kind;
+};
+
+__host__ __device__ inline SweepDyn dyn_of(const TiledSweepParams& p) {
+  return SweepDyn{p.out, p.old, p.est_old, p.use_est, p.res_kind};
+}
+
 // One-pass chunks tolerate terms up to 2^kRedo above the running max (no fp32
 // overflow for <= 2^20 terms); beyond that the warp redoes the chunk exactly.
 constexpr float kRedo = 100.f;
@@ -111,12 +125,13 @@ __device__ __forceinline__ long long atom_owner(const TiledSweepParams& p, long 
 // Finalise one output tile from per-thread accumulators (M, Sm, S2 hold the
 // thread's RB x RP outputs).  Called by every thread of the CTA (it may sync).
 template <int BT, int PT, int RB, int RP, int NT, int kMode>
-__device__ __forceinline__ void tile_epilogue(const TiledSweepParams& p, int tid, int tb, int tp,
+__device__ __forceinline__ void tile_epilogue(const TiledSweepParams& p, const SweepDyn& d,
+                                              int tid, int tb, int tp,
                                               int b0, int p0, int own_lo, const float* M,
                                               const float* Sm, const float* S2, float* s_res) {
   // tid/NT here are the block-local thread index and block size (the caller
   // passes the lane/output groups tb/tp of the sweep's thread map)
-    if (p.res != nullptr && (kMode == kModeTail || p.res_kind != kResNone)) {
+    if (p.res != nullptr && (kMode == kModeTail || d.res_kind != kResNone)) {
       for (int i = tid; i < BT; i += NT) s_res[i] = 0.f;
       __syncthreads();
     }
@@ -142,8 +157,8 @@ __device__ __forceinline__ void tile_epilogue(const TiledSweepParams& p, int tid
       if (kMode == kModeUpdate) {
         const float4 tg = *reinterpret_cast<const float4*>(p.target + row);
         const float tv[4] = {tg.x, tg.y, tg.z, tg.w};
-        if (p.use_est) {
-          const float4 eo = *reinterpret_cast<const float4*>(p.est_old + row);
+        if (d.use_est) {
+          const float4 eo = *reinterpret_cast<const float4*>(d.est_old + row);
           const float ev[4] = {eo.x, eo.y, eo.z, eo.w};
           bool bad = false;
 #pragma unroll
@@ -156,13 +171,13 @@ __device__ __forceinline__ void tile_epilogue(const TiledSweepParams& p, int tid
         float ov[4];
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) ov[rb] = sweep_out(tv[rb], lse[rb]);
-        *reinterpret_cast<float4*>(p.out + row) = make_float4(ov[0], ov[1], ov[2], ov[3]);
-        if (p.res != nullptr && p.res_kind != kResNone) {
+        *reinterpret_cast<float4*>(d.out + row) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+        if (p.res != nullptr && d.res_kind != kResNone) {
           const float4 mg = *reinterpret_cast<const float4*>(p.marg + row);
           const float mv[4] = {mg.x, mg.y, mg.z, mg.w};
           float base[4] = {ov[0], ov[1], ov[2], ov[3]};
-          if (p.res_kind == kResCol) {
-            const float4 od = *reinterpret_cast<const float4*>(p.old + row);
+          if (d.res_kind == kResCol) {
+            const float4 od = *reinterpret_cast<const float4*>(d.old + row);
             base[0] = od.x; base[1] = od.y; base[2] = od.z; base[3] = od.w;
           }
 #pragma unroll
@@ -170,7 +185,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledSweepParams& p, int tid
             rmax[rb] = fmaxf(rmax[rb], fabsf(exp2f(base[rb] + lse[rb]) - mv[rb]));
         }
       } else {  // TAIL: column residual against `old` and the E0 term
-        const float4 od = *reinterpret_cast<const float4*>(p.old + row);
+        const float4 od = *reinterpret_cast<const float4*>(d.old + row);
         const float4 mg = *reinterpret_cast<const float4*>(p.marg + row);
         const float ovv[4] = {od.x, od.y, od.z, od.w};
         const float mv[4] = {mg.x, mg.y, mg.z, mg.w};
@@ -184,7 +199,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledSweepParams& p, int tid
         *reinterpret_cast<float4*>(p.e0 + row) = make_float4(ev[0], ev[1], ev[2], ev[3]);
       }
     }
-    if (p.res != nullptr && (kMode == kModeTail || p.res_kind != kResNone)) {
+    if (p.res != nullptr && (kMode == kModeTail || d.res_kind != kResNone)) {
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
         // NaN must win the max (batch.py:320 compares max <= tol, false for NaN)
@@ -212,25 +227,43 @@ __device__ __forceinline__ void thread_map(int tid, int& tb, int& tp) {
   tp = (warp % WPH) * 2 + (lane >> 4);
 }
 
+// Shared-memory carve-up common to the sweep kernel and the persistent solve.
 template <int BT, int PT, int QC, int RB, int RP, int NSTAGE, bool kGrid, int kMode>
-__global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) >= 512) ? 1 : 2)
-    tiled_sweep_kernel(const __grid_constant__ CUtensorMap tmap_g,
-                       const __grid_constant__ CUtensorMap tmap_x, const TiledSweepParams p) {
+struct SweepSmem {
+  using S = TiledSweep<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>;
+  float* smem;
+  uint64_t* bars;
+  float* s_res;
+  float* s_gq;   // grid mode: q coordinates (x, y) [QC][2]
+  float* s_gp;   // grid mode: p coordinates [PT][2]
+  __device__ explicit SweepSmem(uint8_t* raw) {
+    smem = reinterpret_cast<float*>(raw);
+    bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * S::STAGE_FLOATS);
+    s_res = reinterpret_cast<float*>(bars + 64);
+    s_gq = s_res + BT;
+    s_gp = s_gq + 2 * QC;
+  }
+};
+
+// One half-sweep over this CTA's stream-K range of (tile, row) work: the hot
+// loop.  `seq` counts the TMA stages this CTA has consumed so far, so the
+// mbarrier phases stay consistent when several sweeps run in one kernel.
+template <int BT, int PT, int QC, int RB, int RP, int NSTAGE, bool kGrid, int kMode>
+__device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUtensorMap* tmap_x,
+                                            const TiledSweepParams& p, const SweepDyn& d,
+                                            const SweepSmem<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>& sm,
+                                            uint32_t& seq) {
   using S = TiledSweep<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>;
   constexpr int NT = S::NT;
   constexpr int NV = S::NV;
   constexpr int NOUT = RB * RP;
-
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  float* smem = reinterpret_cast<float*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * S::STAGE_FLOATS);
-  float* s_res = reinterpret_cast<float*>(bars + 64);
-  float* s_gq = s_res + BT;        // grid mode: q coordinates (x, y) [QC][2]
-  float* s_gp = s_gq + 2 * QC;     // grid mode: p coordinates [PT][2]
+  float* smem = sm.smem;
+  uint64_t* bars = sm.bars;
+  float* s_res = sm.s_res;
+  float* s_gq = sm.s_gq;
+  float* s_gp = sm.s_gp;
 
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int warp = tid >> 5;
   int tb, tp;   // lane group (b = tb*RB + rb), output group (p = tp*RP + rp)
   thread_map<BT, RB, NT>(tid, tb, tp);
 
@@ -244,21 +277,9 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
     const long long t = r / Qv;
     return t * nq + (r - t * Qv) / QC;
   };
+  if (a_end <= a_begin) return;   // no rows for this CTA
   const long long g_first = chunk_of(a_begin);
   const int n_local = int(chunk_of(a_end - 1) - g_first + 1);
-
-  if (tid == 0) {
-    for (int s = 0; s < NSTAGE; ++s) mbar_init(&bars[s], 1);
-    fence_barrier_init();
-    if (!kGrid) prefetch_tmap(&tmap_g);
-    prefetch_tmap(&tmap_x);
-  }
-  __syncthreads();
-  // Everything above overlaps the previous kernel's tail; inputs are read below.
-  pdl_wait();
-  unsigned long long dbg_t0 = 0, dbg_tw = 0, dbg_tm = 0;
-  if (p.dbg != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
-  int dbg_merges = 0;
 
   // Output tile tp_idx covers [p0, p0 + PT) but owns (writes) [tp_idx*PT, ...):
   // the last tile is shifted left to end at Pv, so no tile is partial (a
@@ -276,11 +297,11 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
     const long long a = g_first + l;
     int tile, qc, b0, p0;
     atom_coords(a, tile, qc, b0, p0);
-    const int s = l % NSTAGE;
+    const int s = (seq + l) % NSTAGE;
     float* st = smem + s * S::STAGE_FLOATS;
     mbar_arrive_expect_tx(&bars[s], S::TMA_BYTES);
-    if (!kGrid) tma_load_2d(st, &tmap_g, p0, qc * QC, &bars[s]);
-    tma_load_2d(st + S::G_FLOATS, &tmap_x, b0, qc * QC, &bars[s]);
+    if (!kGrid) tma_load_2d(st, tmap_g, p0, qc * QC, &bars[s]);
+    tma_load_2d(st + S::G_FLOATS, tmap_x, b0, qc * QC, &bars[s]);
   };
 
   if (tid == 0) {
@@ -315,8 +336,8 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
       cur_tile = tile;
       seg_q0 = qc;
     }
-    const int s = l % NSTAGE;
-    const uint32_t parity = (l / NSTAGE) & 1;
+    const int s = (seq + l) % NSTAGE;
+    const uint32_t parity = ((seq + l) / NSTAGE) & 1;
     float* st = smem + s * S::STAGE_FLOATS;
     const float* Gs = st;
     const float* Xs = st + S::G_FLOATS;
@@ -351,7 +372,7 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
     // a warp covers 2 output groups; skip it only if both are past Pv (uniform)
     const bool warp_active = __any_sync(0xffffffffu, (p0 + tp * RP) < p.Pv);
     if (warp_active) {
-      if (p.use_est && (l == 0 || qc == 0)) {
+      if (d.use_est && (l == 0 || qc == 0)) {
         // segment start: running max := previous lse (target - old); outputs
         // with a -inf target never need their lse and are parked
 #pragma unroll
@@ -359,7 +380,7 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
           const int pp = min(p0 + tp * RP + rp, p.Pv - 1);
           const size_t row = size_t(pp) * p.Bp + b0 + tb * RB;
           const float4 tg = __ldg(reinterpret_cast<const float4*>(p.target + row));
-          const float4 eo = *reinterpret_cast<const float4*>(p.est_old + row);
+          const float4 eo = *reinterpret_cast<const float4*>(d.est_old + row);
           const float tv[4] = {tg.x, tg.y, tg.z, tg.w};
           const float ev[4] = {eo.x, eo.y, eo.z, eo.w};
 #pragma unroll
@@ -410,7 +431,7 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
             }
         }
       };
-      bool exact = !p.use_est;
+      bool exact = !d.use_est;
       if (!exact) {
         if (p.use_poly) phase3(std::true_type{}); else phase3(std::false_type{});
         // A term above 2^kRedo (or inf/NaN) means the shift was too low for
@@ -520,13 +541,12 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
     // ---- segment end: finalize or hand over to the stream-K merge ---------
     const bool seg_end = (qc == nq - 1) || (l == n_local - 1);
     if (!seg_end) continue;
-    if (p.dbg != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_tw));
     const long long t_first = (long long)tile * Qv;   // first row of this tile
     const long long c_lo = atom_owner(p, t_first);
     const long long c_hi = atom_owner(p, t_first + Qv - 1);
     const int own_lo = (tile / p.ntile_b) * PT;
     if (c_lo == c_hi) {
-      tile_epilogue<BT, PT, RB, RP, NT, kMode>(p, tid, tb, tp, b0, p0, own_lo, M, Sm, S2, s_res);
+      tile_epilogue<BT, PT, RB, RP, NT, kMode>(p, d, tid, tb, tp, b0, p0, own_lo, M, Sm, S2, s_res);
     } else {
       // split tile: leave this piece's (max, sum[, E0 sum]) for the fixup kernel
       const int slot = (a_begin >= t_first) ? 0 : 1;
@@ -540,24 +560,31 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
           __stcg(reinterpret_cast<float4*>(mine + 2 * BT * PT + o),
                  make_float4(S2[o], S2[o + 1], S2[o + 2], S2[o + 3]));
       }
-      ++dbg_merges;
     }
     reset_acc();
     (void)seg_q0;
+    (void)NV;
   }
-  if (p.dbg != nullptr && tid == 0) {
-    unsigned long long t1, smid;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    unsigned int sm;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    smid = sm;
-    p.dbg[4 * blockIdx.x + 0] = dbg_t0;
-    p.dbg[4 * blockIdx.x + 1] = t1;
-    p.dbg[4 * blockIdx.x + 2] = smid | ((unsigned long long)n_local << 16) |
-                                ((unsigned long long)dbg_merges << 32);
-    p.dbg[4 * blockIdx.x + 3] = ((dbg_tw - dbg_t0) & 0xffffffffull) |
-                                (dbg_tm ? ((dbg_tm - dbg_t0) << 32) : 0ull);
+  seq += n_local;
+}
+
+template <int BT, int PT, int QC, int RB, int RP, int NSTAGE, bool kGrid, int kMode>
+__global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) >= 512) ? 1 : 2)
+    tiled_sweep_kernel(const __grid_constant__ CUtensorMap tmap_g,
+                       const __grid_constant__ CUtensorMap tmap_x, const TiledSweepParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const SweepSmem<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode> sm(smem_raw);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) mbar_init(&sm.bars[s], 1);
+    fence_barrier_init();
+    if (!kGrid) prefetch_tmap(&tmap_g);
+    prefetch_tmap(&tmap_x);
   }
+  __syncthreads();
+  // Everything above overlaps the previous kernel's tail; inputs are read below.
+  pdl_wait();
+  uint32_t seq = 0;
+  sweep_phase<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>(&tmap_g, &tmap_x, p, dyn_of(p), sm, seq);
   pdl_launch_dependents();
 }
 
@@ -566,20 +593,22 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
 // the tile epilogue.  One CTA per tile, same thread map as the sweep, so each
 // thread merges exactly the outputs its counterpart accumulated.  Launched
 // right after the sweep with programmatic dependent launch.
-template <int BT, int PT, int QC, int RB, int RP, int kMode>
-__global__ void __launch_bounds__(256) tiled_fixup_kernel(const TiledSweepParams p) {
+// One chunk of NB float4 groups (4 outputs of one lane each) of the split
+// tiles: every thread of the CTA takes one group.  Chunks never straddle tiles
+// (NT*NG is a multiple of NB), so the early exit is CTA-uniform.
+template <int BT, int PT, int QC, int RB, int RP, int kMode, int NB>
+__device__ __forceinline__ void fixup_chunk(const TiledSweepParams& p, const SweepDyn& d, int chunk,
+                                            float* s_res) {
   constexpr int NT = (BT / RB) * (PT / RP);   // the sweep's threads per tile
   constexpr int NOUT = RB * RP;
   constexpr int NG = NOUT / 4;                // float4 groups per sweep thread (one per rb)
-  constexpr int NB = 256;                     // fixup threads per CTA
-  constexpr int CPT = NT * NG / NB;           // fixup CTAs per tile
+  constexpr int CPT = NT * NG / NB;           // chunks per tile
   constexpr int NV = (kMode == kModeTail) ? 3 : 2;
   constexpr int GRP = 8;                      // pieces whose loads are in flight together
   static_assert(RP == 4, "one float4 group = the RP outputs of one lane");
-  __shared__ float s_res[BT];
-  pdl_wait();
-  const int tile = blockIdx.x / CPT;
-  const int e = (blockIdx.x % CPT) * NB + threadIdx.x;   // float4 group within the tile
+  static_assert((NT * NG) % NB == 0, "chunks align with tiles");
+  const int tile = chunk / CPT;
+  const int e = (chunk % CPT) * NB + threadIdx.x;        // float4 group within the tile
   const int vtid = e / NG, rb = e % NG;                  // mirrored sweep thread, its lane
   const long long Qv = p.Qv;
   const long long t_first = (long long)tile * Qv;
@@ -629,7 +658,7 @@ __global__ void __launch_bounds__(256) tiled_fixup_kernel(const TiledSweepParams
     }
   }
   // epilogue for lane b, outputs p0 + tp*RP + r
-  const bool want_res = p.res != nullptr && (kMode == kModeTail || p.res_kind != kResNone);
+  const bool want_res = p.res != nullptr && (kMode == kModeTail || d.res_kind != kResNone);
   if (want_res) {
     for (int i = threadIdx.x; i < BT; i += NB) s_res[i] = 0.f;
     __syncthreads();
@@ -648,18 +677,18 @@ __global__ void __launch_bounds__(256) tiled_fixup_kernel(const TiledSweepParams
     const float lse = lse_final(M[r], Sm[r]);
     if (kMode == kModeUpdate) {
       const float tg = p.target[o];
-      if (p.use_est) {
-        const float est = tg - p.est_old[o];
+      if (d.use_est) {
+        const float est = tg - d.est_old[o];
         if (tg != neg_inf() && isfinite(est) && !(lse >= est - kEstSlack)) atomicOr(p.est_fail, 1);
       }
       const float ov = sweep_out(tg, lse);
-      p.out[o] = ov;
+      d.out[o] = ov;
       if (want_res) {
-        const float base = (p.res_kind == kResCol) ? p.old[o] : ov;
+        const float base = (d.res_kind == kResCol) ? d.old[o] : ov;
         rmax = fmaxf(rmax, fabsf(exp2f(base + lse) - p.marg[o]));
       }
     } else {   // TAIL
-      const float od = p.old[o];
+      const float od = d.old[o];
       p.e0[o] = (S2[r] > 0.f) ? (M[r] + log2f(S2[r]) + od) : neg_inf();
       rmax = fmaxf(rmax, fabsf(exp2f(od + lse) - p.marg[o]));
     }
@@ -672,7 +701,15 @@ __global__ void __launch_bounds__(256) tiled_fixup_kernel(const TiledSweepParams
       const float rv = s_res[i];
       if (rv != 0.f) atomic_max_nonneg(&p.res[tb_idx * BT + i], rv);
     }
+    __syncthreads();   // s_res is reused by the next chunk
   }
+}
+
+template <int BT, int PT, int QC, int RB, int RP, int kMode>
+__global__ void __launch_bounds__(256) tiled_fixup_kernel(const TiledSweepParams p) {
+  __shared__ float s_res[BT];
+  pdl_wait();
+  fixup_chunk<BT, PT, QC, RB, RP, kMode, 256>(p, dyn_of(p), blockIdx.x, s_res);
   pdl_launch_dependents();
 }
 

@@ -197,3 +197,22 @@ def test_polynomial_exp2_share_matches_mufu_only(name, cuda):
     rel = (poly.cost_e0.double() - mufu.cost_e0.double()).abs() / mufu.cost_e0.double().abs()
     assert float(rel.max()) <= 2e-6
     _check_loss_and_grads(g, poly)
+
+
+@pytest.mark.parametrize("name", ["config1", "config1_tol", "lockstep", "zero_mass"])
+def test_persistent_loop_matches_reference(name, cuda):
+    """Opt-in cooperative whole-loop kernel: same results and iteration counts,
+    with the stopping test decided on the device."""
+    skb = _skb()
+    g = load_golden(name)
+    c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
+    res = skb.solve(torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
+                    float(g["lam"]), int(g["max_iters"]), float(g["tol"]),
+                    int(g["check_interval"]), persistent=True)
+    ref = skb.solve(torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
+                    float(g["lam"]), int(g["max_iters"]), float(g["tol"]),
+                    int(g["check_interval"]))
+    assert res.iterations_run == int(g["iterations_run"]) == ref.iterations_run
+    rel = np.abs(res.cost_e0.double().cpu().numpy() - g["cost_e0"]) / g["cost_e0"]
+    assert rel.max() <= LOSS_RTOL
+    assert torch.equal(torch.isneginf(res.log_u), torch.isneginf(ref.log_u))
