@@ -160,8 +160,18 @@ def work_units(cfg: dict) -> float:
     return float(cfg["B"]) * cfg["d"] * cfg["d"] * cfg["iters"]
 
 
-def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic) -> dict:
-    """Dominant kernel = the half-sweep (2*iters launches per step)."""
+KERNEL_OF_PATH = {
+    "tiled": "tiled_sweep_kernel (stream-K online-LSE half-sweep)",
+    "small": "small_solve_kernel (whole solve in one launch, cost in shared memory)",
+    "persistent": "persistent_solve_kernel (cooperative whole loop)",
+    "lane": "lane_col_kernel / lane_row_kernel (per-sample sweep)",
+}
+
+
+def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
+             path: str = "tiled") -> dict:
+    """Dominant kernel = the half-sweep (2*iters per step; one launch each on the
+    tiled path, all inside one launch on the small path)."""
     cells = float(cfg["B"]) * cfg["d"] * cfg["d"]          # cells per sweep launch
     if cfg["cost"] == "per_sample":
         achieved = cells * 4 / (sweep_ms * 1e-3) / 1e9      # algorithmic bytes: C read once
@@ -177,7 +187,7 @@ def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic) -> 
     peak = sms * MUFU_PER_SM_CLK * fmax * 1e6 / 1e12
     out = {"bound": "mufu", "achieved": achieved, "peak": peak, "unit": "Tex2/s",
            "frac": achieved / peak, "traffic": traffic,
-           "kernel": "tiled_sweep_kernel (stream-K online-LSE half-sweep)",
+           "kernel": KERNEL_OF_PATH.get(path, path),
            "algorithmic_per_launch": f"{cells:.4g} ex2 (1 per cell)",
            "peak_source": f"148 SM x {MUFU_PER_SM_CLK} ex2/clk x sm_max_mhz {fmax:.0f} "
                           "(MEASURED_PEAKS.json)"}
@@ -338,6 +348,7 @@ def run_ours(args, cfg, world, rank, local):
             res = step()
             ends[s].record()
             loop_ms.append(res.loop_ms)
+            path = res.path
         torch.cuda.synchronize()
     launches = lib.sinkhorn_launch_count_v1() - launches0
     if world > 1:
@@ -368,9 +379,9 @@ def run_ours(args, cfg, world, rank, local):
         "data": "synthetic",
         "config": {"workload": cfg["workload"], "B_per_gpu": B, "global_batch": B * world,
                    "d1": d, "d2": d, "iters": iters, "lambda": lam, "tolerance": 0.0,
-                   "parallelism": f"batch-sharded dp{world}",
+                   "parallelism": f"batch-sharded dp{world}", "solver_path": path,
                    "l2": "flushed between steps (256 MiB write outside the timed events)"},
-        "roofline": roofline(cfg, sweep_ms, peaks, clocks, load_traffic(args.config)),
+        "roofline": roofline(cfg, sweep_ms, peaks, clocks, load_traffic(args.config), path),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
                 "d2h_bytes_per_step": e2e["d2h"], "path": e2e["path"]},
         "gpu_launches": int(launches),

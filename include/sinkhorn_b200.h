@@ -95,6 +95,7 @@ typedef struct sinkhorn_problem_v1 {
 #define SINKHORN_FLAG_EXACT_MAX 8u       /* always two-pass chunks (no previous-lse estimate) */
 #define SINKHORN_FLAG_MUFU_ONLY 16u      /* every exponential on MUFU (no FMA-pipe polynomial) */
 #define SINKHORN_FLAG_PERSISTENT 32u     /* shared/grid costs: whole loop in one cooperative kernel */
+#define SINKHORN_FLAG_TILED_ONLY 64u     /* never take the single-launch small-problem solver */
 
 typedef struct sinkhorn_options_v1 {
   double lambda;          /* > 0, finite */
@@ -187,6 +188,10 @@ unsigned long long sinkhorn_launch_count_v1(void);
  * estimate overshot the result (estimate mode). */
 unsigned long long sinkhorn_exact_reruns_v1(void);
 float sinkhorn_last_loop_ms_v1(void);
+/* Solver path of this thread's last forward: "small" (one-launch solve,
+ * cost in shared memory), "tiled" (stream-K sweeps), "persistent" (opt-in
+ * cooperative loop) or "lane" (per-sample costs). */
+const char* sinkhorn_last_path_v1(void);
 
 #ifdef __cplusplus
 }

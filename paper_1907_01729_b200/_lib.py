@@ -33,6 +33,7 @@ FLAG_TIME_LOOP = 4
 FLAG_EXACT_MAX = 8
 FLAG_MUFU_ONLY = 16
 FLAG_PERSISTENT = 32
+FLAG_TILED_ONLY = 64
 
 # every symbol include/sinkhorn_b200.h declares
 EXPORTED_SYMBOLS = (
@@ -51,6 +52,7 @@ EXPORTED_SYMBOLS = (
     "sinkhorn_launch_count_v1",
     "sinkhorn_exact_reruns_v1",
     "sinkhorn_last_loop_ms_v1",
+    "sinkhorn_last_path_v1",
 )
 
 
@@ -119,6 +121,7 @@ def _declare(lib):
         "sinkhorn_launch_count_v1": (ctypes.c_ulonglong, []),
         "sinkhorn_exact_reruns_v1": (ctypes.c_ulonglong, []),
         "sinkhorn_last_loop_ms_v1": (ctypes.c_float, []),
+        "sinkhorn_last_path_v1": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

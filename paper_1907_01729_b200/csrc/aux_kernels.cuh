@@ -8,10 +8,6 @@
 
 namespace skb {
 
-// Status word: first error wins, in stream order, which reproduces the
-// reference's check order (shapes on the host, then histograms ffi.ts:111-115,
-// then the cost the CLI validates, core.py:53-63).
-__device__ __forceinline__ void set_status(int* status, int code) { atomicCAS(status, 0, code); }
 
 __global__ void fill_kernel(float* __restrict__ x, size_t n, float v) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;

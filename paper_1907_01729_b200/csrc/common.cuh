@@ -184,4 +184,29 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, in
 __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Grid-wide barrier for a cooperative launch: the counter only grows, so
+// epoch e completes when it reaches e * gridDim.x.  The release reduction and
+// the acquire load (which also invalidates L1) order every CTA's global
+// writes before every later read; the async-proxy fence covers TMA reads of
+// data written with ordinary stores.
+__device__ __forceinline__ void grid_sync(unsigned int* counter, unsigned int& epoch) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++epoch;
+    const unsigned int target = epoch * gridDim.x;
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(counter), "r"(1u) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// Status word: first error wins, in stream order, which reproduces the
+// reference's check order (shapes on the host, then histograms ffi.ts:111-115,
+// then the cost the CLI validates, core.py:53-63).
+__device__ __forceinline__ void set_status(int* status, int code) { atomicCAS(status, 0, code); }
+
 }  // namespace skb

@@ -39,26 +39,6 @@ struct PersistParams {
   int* result;            // out: [0] iterations_run, [1] index of the final log_v buffer
 };
 
-// Grid-wide barrier for a cooperative launch: the counter only grows, so
-// epoch e completes when it reaches e * gridDim.x.  The release reduction and
-// the acquire load (which also invalidates L1) order every CTA's global
-// writes before every later read; the async-proxy fence covers TMA reads of
-// data written with ordinary stores.
-__device__ __forceinline__ void grid_sync(unsigned int* counter, unsigned int& epoch) {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    ++epoch;
-    const unsigned int target = epoch * gridDim.x;
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(counter), "r"(1u) : "memory");
-    unsigned int v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
-}
-
 template <int BT, int PT, int QC, int RB, int RP, int NSTAGE, bool kGrid>
 __global__ void __launch_bounds__((BT / RB) * (PT / RP), 1)
     persistent_solve_kernel(const __grid_constant__ PersistMaps maps,

@@ -25,6 +25,7 @@
 #include "sweep_lane.cuh"
 #include "sweep_tiled.cuh"
 #include "persistent.cuh"
+#include "sweep_small.cuh"
 
 using namespace skb;
 
@@ -33,6 +34,7 @@ namespace {
 thread_local std::string g_last_error;
 thread_local unsigned long long g_launches = 0;   // kernels this thread launched
 thread_local float g_last_loop_ms = -1.f;         // last timed iteration loop (ms)
+thread_local const char* g_last_path = "none";    // solver path of the last forward
 thread_local unsigned long long g_exact_reruns = 0;  // solves redone without estimates
 // Optional cross-rank agreement on the stopping test (batch-sharded solves).
 thread_local sinkhorn_residual_reducer_v1 g_reducer = nullptr;
@@ -551,6 +553,125 @@ struct Solve {
                 : persistent_loop_bt<64, false>(op, allow_est, iters, cur);
   }
 
+  // ---- small shared / grid costs: the whole solve in one launch -----------
+  // (sweep_small.cuh).  Eligible when both cost orientations and the lanes'
+  // potentials fit in one CTA's shared memory and each CTA's share of a sweep
+  // is small enough that launches, not exponentials, would bound the tiled path.
+  static constexpr int kSmallNT = 512;
+  static constexpr long long kSmallMaxCells = 1LL << 17;   // per CTA per half-sweep
+
+  static int pick_group(long long units, long long n) {
+    int best = 1;
+    double bc = 1e300;
+    for (int S = 1; S <= 32; S <<= 1) {
+      const long long rounds = (units * S + kSmallNT - 1) / kSmallNT;
+      const double E = (double)((n + S - 1) / S);
+      const double c = (double)rounds * (2.0 * E + 8.0 * std::log2((double)S) + 10.0);
+      if (c < bc) {
+        bc = c;
+        best = S;
+      }
+    }
+    return best;
+  }
+
+  // Returns a status (non-zero only on a CUDA error); *ok says whether to use it.
+  int plan_small(SmallParams& sp, int& G, size_t& smem, bool* ok) {
+    *ok = false;
+    if (!L.tiled || g_reducer != nullptr || (op.flags & SINKHORN_FLAG_TILED_ONLY)) return 0;
+    if (pr.cost_kind != SINKHORN_COST_SHARED && pr.cost_kind != SINKHORN_COST_GRID2D) return 0;
+    static int smem_optin = 0;
+    if (smem_optin == 0)
+      cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, di.dev);
+    const long long d1 = pr.d1, d2 = pr.d2, B = pr.B;
+    for (int occ = 4; occ >= 1; --occ) {
+      const int Lc = (int)((B + (long long)di.sms * occ - 1) / ((long long)di.sms * occ));
+      if ((long long)Lc * d1 * d2 > kSmallMaxCells) continue;
+      const int Sc = pick_group((long long)Lc * d2, d1), Sr = pick_group((long long)Lc * d1, d2);
+      const int ldc = (int)round_up(d1, 32) + (Sc % 32), ldr = (int)round_up(d2, 32) + (Sr % 32);
+      const size_t bytes = SmallSmem::floats((int)d1, (int)d2, Lc, ldc, ldr) * 4;
+      if (bytes > (size_t)smem_optin / occ - 2048) continue;
+      static bool attr_set = false;
+      auto kern = &small_solve_kernel<kSmallNT>;
+      if (!attr_set) {
+        cudaFuncAttributes fa = {};
+        CK(cudaFuncGetAttributes(&fa, kern));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin - (int)fa.sharedSizeBytes));
+        attr_set = true;
+      }
+      int fit = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, kSmallNT, bytes));
+      if (fit < 1) return 0;
+      G = (int)((B + Lc - 1) / Lc);
+      if (op.tolerance > 0 && G > fit * di.sms) continue;   // the grid barrier needs co-residency
+      smem = bytes;
+      sp = SmallParams{};
+      sp.a2 = (pr.cost_kind == SINKHORN_COST_SHARED) ? F(L.a2) : nullptr;
+      sp.a2t = (pr.cost_kind == SINKHORN_COST_SHARED) ? F(L.a2t) : nullptr;
+      sp.D1p = L.D1p;
+      sp.D2p = L.D2p;
+      sp.grid = pr.cost_kind == SINKHORN_COST_GRID2D;
+      sp.gnx = (int)pr.grid_nx;
+      sp.gk = (float)(-kLog2e / lam);
+      sp.ghx2 = pr.grid_hx * pr.grid_hx;
+      sp.ghy2 = pr.grid_hy * pr.grid_hy;
+      sp.cinv = -lam * kLn2;
+      sp.l2mu = F(L.l2mu);
+      sp.l2nu = F(L.l2nu);
+      sp.mu = F(L.mu);
+      sp.nu = F(L.nu);
+      sp.B = (int)B;
+      sp.Bp = L.Bp;
+      sp.d1 = (int)d1;
+      sp.d2 = (int)d2;
+      sp.L = Lc;
+      sp.Sc = Sc;
+      sp.Sr = Sr;
+      sp.ldc = ldc;
+      sp.ldr = ldr;
+      sp.max_iters = op.max_iters;
+      sp.check_interval = op.check_interval;
+      sp.checks = op.tolerance > 0 ? 1 : 0;
+      sp.tol = (float)op.tolerance;
+      sp.res = F(L.res);
+      sp.cta_res = F(L.part);
+      sp.bar = at<unsigned int>(ws, L.scratch + 32);
+      sp.result = at<int>(ws, L.scratch + 40);
+      sp.status = at<int>(ws, L.status);
+      *ok = true;
+      return 0;
+    }
+    return 0;
+  }
+
+  int small_solve(SmallParams& sp, int G, size_t smem, float* out_cost, float* out_log_u,
+                  float* out_log_v, int* iters) {
+    sp.out_cost = out_cost;
+    sp.out_log_u = out_log_u;
+    sp.out_log_v = out_log_v;
+    CK(cudaMemsetAsync(sp.bar, 0, 4, st));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3(kSmallNT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // grid barrier at the stopping tests
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = sp.checks ? 1 : 0;
+    ++g_launches;
+    CK(cudaLaunchKernelEx(&cfg, &small_solve_kernel<kSmallNT>, sp));
+    if (sp.checks) {
+      CK(cudaMemcpyAsync(iters, sp.result, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    } else {
+      *iters = sp.max_iters;
+    }
+    return 0;
+  }
+
   int read_status(int* out) {
     CK(cudaMemcpyAsync(out, at<int>(ws, L.status), 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -659,7 +780,14 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     validate_cost_kernel<<<grid_for(n), 256, 0, st>>>(cost, n, status);
     CK(cudaGetLastError());
   }
-  if (int e = S.setup_maps()) return e;
+  SmallParams sp;
+  int small_grid = 0;
+  size_t small_smem = 0;
+  bool small = false;
+  if (int e = S.plan_small(sp, small_grid, small_smem, &small)) return e;
+  if (!small) {
+    if (int e = S.setup_maps()) return e;
+  }
 
   // ---- lockstep iteration (batch.py:314-324) ----
   // Optional: CUDA events on the caller's stream around the iteration loop, so
@@ -681,10 +809,14 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   // half-sweep) cost more than the launch gaps they remove.
   const bool persist = L.tiled && g_reducer == nullptr &&
                        (op.flags & SINKHORN_FLAG_PERSISTENT) != 0;
-  if (persist) {
+  if (small) {
+    if (int e = S.small_solve(sp, small_grid, small_smem, out_cost, out_log_u, out_log_v, &iters))
+      return e;
+  } else if (persist) {
     if (int e = S.persistent_loop(op, allow_est, &iters, &cur)) return e;
   }
-  for (int k = 1; !persist && k <= op.max_iters; ++k) {
+  g_last_path = small ? "small" : persist ? "persistent" : L.tiled ? "tiled" : "lane";
+  for (int k = 1; !persist && !small && k <= op.max_iters; ++k) {
     // estimate mode once the potentials have settled past the first sweeps
     S.est = allow_est && k >= kEstFromIter;
     if (!have_next) {
@@ -725,8 +857,14 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   if (timed) CK(cudaEventRecord(ev1, st));
   // ---- tail: residual + stable E0 in one column pass (batch.py:323-337) ----
   S.est = allow_est && iters >= kEstFromIter;
-  if (int e = S.tail(cur)) return e;
-  {
+  if (!small) {
+    if (int e = S.tail(cur)) return e;
+  }
+  if (small) {
+    if (out_residuals)
+      CK(cudaMemcpyAsync(out_residuals, S.F(L.res), (size_t)pr.B * 4, cudaMemcpyDeviceToDevice,
+                         st));
+  } else {
     const int nb = (int)((pr.B + 31) / 32);
     const long long sb = L.tiled ? 1 : L.D2p, sj = L.tiled ? L.Bp : 1;
     ++g_launches;
@@ -794,6 +932,8 @@ unsigned long long sinkhorn_launch_count_v1(void) { return g_launches; }
 unsigned long long sinkhorn_exact_reruns_v1(void) { return g_exact_reruns; }
 
 float sinkhorn_last_loop_ms_v1(void) { return g_last_loop_ms; }
+
+const char* sinkhorn_last_path_v1(void) { return g_last_path; }
 
 size_t sinkhorn_workspace_bytes_v1(const sinkhorn_problem_v1* prob) {
   if (check_problem(prob) != 0) return 0;

@@ -1,0 +1,319 @@
+// sweep_small.cuh -- the whole solve for small shared / grid costs in ONE
+// launch (batch.py:279-337 end to end).
+//
+// When d1*d2 is small (BASELINE config 1: d = 100) a sweep is a few hundred
+// thousand cells and the tiled path is bound by its two launches per
+// half-sweep, not by MUFU.  Here every CTA keeps the cost (both orientations,
+// log2-scaled) and the potentials of its group of lanes in shared memory and
+// runs all iterations itself: lanes are independent, so the only cross-CTA
+// step is the lockstep stopping test every check_interval iterations
+// (batch.py:318-322), a grid barrier on a cooperative launch.
+//
+// Work split inside a CTA: each (lane, output) unit is reduced by a group of
+// S threads (S = 1..32, chosen on the host per orientation), element i read
+// by thread s = i mod S.  The leading dimension of each cost orientation is
+// ld = 32k + S, so the 32/S groups of a warp hit 32 distinct banks.  Every
+// reduction is the exact two-pass one (max, then sum of 2^(x - max)), merged
+// across the group with xor shuffles -- the same arithmetic as the tiled
+// exact chunks, so results match the tiled path to fp32 rounding.
+#pragma once
+
+#include "common.cuh"
+
+namespace skb {
+
+struct SmallParams {
+  const float* a2;    // [D1p][D2p] log2-scaled shared cost (null for grid costs)
+  const float* a2t;   // [D2p][D1p]
+  int D1p, D2p;
+  int grid, gnx;      // grid cost recomputed into shared memory
+  float gk, ghx2, ghy2;
+  float cinv;         // cost = A2 * cinv (E0 weights)
+  const float* l2mu;  // solver layout: element (b, i) at i * Bp + b
+  const float* l2nu;
+  const float* mu;
+  const float* nu;
+  int B, Bp, d1, d2;
+  int L;              // lanes per CTA
+  int Sc, Sr;         // threads per output: column sweep (reduces d1) / row sweep (reduces d2)
+  int ldc, ldr;       // shared leading dims of A2T (column sweep) and A2 (row sweep)
+  int max_iters, check_interval, checks;
+  float tol;
+  float* out_log_u;   // (B, d1) natural log
+  float* out_log_v;   // (B, d2)
+  float* out_cost;    // (B)
+  float* res;         // (B) final residuals
+  float* cta_res;     // [2][gridDim.x] per-check CTA maxima
+  unsigned int* bar;  // grid-barrier counter (zero on entry)
+  int* result;        // [0] iterations_run
+  int* status;
+};
+
+struct SmallSmem {
+  float* A;    // [d1][ldr]  rows i, contiguous over j (row sweep)
+  float* AT;   // [d2][ldc]  rows j, contiguous over i (column sweep)
+  float* f;    // [L][d1] log2 u
+  float* g0;   // [L][d2] log2 v (ping-pong pair)
+  float* g1;
+  float* lmu;  // [L][d1]
+  float* lnu;  // [L][d2]
+  float* mu;   // [L][d1]
+  float* nu;   // [L][d2]
+  unsigned int* rres;   // [L] residual maxima (non-negative float bits)
+  __host__ __device__ static size_t floats(int d1, int d2, int L, int ldc, int ldr) {
+    return (size_t)d1 * ldr + (size_t)d2 * ldc + (size_t)L * (3 * d1 + 5 * d2) + L + 8;
+  }
+  __device__ SmallSmem(float* base, const SmallParams& p) {
+    A = base;
+    AT = A + (size_t)p.d1 * p.ldr;
+    f = AT + (size_t)p.d2 * p.ldc;
+    g0 = f + (size_t)p.L * p.d1;
+    g1 = g0 + (size_t)p.L * p.d2;
+    lmu = g1 + (size_t)p.L * p.d2;
+    lnu = lmu + (size_t)p.L * p.d1;
+    mu = lnu + (size_t)p.L * p.d2;
+    nu = mu + (size_t)p.L * p.d1;
+    rres = reinterpret_cast<unsigned int*>(nu + (size_t)p.L * p.d2);
+  }
+  __device__ float* g(int i) const { return i ? g1 : g0; }
+};
+
+// (max, sum 2^(row + x - max)[, sum of 2^(...) * row * cinv]) of one unit,
+// reduced over the S threads of its group.  All 32 lanes of the warp call it.
+template <bool kTail>
+__device__ __forceinline__ void small_unit_lse(const float* __restrict__ row,
+                                               const float* __restrict__ x, int n, int S, int s,
+                                               bool active, float cinv, float& m_out,
+                                               float& s_out, float& w_out) {
+  float m0 = neg_inf(), m1 = neg_inf(), m2 = neg_inf(), m3 = neg_inf();
+  if (active) {
+    int i = s;
+    for (; i + 3 * S < n; i += 4 * S) {
+      m0 = fmaxf(m0, row[i] + x[i]);
+      m1 = fmaxf(m1, row[i + S] + x[i + S]);
+      m2 = fmaxf(m2, row[i + 2 * S] + x[i + 2 * S]);
+      m3 = fmaxf(m3, row[i + 3 * S] + x[i + 3 * S]);
+    }
+    for (; i < n; i += S) m0 = fmaxf(m0, row[i] + x[i]);
+  }
+  float m = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+  for (int o = 1; o < S; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float mm = (m == neg_inf()) ? 0.f : m;   // all terms -inf: the sum is 0
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f;
+  if (active) {
+    int i = s;
+    for (; i + 3 * S < n; i += 4 * S) {
+      const float e0 = ex2(row[i] + x[i] - mm);
+      const float e1 = ex2(row[i + S] + x[i + S] - mm);
+      const float e2 = ex2(row[i + 2 * S] + x[i + 2 * S] - mm);
+      const float e3 = ex2(row[i + 3 * S] + x[i + 3 * S] - mm);
+      s0 += e0;
+      s1 += e1;
+      s2 += e2;
+      s3 += e3;
+      if (kTail) {
+        w0 = fmaf(e0, row[i] * cinv, w0);
+        w1 = fmaf(e1, row[i + S] * cinv, w1);
+        w0 = fmaf(e2, row[i + 2 * S] * cinv, w0);
+        w1 = fmaf(e3, row[i + 3 * S] * cinv, w1);
+      }
+    }
+    for (; i < n; i += S) {
+      const float e = ex2(row[i] + x[i] - mm);
+      s0 += e;
+      if (kTail) w0 = fmaf(e, row[i] * cinv, w0);
+    }
+  }
+  float sum = (s0 + s1) + (s2 + s3);
+  float w = w0 + w1;
+  for (int o = 1; o < S; o <<= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (kTail) w += __shfl_xor_sync(0xffffffffu, w, o);
+  }
+  m_out = m;
+  s_out = sum;
+  w_out = w;
+}
+
+// One half-sweep over the CTA's nl lanes: out[l][o] = target - LSE_k(M[o][k] + x[l][k]).
+//   kRes 0: plain update; 1: row residual |2^(out + lse) - marg|;
+//   2: column residual against `old` (the check sweep), 3: TAIL (residual
+//   against `old` + the E0 term written to `out`, batch.py:329-337).
+template <int NT, int kRes>
+__device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld, int nout, int nin,
+                                            int S, int nl, const float* __restrict__ x,
+                                            const float* __restrict__ target,
+                                            const float* __restrict__ marg,
+                                            const float* __restrict__ old, float* __restrict__ out,
+                                            unsigned int* rres, float cinv) {
+  const int tid = threadIdx.x;
+  const int gpr = NT / S;   // groups per round
+  const int s = tid % S;
+  const int U = nl * nout;
+  for (int base = 0; base < U; base += gpr) {
+    const int u = base + tid / S;
+    const bool active = u < U;
+    const int l = active ? u / nout : 0;
+    const int o = active ? u - l * nout : 0;
+    float m, sum, w;
+    small_unit_lse<kRes == 3>(M + (size_t)o * ld, x + (size_t)l * nin, nin, S, s, active, cinv, m,
+                              sum, w);
+    if (active && s == 0) {
+      const float lse = lse_final(m, sum);
+      const int idx = l * nout + o;
+      float r = 0.f;
+      if (kRes == 3) {
+        const float ov = old[idx];
+        out[idx] = (w > 0.f) ? (m + log2f(w) + ov) : neg_inf();
+        r = fabsf(exp2f(ov + lse) - marg[idx]);
+      } else {
+        const float nv = sweep_out(target[idx], lse);
+        if (kRes == 1) r = fabsf(exp2f(nv + lse) - marg[idx]);
+        if (kRes == 2) r = fabsf(exp2f(old[idx] + lse) - marg[idx]);
+        out[idx] = nv;
+      }
+      if (kRes != 0) {
+        // NaN must win the max (batch.py:320 compares max <= tol, false for NaN)
+        if (r != r) r = __int_as_float(0x7fc00000);
+        atomicMax(&rres[l], __float_as_uint(r));
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p) {
+  extern __shared__ __align__(16) float small_smem[];
+  const SmallSmem sm(small_smem, p);
+  const int tid = threadIdx.x;
+  const int b0 = blockIdx.x * p.L;
+  const int nl = min(p.L, p.B - b0);
+  __shared__ int s_conv;
+
+  // ---- stage the cost (both orientations) and this CTA's lanes -------------
+  if (p.grid) {
+    for (int e = tid; e < p.d1 * p.d2; e += NT) {
+      const int i = e / p.d2, j = e - i * p.d2;
+      const int yi = i / p.gnx, xi = i - yi * p.gnx;
+      const int yj = j / p.gnx, xj = j - yj * p.gnx;
+      const float dx = float(xi) - float(xj), dy = float(yi) - float(yj);
+      const float a = p.gk * fmaf(p.ghx2, dx * dx, p.ghy2 * dy * dy);
+      sm.A[(size_t)i * p.ldr + j] = a;
+      sm.AT[(size_t)j * p.ldc + i] = a;
+    }
+  } else {
+    for (int e = tid; e < p.d1 * p.d2; e += NT) {
+      const int i = e / p.d2, j = e - i * p.d2;
+      sm.A[(size_t)i * p.ldr + j] = p.a2[(size_t)i * p.D2p + j];
+    }
+    for (int e = tid; e < p.d1 * p.d2; e += NT) {
+      const int j = e / p.d1, i = e - j * p.d1;
+      sm.AT[(size_t)j * p.ldc + i] = p.a2t[(size_t)j * p.D1p + i];
+    }
+  }
+  for (int e = tid; e < nl * p.d1; e += NT) {
+    const int l = e / p.d1, i = e - l * p.d1;
+    const size_t gi = (size_t)i * p.Bp + b0 + l;
+    sm.lmu[e] = p.l2mu[gi];
+    sm.mu[e] = p.mu[gi];
+    sm.f[e] = (p.mu[gi] > 0.f) ? 0.f : neg_inf();   // batch.py:295
+  }
+  for (int e = tid; e < nl * p.d2; e += NT) {
+    const int l = e / p.d2, j = e - l * p.d2;
+    const size_t gj = (size_t)j * p.Bp + b0 + l;
+    sm.lnu[e] = p.l2nu[gj];
+    sm.nu[e] = p.nu[gj];
+  }
+  __syncthreads();
+
+  // ---- lockstep iteration (batch.py:314-324), v first then u ---------------
+  unsigned int epoch = 0;
+  int cur = 0;             // g[cur] holds log_v_k
+  bool have_next = false;  // g[cur] already advanced by a check sweep
+  int iters = 0, check_no = 0;
+  for (int k = 1; k <= p.max_iters; ++k) {
+    if (!have_next) {
+      small_sweep<NT, 0>(sm.AT, p.ldc, p.d2, p.d1, p.Sc, nl, sm.f, sm.lnu, nullptr, nullptr,
+                         sm.g(cur ^ 1), nullptr, 0.f);
+      cur ^= 1;
+    }
+    have_next = false;
+    const bool last = (k == p.max_iters);
+    const bool check = p.checks && (k % p.check_interval == 0) && !last;
+    if (check || last) {
+      for (int l = tid; l < nl; l += NT) sm.rres[l] = 0u;
+      __syncthreads();
+      small_sweep<NT, 1>(sm.A, p.ldr, p.d1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, sm.mu, nullptr,
+                         sm.f, sm.rres, 0.f);
+    } else {
+      small_sweep<NT, 0>(sm.A, p.ldr, p.d1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, nullptr, nullptr,
+                         sm.f, nullptr, 0.f);
+    }
+    iters = k;
+    if (check) {
+      // column sweep k+1 doubles as the column residual of iteration k
+      small_sweep<NT, 2>(sm.AT, p.ldc, p.d2, p.d1, p.Sc, nl, sm.f, sm.lnu, sm.nu, sm.g(cur),
+                         sm.g(cur ^ 1), sm.rres, 0.f);
+      if (tid == 0) {
+        unsigned int mx = 0u;
+        for (int l = 0; l < nl; ++l) mx = max(mx, sm.rres[l]);
+        p.cta_res[(check_no & 1) * gridDim.x + blockIdx.x] = __uint_as_float(mx);
+      }
+      grid_sync(p.bar, epoch);
+      if (tid == 0) {
+        unsigned int mx = 0u;
+        for (int c = 0; c < (int)gridDim.x; ++c) {
+          float v;
+          asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];"
+                       : "=f"(v)
+                       : "l"(p.cta_res + (check_no & 1) * gridDim.x + c));
+          mx = max(mx, __float_as_uint(v));   // NaN bits exceed every finite value
+        }
+        s_conv = ((double)__uint_as_float(mx) <= (double)p.tol) ? 1 : 0;
+      }
+      __syncthreads();
+      ++check_no;
+      if (s_conv) break;   // keep g[cur] = log_v_k; the k+1 sweep is discarded
+      cur ^= 1;
+      have_next = true;
+    }
+  }
+
+  // ---- tail: column residual + E0 terms, then export (batch.py:323-337) -----
+  float* e0t = sm.g(cur ^ 1);
+  small_sweep<NT, 3>(sm.AT, p.ldc, p.d2, p.d1, p.Sc, nl, sm.f, nullptr, sm.nu, sm.g(cur), e0t,
+                     sm.rres, p.cinv);
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int l = warp; l < nl; l += NT / 32) {
+    float m = neg_inf();
+    for (int j = lane; j < p.d2; j += 32) m = fmaxf(m, e0t[l * p.d2 + j]);
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float mm = (m == neg_inf()) ? 0.f : m;
+    float s = 0.f;
+    for (int j = lane; j < p.d2; j += 32) s += ex2(e0t[l * p.d2 + j] - mm);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const float cost = exp2f(lse_final(m, s));
+      p.out_cost[b0 + l] = cost;
+      if (!isfinite(cost)) set_status(p.status, 12);
+      p.res[b0 + l] = __uint_as_float(sm.rres[l]);
+    }
+  }
+  bool nan = false;
+  for (int e = tid; e < nl * p.d1; e += NT) {
+    const float v = sm.f[e];
+    nan |= (v != v);
+    p.out_log_u[(size_t)b0 * p.d1 + e] = v * kLn2;
+  }
+  const float* gv = sm.g(cur);
+  for (int e = tid; e < nl * p.d2; e += NT) {
+    const float v = gv[e];
+    nan |= (v != v);
+    p.out_log_v[(size_t)b0 * p.d2 + e] = v * kLn2;
+  }
+  if (nan) set_status(p.status, 12);   // batch.py:326-327 NaNProduced
+  if (blockIdx.x == 0 && tid == 0) p.result[0] = iters;
+}
+
+}  // namespace skb

@@ -65,6 +65,7 @@ class SolveResult:
     iterations_run: int
     residuals: torch.Tensor   # (B,)
     loop_ms: float = -1.0     # iteration-loop time (CUDA events) when solve(time_loop=True)
+    path: str = ""            # solver path taken ("small", "tiled", "persistent", "lane")
 
 
 def _stream_handle(device: torch.device) -> int:
@@ -135,7 +136,7 @@ def _check_shapes(mu: torch.Tensor, nu: torch.Tensor, cost) -> tuple[int, int, i
 def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.0,
           check_interval: int = 10, validate: bool = True, time_loop: bool = False,
           exact_max: bool = False, mufu_only: bool = False,
-          persistent: bool = False) -> SolveResult:
+          persistent: bool = False, tiled_only: bool = False) -> SolveResult:
     """batch_forward (batch.py:264-349) on the GPU.
 
     mu (B, d1), nu (B, d2) histograms; cost a (d1, d2) tensor shared by all
@@ -159,7 +160,8 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
         int(check_interval), float(tolerance)
     op.flags = (0 if validate else _lib.FLAG_SKIP_VALIDATION) | \
         (_lib.FLAG_TIME_LOOP if time_loop else 0) | (_lib.FLAG_EXACT_MAX if exact_max else 0) | \
-        (_lib.FLAG_MUFU_ONLY if mufu_only else 0) | (_lib.FLAG_PERSISTENT if persistent else 0)
+        (_lib.FLAG_MUFU_ONLY if mufu_only else 0) | (_lib.FLAG_PERSISTENT if persistent else 0) | \
+        (_lib.FLAG_TILED_ONLY if tiled_only else 0)
     out_cost = torch.empty(B, device=dev, dtype=torch.float32)
     log_u = torch.empty(B, d1, device=dev, dtype=torch.float32)
     log_v = torch.empty(B, d2, device=dev, dtype=torch.float32)
@@ -175,7 +177,9 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
             _stream_handle(dev))
     raise_for_status(st, "sinkhorn_forward_device_v1")
     loop_ms = float(lib.sinkhorn_last_loop_ms_v1()) if time_loop else -1.0
-    return SolveResult(out_cost, log_u, log_v, float(lam), int(iters.value), residuals, loop_ms)
+    path = lib.sinkhorn_last_path_v1().decode()
+    return SolveResult(out_cost, log_u, log_v, float(lam), int(iters.value), residuals, loop_ms,
+                       path)
 
 
 def potentials_backward(log_u: torch.Tensor, log_v: torch.Tensor, lam: float,

@@ -27,7 +27,7 @@ def _skb():
     return skb
 
 
-def _run_golden(name, cuda, cost=None):
+def _run_golden(name, cuda, cost=None, **kw):
     skb = _skb()
     g = load_golden(name)
     if cost is None:
@@ -35,8 +35,13 @@ def _run_golden(name, cuda, cost=None):
         cost = torch.tensor(c, dtype=torch.float32, device=cuda)
     res = skb.solve(torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), cost,
                     float(g["lam"]), int(g["max_iters"]), float(g["tol"]),
-                    int(g["check_interval"]))
+                    int(g["check_interval"]), **kw)
     return g, res
+
+
+# Small shared/grid problems take the single-launch solver (sweep_small.cuh)
+# unless tiled_only forces the stream-K tiled sweeps; both must match.
+PATHS = [pytest.param(False, id="auto"), pytest.param(True, id="tiled")]
 
 
 def _check_loss_and_grads(g, res, loss_rtol=LOSS_RTOL, grad_atol=GRAD_ATOL):
@@ -54,10 +59,11 @@ def _check_loss_and_grads(g, res, loss_rtol=LOSS_RTOL, grad_atol=GRAD_ATOL):
     return rel.max()
 
 
+@pytest.mark.parametrize("tiled_only", PATHS)
 @pytest.mark.parametrize("name", ["config1", "rect_37x53", "stability", "config2_subset",
                                   "config5_pin4096"])
-def test_shared_cost_matches_reference(name, cuda):
-    g, res = _run_golden(name, cuda)
+def test_shared_cost_matches_reference(name, tiled_only, cuda):
+    g, res = _run_golden(name, cuda, tiled_only=tiled_only)
     _check_loss_and_grads(g, res)
     # potentials agree up to fp32 rounding of O(c/lambda) values
     lu = res.log_u.double().cpu().numpy()
@@ -67,27 +73,30 @@ def test_shared_cost_matches_reference(name, cuda):
     assert np.all(np.abs(res.residuals.double().cpu().numpy() - g["residuals"]) <= 1e-5)
 
 
-def test_closed_form_2x2(cuda):
+@pytest.mark.parametrize("tiled_only", PATHS)
+def test_closed_form_2x2(tiled_only, cuda):
     """conftest.py:9-24 / ffi.test.ts:101-116: E0 = e^-1/(1+e^-1) +- 1e-6."""
-    g, res = _run_golden("closed_form_2x2", cuda)
+    g, res = _run_golden("closed_form_2x2", cuda, tiled_only=tiled_only)
     k = math.exp(-1.0)
     assert abs(float(res.cost_e0[0]) - k / (1 + k)) <= 1e-6
     _check_loss_and_grads(g, res)
 
 
+@pytest.mark.parametrize("tiled_only", PATHS)
 @pytest.mark.parametrize("name", ["config1_tol", "lockstep"])
-def test_early_stopping_iteration_count(name, cuda):
+def test_early_stopping_iteration_count(name, tiled_only, cuda):
     """Lockstep stopping: identical iterations_run (batch.py:314-324, test_batch.py:77-90)."""
-    g, res = _run_golden(name, cuda)
+    g, res = _run_golden(name, cuda, tiled_only=tiled_only)
     assert res.iterations_run == int(g["iterations_run"])
     assert float(res.residuals.max()) <= float(g["tol"])
     _check_loss_and_grads(g, res)
 
 
-def test_zero_mass_lanes(cuda):
+@pytest.mark.parametrize("tiled_only", PATHS)
+def test_zero_mass_lanes(tiled_only, cuda):
     """-inf exactly where mass is 0; backward refuses the lane (test_batch.py:185-198)."""
     skb = _skb()
-    g, res = _run_golden("zero_mass", cuda)
+    g, res = _run_golden("zero_mass", cuda, tiled_only=tiled_only)
     lu = res.log_u.double().cpu().numpy()
     lv = res.log_v.double().cpu().numpy()
     assert np.array_equal(np.isneginf(lu), np.isneginf(g["log_u"]))
@@ -172,8 +181,8 @@ def test_estimate_mode_matches_exact_two_pass(name, cuda):
     c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
     args = (torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
             float(g["lam"]), int(g["max_iters"]), float(g["tol"]), int(g["check_interval"]))
-    fast = skb.solve(*args)
-    exact = skb.solve(*args, exact_max=True)
+    fast = skb.solve(*args, tiled_only=True)
+    exact = skb.solve(*args, exact_max=True, tiled_only=True)
     assert fast.iterations_run == exact.iterations_run
     rel = (fast.cost_e0.double() - exact.cost_e0.double()).abs() / exact.cost_e0.double().abs()
     assert float(rel.max()) <= 2e-6
@@ -208,7 +217,7 @@ def test_persistent_loop_matches_reference(name, cuda):
     c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
     res = skb.solve(torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
                     float(g["lam"]), int(g["max_iters"]), float(g["tol"]),
-                    int(g["check_interval"]), persistent=True)
+                    int(g["check_interval"]), persistent=True, tiled_only=True)
     ref = skb.solve(torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
                     float(g["lam"]), int(g["max_iters"]), float(g["tol"]),
                     int(g["check_interval"]))
@@ -216,3 +225,52 @@ def test_persistent_loop_matches_reference(name, cuda):
     rel = np.abs(res.cost_e0.double().cpu().numpy() - g["cost_e0"]) / g["cost_e0"]
     assert rel.max() <= LOSS_RTOL
     assert torch.equal(torch.isneginf(res.log_u), torch.isneginf(ref.log_u))
+
+
+def test_small_problem_runs_in_one_solver_launch(cuda):
+    """Config 1 shape: the whole lockstep loop is one kernel launch (plus setup)."""
+    skb = _skb()
+    from paper_1907_01729_b200 import _lib
+
+    lib = _lib.load()
+    g = load_golden("config1")
+    args = (torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda),
+            torch.tensor(g["cost"], dtype=torch.float32, device=cuda), float(g["lam"]),
+            int(g["max_iters"]), 0.0, 10)
+    n0 = lib.sinkhorn_launch_count_v1()
+    skb.solve(*args)
+    small = lib.sinkhorn_launch_count_v1() - n0
+    n0 = lib.sinkhorn_launch_count_v1()
+    skb.solve(*args, tiled_only=True)
+    tiled = lib.sinkhorn_launch_count_v1() - n0
+    assert small <= 8 < 200 <= tiled, (small, tiled)
+
+
+@pytest.mark.parametrize("kind", ["shared", "grid"])
+def test_small_solver_many_lanes_per_cta_lockstep(kind, cuda):
+    """Several lanes per CTA and a cross-CTA lockstep stop, against the oracle."""
+    skb = _skb()
+    from oracle import sinkhorn_oracle as orc
+
+    rng = np.random.default_rng(7)
+    if kind == "shared":
+        B, d1, d2 = 700, 40, 56
+        c = orc.fp32_exact(rng.random((d1, d2)))
+        cost = torch.tensor(c, dtype=torch.float32, device=cuda)
+        lam = 0.2
+    else:
+        B, d1, d2 = 400, 64, 64
+        c = orc.grid2d_cost(8, 8)
+        cost = skb.GridCost(8, 8)
+        lam = 0.5
+    mu = orc.fp32_exact(orc.random_histogram_batch(B, d1, rng))
+    nu = orc.fp32_exact(orc.random_histogram_batch(B, d2, rng))
+    ref = orc.batch_forward(mu, nu, c, lam, max_iters=400, tolerance=1e-5, check_interval=5)
+    res = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda), cost, lam,
+                    400, 1e-5, 5)
+    assert res.iterations_run == ref.iterations_run
+    rel = np.abs(res.cost_e0.double().cpu().numpy() - ref.cost_e0) / ref.cost_e0
+    assert rel.max() <= LOSS_RTOL
+    tiled = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda), cost, lam,
+                      400, 1e-5, 5, tiled_only=True)
+    assert tiled.iterations_run == res.iterations_run
