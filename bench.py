@@ -165,6 +165,7 @@ KERNEL_OF_PATH = {
     "small": "small_solve_kernel (whole solve in one launch, cost in shared memory)",
     "persistent": "persistent_solve_kernel (cooperative whole loop)",
     "lane": "lane_col_kernel / lane_row_kernel (per-sample sweep)",
+    "separable": "sep_sweep_kernel (separable grid LSE: two nested 1-D LSE-GEMMs per sweep)",
 }
 
 
@@ -183,12 +184,17 @@ def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
     sms = 148
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
-    achieved = cells / (sweep_ms * 1e-3) / 1e12            # one ex2 per cell per sweep
+    ex2 = cells                                            # one ex2 per cell per sweep
+    if path == "separable":
+        # nested 1-D LSEs: B * (nx*ny) * (nx + ny) exponentials per sweep
+        ex2 = float(cfg["B"]) * cfg["d"] * (2 * cfg["nx"])
+    achieved = ex2 / (sweep_ms * 1e-3) / 1e12
     peak = sms * MUFU_PER_SM_CLK * fmax * 1e6 / 1e12
     out = {"bound": "mufu", "achieved": achieved, "peak": peak, "unit": "Tex2/s",
            "frac": achieved / peak, "traffic": traffic,
            "kernel": KERNEL_OF_PATH.get(path, path),
-           "algorithmic_per_launch": f"{cells:.4g} ex2 (1 per cell)",
+           "algorithmic_per_launch": (f"{ex2:.4g} ex2 (B*d*(nx+ny), separable)"
+                                      if path == "separable" else f"{cells:.4g} ex2 (1 per cell)"),
            "peak_source": f"148 SM x {MUFU_PER_SM_CLK} ex2/clk x sm_max_mhz {fmax:.0f} "
                           "(MEASURED_PEAKS.json)"}
     if clocks.get("sm_mhz"):

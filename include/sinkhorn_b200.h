@@ -96,6 +96,7 @@ typedef struct sinkhorn_problem_v1 {
 #define SINKHORN_FLAG_MUFU_ONLY 16u      /* every exponential on MUFU (no FMA-pipe polynomial) */
 #define SINKHORN_FLAG_PERSISTENT 32u     /* shared/grid costs: whole loop in one cooperative kernel */
 #define SINKHORN_FLAG_TILED_ONLY 64u     /* never take the single-launch small-problem solver */
+#define SINKHORN_FLAG_DENSE_GRID 128u    /* grid costs: dense on-the-fly sweeps, not separable */
 
 typedef struct sinkhorn_options_v1 {
   double lambda;          /* > 0, finite */
@@ -191,7 +192,7 @@ float sinkhorn_last_loop_ms_v1(void);
 /* Solver path of this thread's last forward: "small" (one-launch solve,
  * cost in shared memory), "tiled" (stream-K sweeps), "persistent" (opt-in
  * cooperative loop) or "lane" (per-sample costs). */
-const char* sinkhorn_last_path_v1(void);
+const char* sinkhorn_last_path_v1(void);   /* ... or "separable" (grid costs) */
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,8 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB_NAME = "libsinkhorn_b200.so"
 SOURCES = ["sinkhorn_abi.cu"]
-HEADERS = ["common.cuh", "sweep_tiled.cuh", "sweep_lane.cuh", "sweep_small.cuh", "persistent.cuh",
+HEADERS = ["common.cuh", "sweep_tiled.cuh", "sweep_lane.cuh", "sweep_small.cuh", "sweep_sep.cuh",
+           "persistent.cuh",
            "aux_kernels.cuh"]
 
 NVCC_FLAGS = [

@@ -34,6 +34,7 @@ FLAG_EXACT_MAX = 8
 FLAG_MUFU_ONLY = 16
 FLAG_PERSISTENT = 32
 FLAG_TILED_ONLY = 64
+FLAG_DENSE_GRID = 128
 
 # every symbol include/sinkhorn_b200.h declares
 EXPORTED_SYMBOLS = (

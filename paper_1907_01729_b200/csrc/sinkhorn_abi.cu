@@ -26,6 +26,7 @@
 #include "sweep_tiled.cuh"
 #include "persistent.cuh"
 #include "sweep_small.cuh"
+#include "sweep_sep.cuh"
 
 using namespace skb;
 
@@ -161,6 +162,7 @@ struct Carver {
 
 struct Layout {
   bool tiled = true;
+  bool sep = false;               // grid cost, separable sweeps (lane-major buffers)
   int64_t B = 0, d1 = 0, d2 = 0;
   int Bp = 0, D1p = 0, D2p = 0;   // padded extents (tiled) / leading dims (lane)
   long long sb1 = 0, si1 = 0, sb2 = 0, si2 = 0;  // element (b,i) at b*sb + i*si
@@ -170,12 +172,16 @@ struct Layout {
   int lane_nsplit = 1, lane_nj = 1, lane_vec = 4;
 };
 
-Layout make_layout(const sinkhorn_problem_v1& pr, int sms) {
+// Grid costs run the separable sweeps on lane-major buffers unless the dense
+// on-the-fly tiled sweeps are requested (SINKHORN_FLAG_DENSE_GRID).
+Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = false) {
   Layout L;
   L.B = pr.B;
   L.d1 = pr.d1;
   L.d2 = pr.d2;
-  L.tiled = (pr.cost_kind != SINKHORN_COST_PER_SAMPLE);
+  L.sep = pr.cost_kind == SINKHORN_COST_GRID2D && !dense_grid;
+  L.tiled = pr.cost_kind == SINKHORN_COST_SHARED ||
+            (pr.cost_kind == SINKHORN_COST_GRID2D && dense_grid);
   Carver c;
   if (L.tiled) {
     L.Bp = (int)round_up(pr.B, pick_bt(pr.B));
@@ -228,12 +234,21 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms) {
     L.counter_count = (size_t)pr.B * L.lane_nj;
   }
   L.res = c.take((size_t)std::max(L.Bp, 1) * 4);
+  if (L.sep) L.part = c.take(std::max<size_t>(L.part_bytes, (size_t)sms * 8 * 2 * 4));
   L.scratch = c.take(64);
   L.counters = c.take(std::max<size_t>(L.counter_count, 1) * 4);
   L.status = c.take(4);
   L.badrow = c.take(4);
   L.total = c.off;
   return L;
+}
+
+// Workspace bytes for a problem under every option set (grid costs can take
+// either the separable or the dense tiled layout).
+size_t workspace_total(const sinkhorn_problem_v1& pr, int sms) {
+  size_t t = make_layout(pr, sms).total;
+  if (pr.cost_kind == SINKHORN_COST_GRID2D) t = std::max(t, make_layout(pr, sms, true).total);
+  return t;
 }
 
 template <typename T>
@@ -384,6 +399,46 @@ struct Solve {
   }
 
   // column half-sweep: g2[dst] = l2nu - LSE_i(A2 + f2)
+  // ---- separable grid sweeps (sweep_sep.cuh) --------------------------------
+#ifndef SKB_SEP_RN
+#define SKB_SEP_RN 2
+#endif
+  using SepS = SepShape<32, SKB_SEP_RN, (SKB_SEP_RN == 2) ? 256 : 128>;
+  static constexpr int kSepNB = SepS::NB;
+  int sep_sweep(int mode, const float* x, const float* target, const float* marg,
+                const float* old, float* out, int res_kind, const float* est_src = nullptr) {
+    SepParams p = {};
+    p.nx = (int)pr.grid_nx;
+    p.ny = (int)pr.grid_ny;
+    p.ax = (float)(-kLog2e / lam) * (pr.grid_hx * pr.grid_hx);
+    p.ay = (float)(-kLog2e / lam) * (pr.grid_hy * pr.grid_hy);
+    p.cinv = -lam * kLn2;
+    p.x = x;
+    p.target = target;
+    p.marg = marg;
+    p.old = old;
+    p.out = out;
+    p.res = F(L.res);
+    p.res_kind = res_kind;
+    p.ld = L.D1p;
+    p.B = (int)pr.B;
+    p.nblk = (p.nx + kSepNB - 1) / kSepNB;
+    p.use_poly = poly ? 1 : 0;
+    p.est_src = est_src;
+    p.redo = at<unsigned int>(ws, L.scratch + 48);
+    const bool tail = mode == kModeTail;
+    const size_t smem = sep_smem_floats<SepS>(p.nx, p.ny, tail) * 4;
+    auto kern = tail ? &sep_sweep_kernel<SepS, kModeTail> : &sep_sweep_kernel<SepS, kModeUpdate>;
+    static size_t attr_bytes[2] = {0, 0};
+    if (attr_bytes[tail] < smem) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_bytes[tail] = smem;
+    }
+    dim3 grid((unsigned)p.nblk, (unsigned)pr.B);
+    CK(launch_pdl(kern, grid, dim3(SepS::NT), smem, st, p));
+    return 0;
+  }
+
   int col_sweep(int dst, int src_old, int res_kind) {
     if (L.tiled) {
       TiledArgs a = {&tm_a2, &tm_f2, (int)pr.d1, (int)pr.d2, L.D1p, L.D2p, F(L.l2nu), F(L.nu),
@@ -393,6 +448,9 @@ struct Solve {
                  ? launch_tiled<true, kModeUpdate>(L, ws, di, a, pr, lam, st)
                  : launch_tiled<false, kModeUpdate>(L, ws, di, a, pr, lam, st);
     }
+    if (L.sep)
+      return sep_sweep(kModeUpdate, F(L.f2), F(L.l2nu), F(L.nu), F(L.g2[src_old]), F(L.g2[dst]),
+                       res_kind, est ? F(L.g2[src_old]) : nullptr);
     return lane_col(kModeUpdate, F(L.g2[dst]), F(L.g2[src_old]), res_kind);
   }
 
@@ -406,6 +464,9 @@ struct Solve {
                  ? launch_tiled<true, kModeUpdate>(L, ws, di, a, pr, lam, st)
                  : launch_tiled<false, kModeUpdate>(L, ws, di, a, pr, lam, st);
     }
+    if (L.sep)
+      return sep_sweep(kModeUpdate, F(L.g2[src]), F(L.l2mu), F(L.mu), nullptr, F(L.f2), res_kind,
+                       est ? F(L.f2) : nullptr);
     LaneSweepParams p = lane_params();
     p.x = F(L.g2[src]);
     p.ldx = L.D2p;
@@ -434,6 +495,8 @@ struct Solve {
                  ? launch_tiled<true, kModeTail>(L, ws, di, a, pr, lam, st)
                  : launch_tiled<false, kModeTail>(L, ws, di, a, pr, lam, st);
     }
+    if (L.sep)
+      return sep_sweep(kModeTail, F(L.f2), nullptr, F(L.nu), F(L.g2[cur]), F(L.e0), kResCol);
     return lane_col(kModeTail, nullptr, F(L.g2[cur]), kResCol);
   }
 
@@ -578,7 +641,8 @@ struct Solve {
   // Returns a status (non-zero only on a CUDA error); *ok says whether to use it.
   int plan_small(SmallParams& sp, int& G, size_t& smem, bool* ok) {
     *ok = false;
-    if (!L.tiled || g_reducer != nullptr || (op.flags & SINKHORN_FLAG_TILED_ONLY)) return 0;
+    if (!(L.tiled || L.sep) || g_reducer != nullptr || (op.flags & SINKHORN_FLAG_TILED_ONLY))
+      return 0;
     if (pr.cost_kind != SINKHORN_COST_SHARED && pr.cost_kind != SINKHORN_COST_GRID2D) return 0;
     static int smem_optin = 0;
     if (smem_optin == 0)
@@ -622,7 +686,10 @@ struct Solve {
       sp.mu = F(L.mu);
       sp.nu = F(L.nu);
       sp.B = (int)B;
-      sp.Bp = L.Bp;
+      sp.sb1 = L.sb1;
+      sp.si1 = L.si1;
+      sp.sb2 = L.sb2;
+      sp.si2 = L.si2;
       sp.d1 = (int)d1;
       sp.d2 = (int)d2;
       sp.L = Lc;
@@ -727,7 +794,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   S.pr = pr;
   S.op = op;
   S.di = device_info();
-  S.L = make_layout(pr, S.di.sms);
+  S.L = make_layout(pr, S.di.sms, (op.flags & SINKHORN_FLAG_DENSE_GRID) != 0);
   S.ws = ws;
   S.st = st;
   S.lam = (float)op.lambda;
@@ -743,6 +810,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   // ---- setup (batch.py:279-296) ----
   CK(cudaMemsetAsync(status, 0, 4, st));
   CK(cudaMemsetAsync(S.est_fail, 0, 4, st));
+  CK(cudaMemsetAsync(at<int>(ws, L.scratch + 48), 0, 4, st));   // estimate redo count
   CK(cudaMemsetAsync(badrow, 0x7f, 4, st));
   CK(cudaMemsetAsync(at<int>(ws, L.counters), 0, std::max<size_t>(L.counter_count, 1) * 4, st));
   CK(cudaMemsetAsync(S.F(L.res), 0, (size_t)std::max(L.Bp, 1) * 4, st));
@@ -815,7 +883,11 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   } else if (persist) {
     if (int e = S.persistent_loop(op, allow_est, &iters, &cur)) return e;
   }
-  g_last_path = small ? "small" : persist ? "persistent" : L.tiled ? "tiled" : "lane";
+  g_last_path = small     ? "small"
+                : persist ? "persistent"
+                : L.tiled ? "tiled"
+                : L.sep   ? "separable"
+                          : "lane";
   for (int k = 1; !persist && !small && k <= op.max_iters; ++k) {
     // estimate mode once the potentials have settled past the first sweeps
     S.est = allow_est && k >= kEstFromIter;
@@ -899,6 +971,12 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
                           out_residuals, ws, ws_bytes, st, false);
     }
   }
+  static const bool stats = getenv("SKB_SEP_STATS") != nullptr;   // diagnostics
+  if (stats && L.sep) {
+    unsigned int redo = 0;
+    cudaMemcpy(&redo, at<unsigned int>(ws, L.scratch + 48), 4, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[skb] separable estimate redos: %u thread tiles\n", redo);
+  }
   if (timed) {
     float ms = -1.f;
     cudaEventElapsedTime(&ms, ev0, ev1);
@@ -937,7 +1015,7 @@ const char* sinkhorn_last_path_v1(void) { return g_last_path; }
 
 size_t sinkhorn_workspace_bytes_v1(const sinkhorn_problem_v1* prob) {
   if (check_problem(prob) != 0) return 0;
-  return make_layout(*prob, device_info().sms).total;
+  return workspace_total(*prob, device_info().sms);
 }
 
 int32_t sinkhorn_forward_device_v1(const sinkhorn_problem_v1* prob,

@@ -29,11 +29,12 @@ struct SmallParams {
   int grid, gnx;      // grid cost recomputed into shared memory
   float gk, ghx2, ghy2;
   float cinv;         // cost = A2 * cinv (E0 weights)
-  const float* l2mu;  // solver layout: element (b, i) at i * Bp + b
-  const float* l2nu;
+  const float* l2mu;  // solver layout: element (b, i) at b * sb1 + i * si1
+  const float* l2nu;  //                 element (b, j) at b * sb2 + j * si2
   const float* mu;
   const float* nu;
-  int B, Bp, d1, d2;
+  long long sb1, si1, sb2, si2;
+  int B, d1, d2;
   int L;              // lanes per CTA
   int Sc, Sr;         // threads per output: column sweep (reduces d1) / row sweep (reduces d2)
   int ldc, ldr;       // shared leading dims of A2T (column sweep) and A2 (row sweep)
@@ -214,14 +215,14 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
   }
   for (int e = tid; e < nl * p.d1; e += NT) {
     const int l = e / p.d1, i = e - l * p.d1;
-    const size_t gi = (size_t)i * p.Bp + b0 + l;
+    const size_t gi = (size_t)(b0 + l) * p.sb1 + (size_t)i * p.si1;
     sm.lmu[e] = p.l2mu[gi];
     sm.mu[e] = p.mu[gi];
     sm.f[e] = (p.mu[gi] > 0.f) ? 0.f : neg_inf();   // batch.py:295
   }
   for (int e = tid; e < nl * p.d2; e += NT) {
     const int l = e / p.d2, j = e - l * p.d2;
-    const size_t gj = (size_t)j * p.Bp + b0 + l;
+    const size_t gj = (size_t)(b0 + l) * p.sb2 + (size_t)j * p.si2;
     sm.lnu[e] = p.l2nu[gj];
     sm.nu[e] = p.nu[gj];
   }

@@ -136,7 +136,8 @@ def _check_shapes(mu: torch.Tensor, nu: torch.Tensor, cost) -> tuple[int, int, i
 def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.0,
           check_interval: int = 10, validate: bool = True, time_loop: bool = False,
           exact_max: bool = False, mufu_only: bool = False,
-          persistent: bool = False, tiled_only: bool = False) -> SolveResult:
+          persistent: bool = False, tiled_only: bool = False,
+          dense_grid: bool = False) -> SolveResult:
     """batch_forward (batch.py:264-349) on the GPU.
 
     mu (B, d1), nu (B, d2) histograms; cost a (d1, d2) tensor shared by all
@@ -161,7 +162,7 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
     op.flags = (0 if validate else _lib.FLAG_SKIP_VALIDATION) | \
         (_lib.FLAG_TIME_LOOP if time_loop else 0) | (_lib.FLAG_EXACT_MAX if exact_max else 0) | \
         (_lib.FLAG_MUFU_ONLY if mufu_only else 0) | (_lib.FLAG_PERSISTENT if persistent else 0) | \
-        (_lib.FLAG_TILED_ONLY if tiled_only else 0)
+        (_lib.FLAG_TILED_ONLY if tiled_only else 0) | (_lib.FLAG_DENSE_GRID if dense_grid else 0)
     out_cost = torch.empty(B, device=dev, dtype=torch.float32)
     log_u = torch.empty(B, d1, device=dev, dtype=torch.float32)
     log_v = torch.empty(B, d2, device=dev, dtype=torch.float32)

@@ -108,11 +108,42 @@ def test_zero_mass_lanes(tiled_only, cuda):
     assert exc.value.lane == int(g["zero_mass_lane"])
 
 
-def test_grid_cost_on_the_fly(cuda):
-    """BASELINE config 3 subset: 64x64 grid, lambda 1e-3, cost never materialised."""
+@pytest.mark.parametrize("dense_grid", [pytest.param(False, id="separable"),
+                                        pytest.param(True, id="dense")])
+def test_grid_cost_on_the_fly(dense_grid, cuda):
+    """BASELINE config 3 subset: 64x64 grid, lambda 1e-3, cost never materialised,
+    through the separable nested LSE (default) and the dense on-the-fly tiles."""
     skb = _skb()
-    g, res = _run_golden("config3_subset", cuda, cost=skb.GridCost(64, 64))
+    g, res = _run_golden("config3_subset", cuda, cost=skb.GridCost(64, 64),
+                         dense_grid=dense_grid)
+    assert res.path == ("tiled" if dense_grid else "separable")
     _check_loss_and_grads(g, res)
+
+
+@pytest.mark.parametrize("nx,ny,tol", [(12, 7, 0.0), (40, 20, 0.0), (33, 70, 1e-4),
+                                       (5, 1, 0.0)])
+def test_separable_grid_ragged_shapes(nx, ny, tol, cuda):
+    """Separable sweeps on ragged grids (partial jx blocks, ny > one m tile,
+    1-D grids) against the oracle's dense float64 cost, incl. lockstep stops."""
+    skb = _skb()
+    from oracle import sinkhorn_oracle as orc
+
+    rng = np.random.default_rng(nx * 100 + ny)
+    B, d = 3, nx * ny
+    mu = orc.fp32_exact(orc.random_histogram_batch(B, d, rng))
+    nu = orc.fp32_exact(orc.random_histogram_batch(B, d, rng))
+    lam = 0.05
+    c = orc.grid2d_cost(nx, ny)
+    ref = orc.batch_forward(mu, nu, c, lam, max_iters=60, tolerance=tol, check_interval=5)
+    res = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda),
+                    skb.GridCost(nx, ny), lam, 60, tol, 5, tiled_only=True)
+    assert res.path == "separable"
+    assert res.iterations_run == ref.iterations_run
+    rel = np.abs(res.cost_e0.double().cpu().numpy() - ref.cost_e0) / ref.cost_e0
+    assert rel.max() <= LOSS_RTOL
+    lu = res.log_u.double().cpu().numpy()
+    assert np.abs(lu - ref.log_u).max() <= 1e-4 * max(1.0, np.abs(ref.log_u).max())
+    assert np.all(np.abs(res.residuals.double().cpu().numpy() - ref.residuals) <= 1e-5)
 
 
 def test_per_sample_cost(cuda):
