@@ -59,7 +59,7 @@ constexpr int QC = 32, RB = 4, RP = 4, NSTAGE = 4;
 constexpr int BT_MAX = 128;   // lane tile: 128 (16 warps, 1 CTA/SM) or 64 (8 warps, 2 CTAs/SM)
 constexpr int PT_MAX = 64;    // output-tile widths: 64 or 56 (picked per sweep, see pick_pt)
 constexpr int TILE_PAD = 64;  // buffer extents padded to 64 (>= every tile / TMA box)
-constexpr int MAX_OCC = 2;
+constexpr int MAX_OCC = SKB_OCC_SMALL > 2 ? SKB_OCC_SMALL : 2;
 constexpr int kEstFromIter = 3;   // first iteration whose sweeps start from the previous lse
 
 template <int BT, int PT, bool kGrid, int kMode>
@@ -72,7 +72,10 @@ struct TiledK {
 
 // Lane tile: 128 lanes (one 16-warp CTA per SM: no inter-CTA warp-priority
 // skew, half as many stream-K pieces per tile) whenever the batch has > 64 lanes.
-int pick_bt(int64_t B) { return B > 64 ? 128 : 64; }
+#ifndef SKB_BT_BIG
+#define SKB_BT_BIG 128
+#endif
+int pick_bt(int64_t B) { return B > 64 ? SKB_BT_BIG : 64; }
 
 // Output-tile width.  Always 64 (8 warps: an even 4 warps per scheduler at 2
 // CTAs/SM; 7-warp tiles left the 4 SMSPs 4/4/3/3).  A ragged extent is covered

@@ -92,6 +92,9 @@ constexpr float kParked = 1.0e30f;   // running max of outputs whose target is -
 #endif
 constexpr int kPolyPairs = SKB_POLY_PAIRS;
 
+#ifndef SKB_OCC_SMALL
+#define SKB_OCC_SMALL 2   // resident 256-thread (64-lane) tiles per SM
+#endif
 template <int BT, int PT, int QC, int RB, int RP, int NSTAGE, bool kGrid, int kMode>
 struct TiledSweep {
   static constexpr int NT = (BT / RB) * (PT / RP);
@@ -105,7 +108,7 @@ struct TiledSweep {
       size_t(NSTAGE) * STAGE_FLOATS * 4 + 64 * 8 /*bars*/ + BT * 4 +
       (kGrid ? (QC + PT) * 8 : 0);
   static_assert(NTB == 16 || NTB == 32, "lane-threads per (half) warp");
-  static constexpr int OCC = (NT >= 512) ? 1 : 2;   // CTAs per SM the launch bounds target
+  static constexpr int OCC = (NT >= 512) ? 1 : SKB_OCC_SMALL;   // CTAs per SM the launch bounds target
   static_assert(NT % 32 == 0, "whole warps");
   static_assert(RB == 4 && RP == 4, "float4 tile loads");
   static_assert(QC % 4 == 0, "unroll");
@@ -569,7 +572,7 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
 }
 
 template <int BT, int PT, int QC, int RB, int RP, int NSTAGE, bool kGrid, int kMode>
-__global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) >= 512) ? 1 : 2)
+__global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) >= 512) ? 1 : SKB_OCC_SMALL)
     tiled_sweep_kernel(const __grid_constant__ CUtensorMap tmap_g,
                        const __grid_constant__ CUtensorMap tmap_x, const TiledSweepParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];

@@ -85,18 +85,21 @@ def launches(path: str) -> None:
         print(f"| {v[0]} | {v[1] / 1e3:.1f} | {100 * v[1] / tot:.1f}% | `{k}` |")
 
 
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
+
 def traffic(rep: str, cfg: str) -> None:
-    rows, _ = raw(rep)
+    rows, units = raw(rep)
     vals = []
     for d in rows:
         try:
-            vals.append(float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"]))
+            vals.append(sum(float(d[k].replace(",", "")) * SCALE.get(units.get(k, "byte"), 1.0)
+                            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum")))
         except (KeyError, ValueError):
             pass
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
                         "ncu_summary.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
-    # ncu reports dram bytes in the report's unit (usually byte); assume bytes
     data[cfg] = {"dram_bytes_per_sweep_launch": sum(vals) / max(len(vals), 1),
                  "source": os.path.basename(rep)}
     json.dump(data, open(path, "w"), indent=1)
