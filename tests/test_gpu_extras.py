@@ -1,0 +1,121 @@
+"""GPU tests beyond the forward/backward parity: dC through the transport plan
+ and the distributed drivers on one device.
+
+dC is checked against the oracle's transport_plan (core.py:363-368) evaluated
+on the reference's own final potentials; the sharded drivers run with a
+one-rank NCCL group, which exercises their collectives and the CUDA shard
+backend (half-sweep C ABI) end to end against the reference fixtures.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import GRAD_ATOL, LOSS_RTOL, golden_cost, load_golden
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _skb():
+    import paper_1907_01729_b200 as skb
+
+    return skb
+
+
+def _plan_grad_ref(g, c):
+    from oracle import sinkhorn_oracle as orc
+
+    up = g["upstream"]
+    if c.ndim == 2:
+        return sum(up[b] * orc.transport_plan(g["log_u"][b], g["log_v"][b], c, float(g["lam"]))
+                   for b in range(len(up)))
+    return np.stack([up[b] * orc.transport_plan(g["log_u"][b], g["log_v"][b], c[b], float(g["lam"]))
+                     for b in range(len(up))])
+
+
+@pytest.mark.parametrize("name", ["config1", "rect_37x53", "config4_subset"])
+def test_plan_gradient_matches_transport_plan(name, cuda):
+    """dC = sum_b up_b P_b (shared) / up_b P_b (per-sample) from the final potentials."""
+    skb = _skb()
+    g = load_golden(name)
+    c = golden_cost(g)
+    want = _plan_grad_ref(g, c)
+    got = skb.plan_gradient(torch.tensor(g["log_u"], dtype=torch.float32, device=cuda),
+                            torch.tensor(g["log_v"], dtype=torch.float32, device=cuda),
+                            torch.tensor(c, dtype=torch.float32, device=cuda), float(g["lam"]),
+                            torch.tensor(g["upstream"], dtype=torch.float32, device=cuda))
+    got = got.double().cpu().numpy()
+    scale = np.abs(want).max()
+    assert np.abs(got - want).max() <= 1e-4 * scale
+
+
+def test_autograd_reaches_the_cost(cuda):
+    """sinkhorn_loss(..., cost.requires_grad) returns dC through the plan."""
+    skb = _skb()
+    g = load_golden("config1")
+    c = golden_cost(g)
+    mu = torch.tensor(g["mu"], device=cuda)
+    nu = torch.tensor(g["nu"], device=cuda)
+    ct = torch.tensor(c, dtype=torch.float32, device=cuda, requires_grad=True)
+    loss = skb.sinkhorn_loss(mu, nu, ct, float(g["lam"]), max_iters=int(g["max_iters"]))
+    loss.backward(torch.tensor(g["upstream"], dtype=torch.float32, device=cuda))
+    want = _plan_grad_ref(g, c)
+    assert np.abs(ct.grad.double().cpu().numpy() - want).max() <= 1e-4 * np.abs(want).max()
+
+
+@pytest.fixture(scope="module")
+def nccl_world1(cuda):
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["config5_pin4096", "rect_37x53", "config1_tol"])
+def test_row_sharded_solve_on_the_device(name, nccl_world1, cuda):
+    """row_sharded_solve + CudaShardBackend (NCCL, one rank) against the reference."""
+    from paper_1907_01729_b200 import distributed as D
+
+    g = load_golden(name)
+    c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
+    mu = torch.tensor(g["mu"], dtype=torch.float32, device=cuda)
+    nu = torch.tensor(g["nu"], dtype=torch.float32, device=cuda)
+    res = D.row_sharded_solve(mu, nu, D.CudaShardBackend(c), float(g["lam"]), int(g["max_iters"]),
+                              float(g["tol"]), int(g["check_interval"]))
+    assert res.iterations_run == int(g["iterations_run"])
+    rel = np.abs(res.cost_e0.double().cpu().numpy() - g["cost_e0"]) / g["cost_e0"]
+    assert rel.max() <= LOSS_RTOL
+    gm, gn = D.row_sharded_backward(res.log_u, res.log_v, float(g["lam"]),
+                                    torch.tensor(g["upstream"], device=cuda))
+    assert np.abs(gm.double().cpu().numpy() - g["grad_mu"]).max() <= GRAD_ATOL
+    assert np.abs(gn.double().cpu().numpy() - g["grad_nu"]).max() <= GRAD_ATOL
+
+
+def test_batch_sharded_solve_on_the_device(nccl_world1, cuda):
+    """batch_sharded_solve (NCCL, one rank): local solve + the final loss all-gather."""
+    from paper_1907_01729_b200 import distributed as D
+
+    g = load_golden("config1_tol")
+    c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
+    res, all_costs = D.batch_sharded_solve(torch.tensor(g["mu"], device=cuda),
+                                           torch.tensor(g["nu"], device=cuda), c,
+                                           float(g["lam"]), int(g["max_iters"]), float(g["tol"]),
+                                           int(g["check_interval"]))
+    assert res.iterations_run == int(g["iterations_run"])
+    rel = np.abs(all_costs.double().cpu().numpy() - g["cost_e0"]) / g["cost_e0"]
+    assert rel.max() <= LOSS_RTOL
