@@ -56,7 +56,6 @@ int fail(int code, const std::string& msg) {
 
 // ---- tiled-sweep configuration ---------------------------------------------
 constexpr int QC = 32, RB = 4, RP = 4, NSTAGE = 4;
-constexpr int BT_MAX = 128;   // lane tile: 128 (16 warps, 1 CTA/SM) or 64 (8 warps, 2 CTAs/SM)
 constexpr int PT_MAX = 64;    // output-tile widths: 64 or 56 (picked per sweep, see pick_pt)
 constexpr int TILE_PAD = 64;  // buffer extents padded to 64 (>= every tile / TMA box)
 constexpr int MAX_OCC = SKB_OCC_SMALL > 2 ? SKB_OCC_SMALL : 2;
@@ -874,7 +873,6 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   int cur = 0;            // g2[cur] holds log_v_k
   bool have_next = false; // g2[cur] already advanced by a check sweep
   int iters = 0;
-  bool converged = false;
   // Opt-in: the whole loop in one cooperative kernel (no launches, device-side
   // stopping test).  Off by default: its grid barriers (~3.5 us each, two per
   // half-sweep) cost more than the launch gaps they remove.
@@ -921,14 +919,13 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
       if (g_reducer) gmax = g_reducer(gmax, g_reducer_user);   // every rank calls it per check
       if (hstatus != 0) break;
       if (gmax <= op.tolerance) {
-        converged = true;   // keep g2[cur] = log_v_k; discard the k+1 sweep
+        // converged: keep g2[cur] = log_v_k; discard the k+1 sweep
         break;
       }
       cur ^= 1;
       have_next = true;
     }
   }
-  (void)converged;
   if (timed) CK(cudaEventRecord(ev1, st));
   // ---- tail: residual + stable E0 in one column pass (batch.py:323-337) ----
   S.est = allow_est && iters >= kEstFromIter;

@@ -147,13 +147,13 @@ __device__ __forceinline__ void tile_epilogue(const TiledSweepParams& p, const S
       const int pp = p0 + tp * RP + rp;
       if (pp >= p.Pv || pp < own_lo) continue;
       const size_t row = size_t(pp) * p.Bp + bb;
-      if (kMode == kModePartial) {
+      if constexpr (kMode == kModePartial) {
         *reinterpret_cast<float4*>(p.pmax + row) =
             make_float4(M[0 * RP + rp], M[1 * RP + rp], M[2 * RP + rp], M[3 * RP + rp]);
         *reinterpret_cast<float4*>(p.psum + row) =
             make_float4(Sm[0 * RP + rp], Sm[1 * RP + rp], Sm[2 * RP + rp], Sm[3 * RP + rp]);
         continue;
-      }
+      } else {
       float lse[RB];
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) lse[rb] = lse_final(M[rb * RP + rp], Sm[rb * RP + rp]);
@@ -201,6 +201,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledSweepParams& p, const S
         }
         *reinterpret_cast<float4*>(p.e0 + row) = make_float4(ev[0], ev[1], ev[2], ev[3]);
       }
+      }   // if constexpr (kMode == kModePartial) ... else
     }
     if (p.res != nullptr && (kMode == kModeTail || d.res_kind != kResNone)) {
 #pragma unroll
