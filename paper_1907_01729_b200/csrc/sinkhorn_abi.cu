@@ -650,27 +650,56 @@ struct Solve {
     if (smem_optin == 0)
       cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, di.dev);
     const long long d1 = pr.d1, d2 = pr.d2, B = pr.B;
+    static bool attr_set = false;
+    auto kern = &small_solve_kernel<kSmallNT>;
+    if (!attr_set) {
+      cudaFuncAttributes fa = {};
+      CK(cudaFuncGetAttributes(&fa, kern));
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              smem_optin - (int)fa.sharedSizeBytes));
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      attr_set = true;
+    }
     for (int occ = 4; occ >= 1; --occ) {
       const int Lc = (int)((B + (long long)di.sms * occ - 1) / ((long long)di.sms * occ));
       if ((long long)Lc * d1 * d2 > kSmallMaxCells) continue;
-      const int Sc = pick_group((long long)Lc * d2, d1), Sr = pick_group((long long)Lc * d1, d2);
+      const int Gl = (int)((B + Lc - 1) / Lc);   // lane groups
+      // spread a lane group over a cluster while SMs are left idle and every
+      // CTA keeps >= 16 outputs per half-sweep
+      int Cc = 1;
+      while (Cc < 8 && (long long)Gl * Cc * 2 <= di.sms && std::min(d1, d2) / (Cc * 2) >= 16)
+        Cc *= 2;
+      static const int force_c = getenv("SKB_SMALL_C") ? atoi(getenv("SKB_SMALL_C")) : 0;
+      if (force_c > 0) Cc = force_c;   // diagnostics: cluster size A/B
+      const long long units_c = (long long)Lc * ((d2 + Cc - 1) / Cc);
+      const long long units_r = (long long)Lc * ((d1 + Cc - 1) / Cc);
+      const int Sc = pick_group(units_c, d1), Sr = pick_group(units_r, d2);
       const int ldc = (int)round_up(d1, 32) + (Sc % 32), ldr = (int)round_up(d2, 32) + (Sr % 32);
-      const size_t bytes = SmallSmem::floats((int)d1, (int)d2, Lc, ldc, ldr) * 4;
+      const size_t bytes = SmallSmem::floats((int)d1, (int)d2, Lc, ldc, ldr, Cc) * 4;
       if (bytes > (size_t)smem_optin / occ - 2048) continue;
-      static bool attr_set = false;
-      auto kern = &small_solve_kernel<kSmallNT>;
-      if (!attr_set) {
-        cudaFuncAttributes fa = {};
-        CK(cudaFuncGetAttributes(&fa, kern));
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                smem_optin - (int)fa.sharedSizeBytes));
-        attr_set = true;
-      }
       int fit = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, kSmallNT, bytes));
       if (fit < 1) return 0;
-      G = (int)((B + Lc - 1) / Lc);
-      if (op.tolerance > 0 && G > fit * di.sms) continue;   // the grid barrier needs co-residency
+      G = Gl * Cc;
+      if (op.tolerance > 0) {   // the grid barrier needs every CTA (cluster) co-resident
+        if (G > fit * di.sms) continue;
+        if (Cc > 1) {
+          cudaLaunchConfig_t qc = {};
+          qc.gridDim = dim3((unsigned)G);
+          qc.blockDim = dim3(kSmallNT);
+          qc.dynamicSmemBytes = bytes;
+          cudaLaunchAttribute qa[1];
+          qa[0].id = cudaLaunchAttributeClusterDimension;
+          qa[0].val.clusterDim.x = (unsigned)Cc;
+          qa[0].val.clusterDim.y = 1;
+          qa[0].val.clusterDim.z = 1;
+          qc.attrs = qa;
+          qc.numAttrs = 1;
+          int nclusters = 0;
+          CK(cudaOccupancyMaxActiveClusters(&nclusters, kern, &qc));
+          if (nclusters < Gl) continue;
+        }
+      }
       smem = bytes;
       sp = SmallParams{};
       sp.a2 = (pr.cost_kind == SINKHORN_COST_SHARED) ? F(L.a2) : nullptr;
@@ -695,6 +724,7 @@ struct Solve {
       sp.d1 = (int)d1;
       sp.d2 = (int)d2;
       sp.L = Lc;
+      sp.C = Cc;
       sp.Sc = Sc;
       sp.Sr = Sr;
       sp.ldc = ldc;
@@ -725,11 +755,20 @@ struct Solve {
     cfg.blockDim = dim3(kSmallNT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;   // grid barrier at the stopping tests
-    attr[0].val.cooperative = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = (unsigned)sp.C;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+    if (sp.checks) {
+      attr[na].id = cudaLaunchAttributeCooperative;   // grid barrier at the stopping tests
+      attr[na].val.cooperative = 1;
+      ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = sp.checks ? 1 : 0;
+    cfg.numAttrs = (unsigned)na;
     ++g_launches;
     CK(cudaLaunchKernelEx(&cfg, &small_solve_kernel<kSmallNT>, sp));
     if (sp.checks) {

@@ -9,6 +9,13 @@
 // step is the lockstep stopping test every check_interval iterations
 // (batch.py:318-322), a grid barrier on a cooperative launch.
 //
+// A lane group can be spread over a thread-block cluster of C CTAs: CTA r of
+// the cluster owns the output slice [r*n/C, (r+1)*n/C) of every half-sweep
+// (and only those rows of the cost), computes it exactly as a lone CTA would,
+// and stores each new potential into every CTA's copy through distributed
+// shared memory; a cluster barrier ends each half-sweep.  More SMs per lane,
+// identical arithmetic.
+//
 // Work split inside a CTA: each (lane, output) unit is reduced by a group of
 // S threads (S = 1..32, chosen on the host per orientation), element i read
 // by thread s = i mod S.  The leading dimension of each cost orientation is
@@ -17,6 +24,8 @@
 // across the group with xor shuffles -- the same arithmetic as the tiled
 // exact chunks, so results match the tiled path to fp32 rounding.
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 
@@ -35,7 +44,8 @@ struct SmallParams {
   const float* nu;
   long long sb1, si1, sb2, si2;
   int B, d1, d2;
-  int L;              // lanes per CTA
+  int L;              // lanes per CTA (per cluster)
+  int C;              // CTAs per cluster sharing a lane group (1 = no cluster)
   int Sc, Sr;         // threads per output: column sweep (reduces d1) / row sweep (reduces d2)
   int ldc, ldr;       // shared leading dims of A2T (column sweep) and A2 (row sweep)
   int max_iters, check_interval, checks;
@@ -50,9 +60,12 @@ struct SmallParams {
   int* status;
 };
 
+__host__ __device__ inline int small_slice(int n, int C, int r) { return (int)((long long)n * r / C); }
+__host__ __device__ inline int small_rows(int n, int C) { return (n + C - 1) / C; }
+
 struct SmallSmem {
-  float* A;    // [d1][ldr]  rows i, contiguous over j (row sweep)
-  float* AT;   // [d2][ldc]  rows j, contiguous over i (column sweep)
+  float* A;    // [rows of this CTA's d1 slice][ldr]  contiguous over j (row sweep)
+  float* AT;   // [rows of this CTA's d2 slice][ldc]  contiguous over i (column sweep)
   float* f;    // [L][d1] log2 u
   float* g0;   // [L][d2] log2 v (ping-pong pair)
   float* g1;
@@ -61,13 +74,14 @@ struct SmallSmem {
   float* mu;   // [L][d1]
   float* nu;   // [L][d2]
   unsigned int* rres;   // [L] residual maxima (non-negative float bits)
-  __host__ __device__ static size_t floats(int d1, int d2, int L, int ldc, int ldr) {
-    return (size_t)d1 * ldr + (size_t)d2 * ldc + (size_t)L * (3 * d1 + 5 * d2) + L + 8;
+  __host__ __device__ static size_t floats(int d1, int d2, int L, int ldc, int ldr, int C) {
+    return (size_t)small_rows(d1, C) * ldr + (size_t)small_rows(d2, C) * ldc +
+           (size_t)L * (3 * d1 + 5 * d2) + L + 8;
   }
   __device__ SmallSmem(float* base, const SmallParams& p) {
     A = base;
-    AT = A + (size_t)p.d1 * p.ldr;
-    f = AT + (size_t)p.d2 * p.ldc;
+    AT = A + (size_t)small_rows(p.d1, p.C) * p.ldr;
+    f = AT + (size_t)small_rows(p.d2, p.C) * p.ldc;
     g0 = f + (size_t)p.L * p.d1;
     g1 = g0 + (size_t)p.L * p.d2;
     lmu = g1 + (size_t)p.L * p.d2;
@@ -136,42 +150,53 @@ __device__ __forceinline__ void small_unit_lse(const float* __restrict__ row,
   w_out = w;
 }
 
-// One half-sweep over the CTA's nl lanes: out[l][o] = target - LSE_k(M[o][k] + x[l][k]).
+// One half-sweep over the CTA's nl lanes and its output slice [o0, o1):
+// out[l][o] = target - LSE_k(M[o - o0][k] + x[l][k]), stored locally and into
+// every other CTA of the cluster (peer[r] = the same buffer in CTA r).
 //   kRes 0: plain update; 1: row residual |2^(out + lse) - marg|;
 //   2: column residual against `old` (the check sweep), 3: TAIL (residual
 //   against `old` + the E0 term written to `out`, batch.py:329-337).
 template <int NT, int kRes>
-__device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld, int nout, int nin,
-                                            int S, int nl, const float* __restrict__ x,
+__device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld, int nout, int o0,
+                                            int o1, int nin, int S, int nl,
+                                            const float* __restrict__ x,
                                             const float* __restrict__ target,
                                             const float* __restrict__ marg,
-                                            const float* __restrict__ old, float* __restrict__ out,
-                                            unsigned int* rres, float cinv) {
+                                            const float* __restrict__ old, float* out,
+                                            unsigned int* rres, float cinv, float* const* peers,
+                                            const float* local_base, int C, int self) {
   const int tid = threadIdx.x;
   const int gpr = NT / S;   // groups per round
   const int s = tid % S;
-  const int U = nl * nout;
+  const int ns = o1 - o0;
+  const int U = nl * ns;
   for (int base = 0; base < U; base += gpr) {
     const int u = base + tid / S;
     const bool active = u < U;
-    const int l = active ? u / nout : 0;
-    const int o = active ? u - l * nout : 0;
+    const int l = active ? u / ns : 0;
+    const int os = active ? u - l * ns : 0;
+    const int o = o0 + os;
     float m, sum, w;
-    small_unit_lse<kRes == 3>(M + (size_t)o * ld, x + (size_t)l * nin, nin, S, s, active, cinv, m,
-                              sum, w);
+    small_unit_lse<kRes == 3>(M + (size_t)os * ld, x + (size_t)l * nin, nin, S, s, active, cinv,
+                              m, sum, w);
     if (active && s == 0) {
       const float lse = lse_final(m, sum);
       const int idx = l * nout + o;
-      float r = 0.f;
+      float r = 0.f, v;
       if (kRes == 3) {
         const float ov = old[idx];
-        out[idx] = (w > 0.f) ? (m + log2f(w) + ov) : neg_inf();
+        v = (w > 0.f) ? (m + log2f(w) + ov) : neg_inf();
         r = fabsf(exp2f(ov + lse) - marg[idx]);
       } else {
-        const float nv = sweep_out(target[idx], lse);
-        if (kRes == 1) r = fabsf(exp2f(nv + lse) - marg[idx]);
+        v = sweep_out(target[idx], lse);
+        if (kRes == 1) r = fabsf(exp2f(v + lse) - marg[idx]);
         if (kRes == 2) r = fabsf(exp2f(old[idx] + lse) - marg[idx]);
-        out[idx] = nv;
+      }
+      out[idx] = v;
+      if (C > 1) {
+        const size_t off = (size_t)(out + idx - local_base);
+        for (int q = 0; q < C; ++q)
+          if (q != self) peers[q][off] = v;   // distributed shared memory
       }
       if (kRes != 0) {
         // NaN must win the max (batch.py:320 compares max <= tol, false for NaN)
@@ -180,7 +205,12 @@ __device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld,
       }
     }
   }
-  __syncthreads();
+}
+
+// End of a half-sweep: every CTA of the cluster has stored its slice everywhere.
+__device__ __forceinline__ void small_sync(int C) {
+  if (C > 1) cooperative_groups::this_cluster().sync();
+  else __syncthreads();
 }
 
 template <int NT>
@@ -188,29 +218,43 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
   extern __shared__ __align__(16) float small_smem[];
   const SmallSmem sm(small_smem, p);
   const int tid = threadIdx.x;
-  const int b0 = blockIdx.x * p.L;
+  const int C = p.C;
+  const int crank = (C > 1) ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+  const int grp = blockIdx.x / C;
+  const int b0 = grp * p.L;
   const int nl = min(p.L, p.B - b0);
+  // this CTA's output slices of the column (over d2) and row (over d1) sweeps
+  const int j0 = small_slice(p.d2, C, crank), j1 = small_slice(p.d2, C, crank + 1);
+  const int i0 = small_slice(p.d1, C, crank), i1 = small_slice(p.d1, C, crank + 1);
   __shared__ int s_conv;
+  __shared__ float* s_peer[8];
+  if (C > 1 && tid < C)
+    s_peer[tid] = cooperative_groups::this_cluster().map_shared_rank(small_smem, tid);
 
-  // ---- stage the cost (both orientations) and this CTA's lanes -------------
+  // ---- stage this CTA's cost rows (both orientations) and the lanes ---------
+  // A rows i in [i0, i1) (row sweep), AT rows j in [j0, j1) (column sweep)
+  const int ni = i1 - i0, nj = j1 - j0;
   if (p.grid) {
-    for (int e = tid; e < p.d1 * p.d2; e += NT) {
-      const int i = e / p.d2, j = e - i * p.d2;
-      const int yi = i / p.gnx, xi = i - yi * p.gnx;
-      const int yj = j / p.gnx, xj = j - yj * p.gnx;
+    for (int e = tid; e < ni * p.d2; e += NT) {
+      const int il = e / p.d2, j = e - il * p.d2, i = i0 + il;
+      const int yi = i / p.gnx, xi = i - yi * p.gnx, yj = j / p.gnx, xj = j - yj * p.gnx;
       const float dx = float(xi) - float(xj), dy = float(yi) - float(yj);
-      const float a = p.gk * fmaf(p.ghx2, dx * dx, p.ghy2 * dy * dy);
-      sm.A[(size_t)i * p.ldr + j] = a;
-      sm.AT[(size_t)j * p.ldc + i] = a;
+      sm.A[(size_t)il * p.ldr + j] = p.gk * fmaf(p.ghx2, dx * dx, p.ghy2 * dy * dy);
+    }
+    for (int e = tid; e < nj * p.d1; e += NT) {
+      const int jl = e / p.d1, i = e - jl * p.d1, j = j0 + jl;
+      const int yi = i / p.gnx, xi = i - yi * p.gnx, yj = j / p.gnx, xj = j - yj * p.gnx;
+      const float dx = float(xi) - float(xj), dy = float(yi) - float(yj);
+      sm.AT[(size_t)jl * p.ldc + i] = p.gk * fmaf(p.ghx2, dx * dx, p.ghy2 * dy * dy);
     }
   } else {
-    for (int e = tid; e < p.d1 * p.d2; e += NT) {
-      const int i = e / p.d2, j = e - i * p.d2;
-      sm.A[(size_t)i * p.ldr + j] = p.a2[(size_t)i * p.D2p + j];
+    for (int e = tid; e < ni * p.d2; e += NT) {
+      const int il = e / p.d2, j = e - il * p.d2;
+      sm.A[(size_t)il * p.ldr + j] = p.a2[(size_t)(i0 + il) * p.D2p + j];
     }
-    for (int e = tid; e < p.d1 * p.d2; e += NT) {
-      const int j = e / p.d1, i = e - j * p.d1;
-      sm.AT[(size_t)j * p.ldc + i] = p.a2t[(size_t)j * p.D1p + i];
+    for (int e = tid; e < nj * p.d1; e += NT) {
+      const int jl = e / p.d1, i = e - jl * p.d1;
+      sm.AT[(size_t)jl * p.ldc + i] = p.a2t[(size_t)(j0 + jl) * p.D1p + i];
     }
   }
   for (int e = tid; e < nl * p.d1; e += NT) {
@@ -226,7 +270,8 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
     sm.lnu[e] = p.l2nu[gj];
     sm.nu[e] = p.nu[gj];
   }
-  __syncthreads();
+  small_sync(C);   // also publishes s_peer; every CTA of the cluster is running
+  float* const* peers = s_peer;
 
   // ---- lockstep iteration (batch.py:314-324), v first then u ---------------
   unsigned int epoch = 0;
@@ -235,8 +280,9 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
   int iters = 0, check_no = 0;
   for (int k = 1; k <= p.max_iters; ++k) {
     if (!have_next) {
-      small_sweep<NT, 0>(sm.AT, p.ldc, p.d2, p.d1, p.Sc, nl, sm.f, sm.lnu, nullptr, nullptr,
-                         sm.g(cur ^ 1), nullptr, 0.f);
+      small_sweep<NT, 0>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, sm.lnu, nullptr,
+                         nullptr, sm.g(cur ^ 1), nullptr, 0.f, peers, small_smem, C, crank);
+      small_sync(C);
       cur ^= 1;
     }
     have_next = false;
@@ -245,17 +291,21 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
     if (check || last) {
       for (int l = tid; l < nl; l += NT) sm.rres[l] = 0u;
       __syncthreads();
-      small_sweep<NT, 1>(sm.A, p.ldr, p.d1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, sm.mu, nullptr,
-                         sm.f, sm.rres, 0.f);
+      small_sweep<NT, 1>(sm.A, p.ldr, p.d1, i0, i1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, sm.mu,
+                         nullptr, sm.f, sm.rres, 0.f, peers, small_smem, C, crank);
     } else {
-      small_sweep<NT, 0>(sm.A, p.ldr, p.d1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, nullptr, nullptr,
-                         sm.f, nullptr, 0.f);
+      small_sweep<NT, 0>(sm.A, p.ldr, p.d1, i0, i1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, nullptr,
+                         nullptr, sm.f, nullptr, 0.f, peers, small_smem, C, crank);
     }
+    small_sync(C);
     iters = k;
     if (check) {
       // column sweep k+1 doubles as the column residual of iteration k
-      small_sweep<NT, 2>(sm.AT, p.ldc, p.d2, p.d1, p.Sc, nl, sm.f, sm.lnu, sm.nu, sm.g(cur),
-                         sm.g(cur ^ 1), sm.rres, 0.f);
+      small_sweep<NT, 2>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, sm.lnu, sm.nu,
+                         sm.g(cur), sm.g(cur ^ 1), sm.rres, 0.f, peers, small_smem, C, crank);
+      small_sync(C);
+      // every CTA publishes the max over its lanes and slices; all CTAs read
+      // all of them behind a grid barrier and take the same decision
       if (tid == 0) {
         unsigned int mx = 0u;
         for (int l = 0; l < nl; ++l) mx = max(mx, sm.rres[l]);
@@ -283,37 +333,51 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
 
   // ---- tail: column residual + E0 terms, then export (batch.py:323-337) -----
   float* e0t = sm.g(cur ^ 1);
-  small_sweep<NT, 3>(sm.AT, p.ldc, p.d2, p.d1, p.Sc, nl, sm.f, nullptr, sm.nu, sm.g(cur), e0t,
-                     sm.rres, p.cinv);
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int l = warp; l < nl; l += NT / 32) {
-    float m = neg_inf();
-    for (int j = lane; j < p.d2; j += 32) m = fmaxf(m, e0t[l * p.d2 + j]);
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    const float mm = (m == neg_inf()) ? 0.f : m;
-    float s = 0.f;
-    for (int j = lane; j < p.d2; j += 32) s += ex2(e0t[l * p.d2 + j] - mm);
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
-      const float cost = exp2f(lse_final(m, s));
-      p.out_cost[b0 + l] = cost;
-      if (!isfinite(cost)) set_status(p.status, 12);
-      p.res[b0 + l] = __uint_as_float(sm.rres[l]);
+  small_sweep<NT, 3>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, nullptr, sm.nu, sm.g(cur),
+                     e0t, sm.rres, p.cinv, peers, small_smem, C, crank);
+  small_sync(C);
+  // the lane residual is the max over the cluster's slices (peer reads)
+  if (C > 1 && crank == 0) {
+    for (int l = tid; l < nl; l += NT) {
+      unsigned int mx = sm.rres[l];
+      for (int q = 1; q < C; ++q)
+        mx = max(mx, *reinterpret_cast<const unsigned int*>(
+                         peers[q] + (reinterpret_cast<const float*>(sm.rres + l) - small_smem)));
+      sm.rres[l] = mx;
     }
   }
-  bool nan = false;
-  for (int e = tid; e < nl * p.d1; e += NT) {
-    const float v = sm.f[e];
-    nan |= (v != v);
-    p.out_log_u[(size_t)b0 * p.d1 + e] = v * kLn2;
+  small_sync(C);   // peers stay resident until the leader has read them
+  if (crank == 0) {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int l = warp; l < nl; l += NT / 32) {
+      float m = neg_inf();
+      for (int j = lane; j < p.d2; j += 32) m = fmaxf(m, e0t[l * p.d2 + j]);
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      const float mm = (m == neg_inf()) ? 0.f : m;
+      float s = 0.f;
+      for (int j = lane; j < p.d2; j += 32) s += ex2(e0t[l * p.d2 + j] - mm);
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) {
+        const float cost = exp2f(lse_final(m, s));
+        p.out_cost[b0 + l] = cost;
+        if (!isfinite(cost)) set_status(p.status, 12);
+        p.res[b0 + l] = __uint_as_float(sm.rres[l]);
+      }
+    }
+    bool nan = false;
+    for (int e = tid; e < nl * p.d1; e += NT) {
+      const float v = sm.f[e];
+      nan |= (v != v);
+      p.out_log_u[(size_t)b0 * p.d1 + e] = v * kLn2;
+    }
+    const float* gv = sm.g(cur);
+    for (int e = tid; e < nl * p.d2; e += NT) {
+      const float v = gv[e];
+      nan |= (v != v);
+      p.out_log_v[(size_t)b0 * p.d2 + e] = v * kLn2;
+    }
+    if (nan) set_status(p.status, 12);   // batch.py:326-327 NaNProduced
   }
-  const float* gv = sm.g(cur);
-  for (int e = tid; e < nl * p.d2; e += NT) {
-    const float v = gv[e];
-    nan |= (v != v);
-    p.out_log_v[(size_t)b0 * p.d2 + e] = v * kLn2;
-  }
-  if (nan) set_status(p.status, 12);   // batch.py:326-327 NaNProduced
   if (blockIdx.x == 0 && tid == 0) p.result[0] = iters;
 }
 

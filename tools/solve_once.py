@@ -19,8 +19,11 @@ ap.add_argument("--iters", type=int, default=None)
 ap.add_argument("--dense-grid", action="store_true")
 ap.add_argument("--tiled-only", action="store_true")
 ap.add_argument("--mufu-only", action="store_true")
+ap.add_argument("--B", type=int, default=None, help="override the config's batch")
 a = ap.parse_args()
-cfg = CONFIGS[a.config]
+cfg = dict(CONFIGS[a.config])
+if a.B:
+    cfg["B"] = a.B
 dev = torch.device("cuda", 0)
 mu, nu, cost = make_inputs(cfg, dev, 1)
 import time  # noqa: E402
@@ -37,5 +40,6 @@ for _ in range(a.reps):
     skb.potentials_backward(r.log_u, r.log_v, cfg["lam"], up)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    print(f"config {a.config} path {r.path} loop_ms {r.loop_ms:.3f} solve_ms "
+    cells = cfg["B"] * cfg["d"] ** 2 * 2 * (a.iters or cfg["iters"])
+    print(f"B {cfg['B']} cells/s {cells / (r.loop_ms * 1e-3):.3e} config {a.config} path {r.path} loop_ms {r.loop_ms:.3f} solve_ms "
           f"{1e3 * (t1 - t0):.3f} backward_ms {1e3 * (t2 - t1):.3f} E0[0] {float(r.cost_e0[0]):.6g}")
