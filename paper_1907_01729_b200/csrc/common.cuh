@@ -205,4 +205,10 @@ __device__ __forceinline__ void grid_sync(unsigned int* counter, unsigned int& e
 // then the cost the CLI validates, core.py:53-63).
 __device__ __forceinline__ void set_status(int* status, int code) { atomicCAS(status, 0, code); }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 }  // namespace skb

@@ -306,7 +306,11 @@ TiledSweepParams build_tiled_params(const Layout& L, void* ws, const TiledArgs& 
   p.ntile_b = L.Bp / BT;
   p.ntile_p = (a.Pv + PT - 1) / PT;
   p.nq = (a.Qv + QC - 1) / QC;
-  p.W = (long long)p.ntile_b * p.ntile_p * a.Qv;   // stream-K over reduction rows
+#ifndef SKB_SEG_ROWS
+#define SKB_SEG_ROWS 12
+#endif
+  p.seg_x = SKB_SEG_ROWS;   // ~3 us of per-segment cost, in rows of a 128x64 tile
+  p.W = (long long)p.ntile_b * p.ntile_p * (a.Qv + p.seg_x);   // virtual rows (atom_begin)
   p.G = G;
   p.target = a.target;
   p.marg = a.marg;
@@ -346,12 +350,47 @@ int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const Tiled
   const int occ = std::min(K::S::OCC, occupancy_tiled(K::fn(), K::S::NT, smem));
   const int G = (int)std::min<long long>(tiled_chunks<BT, PT>(L, a.Pv, a.Qv), (long long)di.sms * occ);
   TiledSweepParams p = build_tiled_params<BT, PT>(L, ws, a, pr, lam, G);
+  // diagnostics (SKB_TIMELINE=n): per-CTA globaltimer stamps of the n-th sweep
+  static const long long tl_at = getenv("SKB_TIMELINE") ? atoll(getenv("SKB_TIMELINE")) : -1;
+  static long long tl_count = 0;
+  static unsigned long long* tl_buf = nullptr;
+  const bool tl = tl_at >= 0 && tl_count++ == tl_at;
+  if (tl) {
+    if (!tl_buf) CK(cudaMalloc(&tl_buf, 8192 * 8));
+    CK(cudaMemsetAsync(tl_buf, 0, 8192 * 8, st));
+    p.dbg = tl_buf;
+  }
   auto kern = &tiled_sweep_kernel<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>;
   CK(launch_pdl(kern, dim3(p.G), dim3(K::S::NT), smem, st, *a.tg, *a.tx, p));
   // merge + epilogue of the tiles the stream-K split cut between CTAs
-  CK(launch_pdl(&tiled_fixup_kernel<BT, PT, QC, RB, RP, kMode>,
-                dim3((unsigned)(p.ntile_b * p.ntile_p * (K::S::NT * 4 / 256))), dim3(256), 0,
-                st, p));
+  const unsigned nfix = (unsigned)(p.ntile_b * p.ntile_p * (K::S::NT * 4 / 256));
+  CK(launch_pdl(&tiled_fixup_kernel<BT, PT, QC, RB, RP, kMode>, dim3(nfix), dim3(256), 0, st, p));
+  if (tl) {
+    std::vector<unsigned long long> h(8192);
+    CK(cudaMemcpyAsync(h.data(), tl_buf, 8192 * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    auto stats = [&](int base, int n, const char* name) {
+      unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+      for (int i = 0; i < n; ++i) {
+        s0 = std::min(s0, h[base + 2 * i]);
+        s1 = std::max(s1, h[base + 2 * i]);
+        e0 = std::min(e0, h[base + 2 * i + 1]);
+        e1 = std::max(e1, h[base + 2 * i + 1]);
+      }
+      fprintf(stderr, "[skb] %s x%d: start %llu..%llu end %llu..%llu (ns)\n", name, n, s0, s1,
+              e0, e1);
+    };
+    stats(0, p.G, "sweep");
+    stats(4096, (int)nfix, "fixup");
+    unsigned long long t0 = ~0ull;
+    for (int c = 0; c < p.G; ++c) t0 = std::min(t0, h[2 * c]);
+    for (int c = 0; c < p.G; ++c) {
+      const long long a0 = atom_begin(p, c), a1 = atom_begin(p, c + 1);
+      const long long segs = (a1 - 1) / p.Qv - a0 / p.Qv + 1;
+      fprintf(stderr, "[skb] cta %d rows %lld segs %lld start %.2f end %.2f us\n", c, a1 - a0,
+              segs, (h[2 * c] - t0) * 1e-3, (h[2 * c + 1] - t0) * 1e-3);
+    }
+  }
   return 0;
 }
 

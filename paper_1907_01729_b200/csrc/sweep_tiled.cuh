@@ -57,6 +57,7 @@ struct TiledSweepParams {
   int gnx;
   float gk, ghx2, ghy2;
   unsigned long long* dbg;   // optional per-CTA timing records (diagnostics), nullable
+  int seg_x;                 // virtual rows charged per tile start (stream-K weighting)
   // Estimate mode: start every output's running max at the previous iteration's
   // log-sum-exp, target - est_old, and reduce each chunk in one pass.
   const float* est_old;      // output-side potentials before this sweep (nullable)
@@ -114,15 +115,25 @@ struct TiledSweep {
   static_assert(QC % 4 == 0, "unroll");
 };
 
-// Even stream-K split over reduction rows: CTA c owns rows [c*W/G, (c+1)*W/G)
-// of the (tile, q) space, so per-CTA work differs by at most one row.
-__device__ __forceinline__ long long atom_begin(const TiledSweepParams& p, long long c) {
-  return (long long)(((unsigned long long)c * (unsigned long long)p.W) / (unsigned long long)p.G);
+// Stream-K split over reduction rows, weighted for segments: every tile is
+// charged X = seg_x virtual rows at its start (the fixed cost of starting a
+// segment: estimate loads, partial chunks, the piece epilogue), and the
+// virtual row space W = ntiles * (Qv + X) is split evenly, so a CTA that
+// crosses a tile boundary gets ~X fewer real rows.
+__host__ __device__ __forceinline__ long long atom_begin(const TiledSweepParams& p, long long c) {
+  const unsigned long long v = ((unsigned long long)c * (unsigned long long)p.W) /
+                               (unsigned long long)p.G;
+  const unsigned long long tq = (unsigned long long)(p.Qv + p.seg_x);
+  const unsigned long long t = v / tq, off = v - t * tq;
+  return (long long)(t * (unsigned long long)p.Qv +
+                     (off > (unsigned long long)p.seg_x ? off - p.seg_x : 0ull));
 }
-// CTA owning row a: the largest c with atom_begin(c) <= a.
-__device__ __forceinline__ long long atom_owner(const TiledSweepParams& p, long long a) {
-  return (long long)(((unsigned long long)(a + 1) * (unsigned long long)p.G - 1) /
-                     (unsigned long long)p.W);
+// CTA owning real row a: the largest c with atom_begin(c) <= a.
+__host__ __device__ __forceinline__ long long atom_owner(const TiledSweepParams& p, long long a) {
+  const unsigned long long t = (unsigned long long)a / (unsigned long long)p.Qv;
+  const unsigned long long va = t * (unsigned long long)(p.Qv + p.seg_x) + p.seg_x +
+                                ((unsigned long long)a - t * (unsigned long long)p.Qv);
+  return (long long)(((va + 1) * (unsigned long long)p.G - 1) / (unsigned long long)p.W);
 }
 
 // Finalise one output tile from per-thread accumulators (M, Sm, S2 hold the
@@ -300,7 +311,7 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
   auto issue = [&](int l) {
     const long long a = g_first + l;
     int tile, qc, b0, p0;
-    atom_coords(a, tile, qc, b0, p0);
+    atom_coords(a, tile, qc, b0, p0);   // thread 0 only, NSTAGE ahead
     const int s = (seq + l) % NSTAGE;
     float* st = smem + s * S::STAGE_FLOATS;
     mbar_arrive_expect_tx(&bars[s], S::TMA_BYTES);
@@ -323,12 +334,17 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
   };
   reset_acc();
 
-  int cur_tile = -1;
-  int seg_q0 = 0;
+  // chunk coordinates walk incrementally (no per-chunk 64-bit division)
+  int tile, qc, b0, p0;
+  atom_coords(g_first, tile, qc, b0, p0);
   for (int l = 0; l < n_local; ++l) {
-    const long long a = g_first + l;
-    int tile, qc, b0, p0;
-    atom_coords(a, tile, qc, b0, p0);
+    if (l > 0 && ++qc == nq) {
+      qc = 0;
+      ++tile;
+      const int tb_idx = tile % p.ntile_b, tp_idx = tile / p.ntile_b;
+      b0 = tb_idx * BT;
+      p0 = (tp_idx == p.ntile_p - 1) ? max(p.Pv - PT, 0) : tp_idx * PT;
+    }
     // this CTA's rows inside the chunk: [k_lo, k_hi) relative to the chunk start
     const long long row0 = (long long)tile * Qv + (long long)qc * QC;
     const int chunk_rows = (int)(Qv - (long long)qc * QC < QC ? Qv - (long long)qc * QC : QC);
@@ -336,10 +352,6 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
     int k_hi = (int)(a_end - row0 < chunk_rows ? a_end - row0 : chunk_rows);
     // rows past Qv are -inf padding: round the natural chunk end up to a pair
     if (k_hi == chunk_rows) k_hi = min(QC, (k_hi + 1) & ~1);
-    if (tile != cur_tile) {
-      cur_tile = tile;
-      seg_q0 = qc;
-    }
     const int s = (seq + l) % NSTAGE;
     const uint32_t parity = ((seq + l) / NSTAGE) & 1;
     float* st = smem + s * S::STAGE_FLOATS;
@@ -367,6 +379,26 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
         Gw[i] = valid ? p.gk * fmaf(p.ghx2, dx * dx, p.ghy2 * dy * dy) : neg_inf();
       }
     }
+    // segment start in estimate mode: running max := previous lse (target -
+    // old).  The loads are issued before the stage wait so their latency
+    // overlaps it; outputs with a -inf target never need their lse (parked).
+    const bool est_init = d.use_est && (l == 0 || qc == 0);
+    if (est_init) {
+#pragma unroll
+      for (int rp = 0; rp < RP; ++rp) {
+        const int pp = min(p0 + tp * RP + rp, p.Pv - 1);
+        const size_t row = size_t(pp) * p.Bp + b0 + tb * RB;
+        const float4 tg = __ldg(reinterpret_cast<const float4*>(p.target + row));
+        const float4 eo = *reinterpret_cast<const float4*>(d.est_old + row);
+        const float tv[4] = {tg.x, tg.y, tg.z, tg.w};
+        const float ev[4] = {eo.x, eo.y, eo.z, eo.w};
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+          const float est = tv[rb] - ev[rb];
+          M[rb * RP + rp] = (tv[rb] == neg_inf()) ? kParked : (isfinite(est) ? est : kNegBig);
+        }
+      }
+    }
     mbar_wait(&bars[s], parity);
     if (kGrid) __syncthreads();
 
@@ -376,24 +408,6 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
     // a warp covers 2 output groups; skip it only if both are past Pv (uniform)
     const bool warp_active = __any_sync(0xffffffffu, (p0 + tp * RP) < p.Pv);
     if (warp_active) {
-      if (d.use_est && (l == 0 || qc == 0)) {
-        // segment start: running max := previous lse (target - old); outputs
-        // with a -inf target never need their lse and are parked
-#pragma unroll
-        for (int rp = 0; rp < RP; ++rp) {
-          const int pp = min(p0 + tp * RP + rp, p.Pv - 1);
-          const size_t row = size_t(pp) * p.Bp + b0 + tb * RB;
-          const float4 tg = __ldg(reinterpret_cast<const float4*>(p.target + row));
-          const float4 eo = *reinterpret_cast<const float4*>(d.est_old + row);
-          const float tv[4] = {tg.x, tg.y, tg.z, tg.w};
-          const float ev[4] = {eo.x, eo.y, eo.z, eo.w};
-#pragma unroll
-          for (int rb = 0; rb < RB; ++rb) {
-            const float est = tv[rb] - ev[rb];
-            M[rb * RP + rp] = (tv[rb] == neg_inf()) ? kParked : (isfinite(est) ? est : kNegBig);
-          }
-        }
-      }
       // Outputs are handled in lane pairs (rb = 2h, 2h+1) so every add is a
       // packed FADD2 with the cost value broadcast: o = (2h + e) * RP + rp.
       uint64_t acc[2][RP], acc2[2][RP];
@@ -449,27 +463,21 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
         if (!__all_sync(0xffffffffu, ok)) {
           exact = true;
         } else {
-          // Fold the chunk in and renormalise the running sum by its own
-          // power-of-two exponent: exact scaling that keeps the shift M at
-          // the running lse (branch-free; no max pass needed).
+          // Fold the chunk in.  Every chunk sum is <= 2^100 (checked above),
+          // so a segment's running sum stays far below the fp32 range without
+          // per-chunk renormalisation; the shift M stays the estimate.
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int rp = 0; rp < RP; ++rp)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int o = (2 * h + e) * RP + rp;
-                const float tot = Sm[o] + (e ? hi2(acc[h][rp]) : lo2(acc[h][rp]));
-                const int bits = __float_as_int(tot);
-                const int ex = ((bits >> 23) & 0xff);
-                const int sh = (ex == 0) ? 0 : ex - 127;            // 0 or denormal: keep
-                Sm[o] = __int_as_float(bits - (sh << 23));
-                if (kMode == kModeTail) {
-                  const float t2 = S2[o] + (e ? hi2(acc2[h][rp]) : lo2(acc2[h][rp]));
-                  S2[o] = ldexpf(t2, -sh);
-                }
-                M[o] += (float)sh;
+            for (int rp = 0; rp < RP; ++rp) {
+              const int o0 = (2 * h) * RP + rp, o1 = (2 * h + 1) * RP + rp;
+              Sm[o0] += lo2(acc[h][rp]);
+              Sm[o1] += hi2(acc[h][rp]);
+              if (kMode == kModeTail) {
+                S2[o0] += lo2(acc2[h][rp]);
+                S2[o1] += hi2(acc2[h][rp]);
               }
+            }
         }
       }
       if (exact) {
@@ -566,8 +574,6 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
       }
     }
     reset_acc();
-    (void)seg_q0;
-    (void)NV;
   }
   seq += n_local;
 }
@@ -587,9 +593,21 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
   __syncthreads();
   // Everything above overlaps the previous kernel's tail; inputs are read below.
   pdl_wait();
-  uint32_t seq = 0;
-  sweep_phase<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>(&tmap_g, &tmap_x, p, dyn_of(p), sm, seq);
+#ifndef SKB_PDL_LATE
+  // let the dependent (fixup) grid launch now: its CTAs take SMs as ours
+  // retire and wait in griddepcontrol.wait for this grid's completion
   pdl_launch_dependents();
+#endif
+  uint32_t seq = 0;
+  if (p.dbg && threadIdx.x == 0) p.dbg[2 * blockIdx.x] = globaltimer_ns();
+  sweep_phase<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>(&tmap_g, &tmap_x, p, dyn_of(p), sm, seq);
+  if (p.dbg) {
+    __syncthreads();
+    if (threadIdx.x == 0) p.dbg[2 * blockIdx.x + 1] = globaltimer_ns();
+  }
+#ifdef SKB_PDL_LATE
+  pdl_launch_dependents();
+#endif
 }
 
 // Merge the stream-K pieces of every split tile in ascending CTA order (the
@@ -713,8 +731,18 @@ template <int BT, int PT, int QC, int RB, int RP, int kMode>
 __global__ void __launch_bounds__(256) tiled_fixup_kernel(const TiledSweepParams p) {
   __shared__ float s_res[BT];
   pdl_wait();
-  fixup_chunk<BT, PT, QC, RB, RP, kMode, 256>(p, dyn_of(p), blockIdx.x, s_res);
+#ifndef SKB_PDL_LATE
   pdl_launch_dependents();
+#endif
+  if (p.dbg && threadIdx.x == 0) p.dbg[4096 + 2 * blockIdx.x] = globaltimer_ns();
+  fixup_chunk<BT, PT, QC, RB, RP, kMode, 256>(p, dyn_of(p), blockIdx.x, s_res);
+  if (p.dbg) {
+    __syncthreads();
+    if (threadIdx.x == 0) p.dbg[4096 + 2 * blockIdx.x + 1] = globaltimer_ns();
+  }
+#ifdef SKB_PDL_LATE
+  pdl_launch_dependents();
+#endif
 }
 
 }  // namespace skb
