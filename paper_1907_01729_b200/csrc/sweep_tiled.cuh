@@ -39,7 +39,7 @@ struct TiledSweepParams {
   int Qv, Pv;          // valid reduce / output extents (d)
   int Bp;              // padded lane count (row stride of dim-major buffers)
   int ntile_b, ntile_p, nq;
-  long long W;         // stream-K units: reduction rows over all tiles = ntiles * Qv
+  long long W;         // stream-K units: virtual rows over all tiles = ntiles * (Qv + seg_x)
   int G;               // grid size (<= W / QC, so every CTA owns >= 1 chunk of rows)
   const float* target; // [Pp][Bp] log2 marginal of the output side
   const float* marg;   // [Pp][Bp] linear marginal of the output side (residuals)
@@ -560,7 +560,7 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
     if (c_lo == c_hi) {
       tile_epilogue<BT, PT, RB, RP, NT, kMode>(p, d, tid, tb, tp, b0, p0, own_lo, M, Sm, S2, s_res);
     } else {
-      // split tile: leave this piece's (max, sum[, E0 sum]) for the fixup kernel
+      // split tile: leave this piece's (max, sum[, E0 sum]) for the merge
       const int slot = (a_begin >= t_first) ? 0 : 1;
       float* mine = p.part + ((c * 2 + slot) * NV) * (size_t)(BT * PT) + tid * NOUT;
 #pragma unroll
@@ -615,34 +615,53 @@ __global__ void __launch_bounds__((BT / RB) * (PT / RP), ((BT / RB) * (PT / RP) 
 // the tile epilogue.  One CTA per tile, same thread map as the sweep, so each
 // thread merges exactly the outputs its counterpart accumulated.  Launched
 // right after the sweep with programmatic dependent launch.
-// One chunk of NB float4 groups (4 outputs of one lane each) of the split
-// tiles: every thread of the CTA takes one group.  Chunks never straddle tiles
-// (NT*NG is a multiple of NB), so the early exit is CTA-uniform.
+// Merge float4 groups [g0, g1) (4 outputs of one lane each) of split tile
+// `tile`: every thread takes one group per round.  (Merging inside the sweep
+// instead -- per-tile piece counters, the contributing CTAs each merging a
+// share once the tile is complete -- measured slower on B200: 11.4 vs 10.0 ms
+// at config 2, so the merge stays a separate PDL-launched pass.)
 template <int BT, int PT, int QC, int RB, int RP, int kMode, int NB>
-__device__ __forceinline__ void fixup_chunk(const TiledSweepParams& p, const SweepDyn& d, int chunk,
-                                            float* s_res) {
+__device__ __forceinline__ void merge_tile_groups(const TiledSweepParams& p, const SweepDyn& d,
+                                                  int tile, int g0, int g1, float* s_res) {
   constexpr int NT = (BT / RB) * (PT / RP);   // the sweep's threads per tile
   constexpr int NOUT = RB * RP;
   constexpr int NG = NOUT / 4;                // float4 groups per sweep thread (one per rb)
-  constexpr int CPT = NT * NG / NB;           // chunks per tile
   constexpr int NV = (kMode == kModeTail) ? 3 : 2;
   constexpr int GRP = 8;                      // pieces whose loads are in flight together
   static_assert(RP == 4, "one float4 group = the RP outputs of one lane");
-  static_assert((NT * NG) % NB == 0, "chunks align with tiles");
-  const int tile = chunk / CPT;
-  const int e = (chunk % CPT) * NB + threadIdx.x;        // float4 group within the tile
-  const int vtid = e / NG, rb = e % NG;                  // mirrored sweep thread, its lane
   const long long Qv = p.Qv;
   const long long t_first = (long long)tile * Qv;
   const long long c_lo = atom_owner(p, t_first);
   const long long c_hi = atom_owner(p, t_first + Qv - 1);
-  if (c_lo == c_hi) return;   // finalised by the sweep itself
-  int tb, tp;
-  thread_map<BT, RB, NT>(vtid, tb, tp);
+  if (c_lo == c_hi) return;   // finalised by the sweep itself (CTA-uniform)
+  // only the tile's first piece can be its CTA's second slot (the CTA began
+  // in an earlier tile); every later piece starts inside this tile
+  const int sl0 = (atom_begin(p, c_lo) < t_first) ? 1 : 0;
   const int tb_idx = tile % p.ntile_b, tp_idx = tile / p.ntile_b;
-  const int b = tb_idx * BT + tb * RB + rb;
   const int p0 = (tp_idx == p.ntile_p - 1) ? max(p.Pv - PT, 0) : tp_idx * PT;
   const int own_lo = tp_idx * PT;
+  const bool want_res = p.res != nullptr && (kMode == kModeTail || d.res_kind != kResNone);
+  for (int gb = g0; gb < g1; gb += NB) {
+  const int e = gb + (int)threadIdx.x;             // float4 group within the tile
+  const bool act = e < g1;
+  const int vtid = (act ? e : g0) / NG, rb = (act ? e : g0) % NG;   // mirrored sweep thread, lane
+  int tb, tp;
+  thread_map<BT, RB, NT>(vtid, tb, tp);
+  const int b = tb_idx * BT + tb * RB + rb;
+  // epilogue inputs do not depend on the pieces: their loads go out first
+  float tgv[4], eov[4], odv[4], mgv[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int pp = min(p0 + tp * RP + r, p.Pv - 1);
+    const size_t o = size_t(pp) * p.Bp + b;
+    tgv[r] = eov[r] = odv[r] = mgv[r] = 0.f;
+    if (kMode == kModeUpdate) {
+      tgv[r] = __ldg(p.target + o);
+      if (d.use_est) eov[r] = d.est_old[o];
+    }
+    if (kMode == kModeTail || d.res_kind == kResCol) odv[r] = d.old[o];
+    if (want_res) mgv[r] = __ldg(p.marg + o);
+  }
   float M[4], Sm[4], S2[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -656,8 +675,8 @@ __device__ __forceinline__ void fixup_chunk(const TiledSweepParams& p, const Swe
 #pragma unroll
     for (int g = 0; g < GRP; ++g) {
       const long long cc = c0 + g;
-      if (cc > c_hi) break;
-      const int sl = (atom_begin(p, cc) >= t_first) ? 0 : 1;
+      if (cc > c_hi || !act) break;
+      const int sl = (cc == c_lo) ? sl0 : 0;
       const float* src = p.part + ((cc * 2 + sl) * NV) * (size_t)(BT * PT) + vtid * NOUT + rb * 4;
       mv[g] = __ldcg(reinterpret_cast<const float4*>(src));
       sv[g] = __ldcg(reinterpret_cast<const float4*>(src + BT * PT));
@@ -665,7 +684,7 @@ __device__ __forceinline__ void fixup_chunk(const TiledSweepParams& p, const Swe
     }
 #pragma unroll
     for (int g = 0; g < GRP; ++g) {
-      if (c0 + g > c_hi) break;   // ascending piece order (batch.py:198-201)
+      if (c0 + g > c_hi || !act) break;   // ascending piece order (batch.py:198-201)
       const float* m2 = reinterpret_cast<const float*>(&mv[g]);
       const float* s2 = reinterpret_cast<const float*>(&sv[g]);
       const float* t2 = reinterpret_cast<const float*>(&tv[g]);
@@ -680,7 +699,6 @@ __device__ __forceinline__ void fixup_chunk(const TiledSweepParams& p, const Swe
     }
   }
   // epilogue for lane b, outputs p0 + tp*RP + r
-  const bool want_res = p.res != nullptr && (kMode == kModeTail || d.res_kind != kResNone);
   if (want_res) {
     for (int i = threadIdx.x; i < BT; i += NB) s_res[i] = 0.f;
     __syncthreads();
@@ -689,7 +707,7 @@ __device__ __forceinline__ void fixup_chunk(const TiledSweepParams& p, const Swe
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int pp = p0 + tp * RP + r;
-    if (pp >= p.Pv || pp < own_lo) continue;
+    if (!act || pp >= p.Pv || pp < own_lo) continue;
     const size_t o = size_t(pp) * p.Bp + b;
     if (kMode == kModePartial) {
       p.pmax[o] = M[r];
@@ -698,21 +716,21 @@ __device__ __forceinline__ void fixup_chunk(const TiledSweepParams& p, const Swe
     }
     const float lse = lse_final(M[r], Sm[r]);
     if (kMode == kModeUpdate) {
-      const float tg = p.target[o];
+      const float tg = tgv[r];
       if (d.use_est) {
-        const float est = tg - d.est_old[o];
+        const float est = tg - eov[r];
         if (tg != neg_inf() && isfinite(est) && !(lse >= est - kEstSlack)) atomicOr(p.est_fail, 1);
       }
       const float ov = sweep_out(tg, lse);
       d.out[o] = ov;
       if (want_res) {
-        const float base = (d.res_kind == kResCol) ? d.old[o] : ov;
-        rmax = fmaxf(rmax, fabsf(exp2f(base + lse) - p.marg[o]));
+        const float base = (d.res_kind == kResCol) ? odv[r] : ov;
+        rmax = fmaxf(rmax, fabsf(exp2f(base + lse) - mgv[r]));
       }
     } else {   // TAIL
-      const float od = d.old[o];
+      const float od = odv[r];
       p.e0[o] = (S2[r] > 0.f) ? (M[r] + log2f(S2[r]) + od) : neg_inf();
-      rmax = fmaxf(rmax, fabsf(exp2f(od + lse) - p.marg[o]));
+      rmax = fmaxf(rmax, fabsf(exp2f(od + lse) - mgv[r]));
     }
   }
   if (want_res) {
@@ -725,6 +743,18 @@ __device__ __forceinline__ void fixup_chunk(const TiledSweepParams& p, const Swe
     }
     __syncthreads();   // s_res is reused by the next chunk
   }
+  }   // rounds of NB groups
+}
+
+template <int BT, int PT, int QC, int RB, int RP, int kMode, int NB>
+__device__ __forceinline__ void fixup_chunk(const TiledSweepParams& p, const SweepDyn& d, int chunk,
+                                            float* s_res) {
+  constexpr int NT = (BT / RB) * (PT / RP);
+  constexpr int GT = NT * (RB * RP / 4);      // float4 groups per tile
+  static_assert(GT % NB == 0, "chunks align with tiles");
+  constexpr int CPT = GT / NB;
+  const int tile = chunk / CPT, g0 = (chunk % CPT) * NB;
+  merge_tile_groups<BT, PT, QC, RB, RP, kMode, NB>(p, d, tile, g0, g0 + NB, s_res);
 }
 
 template <int BT, int PT, int QC, int RB, int RP, int kMode>
