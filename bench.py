@@ -73,13 +73,20 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,timestamp")
 
     def __init__(self, gpu_index: int, interval_ms: int = 500):
         self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
         self.proc = None
         self.gpu = gpu_index
         self.interval_ms = interval_ms
+        self.window = None   # wall-clock (start, end) of the timed region
+
+    def mark(self, t0: float, t1: float) -> None:
+        """The timed region; samples within one interval of it are reported.
+        (The sampler itself starts before the warm-up steps, so nvidia-smi's own
+        start-up never lands inside the timed steps.)"""
+        self.window = (t0, t1)
 
     def __enter__(self):
         try:
@@ -103,15 +110,29 @@ class ClockSampler:
             self.fh.close()
 
     def summary(self) -> dict:
+        import datetime
+
         rows = []
         try:
             with open(self.path) as f:
                 for line in f:
                     parts = [p.strip() for p in line.split(",")]
-                    if len(parts) >= 7:
+                    if len(parts) >= 8:
                         rows.append(parts)
         except OSError:
             pass
+        if self.window is not None and rows:
+            pad = self.interval_ms * 1e-3
+            t0, t1 = self.window[0] - pad, self.window[1] + pad
+            near = []
+            for r in rows:
+                try:
+                    ts = datetime.datetime.strptime(r[7], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    continue
+                if t0 <= ts <= t1:
+                    near.append(r)
+            rows = near or rows[-1:]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
@@ -337,17 +358,18 @@ def run_ours(args, cfg, world, rank, local):
             dist.all_gather_into_tensor(gathered, res.cost_e0)
         return res
 
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     loop_ms = []
-    launches0 = lib.sinkhorn_launch_count_v1()
     with ClockSampler(local, args.clock_interval_ms) as clk:
+        for _ in range(max(args.warmup, 3)):
+            step()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches0 = lib.sinkhorn_launch_count_v1()
+        torch.cuda.synchronize()
+        t_wall0 = time.time()
         for s in range(args.steps):
             flush.zero_()                       # L2 flush between steps (outside the events)
             starts[s].record()
@@ -356,6 +378,7 @@ def run_ours(args, cfg, world, rank, local):
             loop_ms.append(res.loop_ms)
             path = res.path
         torch.cuda.synchronize()
+        clk.mark(t_wall0, time.time())
     launches = lib.sinkhorn_launch_count_v1() - launches0
     if world > 1:
         dist.barrier()
@@ -480,7 +503,8 @@ def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default per config: ~0.3-1 s of timed work, 3 for config 5)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -488,6 +512,11 @@ def main():
     ap.add_argument("--clock-interval-ms", type=int, default=500)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.steps is None:
+        # enough steps that a rare host-side stall (seen on the boxes: one
+        # step in ~100 takes 5-100 ms longer, with or without our sampler)
+        # does not dominate the mean
+        args.steps = {1: 50, 2: 30, 3: 30, 4: 10, 5: 3}[args.config]
     world, rank, local = init_dist()
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)

@@ -1332,12 +1332,38 @@ static bool view_ok(const sinkhorn_view_v1* v, int ndim, int64_t s0, int64_t s1)
 }
 
 namespace {
+// Device scratch of the host-buffer symbols: grow-only, one per host thread
+// and entry point, reused across calls (both symbols run on
+// cudaStreamPerThread and synchronise before they return), so repeated calls
+// never pay for a device allocation.
+struct HostScratch {
+  void* p = nullptr;
+  size_t cap = 0;
+  int dev = -1;
+  ~HostScratch() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t get(size_t n, void** out) {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (p == nullptr || cap < n || dev != d) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      const cudaError_t e = cudaMalloc(&p, n);
+      if (e != cudaSuccess) return e;
+      cap = n;
+      dev = d;
+    }
+    *out = p;
+    return cudaSuccess;
+  }
+};
+thread_local HostScratch g_host_fwd, g_host_bwd;
+
 struct DevBuf {
   void* p = nullptr;
   cudaStream_t st = nullptr;
-  ~DevBuf() {
-    if (p) cudaFreeAsync(p, st);
-  }
 };
 }  // namespace
 
@@ -1370,7 +1396,7 @@ int32_t sinkhorn_forward_v1(const sinkhorn_view_v1* mu, const sinkhorn_view_v1* 
   const size_t o_ws = c.take(ws_bytes);
   DevBuf buf;
   buf.st = st;
-  CK(cudaMallocAsync(&buf.p, c.off, st));
+  CK(g_host_fwd.get(c.off, &buf.p));
   double* d64 = at<double>(buf.p, o_d64);
   CK(cudaMemcpyAsync(d64, mu->data, n_mu * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d64 + n_mu, nu->data, n_nu * 8, cudaMemcpyHostToDevice, st));
@@ -1438,7 +1464,7 @@ int32_t sinkhorn_backward_v1(const sinkhorn_view_v1* log_u, const sinkhorn_view_
   const size_t n1 = (size_t)B * d1, n2 = (size_t)B * d2;
   DevBuf buf;
   buf.st = st;
-  CK(cudaMallocAsync(&buf.p, (2 * n1 + 2 * n2 + B) * 8 + 16, st));
+  CK(g_host_bwd.get((2 * n1 + 2 * n2 + B) * 8 + 16, &buf.p));
   double* u = static_cast<double*>(buf.p);
   double* v = u + n1;
   double* up = v + n2;
