@@ -312,6 +312,7 @@ TiledSweepParams build_tiled_params(const Layout& L, void* ws, const TiledArgs& 
   p.seg_x = SKB_SEG_ROWS;   // ~3 us of per-segment cost, in rows of a 128x64 tile
   p.W = (long long)p.ntile_b * p.ntile_p * (a.Qv + p.seg_x);   // virtual rows (atom_begin)
   p.G = G;
+  p.fast32 = ((unsigned long long)(p.W + 1) * (unsigned long long)(G + 1) < (1ull << 32)) ? 1 : 0;
   p.target = a.target;
   p.marg = a.marg;
   p.out = a.out;
@@ -356,8 +357,8 @@ int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const Tiled
   static unsigned long long* tl_buf = nullptr;
   const bool tl = tl_at >= 0 && tl_count++ == tl_at;
   if (tl) {
-    if (!tl_buf) CK(cudaMalloc(&tl_buf, 8192 * 8));
-    CK(cudaMemsetAsync(tl_buf, 0, 8192 * 8, st));
+    if (!tl_buf) CK(cudaMalloc(&tl_buf, 16384 * 8));
+    CK(cudaMemsetAsync(tl_buf, 0, 16384 * 8, st));
     p.dbg = tl_buf;
   }
   auto kern = &tiled_sweep_kernel<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>;
@@ -366,8 +367,8 @@ int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const Tiled
   const unsigned nfix = (unsigned)(p.ntile_b * p.ntile_p * (K::S::NT * 4 / 256));
   CK(launch_pdl(&tiled_fixup_kernel<BT, PT, QC, RB, RP, kMode>, dim3(nfix), dim3(256), 0, st, p));
   if (tl) {
-    std::vector<unsigned long long> h(8192);
-    CK(cudaMemcpyAsync(h.data(), tl_buf, 8192 * 8, cudaMemcpyDeviceToHost, st));
+    std::vector<unsigned long long> h(16384);
+    CK(cudaMemcpyAsync(h.data(), tl_buf, 16384 * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     auto stats = [&](int base, int n, const char* name) {
       unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
@@ -387,8 +388,13 @@ int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const Tiled
     for (int c = 0; c < p.G; ++c) {
       const long long a0 = atom_begin(p, c), a1 = atom_begin(p, c + 1);
       const long long segs = (a1 - 1) / p.Qv - a0 / p.Qv + 1;
-      fprintf(stderr, "[skb] cta %d rows %lld segs %lld start %.2f end %.2f us\n", c, a1 - a0,
+      fprintf(stderr, "[skb] cta %d rows %lld segs %lld start %.2f end %.2f us chunks", c, a1 - a0,
               segs, (h[2 * c] - t0) * 1e-3, (h[2 * c + 1] - t0) * 1e-3);
+      for (int l = 0; l < 16 && h[8192 + c * 16 + l]; ++l)
+        fprintf(stderr, " %.2f", (h[8192 + c * 16 + l] - t0) * 1e-3);
+      fprintf(stderr, " | first row %lld | setup %.2f issued %.2f waited %.2f\n", a0,
+              (h[12288 + c * 4] - t0) * 1e-3, (h[12288 + c * 4 + 1] - t0) * 1e-3,
+              (h[12288 + c * 4 + 2] - t0) * 1e-3);
     }
   }
   return 0;

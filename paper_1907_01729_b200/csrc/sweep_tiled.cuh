@@ -58,6 +58,7 @@ struct TiledSweepParams {
   float gk, ghx2, ghy2;
   unsigned long long* dbg;   // optional per-CTA timing records (diagnostics), nullable
   int seg_x;                 // virtual rows charged per tile start (stream-K weighting)
+  int fast32;                // W * G and every row index fit in 32 bits: 32-bit index math
   // Estimate mode: start every output's running max at the previous iteration's
   // log-sum-exp, target - est_old, and reduce each chunk in one pass.
   const float* est_old;      // output-side potentials before this sweep (nullable)
@@ -105,9 +106,10 @@ struct TiledSweep {
   static constexpr int X_FLOATS = QC * BT;
   static constexpr int STAGE_FLOATS = G_FLOATS + X_FLOATS;
   static constexpr uint32_t TMA_BYTES = (kGrid ? 0 : G_FLOATS * 4) + X_FLOATS * 4;
+  static constexpr int EST_FLOATS = 2 * RB * RP * NT;   // per-thread estimate rows (tg, old)
   static constexpr size_t SMEM_BYTES =
       size_t(NSTAGE) * STAGE_FLOATS * 4 + 64 * 8 /*bars*/ + BT * 4 +
-      (kGrid ? (QC + PT) * 8 : 0);
+      (kGrid ? (QC + PT) * 8 : 0) + size_t(EST_FLOATS) * 4;
   static_assert(NTB == 16 || NTB == 32, "lane-threads per (half) warp");
   static constexpr int OCC = (NT >= 512) ? 1 : SKB_OCC_SMALL;   // CTAs per SM the launch bounds target
   static_assert(NT % 32 == 0, "whole warps");
@@ -121,6 +123,12 @@ struct TiledSweep {
 // virtual row space W = ntiles * (Qv + X) is split evenly, so a CTA that
 // crosses a tile boundary gets ~X fewer real rows.
 __host__ __device__ __forceinline__ long long atom_begin(const TiledSweepParams& p, long long c) {
+  if (p.fast32) {   // every product below fits in 32 bits (checked on the host)
+    const unsigned v = (unsigned)c * (unsigned)p.W / (unsigned)p.G;
+    const unsigned tq = (unsigned)(p.Qv + p.seg_x);
+    const unsigned t = v / tq, off = v - t * tq;
+    return (long long)(t * (unsigned)p.Qv + (off > (unsigned)p.seg_x ? off - p.seg_x : 0u));
+  }
   const unsigned long long v = ((unsigned long long)c * (unsigned long long)p.W) /
                                (unsigned long long)p.G;
   const unsigned long long tq = (unsigned long long)(p.Qv + p.seg_x);
@@ -130,6 +138,11 @@ __host__ __device__ __forceinline__ long long atom_begin(const TiledSweepParams&
 }
 // CTA owning real row a: the largest c with atom_begin(c) <= a.
 __host__ __device__ __forceinline__ long long atom_owner(const TiledSweepParams& p, long long a) {
+  if (p.fast32) {
+    const unsigned t = (unsigned)a / (unsigned)p.Qv;
+    const unsigned va = t * (unsigned)(p.Qv + p.seg_x) + p.seg_x + ((unsigned)a - t * (unsigned)p.Qv);
+    return (long long)(((va + 1) * (unsigned)p.G - 1) / (unsigned)p.W);
+  }
   const unsigned long long t = (unsigned long long)a / (unsigned long long)p.Qv;
   const unsigned long long va = t * (unsigned long long)(p.Qv + p.seg_x) + p.seg_x +
                                 ((unsigned long long)a - t * (unsigned long long)p.Qv);
@@ -251,12 +264,14 @@ struct SweepSmem {
   float* s_res;
   float* s_gq;   // grid mode: q coordinates (x, y) [QC][2]
   float* s_gp;   // grid mode: p coordinates [PT][2]
+  float* est;    // estimate rows per thread: [2*RP][NT] float4 (target rows, old rows)
   __device__ explicit SweepSmem(uint8_t* raw) {
     smem = reinterpret_cast<float*>(raw);
     bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * S::STAGE_FLOATS);
     s_res = reinterpret_cast<float*>(bars + 64);
     s_gq = s_res + BT;
     s_gp = s_gq + 2 * QC;
+    est = s_gq + (kGrid ? 2 * (QC + PT) : 0);   // 16-byte aligned (all extents are multiples of 4)
   }
 };
 
@@ -289,6 +304,10 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
   const long long Qv = p.Qv;
   // global chunk index of a row: tile * nq + (q / QC)
   auto chunk_of = [&](long long r) {
+    if (p.fast32) {
+      const unsigned t = (unsigned)r / (unsigned)Qv;
+      return (long long)(t * (unsigned)nq + ((unsigned)r - t * (unsigned)Qv) / QC);
+    }
     const long long t = r / Qv;
     return t * nq + (r - t * Qv) / QC;
   };
@@ -300,7 +319,7 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
   // the last tile is shifted left to end at Pv, so no tile is partial (a
   // partial tile's few active warps are latency-bound and stretch the tail).
   auto atom_coords = [&](long long a, int& tile, int& qc, int& b0, int& p0) {
-    tile = int(a / nq);
+    tile = int((unsigned)a / (unsigned)nq);   // chunk indices fit in 32 bits
     qc = int(a - (long long)tile * nq);
     const int tb_idx = tile % p.ntile_b;     // lane tiles innermost: consecutive tiles share G
     const int tp_idx = tile / p.ntile_b;
@@ -319,6 +338,30 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
     tma_load_2d(st + S::G_FLOATS, tmap_x, b0, qc * QC, &bars[s]);
   };
 
+  // Estimate rows (target, previous potential) of a tile's outputs, copied
+  // asynchronously into this thread's slots of sm.est: issued a segment
+  // ahead, so the loads never stall the hot loop and cost no registers.
+  float* est_buf = sm.est;
+  auto est_fetch = [&](int tile_n) {
+    const int tb_n = tile_n % p.ntile_b, tp_n = tile_n / p.ntile_b;
+    const int b0n = tb_n * BT;
+    const int p0n = (tp_n == p.ntile_p - 1) ? max(p.Pv - PT, 0) : tp_n * PT;
+#pragma unroll
+    for (int rp = 0; rp < RP; ++rp) {
+      const int pp = min(p0n + tp * RP + rp, p.Pv - 1);
+      const size_t row = size_t(pp) * p.Bp + b0n + tb * RB;
+      cp_async16(est_buf + (size_t(rp) * NT + tid) * 4, p.target + row);
+      cp_async16(est_buf + (size_t(RP + rp) * NT + tid) * 4, d.est_old + row);
+    }
+    cp_async_commit();
+  };
+  // chunk coordinates walk incrementally (no per-chunk 64-bit division)
+  int tile, qc, b0, p0;
+  atom_coords(g_first, tile, qc, b0, p0);
+  if (d.use_est) est_fetch(tile);
+  const int last_tile = int(chunk_of(a_end - 1) / nq);
+
+  if (p.dbg && tid == 0) p.dbg[12288 + blockIdx.x * 4 + 0] = globaltimer_ns();
   if (tid == 0) {
     for (int l = 0; l < NSTAGE && l < n_local; ++l) issue(l);
   }
@@ -334,9 +377,6 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
   };
   reset_acc();
 
-  // chunk coordinates walk incrementally (no per-chunk 64-bit division)
-  int tile, qc, b0, p0;
-  atom_coords(g_first, tile, qc, b0, p0);
   for (int l = 0; l < n_local; ++l) {
     if (l > 0 && ++qc == nq) {
       qc = 0;
@@ -379,17 +419,20 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
         Gw[i] = valid ? p.gk * fmaf(p.ghx2, dx * dx, p.ghy2 * dy * dy) : neg_inf();
       }
     }
-    // segment start in estimate mode: running max := previous lse (target -
-    // old).  The loads are issued before the stage wait so their latency
-    // overlaps it; outputs with a -inf target never need their lse (parked).
     const bool est_init = d.use_est && (l == 0 || qc == 0);
+    if (p.dbg && tid == 0 && l == 0) p.dbg[12288 + blockIdx.x * 4 + 1] = globaltimer_ns();
+    mbar_wait(&bars[s], parity);
+    if (p.dbg && tid == 0 && l == 0) p.dbg[12288 + blockIdx.x * 4 + 2] = globaltimer_ns();
     if (est_init) {
+      // segment start in estimate mode: running max := previous lse (target -
+      // old), from the rows est_fetch staged; outputs with a -inf target never
+      // need their lse (parked).  Then stage the next segment's rows.
+      cp_async_wait_all();
 #pragma unroll
       for (int rp = 0; rp < RP; ++rp) {
-        const int pp = min(p0 + tp * RP + rp, p.Pv - 1);
-        const size_t row = size_t(pp) * p.Bp + b0 + tb * RB;
-        const float4 tg = __ldg(reinterpret_cast<const float4*>(p.target + row));
-        const float4 eo = *reinterpret_cast<const float4*>(d.est_old + row);
+        const float4 tg = *reinterpret_cast<const float4*>(est_buf + (size_t(rp) * NT + tid) * 4);
+        const float4 eo =
+            *reinterpret_cast<const float4*>(est_buf + (size_t(RP + rp) * NT + tid) * 4);
         const float tv[4] = {tg.x, tg.y, tg.z, tg.w};
         const float ev[4] = {eo.x, eo.y, eo.z, eo.w};
 #pragma unroll
@@ -398,8 +441,8 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
           M[rb * RP + rp] = (tv[rb] == neg_inf()) ? kParked : (isfinite(est) ? est : kNegBig);
         }
       }
+      if (tile < last_tile) est_fetch(tile + 1);
     }
-    mbar_wait(&bars[s], parity);
     if (kGrid) __syncthreads();
 
     // ---- consume: the hot loop --------------------------------------------
@@ -549,6 +592,7 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
     }
     __syncthreads();   // every warp is done with stage s
     if (tid == 0 && l + NSTAGE < n_local) issue(l + NSTAGE);
+    if (p.dbg && tid == 0 && l < 16) p.dbg[8192 + blockIdx.x * 16 + l] = globaltimer_ns();
 
     // ---- segment end: finalize or hand over to the stream-K merge ---------
     const bool seg_end = (qc == nq - 1) || (l == n_local - 1);
