@@ -172,9 +172,23 @@ def make_inputs(cfg: dict, device, seed: int):
         cost = GridCost(cfg["nx"], cfg["nx"])
     elif kind == "per_sample":
         cost = torch.rand(B, d, d, generator=g, device=device, dtype=torch.float32)
+    elif kind == "none":
+        cost = None
     else:
         raise ValueError(kind)
     return mu, nu, cost
+
+
+def index_cost_rows(d: int, r0: int, rows: int, device):
+    """Rows [r0, r0 + rows) of the |i - j|^2 / (d - 1)^2 cost, built in blocks."""
+    import torch
+
+    out = torch.empty(rows, d, device=device, dtype=torch.float32)
+    j = torch.arange(d, device=device, dtype=torch.float64)
+    for a in range(0, rows, 1024):
+        i = torch.arange(r0 + a, r0 + min(a + 1024, rows), device=device, dtype=torch.float64)
+        out[a:a + len(i)] = (((i[:, None] - j[None, :]).abs() / max(d - 1, 1)) ** 2).float()
+    return out
 
 
 def work_units(cfg: dict) -> float:
@@ -187,14 +201,16 @@ KERNEL_OF_PATH = {
     "persistent": "persistent_solve_kernel (cooperative whole loop)",
     "lane": "lane_col_kernel / lane_row_kernel (per-sample sweep)",
     "separable": "sep_sweep_kernel (separable grid LSE: two nested 1-D LSE-GEMMs per sweep)",
+    "row-sharded": "tiled_sweep_kernel through the half-sweep C ABI (this rank's cost rows; "
+                   "whole step incl. NCCL merges per half-sweep)",
 }
 
 
 def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
-             path: str = "tiled") -> dict:
+             path: str = "tiled", share: float = 1.0) -> dict:
     """Dominant kernel = the half-sweep (2*iters per step; one launch each on the
     tiled path, all inside one launch on the small path)."""
-    cells = float(cfg["B"]) * cfg["d"] * cfg["d"]          # cells per sweep launch
+    cells = float(cfg["B"]) * cfg["d"] * cfg["d"] * share  # cells per sweep launch (this GPU)
     if cfg["cost"] == "per_sample":
         achieved = cells * 4 / (sweep_ms * 1e-3) / 1e9      # algorithmic bytes: C read once
         peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -343,15 +359,39 @@ def run_ours(args, cfg, world, rank, local):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if args.sharding is None:
+        args.sharding = "row" if (args.config == 5 and world > 1) else "batch"
     lib = _lib.load()
     peaks = load_peaks()
-    mu, nu, cost = make_inputs(cfg, dev, seed=1234 + rank)
     B, d, lam, iters = cfg["B"], cfg["d"], cfg["lam"], cfg["iters"]
+    row = args.sharding == "row"
+    if row:
+        # BASELINE config 5: the cost's rows are sharded over the ranks; every
+        # column sweep merges (max, sum-exp) pairs across ranks
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=dev)   # also for a 1-rank run
+        from paper_1907_01729_b200 import distributed as D
+
+        if d % world:
+            raise SystemExit(f"row sharding needs d % world == 0 (d={d}, world={world})")
+        mu, nu, _ = make_inputs(dict(cfg, cost="none"), dev, seed=1234)
+        rows = d // world
+        r0 = rank * rows
+        cost = index_cost_rows(d, r0, rows, dev)
+        mu_l = mu[:, r0:r0 + rows].contiguous()
+        backend = D.CudaShardBackend(cost)
+    else:
+        mu, nu, cost = make_inputs(cfg, dev, seed=1234 + rank)
     up = torch.ones(B, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, device=dev, dtype=torch.float32)
-    gathered = torch.empty(B * world, device=dev) if world > 1 else None
+    gathered = torch.empty(B * world, device=dev) if (world > 1 and not row) else None
 
     def step():
+        if row:
+            res = D.row_sharded_solve(mu_l, nu, backend, lam, iters, 0.0, 10, d1_total=d)
+            D.row_sharded_backward(res.log_u, res.log_v, lam, up, d1_total=d)
+            res.loop_ms, res.path = -1.0, "row-sharded"
+            return res
         res = skb.solve(mu, nu, cost, lam, iters, 0.0, 10, validate=True, time_loop=True)
         gm, gn = skb.potentials_backward(res.log_u, res.log_v, lam, up)
         if world > 1:   # the single final loss collective of a batch-sharded step
@@ -385,32 +425,43 @@ def run_ours(args, cfg, world, rank, local):
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     ms = sum(step_ms) / len(step_ms)
     step_stats = {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)}
-    sweep_ms = statistics.median(loop_ms) / (2 * iters)
+    # row sharding has no per-solve loop timer: its half-sweep share is the step's
+    sweep_ms = (statistics.median(loop_ms) if not row else statistics.median(step_ms)) / (2 * iters)
     t = torch.tensor([ms, sweep_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, sweep_ms = float(t[0]), float(t[1])
-    value = world * work_units(cfg) / (ms * 1e-3)
+    # batch sharding: every rank solves its own B lanes (weak scaling);
+    # row sharding: the ranks share one B x d x d problem (strong scaling)
+    jobs = 1 if row else world
+    value = jobs * work_units(cfg) / (ms * 1e-3)
 
     # ---- end to end through the public / reference-facing API with host buffers ----
-    e2e = run_e2e(args, cfg, mu, nu, cost, lam, iters, dev)
+    if row:
+        e2e = run_e2e_row(args, step, mu_l, nu, dev)
+    else:
+        e2e = run_e2e(args, cfg, mu, nu, cost, lam, iters, dev)
     if world > 1:
         te = torch.tensor([e2e["seconds_per_step"]], device=dev, dtype=torch.float64)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e["seconds_per_step"] = float(te[0])
-    e2e_value = world * work_units(cfg) / e2e["seconds_per_step"]
+    e2e_value = jobs * work_units(cfg) / e2e["seconds_per_step"]
 
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": cfg["workload"], "B_per_gpu": B, "global_batch": B * world,
+        "higher_is_better": True, "scaling": "strong" if row else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "B_per_gpu": B, "global_batch": B * jobs,
                    "d1": d, "d2": d, "iters": iters, "lambda": lam, "tolerance": 0.0,
-                   "parallelism": f"batch-sharded dp{world}", "solver_path": path,
+                   "parallelism": (f"row-sharded cost over {world} GPU(s), NCCL (max, sum-exp) "
+                                   "all-reduce per column sweep") if row
+                   else f"batch-sharded dp{world}",
+                   "solver_path": path,
                    "l2": "flushed between steps (256 MiB write outside the timed events)"},
-        "roofline": roofline(cfg, sweep_ms, peaks, clocks, load_traffic(args.config), path),
+        "roofline": roofline(cfg, sweep_ms, peaks, clocks, load_traffic(args.config), path,
+                             share=(1.0 / world) if row else 1.0),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
                 "d2h_bytes_per_step": e2e["d2h"], "path": e2e["path"]},
         "gpu_launches": int(launches),
@@ -422,8 +473,32 @@ def run_ours(args, cfg, world, rank, local):
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
+
+
+def run_e2e_row(args, step_fn, mu_l, nu, dev):
+    """Row-sharded e2e: this rank's histogram columns and nu from pinned host
+    buffers into the same device tensors, the step, the losses back."""
+    import torch
+
+    h_mu, h_nu = mu_l.cpu().pin_memory(), nu.cpu().pin_memory()
+    h_loss = torch.empty(nu.shape[0]).pin_memory()
+    steps = max(1, min(args.steps, 3))
+
+    def one():
+        mu_l.copy_(h_mu, non_blocking=True)
+        nu.copy_(h_nu, non_blocking=True)
+        res = step_fn()
+        h_loss.copy_(res.cost_e0, non_blocking=True)
+        torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    dt = (time.perf_counter() - t0) / steps
+    return {"seconds_per_step": dt, "h2d": 4 * (mu_l.numel() + nu.numel()),
+            "d2h": 4 * nu.shape[0],
+            "path": "row_sharded_solve()+row_sharded_backward() from pinned host tensors"}
 
 
 def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
@@ -510,6 +585,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--clock-interval-ms", type=int, default=500)
+    ap.add_argument("--sharding", choices=["batch", "row"], default=None,
+                    help="multi-GPU split (default: row for config 5 on N>1, else batch)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.steps is None:
