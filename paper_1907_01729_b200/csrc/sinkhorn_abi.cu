@@ -170,6 +170,8 @@ struct Layout {
   long long sb1 = 0, si1 = 0, sb2 = 0, si2 = 0;  // element (b,i) at b*sb + i*si
   size_t a2 = 0, a2t = 0, f2 = 0, g2[2] = {0, 0}, l2mu = 0, l2nu = 0, mu = 0, nu = 0, e0 = 0;
   size_t res = 0, scratch = 0, part = 0, counters = 0, status = 0, badrow = 0, total = 0;
+  size_t sep_ax = 0, sep_ay = 0;   // separable grid: Ax [nx][nblk*32], Ay [ny][sep_ld(ny)]
+  size_t f2T = 0, g2T[2] = {0, 0}; // separable grid: the potentials transposed per lane
   size_t part_bytes = 0, counter_count = 0;
   int lane_nsplit = 1, lane_nj = 1, lane_vec = 4;
 };
@@ -236,7 +238,15 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     L.counter_count = (size_t)pr.B * L.lane_nj;
   }
   L.res = c.take((size_t)std::max(L.Bp, 1) * 4);
-  if (L.sep) L.part = c.take(std::max<size_t>(L.part_bytes, (size_t)sms * 8 * 2 * 4));
+  if (L.sep) {
+    L.part = c.take(std::max<size_t>(L.part_bytes, (size_t)sms * 8 * 2 * 4));
+    const size_t nblk = (size_t)(pr.grid_nx + 31) / 32;
+    L.sep_ax = c.take((size_t)pr.grid_nx * nblk * 32 * 4);
+    L.sep_ay = c.take((size_t)pr.grid_ny * sep_ld((int)pr.grid_ny) * 4);
+    L.f2T = c.take((size_t)L.B * L.D1p * 4);
+    L.g2T[0] = c.take((size_t)L.B * L.D2p * 4);
+    L.g2T[1] = c.take((size_t)L.B * L.D2p * 4);
+  }
   L.scratch = c.take(64);
   L.counters = c.take(std::max<size_t>(L.counter_count, 1) * 4);
   L.status = c.take(4);
@@ -452,15 +462,17 @@ struct Solve {
 #endif
   using SepS = SepShape<32, SKB_SEP_RN, (SKB_SEP_RN == 2) ? 256 : 128>;
   static constexpr int kSepNB = SepS::NB;
-  int sep_sweep(int mode, const float* x, const float* target, const float* marg,
-                const float* old, float* out, int res_kind, const float* est_src = nullptr) {
+  int sep_sweep(int mode, const float* xT, const float* target, const float* marg,
+                const float* old, float* out, float* outT, int res_kind,
+                const float* est_src = nullptr) {
     SepParams p = {};
     p.nx = (int)pr.grid_nx;
     p.ny = (int)pr.grid_ny;
-    p.ax = (float)(-kLog2e / lam) * (pr.grid_hx * pr.grid_hx);
-    p.ay = (float)(-kLog2e / lam) * (pr.grid_hy * pr.grid_hy);
+    p.ax_tab = F(L.sep_ax);
+    p.ay_tab = F(L.sep_ay);
     p.cinv = -lam * kLn2;
-    p.x = x;
+    p.xT = xT;
+    p.outT = outT;
     p.target = target;
     p.marg = marg;
     p.old = old;
@@ -482,7 +494,30 @@ struct Solve {
       attr_bytes[tail] = smem;
     }
     dim3 grid((unsigned)p.nblk, (unsigned)pr.B);
+    // diagnostics (SKB_SEP_TIMELINE=n): per-CTA start / staged / end stamps of the n-th sweep
+    static const long long tl_at = getenv("SKB_SEP_TIMELINE") ? atoll(getenv("SKB_SEP_TIMELINE")) : -1;
+    static long long tl_count = 0;
+    static unsigned long long* tl_buf = nullptr;
+    const bool tl = tl_at >= 0 && tl_count++ == tl_at;
+    const size_t nct = (size_t)grid.x * grid.y;
+    if (tl) {
+      if (!tl_buf) CK(cudaMalloc(&tl_buf, 8 * 4096 * 8));
+      p.dbg = tl_buf;
+    }
     CK(launch_pdl(kern, grid, dim3(SepS::NT), smem, st, p));
+    if (tl) {
+      std::vector<unsigned long long> h(8 * 4096);
+      CK(cudaMemcpyAsync(h.data(), tl_buf, 8 * 4096 * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      unsigned long long t0 = ~0ull;
+      for (size_t c = 0; c < nct; ++c) t0 = std::min(t0, h[4 * c]);
+      for (size_t c = 0; c < nct; ++c)
+        fprintf(stderr, "[skb] sep cta %zu sm %llu start %.2f staged %.2f end %.2f | factors %.2f "
+                "waited %.2f loaded %.2f\n", c, h[4 * c + 3],
+                (h[4 * c] - t0) * 1e-3, (h[4 * c + 1] - t0) * 1e-3, (h[4 * c + 2] - t0) * 1e-3,
+                (h[16384 + 4 * c] - t0) * 1e-3, (h[16384 + 4 * c + 1] - t0) * 1e-3,
+                (h[16384 + 4 * c + 2] - t0) * 1e-3);
+    }
     return 0;
   }
 
@@ -496,8 +531,8 @@ struct Solve {
                  : launch_tiled<false, kModeUpdate>(L, ws, di, a, pr, lam, st);
     }
     if (L.sep)
-      return sep_sweep(kModeUpdate, F(L.f2), F(L.l2nu), F(L.nu), F(L.g2[src_old]), F(L.g2[dst]),
-                       res_kind, est ? F(L.g2[src_old]) : nullptr);
+      return sep_sweep(kModeUpdate, F(L.f2T), F(L.l2nu), F(L.nu), F(L.g2[src_old]), F(L.g2[dst]),
+                       F(L.g2T[dst]), res_kind, est ? F(L.g2[src_old]) : nullptr);
     return lane_col(kModeUpdate, F(L.g2[dst]), F(L.g2[src_old]), res_kind);
   }
 
@@ -512,8 +547,8 @@ struct Solve {
                  : launch_tiled<false, kModeUpdate>(L, ws, di, a, pr, lam, st);
     }
     if (L.sep)
-      return sep_sweep(kModeUpdate, F(L.g2[src]), F(L.l2mu), F(L.mu), nullptr, F(L.f2), res_kind,
-                       est ? F(L.f2) : nullptr);
+      return sep_sweep(kModeUpdate, F(L.g2T[src]), F(L.l2mu), F(L.mu), nullptr, F(L.f2),
+                       F(L.f2T), res_kind, est ? F(L.f2) : nullptr);
     LaneSweepParams p = lane_params();
     p.x = F(L.g2[src]);
     p.ldx = L.D2p;
@@ -543,7 +578,8 @@ struct Solve {
                  : launch_tiled<false, kModeTail>(L, ws, di, a, pr, lam, st);
     }
     if (L.sep)
-      return sep_sweep(kModeTail, F(L.f2), nullptr, F(L.nu), F(L.g2[cur]), F(L.e0), kResCol);
+      return sep_sweep(kModeTail, F(L.f2T), nullptr, F(L.nu), F(L.g2[cur]), F(L.e0), nullptr,
+                       kResCol);
     return lane_col(kModeTail, nullptr, F(L.g2[cur]), kResCol);
   }
 
@@ -932,6 +968,18 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     const size_t n = (size_t)pr.B * pr.d1 * pr.d2;
     ++g_launches;
     validate_cost_kernel<<<grid_for(n), 256, 0, st>>>(cost, n, status);
+    CK(cudaGetLastError());
+  }
+  if (L.sep) {   // the separable sweeps' factor tables (once per solve), log u transposed
+    const int nblk = (int)((pr.grid_nx + 31) / 32);
+    ++g_launches;
+    sep_transpose_kernel<<<grid_for((size_t)pr.B * pr.d1), 256, 0, st>>>(
+        S.F(L.f2), S.F(L.f2T), (int)pr.B, L.D1p, (int)pr.grid_nx, (int)pr.grid_ny);
+    ++g_launches;
+    sep_tables_kernel<<<64, 256, 0, st>>>(S.F(L.sep_ax), S.F(L.sep_ay), (int)pr.grid_nx,
+                                          (int)pr.grid_ny, nblk * 32,
+                                          (float)(-kLog2e / op.lambda) * (pr.grid_hx * pr.grid_hx),
+                                          (float)(-kLog2e / op.lambda) * (pr.grid_hy * pr.grid_hy));
     CK(cudaGetLastError());
   }
   SmallParams sp;

@@ -14,8 +14,12 @@
 //
 // One CTA owns (lane, block of NB jx columns): step 1 produces T(:, block),
 // step 2 the outputs (:, block) -- the blocks of a lane share no work.  Both
-// steps are the same "LSE-GEMM" over shared-memory operands, 4x4 outputs per
-// thread (two passes: max, then sum of 2^(p + q - max)).
+// steps are the same "LSE-GEMM" out(m, n) = LSE_k(P(m, k) + Q(k, n)) over
+// shared-memory operands, 4x2 outputs per thread:
+//   step 1: P^T = x^T [ix][iy] (transposed on staging), Q = Ax block
+//   step 2: P^T = Ay [iy][jy] (symmetric),               Q = T
+// The Ax / Ay tables are built once per solve and arrive by cp.async (no
+// per-CTA arithmetic, no registers) before the PDL wait.
 #pragma once
 
 #include "common.cuh"
@@ -24,9 +28,11 @@ namespace skb {
 
 struct SepParams {
   int nx, ny;
-  float ax, ay;            // log2 factors: Ax(a, b) = ax * (a - b)^2
   float cinv;              // cost = A2 * cinv
-  const float* x;          // input potential, lane-major: (b, k) at b * ld + k
+  const float* ax_tab;     // [nx][nblk*NB] Ax(ix, jx) (log2 units), padded columns finite
+  const float* ay_tab;     // [ny][sep_ld(ny)] Ay(iy, jy)
+  const float* xT;         // input potential transposed, lane-major: (b, ix, iy) at b*ld + ix*ny + iy
+  float* outT;             // update: the new potential transposed (same layout), else null
   const float* target;
   const float* marg;
   const float* old;
@@ -39,6 +45,7 @@ struct SepParams {
   int use_poly;            // part of the exponentials on the FMA pipe
   const float* est_src;    // previous potential of this orientation (estimate mode) or null
   unsigned int* redo;      // count of thread tiles redone exactly (statistics)
+  unsigned long long* dbg; // optional per-CTA timeline (diagnostics), nullable
 };
 
 // Estimate mode: the shifted sum must stay inside [2^kSepLo, 2^kSepHi] so no
@@ -63,15 +70,14 @@ struct SepShape {
   static_assert(NT % TN == 0, "whole m rows of threads");
 };
 
-// floats of shared memory for an nx x ny grid
-__host__ __device__ inline int sep_ldm(int ny) { return (ny + 3) & ~3; }
+// leading dimension (floats) of shared rows indexed by y: padded to 4
+__host__ __device__ inline int sep_ld(int n) { return (n + 3) & ~3; }
 template <class S>
 __host__ __device__ inline size_t sep_smem_floats(int nx, int ny, bool tail) {
-  const int ldm = sep_ldm(ny);
-  return (size_t)nx * ldm          // XT [ix][iy]
+  return std::max((size_t)nx * sep_ld(ny), (size_t)S::NB * (ny + 1))   // XT [ix][iy] / OT [n][jy]
          + (size_t)nx * S::NB      // Ax block [ix][n]
-         + (size_t)ny * ldm        // Ay [iy][jy]
-         + (size_t)ny * S::NB      // T [iy][n]
+         + (size_t)ny * sep_ld(ny) // Ay [iy][jy]
+         + (size_t)ny * S::NB      // T  [iy][n]
          + (tail ? (size_t)ny * S::NB : 0) + S::MT;   // pad: ragged m tiles read past the end
 }
 
@@ -236,76 +242,72 @@ __device__ __forceinline__ bool sep_estimate(const SepParams& p, int b, int m0, 
   return ok;
 }
 
+// Rows of `cols` floats from global (row stride gld) into shared memory (row
+// stride sld): 16-byte cp.async when every row start is 16-byte aligned,
+// 4-byte otherwise.  The caller commits the group.
+template <int NT>
+__device__ __forceinline__ void sep_stage_rows(float* dst, int sld, const float* src, size_t gld,
+                                               int rows, int cols) {
+  const bool v4 = ((cols | sld | (int)(gld & 3)) & 3) == 0 &&
+                  (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  if (v4) {
+    const int c4 = cols >> 2;
+    for (int e = threadIdx.x; e < rows * c4; e += NT) {
+      const int r = e / c4, c = e - r * c4;
+      cp_async16(dst + (size_t)r * sld + 4 * c, src + r * gld + 4 * c);
+    }
+  } else {
+    for (int e = threadIdx.x; e < rows * cols; e += NT) {
+      const int r = e / cols, c = e - r * cols;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                       smem_u32(dst + (size_t)r * sld + c)),
+                   "l"(src + r * gld + c)
+                   : "memory");
+    }
+  }
+}
+
 template <class S, int kMode>
-__global__ void __launch_bounds__(S::NT, (S::NT >= 256) ? 4 : 4) sep_sweep_kernel(const SepParams p) {
+__global__ void __launch_bounds__(S::NT, 4) sep_sweep_kernel(const SepParams p) {
   constexpr bool kTail = (kMode == kModeTail);
   constexpr int NB = S::NB, RN = S::RN, NT = S::NT;
   extern __shared__ __align__(16) float sep_smem[];
-  const int nx = p.nx, ny = p.ny, ldm = sep_ldm(ny);
-  float* XT = sep_smem;
-  float* AX = XT + (size_t)nx * ldm;
-  float* AY = AX + (size_t)nx * NB;
-  float* T = AY + (size_t)ny * ldm;
-  float* R = T + (size_t)ny * NB;   // tail only
+  const int nx = p.nx, ny = p.ny, ldm = sep_ld(ny);
+  float* XT = sep_smem;                      // [nx][ldm]
+  float* AX = XT + (size_t)nx * ldm;         // [nx][NB]
+  float* AY = AX + (size_t)nx * NB;          // [ny][ldm]
+  float* T = AY + (size_t)ny * ldm;          // [ny][NB]
+  float* R = T + (size_t)ny * NB;            // [ny][NB], tail only
   __shared__ unsigned int s_res;
   const int tid = threadIdx.x;
   const int b = blockIdx.y;
   const int jx0 = blockIdx.x * NB;
-  const float* xb = p.x + (size_t)b * p.ld;
 
   if (tid == 0) s_res = 0u;
-  // cost factors first: they do not depend on the previous sweep (PDL overlap)
-  for (int e = tid; e < nx * NB; e += NT) {
-    const int ix = e / NB, n = e - ix * NB;
-    const float d = float(ix - (jx0 + n));
-    AX[e] = p.ax * (d * d);
+  const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+  if (p.dbg && tid == 0) {
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.dbg[4 * cta] = globaltimer_ns();
+    p.dbg[4 * cta + 3] = smid;
   }
-  for (int e = tid; e < ny * ldm; e += NT) {
-    const int iy = e / ldm, jy = e - iy * ldm;
-    const float d = float(iy - jy);
-    AY[e] = p.ay * (d * d);
-  }
+  // everything arrives by cp.async: the cost factors before the PDL wait
+  // (they do not depend on the previous sweep), then the lane's potential,
+  // which the previous sweep also wrote transposed ([ix][iy]) for this copy
+  sep_stage_rows<NT>(AX, NB, p.ax_tab + jx0, (size_t)p.nblk * NB, nx, NB);
+  sep_stage_rows<NT>(AY, ldm, p.ay_tab, (size_t)ldm, ny, ny);
+  cp_async_commit();
   pdl_wait();   // x is the previous sweep's output
-  // the lane's potential, transposed into XT[ix][iy]: consecutive threads take
-  // consecutive rows iy (conflict-free transposed stores), every 16-byte load
-  // of a batch in flight before the first store
-  if ((nx & 3) == 0) {
-    const int nx4 = nx >> 2, n4 = nx4 * ny;
-    for (int base = 0; base < n4; base += NT * 4) {
-      float4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int idx = base + u * NT + tid;
-        if (idx < n4) {
-          const int ix4 = idx / ny, iy = idx - ix4 * ny;
-          v[u] = __ldcg(reinterpret_cast<const float4*>(xb + (size_t)iy * nx) + ix4);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int idx = base + u * NT + tid;
-        if (idx < n4) {
-          const int ix4 = idx / ny, iy = idx - ix4 * ny;
-          float* d = XT + (size_t)(4 * ix4) * ldm + iy;
-          d[0] = v[u].x;
-          d[ldm] = v[u].y;
-          d[2 * ldm] = v[u].z;
-          d[3 * ldm] = v[u].w;
-        }
-      }
-    }
-  } else {
-    for (int e = tid; e < nx * ny; e += NT) {
-      const int iy = e / nx, ix = e - iy * nx;
-      XT[(size_t)ix * ldm + iy] = __ldcg(xb + e);
-    }
-  }
+  sep_stage_rows<NT>(XT, ldm, p.xT + (size_t)b * p.ld, (size_t)ny, nx, ny);
+  cp_async_commit();
+  cp_async_wait_all();
   __syncthreads();
   pdl_launch_dependents();
+  if (p.dbg && tid == 0) p.dbg[4 * cta + 1] = globaltimer_ns();
 
   const int tn = tid % S::TN, tm = tid / S::TN;
   float mx[S::OUT], sm[S::OUT], w[S::OUT];
-  // ---- step 1: T(iy, n) = LSE_ix(Ax(ix, n) + x(iy, ix)) --------------------
+  // ---- step 1: T(iy, n) = LSE_ix(x(iy, ix) + Ax(ix, n)) --------------------
   for (int m0 = 0; m0 < ny; m0 += S::MT) {
     bool done = false;
     if (!kTail && p.est_src != nullptr) {
@@ -333,7 +335,11 @@ __global__ void __launch_bounds__(S::NT, (S::NT >= 256) ? 4 : 4) sep_sweep_kerne
     }
   }
   __syncthreads();
-  // ---- step 2: lse(jy, n) = LSE_iy(Ay(iy, jy) + T(iy, n)); epilogue --------
+  // ---- step 2: lse(jy, n) = LSE_iy(Ay(jy, iy) + T(iy, n)); epilogue --------
+  // The block's new potentials are also collected transposed in OT (XT is
+  // dead after step 1) and written out as whole [jx][iy] rows below.
+  float* OT = XT;
+  const int kOtLd = ny + 1;   // odd: the thread tile's column stores spread over banks
   float rmax = 0.f;
   for (int m0 = 0; m0 < ny; m0 += S::MT) {
     bool done = false;
@@ -373,6 +379,8 @@ __global__ void __launch_bounds__(S::NT, (S::NT >= 256) ? 4 : 4) sep_sweep_kerne
           if (p.res_kind == kResCol) rmax = fmaxf(rmax, fabsf(exp2f(od[a][c] + lse) - mg[a][c]));
         }
         sep_st_row<RN>(p.out + (size_t)b * p.ld + (size_t)jy * nx + jxb, nv);
+#pragma unroll
+        for (int c = 0; c < RN; ++c) OT[(tn * RN + c) * kOtLd + jy] = nv[c];
       }
       continue;
     }
@@ -394,11 +402,19 @@ __global__ void __launch_bounds__(S::NT, (S::NT >= 256) ? 4 : 4) sep_sweep_kerne
         } else {
           const float nv = sweep_out(p.target[k], lse);
           p.out[k] = nv;
+          OT[(tn * RN + c) * kOtLd + jy] = nv;
           if (p.res_kind == kResRow) rmax = fmaxf(rmax, fabsf(exp2f(nv + lse) - p.marg[k]));
           if (p.res_kind == kResCol) rmax = fmaxf(rmax, fabsf(exp2f(p.old[k] + lse) - p.marg[k]));
         }
       }
     }
+  }
+  if (!kTail) {   // the transposed copy the next sweep stages: coalesced rows
+    __syncthreads();
+    const int ncol = min(NB, nx - jx0);
+    float* dst = p.outT + (size_t)b * p.ld + (size_t)jx0 * ny;
+    for (int r = tid / 32; r < ncol; r += NT / 32)
+      for (int jy = tid % 32; jy < ny; jy += 32) dst[(size_t)r * ny + jy] = OT[r * kOtLd + jy];
   }
   if (kTail || p.res_kind != kResNone) {
     // NaN must win the max (batch.py:320 compares max <= tol, false for NaN)
@@ -406,6 +422,45 @@ __global__ void __launch_bounds__(S::NT, (S::NT >= 256) ? 4 : 4) sep_sweep_kerne
     atomicMax(&s_res, __float_as_uint(rmax));
     __syncthreads();
     if (tid == 0) atomic_max_nonneg(&p.res[b], __uint_as_float(s_res));
+  }
+  if (p.dbg) {
+    __syncthreads();
+    if (tid == 0) p.dbg[4 * cta + 2] = globaltimer_ns();
+  }
+}
+
+// Per-lane transpose [ny][nx] -> [nx][ny] of a lane-major potential (the
+// initial log u of the separable path; later sweeps write both layouts).
+__global__ void sep_transpose_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                     int B, int ld, int nx, int ny) {
+  const size_t n = (size_t)B * nx * ny;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const int b = (int)(e / ((size_t)nx * ny));
+    const int k = (int)(e - (size_t)b * nx * ny);
+    const int iy = k / nx, ix = k - iy * nx;
+    dst[(size_t)b * ld + (size_t)ix * ny + iy] = src[(size_t)b * ld + k];
+  }
+}
+
+// The factor tables of one grid, built once per solve: Ax(ix, jx) for jx up to
+// nblk*NB (padded columns hold finite values; their outputs are never stored)
+// and Ay(iy, jy) with a leading dimension of sep_ld(ny).
+__global__ void sep_tables_kernel(float* ax_tab, float* ay_tab, int nx, int ny, int axcols,
+                                  float ax, float ay) {
+  const int ldy = sep_ld(ny);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nx * axcols + ny * ldy;
+       e += gridDim.x * blockDim.x) {
+    if (e < nx * axcols) {
+      const int i = e / axcols, j = e - i * axcols;
+      const float d = float(i - j);
+      ax_tab[e] = ax * (d * d);
+    } else {
+      const int f = e - nx * axcols;
+      const int i = f / ldy, j = f - i * ldy;
+      const float d = float(i - j);
+      ay_tab[f] = ay * (d * d);
+    }
   }
 }
 
