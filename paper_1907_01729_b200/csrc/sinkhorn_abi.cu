@@ -850,8 +850,26 @@ struct Solve {
     }
     cfg.attrs = attr;
     cfg.numAttrs = (unsigned)na;
+    static const bool tl = getenv("SKB_SMALL_TIMELINE") != nullptr;   // diagnostics
+    static unsigned long long* tl_buf = nullptr;
+    if (tl) {
+      if (!tl_buf) CK(cudaMalloc(&tl_buf, 64 * 8));
+      CK(cudaMemsetAsync(tl_buf, 0, 64 * 8, st));
+      sp.dbg = tl_buf;
+    }
     ++g_launches;
     CK(cudaLaunchKernelEx(&cfg, &small_solve_kernel<kSmallNT>, sp));
+    if (tl) {
+      unsigned long long h[64];
+      CK(cudaMemcpyAsync(h, tl_buf, sizeof(h), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int k = 1; k <= 8; ++k)
+        fprintf(stderr, "[skb] small it %d: col %.2f sync %.2f row %.2f sync %.2f us\n", k,
+                (h[4 * k] - (k == 1 ? h[0] : h[4 * k - 1])) * 1e-3, (h[4 * k + 1] - h[4 * k]) * 1e-3,
+                (h[4 * k + 2] - h[4 * k + 1]) * 1e-3, (h[4 * k + 3] - h[4 * k + 2]) * 1e-3);
+      fprintf(stderr, "[skb] small C %d L %d Sc %d Sr %d grid %d\n", sp.C, sp.L, sp.Sc, sp.Sr,
+              (int)cfg.gridDim.x);
+    }
     if (sp.checks) {
       CK(cudaMemcpyAsync(iters, sp.result, 4, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));

@@ -58,6 +58,7 @@ struct SmallParams {
   unsigned int* bar;  // grid-barrier counter (zero on entry)
   int* result;        // [0] iterations_run
   int* status;
+  unsigned long long* dbg;   // optional timeline of CTA 0 (diagnostics), nullable
 };
 
 __host__ __device__ inline int small_slice(int n, int C, int r) { return (int)((long long)n * r / C); }
@@ -278,11 +279,15 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
   int cur = 0;             // g[cur] holds log_v_k
   bool have_next = false;  // g[cur] already advanced by a check sweep
   int iters = 0, check_no = 0;
+  const bool tl = p.dbg != nullptr && blockIdx.x == 0 && tid == 0;
+  if (tl) p.dbg[0] = globaltimer_ns();
   for (int k = 1; k <= p.max_iters; ++k) {
     if (!have_next) {
       small_sweep<NT, 0>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, sm.lnu, nullptr,
                          nullptr, sm.g(cur ^ 1), nullptr, 0.f, peers, small_smem, C, crank);
+      if (tl && k <= 8) p.dbg[4 * k] = globaltimer_ns();
       small_sync(C);
+      if (tl && k <= 8) p.dbg[4 * k + 1] = globaltimer_ns();
       cur ^= 1;
     }
     have_next = false;
@@ -297,7 +302,9 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
       small_sweep<NT, 0>(sm.A, p.ldr, p.d1, i0, i1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, nullptr,
                          nullptr, sm.f, nullptr, 0.f, peers, small_smem, C, crank);
     }
+    if (tl && k <= 8) p.dbg[4 * k + 2] = globaltimer_ns();
     small_sync(C);
+    if (tl && k <= 8) p.dbg[4 * k + 3] = globaltimer_ns();
     iters = k;
     if (check) {
       // column sweep k+1 doubles as the column residual of iteration k
