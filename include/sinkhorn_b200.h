@@ -124,6 +124,20 @@ int32_t sinkhorn_forward_device_v1(const sinkhorn_problem_v1* prob,
                                    float* out_residuals, void* workspace,
                                    size_t workspace_bytes, void* stream);
 
+/* Warm start (the reference has no such API, batch.py:295
+ * always starts from log_u = 0 on the support): as sinkhorn_forward_device_v1,
+ * but the iteration starts from init_log_u (B, d1) natural log, device fp32,
+ * kept -inf off the support.  init_log_u == NULL is a cold start.  Running
+ * k1 iterations, then k2 more from the returned log_u, equals one run of
+ * k1 + k2 iterations. */
+int32_t sinkhorn_forward_warm_device_v1(const sinkhorn_problem_v1* prob,
+                                        const sinkhorn_options_v1* opt, const float* mu,
+                                        const float* nu, const float* cost,
+                                        const float* init_log_u, float* out_cost,
+                                        float* out_log_u, float* out_log_v,
+                                        int32_t* out_iterations, float* out_residuals,
+                                        void* workspace, size_t workspace_bytes, void* stream);
+
 /* batch_backward (batch.py:352-375): grad = upstream[b]*lambda*(x - mean_i x).
  * Any -inf in a lane returns 13; `out_zero_mass_lane` (host, may be NULL)
  * receives the first such lane.  No workspace beyond 64 bytes (passed). */

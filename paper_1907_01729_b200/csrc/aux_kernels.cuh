@@ -283,6 +283,15 @@ __global__ void __launch_bounds__(256) import_potential_kernel(const float* __re
   }
 }
 
+// Warm start: an imported log u stays -inf off the support (mu = 0), as the
+// reference's initial potential does (batch.py:295).
+__global__ void mask_potential_kernel(float* __restrict__ x, const float* __restrict__ lin,
+                                      size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    if (!(lin[i] > 0.f)) x[i] = neg_inf();
+}
+
 // double <-> float conversions for the host-buffer (float64) ABI layer.
 __global__ void f64_to_f32_kernel(const double* __restrict__ a, float* __restrict__ b, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;

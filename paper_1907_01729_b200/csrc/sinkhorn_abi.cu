@@ -722,6 +722,8 @@ struct Solve {
   }
 
   // Returns a status (non-zero only on a CUDA error); *ok says whether to use it.
+  bool warm = false;   // the solve starts from a caller's log u (f2 holds it)
+
   int plan_small(SmallParams& sp, int& G, size_t& smem, bool* ok) {
     *ok = false;
     if (!(L.tiled || L.sep) || g_reducer != nullptr || (op.flags & SINKHORN_FLAG_TILED_ONLY))
@@ -797,6 +799,7 @@ struct Solve {
       sp.l2nu = F(L.l2nu);
       sp.mu = F(L.mu);
       sp.nu = F(L.nu);
+      sp.f2_init = warm ? F(L.f2) : nullptr;
       sp.B = (int)B;
       sp.sb1 = L.sb1;
       sp.si1 = L.si1;
@@ -929,7 +932,8 @@ int check_options(const sinkhorn_options_v1* op) {
 int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, const float* mu,
                  const float* nu, const float* cost, float* out_cost, float* out_log_u,
                  float* out_log_v, int32_t* out_iterations, float* out_residuals, void* ws,
-                 size_t ws_bytes, cudaStream_t st, bool allow_est = true) {
+                 size_t ws_bytes, cudaStream_t st, bool allow_est = true,
+                 const float* init_log_u = nullptr) {
   Solve S;
   S.pr = pr;
   S.op = op;
@@ -940,6 +944,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   S.lam = (float)op.lambda;
   S.cost = cost;
   S.poly = (op.flags & SINKHORN_FLAG_MUFU_ONLY) == 0;
+  S.warm = init_log_u != nullptr;
   const Layout& L = S.L;
   if (ws_bytes < L.total || ws == nullptr)
     return fail(SINKHORN_STATUS_WORKSPACE, "workspace too small");
@@ -974,6 +979,16 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     if (int e = fill(S.F(L.g2[1]), (size_t)(L.tiled ? (size_t)L.D2p * L.Bp : (size_t)L.B * L.D2p),
                      neg_inf_host(), st))
       return e;
+  }
+  if (init_log_u != nullptr) {   // warm start: log u from the caller, -inf off the support
+    dim3 gi((unsigned)((L.D1p + 31) / 32), (unsigned)((L.Bp + 31) / 32));
+    ++g_launches;
+    import_potential_kernel<<<gi, 256, 0, st>>>(init_log_u, (int)pr.B, (int)pr.d1, L.Bp, L.D1p,
+                                                L.sb1, L.si1, S.F(L.f2));
+    const size_t n1 = L.tiled ? (size_t)L.D1p * L.Bp : (size_t)L.B * L.D1p;
+    ++g_launches;
+    mask_potential_kernel<<<grid_for(n1), 256, 0, st>>>(S.F(L.f2), S.F(L.mu), n1);
+    CK(cudaGetLastError());
   }
   if (pr.cost_kind == SINKHORN_COST_SHARED) {
     dim3 g((unsigned)((L.D2p + 31) / 32), (unsigned)((L.D1p + 31) / 32));
@@ -1118,7 +1133,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
         cudaEventDestroy(ev1);
       }
       return forward_impl(pr, op, mu, nu, cost, out_cost, out_log_u, out_log_v, out_iterations,
-                          out_residuals, ws, ws_bytes, st, false);
+                          out_residuals, ws, ws_bytes, st, false, init_log_u);
     }
   }
   static const bool stats = getenv("SKB_SEP_STATS") != nullptr;   // diagnostics
@@ -1189,6 +1204,30 @@ int32_t sinkhorn_forward_device_v1(const sinkhorn_problem_v1* prob,
                       out_residuals, workspace, workspace_bytes,
                       static_cast<cudaStream_t>(stream),
                       (opt->flags & SINKHORN_FLAG_EXACT_MAX) == 0);
+}
+
+int32_t sinkhorn_forward_warm_device_v1(const sinkhorn_problem_v1* prob,
+                                   const sinkhorn_options_v1* opt, const float* mu,
+                                   const float* nu, const float* cost, const float* init_log_u,
+                                   float* out_cost,
+                                   float* out_log_u, float* out_log_v, int32_t* out_iterations,
+                                   float* out_residuals, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  if (int e = check_problem(prob)) return e;
+  if (prob->B == 0) {   // ffi.ts:107-109
+    if (out_iterations) *out_iterations = 0;
+    return 0;
+  }
+  if (prob->d1 == 0 || prob->d2 == 0)
+    return fail(SINKHORN_STATUS_INVALID_HISTOGRAM, "empty histogram cannot sum to 1");
+  if (int e = check_options(opt)) return e;
+  if (!mu || !nu || !out_cost || !out_log_u || !out_log_v ||
+      (prob->cost_kind != SINKHORN_COST_GRID2D && !cost))
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
+  return forward_impl(*prob, *opt, mu, nu, cost, out_cost, out_log_u, out_log_v, out_iterations,
+                      out_residuals, workspace, workspace_bytes,
+                      static_cast<cudaStream_t>(stream),
+                      (opt->flags & SINKHORN_FLAG_EXACT_MAX) == 0, init_log_u);
 }
 
 

@@ -42,6 +42,7 @@ struct SmallParams {
   const float* l2nu;  //                 element (b, j) at b * sb2 + j * si2
   const float* mu;
   const float* nu;
+  const float* f2_init;   // warm start: log2 u in the solver layout (null: cold start)
   long long sb1, si1, sb2, si2;
   int B, d1, d2;
   int L;              // lanes per CTA (per cluster)
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
     const size_t gi = (size_t)(b0 + l) * p.sb1 + (size_t)i * p.si1;
     sm.lmu[e] = p.l2mu[gi];
     sm.mu[e] = p.mu[gi];
-    sm.f[e] = (p.mu[gi] > 0.f) ? 0.f : neg_inf();   // batch.py:295
+    sm.f[e] = p.f2_init ? p.f2_init[gi] : ((p.mu[gi] > 0.f) ? 0.f : neg_inf());   // batch.py:295
   }
   for (int e = tid; e < nl * p.d2; e += NT) {
     const int l = e / p.d2, j = e - l * p.d2;

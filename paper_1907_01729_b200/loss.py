@@ -137,13 +137,15 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
           check_interval: int = 10, validate: bool = True, time_loop: bool = False,
           exact_max: bool = False, mufu_only: bool = False,
           persistent: bool = False, tiled_only: bool = False,
-          dense_grid: bool = False) -> SolveResult:
+          dense_grid: bool = False, init_log_u=None) -> SolveResult:
     """batch_forward (batch.py:264-349) on the GPU.
 
     mu (B, d1), nu (B, d2) histograms; cost a (d1, d2) tensor shared by all
     lanes, a (B, d1, d2) per-sample tensor, or a GridCost.  Inputs are cast
     to contiguous float32 on the current CUDA device.  ``exact_max`` forces
     the two-pass chunk reduction (no previous-iteration lse estimate).
+    ``init_log_u`` (B, d1) warm-starts the iteration from a previous solve's
+    log_u instead of 0 on the support (no reference API; batch.py:295).
     """
     mu, nu = torch.as_tensor(mu), torch.as_tensor(nu)
     if not isinstance(cost, GridCost):
@@ -171,11 +173,21 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
         nbytes = lib.sinkhorn_workspace_bytes_v1(ctypes.byref(pr))
         ws = _workspace(dev, nbytes)
         iters = ctypes.c_int32(0)
-        st = lib.sinkhorn_forward_device_v1(
-            ctypes.byref(pr), ctypes.byref(op), _ptr(mu), _ptr(nu),
-            None if isinstance(cost, GridCost) else _ptr(cost), _ptr(out_cost), _ptr(log_u),
-            _ptr(log_v), ctypes.byref(iters), _ptr(residuals), _ptr(ws), ws.numel(),
-            _stream_handle(dev))
+        if init_log_u is not None:
+            init = _as_f32_cuda(init_log_u, dev)
+            if tuple(init.shape) != (B, d1):
+                raise ShapeMismatch(f"init_log_u must be ({B}, {d1}), got {tuple(init.shape)}")
+            st = lib.sinkhorn_forward_warm_device_v1(
+                ctypes.byref(pr), ctypes.byref(op), _ptr(mu), _ptr(nu),
+                None if isinstance(cost, GridCost) else _ptr(cost), _ptr(init), _ptr(out_cost),
+                _ptr(log_u), _ptr(log_v), ctypes.byref(iters), _ptr(residuals), _ptr(ws),
+                ws.numel(), _stream_handle(dev))
+        else:
+            st = lib.sinkhorn_forward_device_v1(
+                ctypes.byref(pr), ctypes.byref(op), _ptr(mu), _ptr(nu),
+                None if isinstance(cost, GridCost) else _ptr(cost), _ptr(out_cost), _ptr(log_u),
+                _ptr(log_v), ctypes.byref(iters), _ptr(residuals), _ptr(ws), ws.numel(),
+                _stream_handle(dev))
     raise_for_status(st, "sinkhorn_forward_device_v1")
     loop_ms = float(lib.sinkhorn_last_loop_ms_v1()) if time_loop else -1.0
     path = lib.sinkhorn_last_path_v1().decode()

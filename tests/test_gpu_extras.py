@@ -119,3 +119,41 @@ def test_batch_sharded_solve_on_the_device(nccl_world1, cuda):
     assert res.iterations_run == int(g["iterations_run"])
     rel = np.abs(all_costs.double().cpu().numpy() - g["cost_e0"]) / g["cost_e0"]
     assert rel.max() <= LOSS_RTOL
+
+
+@pytest.mark.parametrize("case", ["small", "tiled", "separable", "per_sample"])
+def test_warm_start_continues_the_iteration(case, cuda):
+    """k1 iterations, then k2 more from the returned log_u, equal one run of
+    k1 + k2 iterations (the k-th iterate depends only on log_u_{k-1}), on every
+    solver path; a warm start from a converged solution stays there."""
+    skb = _skb()
+    from oracle import sinkhorn_oracle as orc
+
+    rng = np.random.default_rng(11)
+    kw = {}
+    if case == "per_sample":
+        B, d = 6, 48
+        cost = torch.rand(B, d, d, device=cuda)
+    elif case == "separable":
+        B, d = 6, 12 * 7
+        cost = skb.GridCost(12, 7)
+        kw = {"tiled_only": True}
+    else:
+        B, d = 6, 60
+        cost = torch.tensor(orc.fp32_exact(orc.index_grid_cost(d)), dtype=torch.float32,
+                            device=cuda)
+        kw = {"tiled_only": case == "tiled"}
+    mu = torch.tensor(orc.fp32_exact(orc.random_histogram_batch(B, d, rng)), device=cuda)
+    nu = torch.tensor(orc.fp32_exact(orc.random_histogram_batch(B, d, rng)), device=cuda)
+    mu[2, 5] = 0.0
+    mu[2] /= mu[2].sum()
+    lam = 0.1
+    full = skb.solve(mu, nu, cost, lam, 40, 0.0, **kw)
+    first = skb.solve(mu, nu, cost, lam, 25, 0.0, **kw)
+    rest = skb.solve(mu, nu, cost, lam, 15, 0.0, init_log_u=first.log_u, **kw)
+    rel = ((rest.cost_e0 - full.cost_e0).abs() / full.cost_e0).max()
+    assert float(rel) <= 2e-6
+    fin = torch.isfinite(full.log_u)
+    assert torch.equal(fin, torch.isfinite(rest.log_u))
+    assert float((rest.log_u[fin] - full.log_u[fin]).abs().max()) <= 1e-4
+    assert bool(torch.isneginf(rest.log_u[2, 5]))
