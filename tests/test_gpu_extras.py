@@ -157,3 +157,44 @@ def test_warm_start_continues_the_iteration(case, cuda):
     assert torch.equal(fin, torch.isfinite(rest.log_u))
     assert float((rest.log_u[fin] - full.log_u[fin]).abs().max()) <= 1e-4
     assert bool(torch.isneginf(rest.log_u[2, 5]))
+
+
+def test_config5_pin_at_d16384(cuda):
+    """config 5's 1-D index-grid path pinned to the reference at d=16384
+    (2 lanes x 20 iterations; d=65536 is infeasible for the reference)."""
+    skb = _skb()
+    g = load_golden("config5_pin16384")
+    c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
+    res = skb.solve(torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
+                    float(g["lam"]), int(g["max_iters"]), 0.0)
+    rel = np.abs(res.cost_e0.double().cpu().numpy() - g["cost_e0"]) / g["cost_e0"]
+    assert rel.max() <= LOSS_RTOL
+    gm, gn = skb.potentials_backward(res.log_u, res.log_v, float(g["lam"]),
+                                     torch.ones(2, device=cuda))
+    assert np.abs(gm.double().cpu().numpy() - g["grad_mu"]).max() <= GRAD_ATOL
+    assert np.abs(gn.double().cpu().numpy() - g["grad_nu"]).max() <= GRAD_ATOL
+
+
+def test_row_sharded_matches_fused_solve_at_d65536(nccl_world1, cuda):
+    """at config 5's full d the row-sharded driver (here one rank) is
+    cross-checked against the build's own fused single-GPU solve."""
+    skb = _skb()
+    from paper_1907_01729_b200 import distributed as D
+
+    d, B, lam, iters = 65536, 2, 0.05, 3
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(5)
+    mu = torch.rand(B, d, generator=gen, device=cuda, dtype=torch.float64) + 0.5
+    nu = torch.rand(B, d, generator=gen, device=cuda, dtype=torch.float64) + 0.5
+    mu, nu = (mu / mu.sum(1, keepdim=True)).float(), (nu / nu.sum(1, keepdim=True)).float()
+    c = torch.empty(d, d, device=cuda)
+    j = torch.arange(d, device=cuda, dtype=torch.float64)
+    for a in range(0, d, 4096):
+        i = torch.arange(a, a + 4096, device=cuda, dtype=torch.float64)
+        c[a:a + 4096] = (((i[:, None] - j[None, :]).abs() / (d - 1)) ** 2).float()
+    fused = skb.solve(mu, nu, c, lam, iters, 0.0)
+    torch.cuda.empty_cache()
+    rows = D.row_sharded_solve(mu, nu, D.CudaShardBackend(c), lam, iters, 0.0, d1_total=d)
+    rel = ((rows.cost_e0.double() - fused.cost_e0.double()).abs() / fused.cost_e0.double()).max()
+    assert float(rel) <= 1e-5
+    assert float((rows.log_u - fused.log_u).abs().max()) <= 1e-3
