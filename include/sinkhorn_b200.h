@@ -97,6 +97,8 @@ typedef struct sinkhorn_problem_v1 {
 #define SINKHORN_FLAG_PERSISTENT 32u     /* shared/grid costs: whole loop in one cooperative kernel */
 #define SINKHORN_FLAG_TILED_ONLY 64u     /* never take the single-launch small-problem solver */
 #define SINKHORN_FLAG_DENSE_GRID 128u    /* grid costs: dense on-the-fly sweeps, not separable */
+#define SINKHORN_FLAG_NO_FUSED 256u      /* shared costs: two half-sweeps per iteration, not the
+                                            fused row->column pass (sweep_fused.cuh) */
 
 typedef struct sinkhorn_options_v1 {
   double lambda;          /* > 0, finite */

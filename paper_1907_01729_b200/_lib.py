@@ -35,6 +35,7 @@ FLAG_MUFU_ONLY = 16
 FLAG_PERSISTENT = 32
 FLAG_TILED_ONLY = 64
 FLAG_DENSE_GRID = 128
+FLAG_NO_FUSED = 256
 
 # every symbol include/sinkhorn_b200.h declares
 EXPORTED_SYMBOLS = (

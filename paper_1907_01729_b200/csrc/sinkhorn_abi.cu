@@ -27,6 +27,7 @@
 #include "persistent.cuh"
 #include "sweep_small.cuh"
 #include "sweep_sep.cuh"
+#include "sweep_fused.cuh"
 
 using namespace skb;
 
@@ -174,20 +175,61 @@ struct Layout {
   size_t f2T = 0, g2T[2] = {0, 0}; // separable grid: the potentials transposed per lane
   size_t part_bytes = 0, counter_count = 0;
   int lane_nsplit = 1, lane_nj = 1, lane_vec = 4;
+  bool fused = false;             // shared cost, one fused row->column pass per iteration
+  int fused_nct = 0, fused_maxseg = 0;
 };
+
+// Fused passes (sweep_fused.cuh): shared stored cost, both padded extents
+// within the register-resident row (NQ <= kFusedMaxNQ 64-column chunks).
+constexpr int kFusedMaxNQ = kFusedMaxChunks;
+bool fused_eligible(const sinkhorn_problem_v1& pr) {
+  return pr.cost_kind == SINKHORN_COST_SHARED && pr.B >= 1 &&
+         round_up(pr.d1, TILE_PAD) <= 64 * kFusedMaxNQ && round_up(pr.d2, TILE_PAD) <= 64 * kFusedMaxNQ;
+}
 
 // Grid costs run the separable sweeps on lane-major buffers unless the dense
 // on-the-fly tiled sweeps are requested (SINKHORN_FLAG_DENSE_GRID).
-Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = false) {
+Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = false,
+                   bool fused = false) {
   Layout L;
   L.B = pr.B;
   L.d1 = pr.d1;
   L.d2 = pr.d2;
+  L.fused = fused && fused_eligible(pr);
   L.sep = pr.cost_kind == SINKHORN_COST_GRID2D && !dense_grid;
-  L.tiled = pr.cost_kind == SINKHORN_COST_SHARED ||
-            (pr.cost_kind == SINKHORN_COST_GRID2D && dense_grid);
+  L.tiled = !L.fused && (pr.cost_kind == SINKHORN_COST_SHARED ||
+                         (pr.cost_kind == SINKHORN_COST_GRID2D && dense_grid));
   Carver c;
-  if (L.tiled) {
+  if (L.fused) {
+    // lane-major potentials [B][Dp], Dp = the cost rows' padded length
+    L.Bp = (int)pr.B;
+    L.D1p = (int)round_up(pr.d1, TILE_PAD);
+    L.D2p = (int)round_up(pr.d2, TILE_PAD);
+    L.sb1 = L.D1p;
+    L.si1 = 1;
+    L.sb2 = L.D2p;
+    L.si2 = 1;
+    L.a2 = c.take((size_t)L.D1p * L.D2p * 4);
+    L.a2t = c.take((size_t)L.D2p * L.D1p * 4);
+    const size_t n1 = (size_t)L.B * L.D1p * 4, n2 = (size_t)L.B * L.D2p * 4;
+    L.f2 = c.take(n1);
+    L.g2[0] = c.take(n2);
+    L.g2[1] = c.take(n2);
+    L.l2mu = c.take(n1);
+    L.l2nu = c.take(n2);
+    L.mu = c.take(n1);
+    L.nu = c.take(n2);
+    L.e0 = c.take(std::max(n1, n2));
+    const int nw = fused_warps(L.D2p / 64);
+    const long long groups = (pr.B + nw - 1) / nw;
+    const long long U = groups * pr.d1;
+    L.fused_nct = (int)std::min<long long>(sms, U);
+    const long long per = (U + L.fused_nct - 1) / L.fused_nct;
+    L.fused_maxseg = (int)((per - 1) / pr.d1 + 2);
+    L.part_bytes = (size_t)L.fused_nct * L.fused_maxseg * nw * L.D2p * 4;
+    L.part = c.take(L.part_bytes);
+    L.counter_count = 1;
+  } else if (L.tiled) {
     L.Bp = (int)round_up(pr.B, pick_bt(pr.B));
     L.D1p = (int)round_up(pr.d1, TILE_PAD);
     L.D2p = (int)round_up(pr.d2, TILE_PAD);
@@ -259,6 +301,7 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
 // either the separable or the dense tiled layout).
 size_t workspace_total(const sinkhorn_problem_v1& pr, int sms) {
   size_t t = make_layout(pr, sms).total;
+  if (fused_eligible(pr)) t = std::max(t, make_layout(pr, sms, false, true).total);
   if (pr.cost_kind == SINKHORN_COST_GRID2D) t = std::max(t, make_layout(pr, sms, true).total);
   return t;
 }
@@ -581,6 +624,104 @@ struct Solve {
       return sep_sweep(kModeTail, F(L.f2T), nullptr, F(L.nu), F(L.g2[cur]), F(L.e0), nullptr,
                        kResCol);
     return lane_col(kModeTail, nullptr, F(L.g2[cur]), kResCol);
+  }
+
+  // ---- fused row->column passes (sweep_fused.cuh) ---------------------------
+  template <int NQ, bool kRowOnly, bool kTail>
+  int launch_fused_t(const FusedParams& fp) {
+    auto kern = &fused_pass_kernel<NQ, kRowOnly, kTail>;
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)fused_smem_bytes<NQ>()));
+      attr = true;
+    }
+    const size_t smem = (size_t)kFusedStages * fp.rowlen * 4 + kFusedStages * 8;
+    ++g_launches;
+    CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(fused_warps(NQ) * 32), smem, st, fp));
+    return 0;
+  }
+  template <int NQ, bool kRowOnly>
+  int launch_fused_nq(const FusedParams& fp) {
+    if constexpr (NQ > kFusedMaxChunks) {
+      return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
+    } else {
+      if (fp.nq != NQ) return launch_fused_nq<NQ + 1, kRowOnly>(fp);
+      if constexpr (kRowOnly) return launch_fused_t<NQ, true, false>(fp);
+      return fp.e0 != nullptr ? launch_fused_t<NQ, false, true>(fp)
+                              : launch_fused_t<NQ, false, false>(fp);
+    }
+  }
+  template <bool kRowOnly>
+  int launch_fused(const FusedParams& fp) {
+    return launch_fused_nq<1, kRowOnly>(fp);
+  }
+  FusedParams fused_common() const {
+    FusedParams fp = {};
+    fp.B = (int)pr.B;
+    fp.status = at<int>(ws, L.status);
+    fp.e0_log2scale = std::log2(lam * kLn2);
+    return fp;
+  }
+  // first column sweep (no plan yet): g2[dst] = l2nu - LSE_i(A2^T[j, i] + f2[i])
+  int fused_row_only(int dst) {
+    FusedParams fp = fused_common();
+    const int nw = fused_warps(L.D1p / 64);
+    const long long groups = (pr.B + nw - 1) / nw;
+    fp.nrows = (int)pr.d2;
+    fp.rowlen = L.D1p;
+    fp.nq = L.D1p / 64;
+    fp.U = groups * pr.d2;
+    fp.nct = (int)std::min<long long>(di.sms, fp.U);
+    fp.a2 = F(L.a2t);
+    fp.x = F(L.f2);
+    fp.target = F(L.l2nu);
+    fp.marg = F(L.nu);
+    fp.out = F(L.g2[dst]);
+    fp.ldo = L.D2p;
+    return launch_fused<true>(fp);
+  }
+  // iteration k: u_k from v_k = g2[cur] (row sweep), then v_{k+1} into
+  // g2[cur ^ 1] from the plan's column marginal; residuals / E0 row terms on request
+  int fused_iteration(int cur, bool res, bool e0) {
+    FusedParams fp = fused_common();
+    const int nw = fused_warps(L.D2p / 64);
+    const long long groups = (pr.B + nw - 1) / nw;
+    fp.nrows = (int)pr.d1;
+    fp.rowlen = L.D2p;
+    fp.nq = L.D2p / 64;
+    fp.U = groups * pr.d1;
+    fp.nct = L.fused_nct;
+    fp.maxseg = L.fused_maxseg;
+    fp.a2 = F(L.a2);
+    fp.x = F(L.g2[cur]);
+    fp.target = F(L.l2mu);
+    fp.marg = F(L.mu);
+    fp.out = F(L.f2);
+    fp.ldo = L.D1p;
+    fp.part = F(L.part);
+    fp.res = (res || e0) ? F(L.res) : nullptr;   // kTail: residual and E0 together
+    fp.e0 = (res || e0) ? F(L.e0) : nullptr;
+    if (int e = launch_fused<false>(fp)) return e;
+    FusedMergeParams mp = {};
+    mp.B = (int)pr.B;
+    mp.nrows = (int)pr.d1;
+    mp.rowlen = L.D2p;
+    mp.nw = nw;
+    mp.U = fp.U;
+    mp.nct = fp.nct;
+    mp.maxseg = fp.maxseg;
+    mp.part = F(L.part);
+    mp.v_old = F(L.g2[cur]);
+    mp.v_new = F(L.g2[cur ^ 1]);
+    mp.target = F(L.l2nu);
+    mp.marg = F(L.nu);
+    mp.res = res ? F(L.res) : nullptr;
+    mp.est_fail = est_fail;
+    ++g_launches;
+    CK(launch_pdl(&fused_merge_kernel, dim3((unsigned)((L.D2p + 511) / 512), (unsigned)pr.B),
+                  dim3(256), 0, st, mp));
+    return 0;
   }
 
   LaneSweepParams lane_params() {
@@ -945,6 +1086,16 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   S.cost = cost;
   S.poly = (op.flags & SINKHORN_FLAG_MUFU_ONLY) == 0;
   S.warm = init_log_u != nullptr;
+  // one fused row->column pass per iteration for shared costs, unless the
+  // problem takes the single-launch small solver (or this is the exact rerun)
+  if (allow_est && !(op.flags & SINKHORN_FLAG_NO_FUSED) && fused_eligible(pr)) {
+    SmallParams sp0;
+    int g0 = 0;
+    size_t sm0 = 0;
+    bool small0 = false;
+    if (int e = S.plan_small(sp0, g0, sm0, &small0)) return e;
+    if (!small0) S.L = make_layout(pr, S.di.sms, false, true);
+  }
   const Layout& L = S.L;
   if (ws_bytes < L.total || ws == nullptr)
     return fail(SINKHORN_STATUS_WORKSPACE, "workspace too small");
@@ -1051,10 +1202,41 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   }
   g_last_path = small     ? "small"
                 : persist ? "persistent"
+                : L.fused ? "fused"
                 : L.tiled ? "tiled"
                 : L.sep   ? "separable"
                           : "lane";
-  for (int k = 1; !persist && !small && k <= op.max_iters; ++k) {
+  if (L.fused && !small) {
+    // v_1 from u_0, then one fused pass (+ column merge) per iteration
+    if (int e = S.fused_row_only(1)) return e;
+    cur = 1;
+    for (int k = 1; k <= op.max_iters; ++k) {
+      const bool last = (k == op.max_iters);
+      const bool check = checks && (k % op.check_interval == 0) && !last;
+      if (check || last) {
+        if (int e = S.zero_res()) return e;
+      }
+      if (int e = S.fused_iteration(cur, check || last, check || last)) return e;
+      iters = k;
+      if (last) break;
+      if (check) {
+        ++g_launches;
+        reduce_max_kernel<<<1, 256, 0, st>>>(S.F(L.res), (int)pr.B, S.F(L.scratch));
+        CK(cudaGetLastError());
+        float hmax = 0.f;
+        int hstatus = 0;
+        CK(cudaMemcpyAsync(&hmax, S.F(L.scratch), 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&hstatus, status, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        double gmax = (hstatus != 0) ? NAN : (double)hmax;
+        if (g_reducer) gmax = g_reducer(gmax, g_reducer_user);
+        if (hstatus != 0) break;
+        if (gmax <= op.tolerance) break;   // converged: g2[cur] = log_v_k, f2 = log_u_k
+      }
+      cur ^= 1;
+    }
+  }
+  for (int k = 1; !persist && !small && !L.fused && k <= op.max_iters; ++k) {
     // estimate mode once the potentials have settled past the first sweeps
     S.est = allow_est && k >= kEstFromIter;
     if (!have_next) {
@@ -1094,7 +1276,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   if (timed) CK(cudaEventRecord(ev1, st));
   // ---- tail: residual + stable E0 in one column pass (batch.py:323-337) ----
   S.est = allow_est && iters >= kEstFromIter;
-  if (!small) {
+  if (!small && !L.fused) {   // the fused passes already produced the tail terms
     if (int e = S.tail(cur)) return e;
   }
   if (small) {
@@ -1105,8 +1287,12 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     const int nb = (int)((pr.B + 31) / 32);
     const long long sb = L.tiled ? 1 : L.D2p, sj = L.tiled ? L.Bp : 1;
     ++g_launches;
-    e0_finalize_kernel<<<nb, 256, 0, st>>>(S.F(L.e0), (int)pr.B, (int)pr.d2, sb, sj, out_cost,
-                                           status, 0);
+    if (L.fused)   // per-row E0 terms of the fused passes
+      e0_rows_finalize_kernel<<<(unsigned)((pr.B + 7) / 8), 256, 0, st>>>(
+          S.F(L.e0), (int)pr.B, (int)pr.d1, L.D1p, out_cost, status);
+    else           // per-column E0 terms of the tail pass
+      e0_finalize_kernel<<<nb, 256, 0, st>>>(S.F(L.e0), (int)pr.B, (int)pr.d2, sb, sj, out_cost,
+                                             status, 0);
     dim3 gu((unsigned)((pr.d1 + 31) / 32), (unsigned)((pr.B + 31) / 32));
     ++g_launches;
     export_potential_kernel<<<gu, 256, 0, st>>>(S.F(L.f2), (int)pr.B, (int)pr.d1, L.sb1, L.si1,
@@ -1123,7 +1309,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   if (out_iterations) *out_iterations = iters;
   int hstatus = 0;
   if (int e = S.read_status(&hstatus)) return e;
-  if (allow_est && L.tiled) {
+  if (allow_est && (L.tiled || L.fused)) {
     int hfail = 0;
     CK(cudaMemcpy(&hfail, S.est_fail, 4, cudaMemcpyDeviceToHost));
     if (hfail) {   // an estimate overshot: recompute the whole solve exactly
@@ -1498,7 +1684,7 @@ int32_t sinkhorn_forward_v1(const sinkhorn_view_v1* mu, const sinkhorn_view_v1* 
   cudaStream_t st = cudaStreamPerThread;
   const size_t n_mu = (size_t)B * d1, n_nu = (size_t)B * d2, n_c = (size_t)d1 * d2;
   sinkhorn_problem_v1 pr = {B, d1, d2, SINKHORN_COST_SHARED, 0, 0, 0.f, 0.f};
-  const size_t ws_bytes = make_layout(pr, device_info().sms).total;
+  const size_t ws_bytes = workspace_total(pr, device_info().sms);
   // one device allocation: f64 staging + f32 inputs/outputs + solver workspace
   Carver c;
   const size_t o_d64 = c.take(std::max(n_mu + n_nu + n_c, n_mu + n_nu + (size_t)B) * 8);

@@ -1,0 +1,488 @@
+// sweep_fused.cuh -- one fused row->column pass per Sinkhorn iteration for a
+// stored cost shared by every lane (BASELINE config 2).
+//
+// The reference runs an iteration as two half-sweeps (batch.py:314-316):
+//     log_v = log_nu - LSE_i(A + log_u)        (column sweep)
+//     log_u = log_mu - LSE_j(A + log_v)        (row sweep)
+// each with one exponential per cell.  Here the column sweep of iteration
+// k+1 is folded into the row sweep of iteration k.  After row i of lane b is
+// reduced, with t_j = A2[i,j] + v_j, m = max_j t_j, e_j = 2^(t_j - m) and
+// S = sum_j e_j:
+//     u_i = l2mu_i - (m + log2 S)                         (the row sweep)
+//     P_ij = 2^(u_i + A2[i,j] + v_j) = e_j * (mu_i / S)   (the plan entries)
+// so the plan's column marginal colsum_j = sum_i P_ij needs no further
+// exponential: it is an FFMA per cell on the e_j already in registers.  Then
+//     LSE_i(A2[:,j] + u) = log2(colsum_j) - v_j
+//     v'_j = l2nu_j - LSE_i(...) = v_j + l2nu_j - log2(colsum_j)
+// which is the reference's column update, and |colsum_j - nu_j| is its column
+// residual (batch.py:303-309).  One exponential per cell per iteration instead
+// of two: the MUFU roofline of the whole iteration halves.
+//
+// Range: every P_ij <= mu_i <= 1, so the sums cannot overflow.  Terms below
+// 2^-126 flush to zero; they are negligible against colsum_j unless colsum_j
+// itself is tiny, so the merge checks colsum_j >= 2^-60 (relevant terms are
+// then >= 2^-60 * 2^-24 / d1 >> 2^-126) and otherwise flags the solve, which
+// the host reruns with the exact two-half-sweep path.  The row reduction is
+// exact two-pass (max, then one exponential per cell) in registers.
+//
+// Decomposition: a CTA has 16 warps, one lane each (a "group" of 16 lanes);
+// every warp reduces the same cost row for its own lane, so a cost row is
+// staged once in shared memory (cp.async.bulk, a ring of kFusedStages rows)
+// and read by 16 lanes.  The (group, row) units are split evenly over one CTA
+// per SM (stream-K); each CTA writes the column partials of every group
+// segment it covers, and fused_merge_kernel sums them in ascending CTA order
+// (deterministic, like the reference's ascending span merge, batch.py:198-201)
+// and applies the column update.  Lane-major buffers: x[b*ld + j].
+//
+// The same kernel with kRowOnly and the transposed cost runs the first column
+// sweep (v_1 from u_0, batch.py:315), where no plan exists yet.
+#pragma once
+
+#include "common.cuh"
+
+#include <type_traits>
+
+namespace skb {
+
+constexpr int kFusedWarps = 16;    // max lanes per group = warps per CTA
+// Lanes per group for a row of nq chunks: 16 warps while the row's registers
+// (potentials, plan partials, exponentials: 6 per chunk) fit in 128, else 12
+// warps with up to 168 registers.
+__host__ __device__ constexpr int fused_warps(int nq) { return nq <= 13 ? 16 : 12; }
+constexpr int kFusedStages = 8;    // cost rows in flight per CTA
+constexpr int kFusedMaxChunks = 16;  // row length <= 1024 columns
+constexpr float kFusedMinColsum = 8.673617379884035e-19f;   // 2^-60
+
+struct FusedParams {
+  int B;                  // lanes
+  int nrows;              // output rows of this pass (d1 main pass, d2 row-only pass)
+  int rowlen;             // padded row length = 64 * nq (= leading dim of x and of part rows)
+  int nq;                 // 64-column chunks per row (<= NQ)
+  long long U;            // units = groups * nrows
+  int nct;                // CTAs
+  int maxseg;             // partial slots per CTA
+  const float* a2;        // [>= nrows][rowlen] log2 cost rows (A2, or A2^T for kRowOnly)
+  const float* x;         // [B][rowlen] reduced-side potentials (log2)
+  const float* target;    // [B][ldo] output-side log2 marginal
+  const float* marg;      // [B][ldo] output-side linear marginal
+  float* out;             // [B][ldo] output-side potentials
+  int ldo;
+  float* part;            // [nct][maxseg][16][rowlen] plan column partials (main pass)
+  float* res;             // [B] row residual, atomic max (nullable)
+  float* e0;              // [B][ldo] log2 E0 row terms (nullable)
+  float e0_log2scale;     // log2(lambda * ln2): c = -A2 * lambda * ln2
+  const int* status;      // abort if validation failed
+};
+
+struct FusedMergeParams {
+  int B, nrows, rowlen;   // rowlen = padded output length (ld of v, part rows)
+  int nw;                 // lanes per group of the fused pass
+  long long U;
+  int nct, maxseg;
+  const float* part;
+  const float* v_old;     // [B][rowlen] v_k
+  float* v_new;           // [B][rowlen] v_{k+1}
+  const float* target;    // [B][rowlen] l2nu
+  const float* marg;      // [B][rowlen] nu
+  float* res;             // [B] column residual, atomic max (nullable)
+  int* est_fail;          // set when a column's plan mass is below 2^-60
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// shared-window (u32) address forms, computed once per CTA
+__device__ __forceinline__ void bulk_g2s_s(uint32_t dst, const void* src, uint32_t bytes,
+                                           uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_s(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t lds64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__host__ __device__ inline long long fused_seg_start(long long U, int nct, int c) {
+  return (long long)c * U / nct;
+}
+
+template <int NQ>
+__host__ __device__ constexpr size_t fused_smem_bytes() {
+  return (size_t)kFusedStages * NQ * 64 * 4 + kFusedStages * 8;
+}
+
+constexpr float kFusedEstLo = 8.673617379884035e-19f;   // 2^-60
+constexpr float kFusedEstHi = 1.2676506002282294e30f;   // 2^100
+
+// The rows of one (lane group, row range) segment.  The main pass shifts each
+// row's exponentials by the row's previous log-sum-exp (target - old u_i):
+// the potentials move little between iterations, so the sum stays in
+// [2^-60, 2^100] and no max pass is needed; a row outside that range (or with
+// no previous value) is redone with the exact two-pass reduction from the
+// staged cost row.  The row-only pass is always exact.
+template <int NQ, int NW, bool kRowOnly, bool kTail>
+__device__ __forceinline__ void fused_segment(const FusedParams& p, const float* ring,
+                                              uint32_t full_s, int* rel, int& r, int& s,
+                                              uint32_t& par, int n, int g, int i_begin, int i_end,
+                                              int sidx) {
+  constexpr bool kGuard = false;   // every pass is instantiated for its exact chunk count
+  const int rowlen = p.rowlen;
+  const int warp = warp_id(), lane = lane_id();
+  const int b = g * NW + warp;
+  const bool act = b < p.B;   // warp-uniform; idle warps compute on -inf and store nothing
+  auto chunk_on = [&](int q) { return !kGuard || q < p.nq; };
+  const uint32_t row_bytes = (uint32_t)rowlen * 4u;
+
+  uint64_t xv[NQ], acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    float2 v2 = make_float2(neg_inf(), neg_inf());
+    if (act && chunk_on(q))
+      v2 = __ldg(reinterpret_cast<const float2*>(p.x + (size_t)b * rowlen + 2 * lane + 64 * q));
+    xv[q] = pk2(v2.x, v2.y);
+    acc[q] = 0ull;
+  }
+  // per-row scalars, 32 rows per window, prefetched one window ahead: target,
+  // linear marginal and (main pass) the previous potential of the row
+  const float* tg_b = p.target + (size_t)b * p.ldo;
+  const float* mg_b = p.marg + (size_t)b * p.ldo;
+  float* out_b = p.out + (size_t)b * p.ldo;
+  float* e0_b = kTail ? p.e0 + (size_t)b * p.ldo : nullptr;
+  auto ld_win = [&](int base, float& tw, float& mw, float& ow) {
+    const int i = base + lane;
+    const bool ok = act && i < i_end;
+    tw = ok ? __ldg(tg_b + i) : 0.f;
+    mw = (!kRowOnly && ok) ? __ldg(mg_b + i) : 0.f;
+    ow = (!kRowOnly && ok) ? out_b[i] : 0.f;
+  };
+  float tw, mw, ow, tw_n, mw_n, ow_n;
+  ld_win(i_begin, tw, mw, ow);
+  ld_win(i_begin + 32, tw_n, mw_n, ow_n);
+  float rres = 0.f;
+  const float* ring_l = ring + 2 * lane;
+
+  for (int i = i_begin; i < i_end; ++i) {
+    const int wi = (i - i_begin) & 31;
+    const float tgt = __shfl_sync(0xffffffffu, tw, wi);
+    const float mgl = __shfl_sync(0xffffffffu, mw, wi);
+    const float uold = __shfl_sync(0xffffffffu, ow, wi);
+    if (wi == 31) {
+      tw = tw_n;
+      mw = mw_n;
+      ow = ow_n;
+      ld_win(i + 33, tw_n, mw_n, ow_n);
+    }
+    const float* row = ring_l + s * rowlen;
+    mbar_wait_s(full_s + 8u * (uint32_t)s, par);
+    uint64_t t[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      if (chunk_on(q)) {
+        const float2 a = *reinterpret_cast<const float2*>(row + 64 * q);
+        t[q] = fadd2(pk2(a.x, a.y), xv[q]);
+      }
+    }
+    float ms = tgt - uold;
+    bool exact = kRowOnly || !(ms > -3.0e38f && ms < 3.0e38f);
+    float S = 0.f;
+    if (!exact) {
+      const uint64_t nm = pk2(-ms, -ms);
+      uint64_t s0 = 0ull, s1 = 0ull;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const uint64_t d = fadd2(t[q], nm);
+        t[q] = pk2(ex2(lo2(d)), ex2(hi2(d)));
+        if (q & 1) s1 = fadd2(s1, t[q]);
+        else       s0 = fadd2(s0, t[q]);
+      }
+      const uint64_t s01 = fadd2(s0, s1);
+      S = lo2(s01) + hi2(s01);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+      // (idle warps never redo: their rows are all -inf)
+      exact = act && !(S >= kFusedEstLo && S <= kFusedEstHi);
+    }
+    if (exact) {   // warp-uniform; rare after the first iterations
+      float m0 = neg_inf(), m1 = neg_inf();
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        if (chunk_on(q)) {
+          const float2 a = *reinterpret_cast<const float2*>(row + 64 * q);
+          t[q] = fadd2(pk2(a.x, a.y), xv[q]);
+          if (q & 1) m1 = fmax3(m1, lo2(t[q]), hi2(t[q]));
+          else       m0 = fmax3(m0, lo2(t[q]), hi2(t[q]));
+        }
+      }
+      float m = fmaxf(m0, m1);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+      ms = fmaxf(m, kNegBig);   // an all -inf row gives e = 0, S = 0
+      const uint64_t nm = pk2(-ms, -ms);
+      uint64_t s0 = 0ull, s1 = 0ull;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        if (chunk_on(q)) {
+          const uint64_t d = fadd2(t[q], nm);
+          t[q] = pk2(ex2(lo2(d)), ex2(hi2(d)));
+          if (q & 1) s1 = fadd2(s1, t[q]);
+          else       s0 = fadd2(s0, t[q]);
+        }
+      }
+      const uint64_t s01 = fadd2(s0, s1);
+      S = lo2(s01) + hi2(s01);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+    }
+    const float lse = S > 0.f ? ms + lg2(S) : neg_inf();
+    const float o = sweep_out(tgt, lse);
+    if (act && lane == 0) out_b[i] = o;
+    if constexpr (!kRowOnly) {
+      const float a = S > 0.f ? __fdividef(mgl, S) : 0.f;   // mu_i / S: P_ij = e_j * a
+      const uint64_t av2 = pk2(a, a);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) acc[q] = ffma2(t[q], av2, acc[q]);
+      if constexpr (kTail) {
+        rres = fmaxf(rres, fabsf(exp2f(o + lse) - mgl));
+        // E0 row term: a * sum_j e_j * c_ij, c = -A2 * lambda * ln2
+        float qs = 0.f;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const float2 av = *reinterpret_cast<const float2*>(row + 64 * q);
+          // padding columns hold A2 = -inf
+          qs = fmaf(lo2(t[q]), av.x > -3.0e38f ? -av.x : 0.f, qs);
+          qs = fmaf(hi2(t[q]), av.y > -3.0e38f ? -av.y : 0.f, qs);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, off);
+        if (act && lane == 0)
+          e0_b[i] = (a > 0.f && qs > 0.f) ? log2f(a) + log2f(qs) + p.e0_log2scale : neg_inf();
+      }
+    }
+    // release the slot; the last warp to do so refills it with the row
+    // kFusedStages stream positions ahead (no producer warp, no waiting)
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&rel[s], 1) == NW - 1) {
+        rel[s] = 0;
+        if (r + kFusedStages < n) {
+          fence_proxy_async();
+          int nrow = i + kFusedStages;
+          while (nrow >= p.nrows) nrow -= p.nrows;
+          const uint32_t bar = full_s + 8u * (uint32_t)s;
+          mbar_arrive_expect_tx_s(bar, row_bytes);
+          bulk_g2s_s(smem_u32(ring + s * rowlen), p.a2 + (size_t)nrow * rowlen, row_bytes, bar);
+        }
+      }
+    }
+    ++r;
+    if (++s == kFusedStages) {
+      s = 0;
+      par ^= 1u;
+    }
+  }
+
+  if constexpr (!kRowOnly) {
+    if (act) {
+      float* dst = p.part + (((size_t)blockIdx.x * p.maxseg + sidx) * NW + warp) * (size_t)rowlen;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        *reinterpret_cast<float2*>(dst + 2 * lane + 64 * q) = make_float2(lo2(acc[q]), hi2(acc[q]));
+    }
+  }
+  if constexpr (kTail) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) rres = fmaxf(rres, __shfl_xor_sync(0xffffffffu, rres, off));
+    if (act && lane == 0) atomic_max_nonneg(&p.res[b], rres);
+  }
+}
+
+// NQ chunks of 64 columns per row, instantiated for the exact chunk count
+// (no per-chunk guards, so the chunks interleave freely).
+// kTail (check and last iterations): row residual + E0 row terms as well.
+template <int NQ, bool kRowOnly, bool kTail, int NW = fused_warps(NQ)>
+__global__ void __launch_bounds__(NW * 32, 1) fused_pass_kernel(const FusedParams p) {
+  extern __shared__ __align__(128) unsigned char fsm[];
+  __shared__ int rel[kFusedStages];   // warps that released each ring slot
+  const int rowlen = p.rowlen;
+  float* ring = reinterpret_cast<float*>(fsm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(fsm + (size_t)kFusedStages * rowlen * 4);
+  const long long u0 = fused_seg_start(p.U, p.nct, blockIdx.x);
+  const long long u1 = fused_seg_start(p.U, p.nct, blockIdx.x + 1);
+  const int n = (int)(u1 - u0);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kFusedStages; ++s) {
+      mbar_init(&full[s], 1);
+      rel[s] = 0;
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  // the cost rows do not depend on the previous launch: start streaming them
+  // before the programmatic-dependent-launch wait
+  const int npre = n < kFusedStages ? n : kFusedStages;
+  if (threadIdx.x == 0) {
+    const uint32_t row_bytes = (uint32_t)rowlen * 4u;
+    int row = (int)(u0 % p.nrows);
+    for (int r = 0; r < npre; ++r) {
+      mbar_arrive_expect_tx(&full[r], row_bytes);
+      bulk_g2s(ring + (size_t)r * rowlen, p.a2 + (size_t)row * rowlen, row_bytes, &full[r]);
+      if (++row == p.nrows) row = 0;
+    }
+  }
+  pdl_wait();
+  if (p.status != nullptr && *p.status != 0) {   // validation failed: drain and leave
+    if (threadIdx.x == 0)
+      for (int r = 0; r < npre; ++r) mbar_wait(&full[r], 0);
+    __syncthreads();
+    return;
+  }
+
+  int r = 0, s = 0;   // position in this CTA's row stream, its ring slot and phase
+  uint32_t par = 0;
+  const uint32_t full_s = smem_u32(full);
+  long long u = u0;
+  const int g_first = (int)(u0 / p.nrows);
+  while (u < u1) {
+    const int g = (int)(u / p.nrows);
+    const int i_begin = (int)(u - (long long)g * p.nrows);
+    const long long seg_end = (long long)(g + 1) * p.nrows < u1 ? (long long)(g + 1) * p.nrows : u1;
+    const int i_end = (int)(seg_end - (long long)g * p.nrows);
+    fused_segment<NQ, NW, kRowOnly, kTail>(p, ring, full_s, rel, r, s, par, n, g, i_begin, i_end,
+                                           g - g_first);
+    u = seg_end;
+  }
+  pdl_launch_dependents();
+}
+
+// Column update from the plan partials: colsum_j = sum over the CTAs that
+// covered lane b's group (ascending), v'_j = v_j + l2nu_j - log2(colsum_j),
+// column residual |colsum_j - nu_j|.  grid (ceil(rowlen / 256), B).
+__global__ void __launch_bounds__(256) fused_merge_kernel(const FusedMergeParams p) {
+  __shared__ int s_off[256];  // partial rows of this lane (rowlen units), ascending CTA (nct <= 256)
+  __shared__ int s_c0, s_n;
+  const int b = blockIdx.y;
+  const int g = b / p.nw, w = b % p.nw;
+  if (threadIdx.x == 0) {
+    const long long ua = (long long)g * p.nrows, ub = ua + p.nrows - 1;
+    s_c0 = (int)(((ua + 1) * p.nct - 1) / p.U);
+    s_n = (int)(((ub + 1) * p.nct - 1) / p.U) - s_c0 + 1;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < s_n) {   // every covering CTA has >= 1 unit (U >= nct)
+    const int c = s_c0 + threadIdx.x;
+    const long long s0 = fused_seg_start(p.U, p.nct, c);
+    s_off[threadIdx.x] = (int)(((long long)c * p.maxseg + (g - (int)(s0 / p.nrows))) * p.nw + w);
+  }
+  __syncthreads();
+  pdl_wait();
+  const int j = (blockIdx.x * 256 + threadIdx.x) * 2;   // two columns per thread
+  float rr = 0.f;
+  if (j < p.rowlen) {
+    const int np = s_n;
+    float2 cs = make_float2(0.f, 0.f);
+    int k = 0;
+    for (; k + 4 <= np; k += 4) {   // four loads in flight, summed in ascending order
+      float2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v[u] = __ldcg(reinterpret_cast<const float2*>(p.part + (size_t)s_off[k + u] * p.rowlen + j));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cs.x += v[u].x;
+        cs.y += v[u].y;
+      }
+    }
+    for (; k < np; ++k) {
+      const float2 v = __ldcg(reinterpret_cast<const float2*>(p.part + (size_t)s_off[k] * p.rowlen + j));
+      cs.x += v.x;
+      cs.y += v.y;
+    }
+    const size_t o = (size_t)b * p.rowlen + j;
+    const float2 tg = *reinterpret_cast<const float2*>(p.target + o);
+    const float2 vo = *reinterpret_cast<const float2*>(p.v_old + o);
+    float2 vn = make_float2(neg_inf(), neg_inf());
+    bool bad = false;
+    if (tg.x != neg_inf()) {
+      vn.x = vo.x + tg.x - log2f(cs.x);
+      bad |= !(cs.x >= kFusedMinColsum) || !(vn.x == vn.x);
+    }
+    if (tg.y != neg_inf()) {
+      vn.y = vo.y + tg.y - log2f(cs.y);
+      bad |= !(cs.y >= kFusedMinColsum) || !(vn.y == vn.y);
+    }
+    if (bad) *p.est_fail = 1;
+    *reinterpret_cast<float2*>(p.v_new + o) = vn;
+    if (p.res != nullptr) {
+      const float2 mg = *reinterpret_cast<const float2*>(p.marg + o);
+      rr = fmaxf(fabsf(cs.x - mg.x), fabsf(cs.y - mg.y));
+    }
+  }
+  if (p.res != nullptr) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) rr = fmaxf(rr, __shfl_xor_sync(0xffffffffu, rr, off));
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(&p.res[b], rr);
+  }
+  pdl_launch_dependents();
+}
+
+// E0 per lane from per-row log2 terms e0[b][i] (lane-major rows): one warp
+// per lane, (max, sum) merge by shuffles.
+__global__ void __launch_bounds__(256) e0_rows_finalize_kernel(const float* __restrict__ e0, int B,
+                                                               int d, int ld,
+                                                               float* __restrict__ out_cost,
+                                                               int* status) {
+  const int b = blockIdx.x * 8 + warp_id();
+  if (b >= B) return;
+  const float* row = e0 + (size_t)b * ld;
+  float m = kNegBig, s = 0.f;
+  for (int i = lane_id(); i < d; i += 32) {
+    const float v = row[i];
+    if (v > m + kLazy) {
+      s *= ex2(m - v);
+      m = v;
+    }
+    s += ex2(v - m);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+    lse_merge(m, s, m2, s2);
+  }
+  if (lane_id() == 0) {
+    const float cost = exp2f(lse_final(m, s));
+    out_cost[b] = cost;
+    if (!isfinite(cost)) set_status(status, 12);
+  }
+}
+
+}  // namespace skb

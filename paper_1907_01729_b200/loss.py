@@ -137,7 +137,7 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
           check_interval: int = 10, validate: bool = True, time_loop: bool = False,
           exact_max: bool = False, mufu_only: bool = False,
           persistent: bool = False, tiled_only: bool = False,
-          dense_grid: bool = False, init_log_u=None) -> SolveResult:
+          dense_grid: bool = False, init_log_u=None, fused: bool = True) -> SolveResult:
     """batch_forward (batch.py:264-349) on the GPU.
 
     mu (B, d1), nu (B, d2) histograms; cost a (d1, d2) tensor shared by all
@@ -146,6 +146,8 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
     the two-pass chunk reduction (no previous-iteration lse estimate).
     ``init_log_u`` (B, d1) warm-starts the iteration from a previous solve's
     log_u instead of 0 on the support (no reference API; batch.py:295).
+    ``fused=False`` runs shared costs as two half-sweeps per iteration instead
+    of the fused row->column pass (sweep_fused.cuh).
     """
     mu, nu = torch.as_tensor(mu), torch.as_tensor(nu)
     if not isinstance(cost, GridCost):
@@ -164,7 +166,8 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
     op.flags = (0 if validate else _lib.FLAG_SKIP_VALIDATION) | \
         (_lib.FLAG_TIME_LOOP if time_loop else 0) | (_lib.FLAG_EXACT_MAX if exact_max else 0) | \
         (_lib.FLAG_MUFU_ONLY if mufu_only else 0) | (_lib.FLAG_PERSISTENT if persistent else 0) | \
-        (_lib.FLAG_TILED_ONLY if tiled_only else 0) | (_lib.FLAG_DENSE_GRID if dense_grid else 0)
+        (_lib.FLAG_TILED_ONLY if tiled_only else 0) | (_lib.FLAG_DENSE_GRID if dense_grid else 0) | \
+        (0 if fused else _lib.FLAG_NO_FUSED)
     out_cost = torch.empty(B, device=dev, dtype=torch.float32)
     log_u = torch.empty(B, d1, device=dev, dtype=torch.float32)
     log_v = torch.empty(B, d2, device=dev, dtype=torch.float32)

@@ -40,8 +40,12 @@ def _run_golden(name, cuda, cost=None, **kw):
 
 
 # Small shared/grid problems take the single-launch solver (sweep_small.cuh)
-# unless tiled_only forces the stream-K tiled sweeps; both must match.
-PATHS = [pytest.param(False, id="auto"), pytest.param(True, id="tiled")]
+# unless tiled_only forces the sweeps: the fused row->column passes
+# (sweep_fused.cuh, shared costs with d <= 1024) or, with fused=False, the
+# stream-K tiled half-sweeps.  All of them must match.
+PATHS = [pytest.param({}, id="auto"),
+         pytest.param({"tiled_only": True, "fused": False}, id="tiled"),
+         pytest.param({"tiled_only": True}, id="fused")]
 
 
 def _check_loss_and_grads(g, res, loss_rtol=LOSS_RTOL, grad_atol=GRAD_ATOL):
@@ -59,11 +63,11 @@ def _check_loss_and_grads(g, res, loss_rtol=LOSS_RTOL, grad_atol=GRAD_ATOL):
     return rel.max()
 
 
-@pytest.mark.parametrize("tiled_only", PATHS)
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name", ["config1", "rect_37x53", "stability", "config2_subset",
                                   "config5_pin4096"])
-def test_shared_cost_matches_reference(name, tiled_only, cuda):
-    g, res = _run_golden(name, cuda, tiled_only=tiled_only)
+def test_shared_cost_matches_reference(name, path, cuda):
+    g, res = _run_golden(name, cuda, **path)
     _check_loss_and_grads(g, res)
     # potentials agree up to fp32 rounding of O(c/lambda) values
     lu = res.log_u.double().cpu().numpy()
@@ -73,30 +77,30 @@ def test_shared_cost_matches_reference(name, tiled_only, cuda):
     assert np.all(np.abs(res.residuals.double().cpu().numpy() - g["residuals"]) <= 1e-5)
 
 
-@pytest.mark.parametrize("tiled_only", PATHS)
-def test_closed_form_2x2(tiled_only, cuda):
+@pytest.mark.parametrize("path", PATHS)
+def test_closed_form_2x2(path, cuda):
     """conftest.py:9-24 / ffi.test.ts:101-116: E0 = e^-1/(1+e^-1) +- 1e-6."""
-    g, res = _run_golden("closed_form_2x2", cuda, tiled_only=tiled_only)
+    g, res = _run_golden("closed_form_2x2", cuda, **path)
     k = math.exp(-1.0)
     assert abs(float(res.cost_e0[0]) - k / (1 + k)) <= 1e-6
     _check_loss_and_grads(g, res)
 
 
-@pytest.mark.parametrize("tiled_only", PATHS)
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name", ["config1_tol", "lockstep"])
-def test_early_stopping_iteration_count(name, tiled_only, cuda):
+def test_early_stopping_iteration_count(name, path, cuda):
     """Lockstep stopping: identical iterations_run (batch.py:314-324, test_batch.py:77-90)."""
-    g, res = _run_golden(name, cuda, tiled_only=tiled_only)
+    g, res = _run_golden(name, cuda, **path)
     assert res.iterations_run == int(g["iterations_run"])
     assert float(res.residuals.max()) <= float(g["tol"])
     _check_loss_and_grads(g, res)
 
 
-@pytest.mark.parametrize("tiled_only", PATHS)
-def test_zero_mass_lanes(tiled_only, cuda):
+@pytest.mark.parametrize("path", PATHS)
+def test_zero_mass_lanes(path, cuda):
     """-inf exactly where mass is 0; backward refuses the lane (test_batch.py:185-198)."""
     skb = _skb()
-    g, res = _run_golden("zero_mass", cuda, tiled_only=tiled_only)
+    g, res = _run_golden("zero_mass", cuda, **path)
     lu = res.log_u.double().cpu().numpy()
     lv = res.log_v.double().cpu().numpy()
     assert np.array_equal(np.isneginf(lu), np.isneginf(g["log_u"]))
@@ -212,8 +216,8 @@ def test_estimate_mode_matches_exact_two_pass(name, cuda):
     c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
     args = (torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
             float(g["lam"]), int(g["max_iters"]), float(g["tol"]), int(g["check_interval"]))
-    fast = skb.solve(*args, tiled_only=True)
-    exact = skb.solve(*args, exact_max=True, tiled_only=True)
+    fast = skb.solve(*args, tiled_only=True, fused=False)
+    exact = skb.solve(*args, exact_max=True, tiled_only=True, fused=False)
     assert fast.iterations_run == exact.iterations_run
     rel = (fast.cost_e0.double() - exact.cost_e0.double()).abs() / exact.cost_e0.double().abs()
     assert float(rel.max()) <= 2e-6
@@ -248,7 +252,7 @@ def test_persistent_loop_matches_reference(name, cuda):
     c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
     res = skb.solve(torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
                     float(g["lam"]), int(g["max_iters"]), float(g["tol"]),
-                    int(g["check_interval"]), persistent=True, tiled_only=True)
+                    int(g["check_interval"]), persistent=True, tiled_only=True, fused=False)
     ref = skb.solve(torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
                     float(g["lam"]), int(g["max_iters"]), float(g["tol"]),
                     int(g["check_interval"]))
@@ -272,7 +276,7 @@ def test_small_problem_runs_in_one_solver_launch(cuda):
     skb.solve(*args)
     small = lib.sinkhorn_launch_count_v1() - n0
     n0 = lib.sinkhorn_launch_count_v1()
-    skb.solve(*args, tiled_only=True)
+    skb.solve(*args, tiled_only=True, fused=False)
     tiled = lib.sinkhorn_launch_count_v1() - n0
     assert small <= 8 < 200 <= tiled, (small, tiled)
 
@@ -305,3 +309,58 @@ def test_small_solver_many_lanes_per_cta_lockstep(kind, cuda):
     tiled = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda), cost, lam,
                       400, 1e-5, 5, tiled_only=True)
     assert tiled.iterations_run == res.iterations_run
+
+
+def test_fused_pass_is_the_shared_cost_path_and_matches_tiled(cuda):
+    """Shared costs with d <= 1024 run one fused row->column pass per
+    iteration (sweep_fused.cuh); it agrees with the two-half-sweep tiled path
+    and with the reference."""
+    skb = _skb()
+    g = load_golden("config2_subset")
+    c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
+    args = (torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
+            float(g["lam"]), int(g["max_iters"]), float(g["tol"]), int(g["check_interval"]))
+    fused = skb.solve(*args, tiled_only=True)
+    tiled = skb.solve(*args, tiled_only=True, fused=False)
+    assert fused.path == "fused" and tiled.path == "tiled"
+    _check_loss_and_grads(g, fused)
+    rel = (fused.cost_e0.double() - tiled.cost_e0.double()).abs() / tiled.cost_e0.double()
+    assert float(rel.max()) <= 2e-6
+    fin = torch.isfinite(tiled.log_v)
+    assert torch.equal(fin, torch.isfinite(fused.log_v))
+    scale = max(1.0, float(tiled.log_v[fin].abs().max()))
+    assert float((fused.log_v[fin] - tiled.log_v[fin]).abs().max()) <= 2e-5 * scale
+
+
+@pytest.mark.parametrize("B,d1,d2,tol", [(37, 50, 70, 1e-5), (16, 64, 64, 0.0), (130, 130, 97, 0.0),
+                                         (300, 200, 1000, 0.0), (5, 1000, 33, 1e-4)])
+def test_fused_pass_ragged_shapes_against_oracle(B, d1, d2, tol, cuda):
+    """Ragged lane groups (B not a multiple of 16), rectangular costs, padded
+    rows and lockstep stops through the fused passes."""
+    skb = _skb()
+    from oracle import sinkhorn_oracle as orc
+
+    rng = np.random.default_rng(B * 7 + d1)
+    mu = orc.fp32_exact(orc.random_histogram_batch(B, d1, rng))
+    nu = orc.fp32_exact(orc.random_histogram_batch(B, d2, rng))
+    mu[1 % B, 3] = 0.0           # a zero-mass bin on each side
+    mu[1 % B] = orc.fp32_exact(mu[1 % B] / mu[1 % B].sum())
+    nu[0, d2 - 1] = 0.0
+    nu[0] = orc.fp32_exact(nu[0] / nu[0].sum())
+    c = orc.fp32_exact(rng.random((d1, d2)) * 2.0)
+    lam, iters = 0.1, 60
+    ref = orc.batch_forward(mu, nu, c, lam, max_iters=iters, tolerance=tol, check_interval=10)
+    res = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda),
+                    torch.tensor(c, dtype=torch.float32, device=cuda), lam, iters, tol, 10,
+                    tiled_only=True)
+    assert res.path == "fused"
+    assert res.iterations_run == ref.iterations_run
+    rel = np.abs(res.cost_e0.double().cpu().numpy() - ref.cost_e0) / ref.cost_e0
+    assert rel.max() <= LOSS_RTOL
+    lu, lv = res.log_u.double().cpu().numpy(), res.log_v.double().cpu().numpy()
+    assert np.array_equal(np.isneginf(lu), np.isneginf(ref.log_u))
+    assert np.array_equal(np.isneginf(lv), np.isneginf(ref.log_v))
+    fu = np.isfinite(ref.log_u)
+    assert np.abs(lu[fu] - ref.log_u[fu]).max() <= 1e-3 * max(1.0, np.abs(ref.log_u[fu]).max())
+    res_r = res.residuals.double().cpu().numpy()
+    assert np.allclose(res_r, ref.residuals, atol=2e-6), (res_r[:4], ref.residuals[:4])
