@@ -223,7 +223,7 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     const int nw = fused_warps(L.D2p / 64);
     const long long groups = (pr.B + nw - 1) / nw;
     const long long U = groups * pr.d1;
-    L.fused_nct = (int)std::min<long long>(sms, U);
+    L.fused_nct = (int)std::max<long long>(1, std::min<long long>(sms, U));
     const long long per = (U + L.fused_nct - 1) / L.fused_nct;
     L.fused_maxseg = (int)((per - 1) / pr.d1 + 2);
     L.part_bytes = (size_t)L.fused_nct * L.fused_maxseg * nw * L.D2p * 4;
@@ -672,7 +672,7 @@ struct Solve {
     fp.rowlen = L.D1p;
     fp.nq = L.D1p / 64;
     fp.U = groups * pr.d2;
-    fp.nct = (int)std::min<long long>(di.sms, fp.U);
+    fp.nct = (int)std::max<long long>(1, std::min<long long>(di.sms, fp.U));
     fp.a2 = F(L.a2t);
     fp.x = F(L.f2);
     fp.target = F(L.l2nu);
