@@ -196,6 +196,8 @@ def work_units(cfg: dict) -> float:
 
 
 KERNEL_OF_PATH = {
+    "fused": "fused_pass_kernel + fused_merge_kernel (one fused row->column pass per iteration: "
+             "row LSE, plan column partials, column update)",
     "tiled": "tiled_sweep_kernel (stream-K online-LSE half-sweep)",
     "small": "small_solve_kernel (whole solve in one launch, cost in shared memory)",
     "persistent": "persistent_solve_kernel (cooperative whole loop)",
@@ -209,7 +211,9 @@ KERNEL_OF_PATH = {
 def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
              path: str = "tiled", share: float = 1.0) -> dict:
     """Dominant kernel = the half-sweep (2*iters per step; one launch each on the
-    tiled path, all inside one launch on the small path)."""
+    tiled path, all inside one launch on the small path), or on the fused path
+    the fused pass (iters per step, one exponential per cell: the column
+    half-sweep is an FFMA on the row sweep's plan entries)."""
     cells = float(cfg["B"]) * cfg["d"] * cfg["d"] * share  # cells per sweep launch (this GPU)
     if cfg["cost"] == "per_sample":
         achieved = cells * 4 / (sweep_ms * 1e-3) / 1e9      # algorithmic bytes: C read once
@@ -222,6 +226,12 @@ def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
     sms = 148
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
     ex2 = cells                                            # one ex2 per cell per sweep
+    if path == "fused":
+        # one launch = one whole iteration; SURVEY 8(d) counts 2 ex2 per
+        # cell-iteration (one per half-sweep).  The fused linear pass itself
+        # evaluates no per-cell exponential (K = 2^A2 is precomputed), so this
+        # fraction can exceed 1: it is the exp-pipe roofline of the direct method.
+        ex2 = 2 * cells
     if path == "separable":
         # nested 1-D LSEs: B * (nx*ny) * (nx + ny) exponentials per sweep
         ex2 = float(cfg["B"]) * cfg["d"] * (2 * cfg["nx"])
@@ -231,7 +241,11 @@ def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
            "frac": achieved / peak, "traffic": traffic,
            "kernel": KERNEL_OF_PATH.get(path, path),
            "algorithmic_per_launch": (f"{ex2:.4g} ex2 (B*d*(nx+ny), separable)"
-                                      if path == "separable" else f"{cells:.4g} ex2 (1 per cell)"),
+                                      if path == "separable" else
+                                      f"{2 * cells:.4g} ex2-equivalent (2 per cell-iteration, "
+                                      "SURVEY 8(d); the fused pass computes K_ij*2^(v_j-vmax) "
+                                      "products, no per-cell ex2)" if path == "fused"
+                                      else f"{cells:.4g} ex2 (1 per cell)"),
            "peak_source": f"148 SM x {MUFU_PER_SM_CLK} ex2/clk x sm_max_mhz {fmax:.0f} "
                           "(MEASURED_PEAKS.json)"}
     if clocks.get("sm_mhz"):
@@ -426,7 +440,9 @@ def run_ours(args, cfg, world, rank, local):
     ms = sum(step_ms) / len(step_ms)
     step_stats = {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)}
     # row sharding has no per-solve loop timer: its half-sweep share is the step's
-    sweep_ms = (statistics.median(loop_ms) if not row else statistics.median(step_ms)) / (2 * iters)
+    launches_per_iter = 1 if path == "fused" else 2   # fused: one pass (+ merge) per iteration
+    sweep_ms = (statistics.median(loop_ms) if not row else statistics.median(step_ms)) / (
+        launches_per_iter * iters)
     t = torch.tensor([ms, sweep_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

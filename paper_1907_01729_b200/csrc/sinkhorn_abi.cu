@@ -171,6 +171,7 @@ struct Layout {
   long long sb1 = 0, si1 = 0, sb2 = 0, si2 = 0;  // element (b,i) at b*sb + i*si
   size_t a2 = 0, a2t = 0, f2 = 0, g2[2] = {0, 0}, l2mu = 0, l2nu = 0, mu = 0, nu = 0, e0 = 0;
   size_t res = 0, scratch = 0, part = 0, counters = 0, status = 0, badrow = 0, total = 0;
+  size_t kmat = 0;                // fused: K = 2^A2 [D1p][D2p]
   size_t sep_ax = 0, sep_ay = 0;   // separable grid: Ax [nx][nblk*32], Ay [ny][sep_ld(ny)]
   size_t f2T = 0, g2T[2] = {0, 0}; // separable grid: the potentials transposed per lane
   size_t part_bytes = 0, counter_count = 0;
@@ -211,6 +212,7 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     L.si2 = 1;
     L.a2 = c.take((size_t)L.D1p * L.D2p * 4);
     L.a2t = c.take((size_t)L.D2p * L.D1p * 4);
+    L.kmat = c.take((size_t)L.D1p * L.D2p * 4);
     const size_t n1 = (size_t)L.B * L.D1p * 4, n2 = (size_t)L.B * L.D2p * 4;
     L.f2 = c.take(n1);
     L.g2[0] = c.take(n2);
@@ -627,9 +629,9 @@ struct Solve {
   }
 
   // ---- fused row->column passes (sweep_fused.cuh) ---------------------------
-  template <int NQ, bool kRowOnly, bool kTail>
+  template <int NQ, bool kRowOnly, bool kTail, bool kLin>
   int launch_fused_t(const FusedParams& fp) {
-    auto kern = &fused_pass_kernel<NQ, kRowOnly, kTail>;
+    auto kern = &fused_pass_kernel<NQ, kRowOnly, kTail, kLin>;
     static bool attr = false;
     if (!attr) {
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -647,9 +649,9 @@ struct Solve {
       return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
     } else {
       if (fp.nq != NQ) return launch_fused_nq<NQ + 1, kRowOnly>(fp);
-      if constexpr (kRowOnly) return launch_fused_t<NQ, true, false>(fp);
-      return fp.e0 != nullptr ? launch_fused_t<NQ, false, true>(fp)
-                              : launch_fused_t<NQ, false, false>(fp);
+      if constexpr (kRowOnly) return launch_fused_t<NQ, true, false, false>(fp);
+      return fp.e0 != nullptr ? launch_fused_t<NQ, false, true, false>(fp)
+                              : launch_fused_t<NQ, false, false, true>(fp);
     }
   }
   template <bool kRowOnly>
@@ -660,6 +662,7 @@ struct Solve {
     FusedParams fp = {};
     fp.B = (int)pr.B;
     fp.status = at<int>(ws, L.status);
+    fp.est_fail = est_fail;
     fp.e0_log2scale = std::log2(lam * kLn2);
     return fp;
   }
@@ -693,7 +696,10 @@ struct Solve {
     fp.U = groups * pr.d1;
     fp.nct = L.fused_nct;
     fp.maxseg = L.fused_maxseg;
-    fp.a2 = F(L.a2);
+    // check / last iterations: log-domain rows (residual and E0 terms);
+    // the others: linear rows K_ij * 2^(v_j - vmax) with a log-domain fallback
+    fp.a2 = (res || e0) ? F(L.a2) : F(L.kmat);
+    fp.a2log = F(L.a2);
     fp.x = F(L.g2[cur]);
     fp.target = F(L.l2mu);
     fp.marg = F(L.mu);
@@ -1148,6 +1154,12 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
                                          (float)(-1.4426950408889634 / op.lambda), S.F(L.a2),
                                          S.F(L.a2t), status);
     CK(cudaGetLastError());
+    if (L.fused) {
+      const size_t nk = (size_t)L.D1p * L.D2p;
+      ++g_launches;
+      kernel_matrix_kernel<<<grid_for(nk), 256, 0, st>>>(S.F(L.a2), S.F(L.kmat), nk);
+      CK(cudaGetLastError());
+    }
   } else if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE && !(op.flags & SINKHORN_FLAG_SKIP_VALIDATION)) {
     const size_t n = (size_t)pr.B * pr.d1 * pr.d2;
     ++g_launches;
@@ -1309,7 +1321,8 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   if (out_iterations) *out_iterations = iters;
   int hstatus = 0;
   if (int e = S.read_status(&hstatus)) return e;
-  if (allow_est && (L.tiled || L.fused)) {
+  static const bool no_rerun = getenv("SKB_NO_RERUN") != nullptr;   // diagnostics
+  if (allow_est && (L.tiled || L.fused) && !no_rerun) {
     int hfail = 0;
     CK(cudaMemcpy(&hfail, S.est_fail, 4, cudaMemcpyDeviceToHost));
     if (hfail) {   // an estimate overshot: recompute the whole solve exactly

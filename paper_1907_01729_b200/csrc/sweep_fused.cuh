@@ -61,7 +61,9 @@ struct FusedParams {
   long long U;            // units = groups * nrows
   int nct;                // CTAs
   int maxseg;             // partial slots per CTA
-  const float* a2;        // [>= nrows][rowlen] log2 cost rows (A2, or A2^T for kRowOnly)
+  const float* a2;        // [>= nrows][rowlen] rows streamed through the ring: log2 cost
+                          // (A2, or A2^T for kRowOnly), or the kernel K = 2^A2 (kLin)
+  const float* a2log;     // [>= nrows][rowlen] log2 cost rows (kLin's exact fallback)
   const float* x;         // [B][rowlen] reduced-side potentials (log2)
   const float* target;    // [B][ldo] output-side log2 marginal
   const float* marg;      // [B][ldo] output-side linear marginal
@@ -72,6 +74,7 @@ struct FusedParams {
   float* e0;              // [B][ldo] log2 E0 row terms (nullable)
   float e0_log2scale;     // log2(lambda * ln2): c = -A2 * lambda * ln2
   const int* status;      // abort if validation failed
+  int* est_fail;          // kLin: more fallback rows than a warp can queue -> exact rerun
 };
 
 struct FusedMergeParams {
@@ -125,6 +128,22 @@ __device__ __forceinline__ uint64_t lds64(uint32_t addr) {
   return v;
 }
 
+// Ring-slot release count.  Relaxed: a warp only counts itself after
+// __syncwarp, when every lane has consumed its shared-memory reads of the slot;
+// the last one fences the async proxy before the bulk copy overwrites it.
+__device__ __forceinline__ int atom_add_relaxed_cta(int* addr, int v) {
+  int old;
+  asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], %2;"
+               : "=r"(old) : "r"(smem_u32(addr)), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -147,9 +166,11 @@ constexpr float kFusedEstHi = 1.2676506002282294e30f;   // 2^100
 // [2^-60, 2^100] and no max pass is needed; a row outside that range (or with
 // no previous value) is redone with the exact two-pass reduction from the
 // staged cost row.  The row-only pass is always exact.
-template <int NQ, int NW, bool kRowOnly, bool kTail>
+constexpr int kFusedRedoMax = 32;   // queued log-domain fallback rows per warp and segment
+
+template <int NQ, int NW, bool kRowOnly, bool kTail, bool kLin>
 __device__ __forceinline__ void fused_segment(const FusedParams& p, const float* ring,
-                                              uint32_t full_s, int* rel, int& r, int& s,
+                                              uint32_t full_s, int* rel, int* redo, int& r, int& s,
                                               uint32_t& par, int n, int g, int i_begin, int i_end,
                                               int sidx) {
   constexpr bool kGuard = false;   // every pass is instantiated for its exact chunk count
@@ -161,13 +182,25 @@ __device__ __forceinline__ void fused_segment(const FusedParams& p, const float*
   const uint32_t row_bytes = (uint32_t)rowlen * 4u;
 
   uint64_t xv[NQ], acc[NQ];
+  const float* x_b = p.x + (size_t)b * rowlen + 2 * lane;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     float2 v2 = make_float2(neg_inf(), neg_inf());
-    if (act && chunk_on(q))
-      v2 = __ldg(reinterpret_cast<const float2*>(p.x + (size_t)b * rowlen + 2 * lane + 64 * q));
+    if (act && chunk_on(q)) v2 = __ldg(reinterpret_cast<const float2*>(x_b + 64 * q));
     xv[q] = pk2(v2.x, v2.y);
     acc[q] = 0ull;
+  }
+  // kLin: the lane's potentials as X_j = 2^(v_j - vmax) <= 1, so a row's terms
+  // 2^(A2_ij + v_j - vmax) = K_ij * X_j are products (no exponential per cell)
+  float vmax = neg_inf();
+  if constexpr (kLin) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) vmax = fmax3(vmax, lo2(xv[q]), hi2(xv[q]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, off));
+    vmax = fmaxf(vmax, kNegBig);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) xv[q] = pk2(ex2(lo2(xv[q]) - vmax), ex2(hi2(xv[q]) - vmax));
   }
   // per-row scalars, 32 rows per window, prefetched one window ahead: target,
   // linear marginal and (main pass) the previous potential of the row
@@ -185,9 +218,13 @@ __device__ __forceinline__ void fused_segment(const FusedParams& p, const float*
   float tw, mw, ow, tw_n, mw_n, ow_n;
   ld_win(i_begin, tw, mw, ow);
   ld_win(i_begin + 32, tw_n, mw_n, ow_n);
-  float rres = 0.f;
+  float rres = 0.f, ob = 0.f;
+  int nredo = 0;
   const float* ring_l = ring + 2 * lane;
 
+  // two rows per trip: the accumulators alternate between two register sets
+  // instead of being copied back at every loop edge
+#pragma unroll 2
   for (int i = i_begin; i < i_end; ++i) {
     const int wi = (i - i_begin) & 31;
     const float tgt = __shfl_sync(0xffffffffu, tw, wi);
@@ -202,23 +239,44 @@ __device__ __forceinline__ void fused_segment(const FusedParams& p, const float*
     const float* row = ring_l + s * rowlen;
     mbar_wait_s(full_s + 8u * (uint32_t)s, par);
     uint64_t t[NQ];
+    float ms, S = 0.f;
+    bool exact;
+    // row epilogue: u_i, plan column partials acc += e * mu_i / S, tail terms
+    // (called at the end of each branch below, so t never merges across them)
+    auto finish = [&](float ms, float S) {
+      const float lse = S > 0.f ? ms + lg2(S) : neg_inf();
+      const float o = sweep_out(tgt, lse);
+      if (lane == wi) ob = o;   // stored 32 rows at a time below
+      if constexpr (!kRowOnly) {
+        const float a = S > 0.f ? mgl * rcp_approx(S) : 0.f;   // mu_i / S: P_ij = e_j * a
+        const uint64_t av2 = pk2(a, a);
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      if (chunk_on(q)) {
-        const float2 a = *reinterpret_cast<const float2*>(row + 64 * q);
-        t[q] = fadd2(pk2(a.x, a.y), xv[q]);
+        for (int q = 0; q < NQ; ++q) ffma2_acc(acc[q], t[q], av2);
+        if constexpr (kTail) {
+          rres = fmaxf(rres, fabsf(exp2f(o + lse) - mgl));
+          // E0 row term: a * sum_j e_j * c_ij, c = -A2 * lambda * ln2
+          float qs = 0.f;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const float2 av = *reinterpret_cast<const float2*>(row + 64 * q);
+            // padding columns hold A2 = -inf
+            qs = fmaf(lo2(t[q]), av.x > -3.0e38f ? -av.x : 0.f, qs);
+            qs = fmaf(hi2(t[q]), av.y > -3.0e38f ? -av.y : 0.f, qs);
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, off);
+          if (act && lane == 0)
+            e0_b[i] = (a > 0.f && qs > 0.f) ? log2f(a) + log2f(qs) + p.e0_log2scale : neg_inf();
+        }
       }
-    }
-    float ms = tgt - uold;
-    bool exact = kRowOnly || !(ms > -3.0e38f && ms < 3.0e38f);
-    float S = 0.f;
-    if (!exact) {
-      const uint64_t nm = pk2(-ms, -ms);
+    };
+
+    if constexpr (kLin) {
       uint64_t s0 = 0ull, s1 = 0ull;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        const uint64_t d = fadd2(t[q], nm);
-        t[q] = pk2(ex2(lo2(d)), ex2(hi2(d)));
+        const float2 k2 = *reinterpret_cast<const float2*>(row + 64 * q);
+        t[q] = fmul2(pk2(k2.x, k2.y), xv[q]);
         if (q & 1) s1 = fadd2(s1, t[q]);
         else       s0 = fadd2(s0, t[q]);
       }
@@ -226,71 +284,89 @@ __device__ __forceinline__ void fused_segment(const FusedParams& p, const float*
       S = lo2(s01) + hi2(s01);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
-      // (idle warps never redo: their rows are all -inf)
-      exact = act && !(S >= kFusedEstLo && S <= kFusedEstHi);
-    }
-    if (exact) {   // warp-uniform; rare after the first iterations
-      float m0 = neg_inf(), m1 = neg_inf();
+      // a row whose terms underflow (S < 2^-60) contributes nothing here and is
+      // queued for the log-domain fallback after the segment (idle warps: all -inf)
+      const bool ok = !act || S >= kFusedEstLo;
+      if (!ok && lane == 0) {
+        if (nredo < kFusedRedoMax) redo[nredo] = i;
+        else *p.est_fail = 1;
+      }
+      nredo += ok ? 0 : 1;
+      const float lse = vmax + lg2(S);
+      if (lane == wi) ob = sweep_out(tgt, lse);
+      const float a = ok ? mgl * rcp_approx(S) : 0.f;   // mu_i / S: P_ij = e_j * a
+      const uint64_t av2 = pk2(a, a);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) ffma2_acc(acc[q], t[q], av2);
+    } else {
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         if (chunk_on(q)) {
           const float2 a = *reinterpret_cast<const float2*>(row + 64 * q);
           t[q] = fadd2(pk2(a.x, a.y), xv[q]);
-          if (q & 1) m1 = fmax3(m1, lo2(t[q]), hi2(t[q]));
-          else       m0 = fmax3(m0, lo2(t[q]), hi2(t[q]));
         }
       }
-      float m = fmaxf(m0, m1);
+      ms = tgt - uold;
+      exact = kRowOnly || !(ms > -3.0e38f && ms < 3.0e38f);
+      if (!exact) {
+        const uint64_t nm = pk2(-ms, -ms);
+        uint64_t s0 = 0ull, s1 = 0ull;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-      ms = fmaxf(m, kNegBig);   // an all -inf row gives e = 0, S = 0
-      const uint64_t nm = pk2(-ms, -ms);
-      uint64_t s0 = 0ull, s1 = 0ull;
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        if (chunk_on(q)) {
+        for (int q = 0; q < NQ; ++q) {
           const uint64_t d = fadd2(t[q], nm);
           t[q] = pk2(ex2(lo2(d)), ex2(hi2(d)));
           if (q & 1) s1 = fadd2(s1, t[q]);
           else       s0 = fadd2(s0, t[q]);
         }
+        const uint64_t s01 = fadd2(s0, s1);
+        S = lo2(s01) + hi2(s01);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+        // (idle warps never redo: their rows are all -inf)
+        exact = act && !(S >= kFusedEstLo && S <= kFusedEstHi);
       }
-      const uint64_t s01 = fadd2(s0, s1);
-      S = lo2(s01) + hi2(s01);
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
-    }
-    const float lse = S > 0.f ? ms + lg2(S) : neg_inf();
-    const float o = sweep_out(tgt, lse);
-    if (act && lane == 0) out_b[i] = o;
-    if constexpr (!kRowOnly) {
-      const float a = S > 0.f ? __fdividef(mgl, S) : 0.f;   // mu_i / S: P_ij = e_j * a
-      const uint64_t av2 = pk2(a, a);
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) acc[q] = ffma2(t[q], av2, acc[q]);
-      if constexpr (kTail) {
-        rres = fmaxf(rres, fabsf(exp2f(o + lse) - mgl));
-        // E0 row term: a * sum_j e_j * c_ij, c = -A2 * lambda * ln2
-        float qs = 0.f;
+      if (exact) {   // warp-uniform; rare after the first iterations
+        float m0 = neg_inf(), m1 = neg_inf();
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-          const float2 av = *reinterpret_cast<const float2*>(row + 64 * q);
-          // padding columns hold A2 = -inf
-          qs = fmaf(lo2(t[q]), av.x > -3.0e38f ? -av.x : 0.f, qs);
-          qs = fmaf(hi2(t[q]), av.y > -3.0e38f ? -av.y : 0.f, qs);
+          if (chunk_on(q)) {
+            const float2 a = *reinterpret_cast<const float2*>(row + 64 * q);
+            t[q] = fadd2(pk2(a.x, a.y), xv[q]);
+            if (q & 1) m1 = fmax3(m1, lo2(t[q]), hi2(t[q]));
+            else       m0 = fmax3(m0, lo2(t[q]), hi2(t[q]));
+          }
         }
+        float m = fmaxf(m0, m1);
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, off);
-        if (act && lane == 0)
-          e0_b[i] = (a > 0.f && qs > 0.f) ? log2f(a) + log2f(qs) + p.e0_log2scale : neg_inf();
+        for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+        ms = fmaxf(m, kNegBig);   // an all -inf row gives e = 0, S = 0
+        const uint64_t nm = pk2(-ms, -ms);
+        uint64_t s0 = 0ull, s1 = 0ull;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          if (chunk_on(q)) {
+            const uint64_t d = fadd2(t[q], nm);
+            t[q] = pk2(ex2(lo2(d)), ex2(hi2(d)));
+            if (q & 1) s1 = fadd2(s1, t[q]);
+            else       s0 = fadd2(s0, t[q]);
+          }
+        }
+        const uint64_t s01 = fadd2(s0, s1);
+        S = lo2(s01) + hi2(s01);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
       }
+      finish(ms, S);
+    }
+    if (wi == 31 || i + 1 == i_end) {   // this window's u_i, one coalesced store
+      const int i0 = i - wi;
+      if (act && lane <= wi) out_b[i0 + lane] = ob;
     }
     // release the slot; the last warp to do so refills it with the row
     // kFusedStages stream positions ahead (no producer warp, no waiting)
     __syncwarp();
     if (lane == 0) {
-      __threadfence_block();
-      if (atomicAdd(&rel[s], 1) == NW - 1) {
+      if (atom_add_relaxed_cta(&rel[s], 1) == NW - 1) {
         rel[s] = 0;
         if (r + kFusedStages < n) {
           fence_proxy_async();
@@ -309,6 +385,48 @@ __device__ __forceinline__ void fused_segment(const FusedParams& p, const float*
     }
   }
 
+  if constexpr (kLin) {
+    // queued rows in the log domain, from L2: A2 row + potentials, exact two-pass
+    __syncwarp();
+    const int nq_redo = nredo < kFusedRedoMax ? nredo : kFusedRedoMax;
+    for (int k = 0; k < nq_redo; ++k) {
+      const int i = redo[k];
+      const float* arow = p.a2log + (size_t)i * rowlen + 2 * lane;
+      uint64_t t[NQ];
+      float m0 = neg_inf(), m1 = neg_inf();
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const float2 a = __ldg(reinterpret_cast<const float2*>(arow + 64 * q));
+        const float2 v = __ldg(reinterpret_cast<const float2*>(x_b + 64 * q));
+        t[q] = fadd2(pk2(a.x, a.y), pk2(v.x, v.y));
+        if (q & 1) m1 = fmax3(m1, lo2(t[q]), hi2(t[q]));
+        else       m0 = fmax3(m0, lo2(t[q]), hi2(t[q]));
+      }
+      float m = fmaxf(m0, m1);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+      const float ms = fmaxf(m, kNegBig);
+      const uint64_t nm = pk2(-ms, -ms);
+      uint64_t s0 = 0ull, s1 = 0ull;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const uint64_t d = fadd2(t[q], nm);
+        t[q] = pk2(ex2(lo2(d)), ex2(hi2(d)));
+        if (q & 1) s1 = fadd2(s1, t[q]);
+        else       s0 = fadd2(s0, t[q]);
+      }
+      const uint64_t s01 = fadd2(s0, s1);
+      float S = lo2(s01) + hi2(s01);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+      const float lse = S > 0.f ? ms + lg2(S) : neg_inf();
+      if (lane == 0) out_b[i] = sweep_out(__ldg(tg_b + i), lse);
+      const float a = S > 0.f ? __ldg(mg_b + i) * rcp_approx(S) : 0.f;
+      const uint64_t av2 = pk2(a, a);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) ffma2_acc(acc[q], t[q], av2);
+    }
+  }
   if constexpr (!kRowOnly) {
     if (act) {
       float* dst = p.part + (((size_t)blockIdx.x * p.maxseg + sidx) * NW + warp) * (size_t)rowlen;
@@ -327,10 +445,13 @@ __device__ __forceinline__ void fused_segment(const FusedParams& p, const float*
 // NQ chunks of 64 columns per row, instantiated for the exact chunk count
 // (no per-chunk guards, so the chunks interleave freely).
 // kTail (check and last iterations): row residual + E0 row terms as well.
-template <int NQ, bool kRowOnly, bool kTail, int NW = fused_warps(NQ)>
+// kLin (the other main passes): the ring streams K = 2^A2 rows and a row's
+// terms are K_ij * 2^(v_j - vmax_b): products instead of exponentials.
+template <int NQ, bool kRowOnly, bool kTail, bool kLin = false, int NW = fused_warps(NQ)>
 __global__ void __launch_bounds__(NW * 32, 1) fused_pass_kernel(const FusedParams p) {
   extern __shared__ __align__(128) unsigned char fsm[];
   __shared__ int rel[kFusedStages];   // warps that released each ring slot
+  __shared__ int redo_rows[kLin ? NW * kFusedRedoMax : 1];
   const int rowlen = p.rowlen;
   float* ring = reinterpret_cast<float*>(fsm);
   uint64_t* full = reinterpret_cast<uint64_t*>(fsm + (size_t)kFusedStages * rowlen * 4);
@@ -376,8 +497,9 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_pass_kernel(const FusedParam
     const int i_begin = (int)(u - (long long)g * p.nrows);
     const long long seg_end = (long long)(g + 1) * p.nrows < u1 ? (long long)(g + 1) * p.nrows : u1;
     const int i_end = (int)(seg_end - (long long)g * p.nrows);
-    fused_segment<NQ, NW, kRowOnly, kTail>(p, ring, full_s, rel, r, s, par, n, g, i_begin, i_end,
-                                           g - g_first);
+    fused_segment<NQ, NW, kRowOnly, kTail, kLin>(p, ring, full_s, rel,
+                                                 redo_rows + (kLin ? warp_id() * kFusedRedoMax : 0),
+                                                 r, s, par, n, g, i_begin, i_end, g - g_first);
     u = seg_end;
   }
   pdl_launch_dependents();
@@ -452,6 +574,13 @@ __global__ void __launch_bounds__(256) fused_merge_kernel(const FusedMergeParams
     if ((threadIdx.x & 31) == 0) atomic_max_nonneg(&p.res[b], rr);
   }
   pdl_launch_dependents();
+}
+
+// K = 2^A2 for the fused passes' linear rows (padding -inf -> 0).
+__global__ void kernel_matrix_kernel(const float* __restrict__ a2, float* __restrict__ k, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    k[i] = ex2(a2[i]);
 }
 
 // E0 per lane from per-row log2 terms e0[b][i] (lane-major rows): one warp
