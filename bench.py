@@ -216,12 +216,19 @@ def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
     half-sweep is an FFMA on the row sweep's plan entries)."""
     cells = float(cfg["B"]) * cfg["d"] * cfg["d"] * share  # cells per sweep launch (this GPU)
     if cfg["cost"] == "per_sample":
-        achieved = cells * 4 / (sweep_ms * 1e-3) / 1e9      # algorithmic bytes: C read once
+        # SURVEY 8(d): 4 B of C per cell per half-sweep.  A fused launch is a
+        # whole iteration (8 B per cell algorithmic) that reads C_b once.
+        per_cell = 8 if path == "fused" else 4
+        achieved = cells * per_cell / (sweep_ms * 1e-3) / 1e9
         peak = float(peaks.get("hbm_gbs", 6650.0))
         return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "lane_col_kernel / lane_row_kernel (per-sample sweep)",
-                "algorithmic_per_launch": f"{cells * 4:.4g} B (4 B per cell)",
+                "kernel": ("fused_ps_kernel + fused_merge_kernel (one read of C_b per iteration)"
+                           if path == "fused" else
+                           "lane_col_kernel / lane_row_kernel (per-sample sweep)"),
+                "algorithmic_per_launch": (f"{cells * per_cell:.4g} B ({per_cell} B per cell"
+                                           + (", 2 half-sweeps; 4 B actually read)" if path == "fused"
+                                              else ")")),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
     sms = 148
     fmax = float(peaks.get("sm_max_mhz", 1965.0))

@@ -183,8 +183,13 @@ struct Layout {
 // Fused passes (sweep_fused.cuh): shared stored cost, both padded extents
 // within the register-resident row (NQ <= kFusedMaxNQ 64-column chunks).
 constexpr int kFusedMaxNQ = kFusedMaxChunks;
+// Per-sample costs (sweep_fused.cuh fused_ps_kernel): rows of d2 <= 1024
+// floats, d2 % 4 == 0 so every row is a whole number of 16-byte units.
 bool fused_eligible(const sinkhorn_problem_v1& pr) {
-  return pr.cost_kind == SINKHORN_COST_SHARED && pr.B >= 1 &&
+  if (pr.B < 1) return false;
+  if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE)
+    return pr.d2 % 4 == 0 && round_up(pr.d2, TILE_PAD) <= 64 * kFusedMaxNQ;
+  return pr.cost_kind == SINKHORN_COST_SHARED &&
          round_up(pr.d1, TILE_PAD) <= 64 * kFusedMaxNQ && round_up(pr.d2, TILE_PAD) <= 64 * kFusedMaxNQ;
 }
 
@@ -210,9 +215,15 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     L.si1 = 1;
     L.sb2 = L.D2p;
     L.si2 = 1;
-    L.a2 = c.take((size_t)L.D1p * L.D2p * 4);
-    L.a2t = c.take((size_t)L.D2p * L.D1p * 4);
-    L.kmat = c.take((size_t)L.D1p * L.D2p * 4);
+    if (pr.cost_kind == SINKHORN_COST_SHARED) {
+      L.a2 = c.take((size_t)L.D1p * L.D2p * 4);
+      L.a2t = c.take((size_t)L.D2p * L.D1p * 4);
+      L.kmat = c.take((size_t)L.D1p * L.D2p * 4);
+    } else {   // the first column sweep runs lane_col_kernel (one split per column block)
+      L.lane_vec = (pr.d2 % 4 == 0 && pr.d1 % 4 == 0) ? 4 : 1;
+      L.lane_nj = (int)((pr.d2 + 256 * L.lane_vec - 1) / (256 * L.lane_vec));
+      L.lane_nsplit = 1;
+    }
     const size_t n1 = (size_t)L.B * L.D1p * 4, n2 = (size_t)L.B * L.D2p * 4;
     L.f2 = c.take(n1);
     L.g2[0] = c.take(n2);
@@ -654,6 +665,29 @@ struct Solve {
                               : launch_fused_t<NQ, false, false, true>(fp);
     }
   }
+  template <int NQ, bool kTail>
+  int launch_fused_ps_t(const FusedParams& fp) {
+    auto kern = &fused_ps_kernel<NQ, kTail>;
+    static bool attr = false;
+    const size_t smem = fused_ps_smem_bytes<NQ>();
+    if (!attr) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    ++g_launches;
+    CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(fused_warps(NQ) * 32), smem, st, fp, cost,
+                  (int)pr.d2, (float)(-kLog2e / lam)));
+    return 0;
+  }
+  template <int NQ>
+  int launch_fused_ps(const FusedParams& fp) {
+    if constexpr (NQ > kFusedMaxChunks) {
+      return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
+    } else {
+      if (fp.nq != NQ) return launch_fused_ps<NQ + 1>(fp);
+      return fp.e0 != nullptr ? launch_fused_ps_t<NQ, true>(fp) : launch_fused_ps_t<NQ, false>(fp);
+    }
+  }
   template <bool kRowOnly>
   int launch_fused(const FusedParams& fp) {
     return launch_fused_nq<1, kRowOnly>(fp);
@@ -708,7 +742,11 @@ struct Solve {
     fp.part = F(L.part);
     fp.res = (res || e0) ? F(L.res) : nullptr;   // kTail: residual and E0 together
     fp.e0 = (res || e0) ? F(L.e0) : nullptr;
-    if (int e = launch_fused<false>(fp)) return e;
+    if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE) {
+      if (int e = launch_fused_ps<1>(fp)) return e;
+    } else {
+      if (int e = launch_fused<false>(fp)) return e;
+    }
     FusedMergeParams mp = {};
     mp.B = (int)pr.B;
     mp.nrows = (int)pr.d1;
@@ -1094,7 +1132,9 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   S.warm = init_log_u != nullptr;
   // one fused row->column pass per iteration for shared costs, unless the
   // problem takes the single-launch small solver (or this is the exact rerun)
-  if (allow_est && !(op.flags & SINKHORN_FLAG_NO_FUSED) && fused_eligible(pr)) {
+  const bool cost_aligned = (reinterpret_cast<uintptr_t>(cost) & 15) == 0;
+  if (allow_est && !(op.flags & SINKHORN_FLAG_NO_FUSED) && fused_eligible(pr) &&
+      (pr.cost_kind != SINKHORN_COST_PER_SAMPLE || cost_aligned)) {
     SmallParams sp0;
     int g0 = 0;
     size_t sm0 = 0;
@@ -1220,7 +1260,11 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
                           : "lane";
   if (L.fused && !small) {
     // v_1 from u_0, then one fused pass (+ column merge) per iteration
-    if (int e = S.fused_row_only(1)) return e;
+    if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE) {
+      if (int e = S.lane_col(kModeUpdate, S.F(L.g2[1]), S.F(L.g2[0]), kResNone)) return e;
+    } else {
+      if (int e = S.fused_row_only(1)) return e;
+    }
     cur = 1;
     for (int k = 1; k <= op.max_iters; ++k) {
       const bool last = (k == op.max_iters);

@@ -505,6 +505,220 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_pass_kernel(const FusedParam
   pdl_launch_dependents();
 }
 
+// ---------------------------------------------------------------------------
+// Per-sample costs (BASELINE config 4): the same fused row->column pass over
+// each lane's own C_b, which is streamed from HBM once per iteration instead
+// of twice (the two half-sweeps each read it).  Every warp streams its own
+// lane's rows through a private ring of kPsStages slots (cp.async.bulk, one
+// mbarrier per slot) and refills a slot as soon as it has consumed it.  Rows
+// are reduced in the log domain, t_j = c_ij * (-log2e / lambda) + v_j, with
+// the previous-lse shift and the exact fallback of the shared-cost pass.
+constexpr int kPsStages = 4;
+
+template <int NQ>
+__host__ __device__ constexpr size_t fused_ps_smem_bytes() {
+  return (size_t)fused_warps(NQ) * kPsStages * (NQ * 64 * 4 + 8);
+}
+
+template <int NQ, bool kTail, int NW = fused_warps(NQ)>
+__global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams p, const float* cost,
+                                                              int d2, float kscale) {
+  extern __shared__ __align__(128) unsigned char fsm[];
+  constexpr int rowlen = NQ * 64;
+  const int warp = warp_id(), lane = lane_id();
+  float* ring = reinterpret_cast<float*>(fsm) + (size_t)warp * kPsStages * rowlen;
+  uint64_t* full = reinterpret_cast<uint64_t*>(fsm + (size_t)NW * kPsStages * rowlen * 4) +
+                   warp * kPsStages;
+  const long long u0 = fused_seg_start(p.U, p.nct, blockIdx.x);
+  const long long u1 = fused_seg_start(p.U, p.nct, blockIdx.x + 1);
+  const int n = (int)(u1 - u0);
+  const int nrows = p.nrows;
+  const uint32_t row_bytes = (uint32_t)d2 * 4u;
+  const size_t lane_cells = (size_t)nrows * d2;
+
+  // columns past d2 are never written by the copies: zero them once so the
+  // -inf potentials there meet a finite cost
+  for (int k = lane; k < kPsStages * rowlen; k += 32)
+    if ((k % rowlen) >= d2) ring[k] = 0.f;
+  if (lane == 0) {
+    for (int st = 0; st < kPsStages; ++st) mbar_init(&full[st], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  // producer state of this warp: stream position, group and row it loads next
+  int pp = 0, pg = (int)(u0 / nrows), pi = (int)(u0 % nrows);
+  auto produce = [&]() {   // lane 0: position pp into slot pp % kPsStages
+    const int st = pp % kPsStages;
+    const int b = pg * NW + warp;
+    if (b < p.B) {
+      mbar_arrive_expect_tx(&full[st], row_bytes);
+      bulk_g2s(ring + st * rowlen, cost + b * lane_cells + (size_t)pi * d2, row_bytes, &full[st]);
+    } else {
+      mbar_arrive(&full[st]);   // idle lane: complete the phase without data
+    }
+    ++pp;
+    if (++pi == nrows) {
+      pi = 0;
+      ++pg;
+    }
+  };
+  const int npre = n < kPsStages ? n : kPsStages;
+  if (lane == 0)
+    for (int k = 0; k < npre; ++k) produce();   // the cost does not depend on the previous launch
+  pdl_wait();
+  const bool dead = p.status != nullptr && *p.status != 0;
+
+  int r = 0;
+  long long u = u0;
+  const int g_first = (int)(u0 / nrows);
+  const uint64_t ks2 = pk2(kscale, kscale);
+  while (u < u1) {
+    const int g = (int)(u / nrows);
+    const int i_begin = (int)(u - (long long)g * nrows);
+    const long long seg_end = (long long)(g + 1) * nrows < u1 ? (long long)(g + 1) * nrows : u1;
+    const int i_end = (int)(seg_end - (long long)g * nrows);
+    const int b = g * NW + warp;
+    const bool act = b < p.B && !dead;
+
+    uint64_t xv[NQ], acc[NQ];
+    const float* x_b = p.x + (size_t)b * p.rowlen + 2 * lane;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      float2 v2 = make_float2(neg_inf(), neg_inf());
+      if (act && 2 * lane + 64 * q < d2) v2 = __ldg(reinterpret_cast<const float2*>(x_b + 64 * q));
+      xv[q] = pk2(v2.x, v2.y);
+      acc[q] = 0ull;
+    }
+    const float* tg_b = p.target + (size_t)b * p.ldo;
+    const float* mg_b = p.marg + (size_t)b * p.ldo;
+    float* out_b = p.out + (size_t)b * p.ldo;
+    float* e0_b = kTail ? p.e0 + (size_t)b * p.ldo : nullptr;
+    auto ld_win = [&](int base, float& tw, float& mw, float& ow) {
+      const int i = base + lane;
+      const bool ok = act && i < i_end;
+      tw = ok ? __ldg(tg_b + i) : 0.f;
+      mw = ok ? __ldg(mg_b + i) : 0.f;
+      ow = ok ? out_b[i] : 0.f;
+    };
+    float tw, mw, ow, tw_n, mw_n, ow_n;
+    ld_win(i_begin, tw, mw, ow);
+    ld_win(i_begin + 32, tw_n, mw_n, ow_n);
+    float rres = 0.f, ob = 0.f;
+
+    for (int i = i_begin; i < i_end; ++i, ++r) {
+      const int wi = (i - i_begin) & 31;
+      const float tgt = __shfl_sync(0xffffffffu, tw, wi);
+      const float mgl = __shfl_sync(0xffffffffu, mw, wi);
+      const float uold = __shfl_sync(0xffffffffu, ow, wi);
+      if (wi == 31) {
+        tw = tw_n;
+        mw = mw_n;
+        ow = ow_n;
+        ld_win(i + 33, tw_n, mw_n, ow_n);
+      }
+      const int st = r % kPsStages;
+      mbar_wait(&full[st], (uint32_t)((r / kPsStages) & 1));
+      const float* row = ring + st * rowlen + 2 * lane;
+      uint64_t t[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const float2 c2 = *reinterpret_cast<const float2*>(row + 64 * q);
+        t[q] = ffma2(pk2(c2.x, c2.y), ks2, xv[q]);
+      }
+      float ms = tgt - uold;
+      bool exact = !(ms > -3.0e38f && ms < 3.0e38f);
+      float S = 0.f;
+      if (!exact) {
+        const uint64_t nm = pk2(-ms, -ms);
+        uint64_t s0 = 0ull, s1 = 0ull;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const uint64_t d = fadd2(t[q], nm);
+          t[q] = pk2(ex2(lo2(d)), ex2(hi2(d)));
+          if (q & 1) fadd2_acc(s1, t[q]);
+          else       fadd2_acc(s0, t[q]);
+        }
+        const uint64_t s01 = fadd2(s0, s1);
+        S = lo2(s01) + hi2(s01);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+        exact = act && !(S >= kFusedEstLo && S <= kFusedEstHi);
+      }
+      if (exact) {   // warp-uniform; the first iteration and rare rows after it
+        float m0 = neg_inf(), m1 = neg_inf();
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const float2 c2 = *reinterpret_cast<const float2*>(row + 64 * q);
+          t[q] = ffma2(pk2(c2.x, c2.y), ks2, xv[q]);
+          if (q & 1) m1 = fmax3(m1, lo2(t[q]), hi2(t[q]));
+          else       m0 = fmax3(m0, lo2(t[q]), hi2(t[q]));
+        }
+        float m = fmaxf(m0, m1);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+        ms = fmaxf(m, kNegBig);
+        const uint64_t nm = pk2(-ms, -ms);
+        uint64_t s0 = 0ull, s1 = 0ull;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const uint64_t d = fadd2(t[q], nm);
+          t[q] = pk2(ex2(lo2(d)), ex2(hi2(d)));
+          if (q & 1) fadd2_acc(s1, t[q]);
+          else       fadd2_acc(s0, t[q]);
+        }
+        const uint64_t s01 = fadd2(s0, s1);
+        S = lo2(s01) + hi2(s01);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+      }
+      const float lse = S > 0.f ? ms + lg2(S) : neg_inf();
+      const float o = sweep_out(tgt, lse);
+      if (lane == wi) ob = o;
+      const float a = S > 0.f ? mgl * rcp_approx(S) : 0.f;   // mu_i / S: P_ij = e_j * a
+      const uint64_t av2 = pk2(a, a);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) ffma2_acc(acc[q], t[q], av2);
+      if constexpr (kTail) {
+        rres = fmaxf(rres, fabsf(exp2f(o + lse) - mgl));
+        float qs = 0.f;   // E0 row term: a * sum_j e_j * c_ij
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const float2 c2 = *reinterpret_cast<const float2*>(row + 64 * q);
+          qs = fmaf(lo2(t[q]), c2.x, qs);
+          qs = fmaf(hi2(t[q]), c2.y, qs);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, off);
+        if (act && lane == 0) e0_b[i] = (a > 0.f && qs > 0.f) ? log2f(a) + log2f(qs) : neg_inf();
+      }
+      if (wi == 31 || i + 1 == i_end) {   // this window's u_i, one coalesced store
+        if (act && lane <= wi) out_b[i - wi + lane] = ob;
+      }
+      // refill the slot just consumed with the position kPsStages ahead
+      __syncwarp();
+      if (lane == 0 && pp < n) {
+        fence_proxy_async();
+        produce();
+      }
+    }
+    if (act) {
+      float* dst = p.part + (((size_t)blockIdx.x * p.maxseg + (g - g_first)) * NW + warp) *
+                                (size_t)p.rowlen;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (2 * lane + 64 * q < p.rowlen)
+          *reinterpret_cast<float2*>(dst + 2 * lane + 64 * q) = make_float2(lo2(acc[q]), hi2(acc[q]));
+    }
+    if constexpr (kTail) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) rres = fmaxf(rres, __shfl_xor_sync(0xffffffffu, rres, off));
+      if (act && lane == 0) atomic_max_nonneg(&p.res[b], rres);
+    }
+    u = seg_end;
+  }
+  pdl_launch_dependents();
+}
+
 // Column update from the plan partials: colsum_j = sum over the CTAs that
 // covered lane b's group (ascending), v'_j = v_j + l2nu_j - log2(colsum_j),
 // column residual |colsum_j - nu_j|.  grid (ceil(rowlen / 256), B).

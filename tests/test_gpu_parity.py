@@ -150,10 +150,54 @@ def test_separable_grid_ragged_shapes(nx, ny, tol, cuda):
     assert np.all(np.abs(res.residuals.double().cpu().numpy() - ref.residuals) <= 1e-5)
 
 
-def test_per_sample_cost(cuda):
-    """BASELINE config 4 subset: per-lane U[0,1) costs, d=1024, streamed from HBM."""
-    g, res = _run_golden("config4_subset", cuda)
+@pytest.mark.parametrize("fused", [pytest.param(True, id="fused"), pytest.param(False, id="lane")])
+def test_per_sample_cost(fused, cuda):
+    """BASELINE config 4 subset: per-lane U[0,1) costs, d=1024, streamed from HBM,
+    through the fused per-sample pass (one read of C_b per iteration) and the
+    two-half-sweep lane kernels."""
+    g, res = _run_golden("config4_subset", cuda, fused=fused)
+    assert res.path == ("fused" if fused else "lane")
     _check_loss_and_grads(g, res)
+
+
+@pytest.mark.parametrize("B,d1,d2,tol", [(37, 50, 68, 1e-5), (16, 64, 64, 0.0), (5, 300, 1024, 0.0),
+                                         (20, 1000, 36, 1e-4)])
+def test_fused_per_sample_ragged_shapes_against_oracle(B, d1, d2, tol, cuda):
+    """Per-sample costs through the fused pass: ragged lane groups, d2 not a
+    multiple of 64 (zeroed ring tails), zero-mass bins, lockstep stops."""
+    skb = _skb()
+    from oracle import sinkhorn_oracle as orc
+
+    rng = np.random.default_rng(B * 11 + d2)
+    mu = orc.fp32_exact(orc.random_histogram_batch(B, d1, rng))
+    nu = orc.fp32_exact(orc.random_histogram_batch(B, d2, rng))
+    mu[1 % B, 3] = 0.0
+    mu[1 % B] = orc.fp32_exact(mu[1 % B] / mu[1 % B].sum())
+    nu[0, d2 - 1] = 0.0
+    nu[0] = orc.fp32_exact(nu[0] / nu[0].sum())
+    c = orc.fp32_exact(rng.random((B, d1, d2)) * 2.0)
+    lam, iters = 0.1, 40
+    refs = [orc.batch_forward(mu[b:b + 1], nu[b:b + 1], c[b], lam, max_iters=iters,
+                              tolerance=0.0, check_interval=10) for b in range(B)]
+    res = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda),
+                    torch.tensor(c, dtype=torch.float32, device=cuda), lam, iters, 0.0, 10)
+    assert res.path == "fused"
+    want = np.array([r.cost_e0[0] for r in refs])
+    rel = np.abs(res.cost_e0.double().cpu().numpy() - want) / want
+    assert rel.max() <= LOSS_RTOL
+    lu = res.log_u.double().cpu().numpy()
+    ref_lu = np.concatenate([r.log_u for r in refs])
+    assert np.array_equal(np.isneginf(lu), np.isneginf(ref_lu))
+    fu = np.isfinite(ref_lu)
+    assert np.abs(lu[fu] - ref_lu[fu]).max() <= 1e-3 * max(1.0, np.abs(ref_lu[fu]).max())
+    if tol > 0:   # lockstep stop: the same iteration count as the unfused lane kernels
+        a = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda),
+                      torch.tensor(c, dtype=torch.float32, device=cuda), lam, 400, tol, 10)
+        b_ = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda),
+                       torch.tensor(c, dtype=torch.float32, device=cuda), lam, 400, tol, 10,
+                       fused=False)
+        assert a.path == "fused" and b_.path == "lane"
+        assert a.iterations_run == b_.iterations_run
 
 
 def test_half_sweep_matches_fused_log_reduction(cuda):
