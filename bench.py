@@ -212,8 +212,8 @@ def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
              path: str = "tiled", share: float = 1.0) -> dict:
     """Dominant kernel = the half-sweep (2*iters per step; one launch each on the
     tiled path, all inside one launch on the small path), or on the fused path
-    the fused pass (iters per step, one exponential per cell: the column
-    half-sweep is an FFMA on the row sweep's plan entries)."""
+    the fused pass (iters per step: the column half-sweep is an FFMA on the row
+    sweep's plan entries, so one launch does a whole iteration's work)."""
     cells = float(cfg["B"]) * cfg["d"] * cfg["d"] * share  # cells per sweep launch (this GPU)
     if cfg["cost"] == "per_sample":
         # SURVEY 8(d): 4 B of C per cell per half-sweep.  A fused launch is a
@@ -221,8 +221,12 @@ def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
         per_cell = 8 if path == "fused" else 4
         achieved = cells * per_cell / (sweep_ms * 1e-3) / 1e9
         peak = float(peaks.get("hbm_gbs", 6650.0))
-        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic,
+        out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+               "frac": achieved / peak, "traffic": traffic}
+        if path == "fused":   # what the fused kernel actually streams: C_b once
+            read = cells * 4 / (sweep_ms * 1e-3) / 1e9
+            out.update({"achieved_read": read, "frac_read": read / peak})
+        return {**out,
                 "kernel": ("fused_ps_kernel + fused_merge_kernel (one read of C_b per iteration)"
                            if path == "fused" else
                            "lane_col_kernel / lane_row_kernel (per-sample sweep)"),

@@ -121,7 +121,8 @@ def test_batch_sharded_solve_on_the_device(nccl_world1, cuda):
     assert rel.max() <= LOSS_RTOL
 
 
-@pytest.mark.parametrize("case", ["small", "tiled", "separable", "per_sample"])
+@pytest.mark.parametrize("case", ["small", "fused", "tiled", "separable", "per_sample",
+                                  "per_sample_lane"])
 def test_warm_start_continues_the_iteration(case, cuda):
     """k1 iterations, then k2 more from the returned log_u, equal one run of
     k1 + k2 iterations (the k-th iterate depends only on log_u_{k-1}), on every
@@ -131,9 +132,10 @@ def test_warm_start_continues_the_iteration(case, cuda):
 
     rng = np.random.default_rng(11)
     kw = {}
-    if case == "per_sample":
+    if case.startswith("per_sample"):
         B, d = 6, 48
         cost = torch.rand(B, d, d, device=cuda)
+        kw = {"fused": case == "per_sample"}
     elif case == "separable":
         B, d = 6, 12 * 7
         cost = skb.GridCost(12, 7)
@@ -142,7 +144,7 @@ def test_warm_start_continues_the_iteration(case, cuda):
         B, d = 6, 60
         cost = torch.tensor(orc.fp32_exact(orc.index_grid_cost(d)), dtype=torch.float32,
                             device=cuda)
-        kw = {"tiled_only": case == "tiled"}
+        kw = {"tiled_only": case != "small", "fused": case != "tiled"}
     mu = torch.tensor(orc.fp32_exact(orc.random_histogram_batch(B, d, rng)), device=cuda)
     nu = torch.tensor(orc.fp32_exact(orc.random_histogram_batch(B, d, rng)), device=cuda)
     mu[2, 5] = 0.0
