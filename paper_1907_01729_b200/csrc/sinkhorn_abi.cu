@@ -1114,6 +1114,52 @@ int check_options(const sinkhorn_options_v1* op) {
   return 0;
 }
 
+// ---- CUDA graphs of the fused iteration loop (tolerance 0) -----------------
+struct FusedGraphKey {
+  const void* ws;
+  const float* cost;
+  int64_t B, d1, d2;
+  int32_t kind;
+  double lambda;
+  int32_t max_iters;
+  int dev;
+  bool operator==(const FusedGraphKey& o) const {
+    return ws == o.ws && cost == o.cost && B == o.B && d1 == o.d1 && d2 == o.d2 && kind == o.kind &&
+           lambda == o.lambda && max_iters == o.max_iters && dev == o.dev;
+  }
+};
+struct FusedGraph {
+  FusedGraphKey key;
+  bool seen = false;
+  cudaGraphExec_t exec = nullptr;
+  unsigned long long launches = 0;
+  int iters = 0, cur = 0;
+  unsigned long long used = 0;
+};
+thread_local std::vector<FusedGraph> g_fused_graphs;   // a few recent problems per thread
+thread_local unsigned long long g_fused_graph_clock = 0;
+const bool g_no_graph = getenv("SKB_NO_GRAPH") != nullptr;   // diagnostics
+
+FusedGraph* fused_graph_slot(const FusedGraphKey& k) {
+  ++g_fused_graph_clock;
+  for (auto& g : g_fused_graphs)
+    if (g.key == k) {
+      g.used = g_fused_graph_clock;
+      return &g;
+    }
+  if (g_fused_graphs.size() >= 8) {   // evict the least recently used
+    auto it = std::min_element(g_fused_graphs.begin(), g_fused_graphs.end(),
+                               [](const FusedGraph& a, const FusedGraph& b) { return a.used < b.used; });
+    if (it->exec) cudaGraphExecDestroy(it->exec);
+    g_fused_graphs.erase(it);
+  }
+  FusedGraph g;
+  g.key = k;
+  g.used = g_fused_graph_clock;
+  g_fused_graphs.push_back(g);
+  return &g_fused_graphs.back();
+}
+
 int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, const float* mu,
                  const float* nu, const float* cost, float* out_cost, float* out_log_u,
                  float* out_log_v, int32_t* out_iterations, float* out_residuals, void* ws,
@@ -1260,36 +1306,74 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
                           : "lane";
   if (L.fused && !small) {
     // v_1 from u_0, then one fused pass (+ column merge) per iteration
-    if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE) {
-      if (int e = S.lane_col(kModeUpdate, S.F(L.g2[1]), S.F(L.g2[0]), kResNone)) return e;
-    } else {
-      if (int e = S.fused_row_only(1)) return e;
+    auto fused_loop = [&]() -> int {
+      if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE) {
+        if (int e = S.lane_col(kModeUpdate, S.F(L.g2[1]), S.F(L.g2[0]), kResNone)) return e;
+      } else {
+        if (int e = S.fused_row_only(1)) return e;
+      }
+      cur = 1;
+      for (int k = 1; k <= op.max_iters; ++k) {
+        const bool last = (k == op.max_iters);
+        const bool check = checks && (k % op.check_interval == 0) && !last;
+        if (check || last) {
+          if (int e = S.zero_res()) return e;
+        }
+        if (int e = S.fused_iteration(cur, check || last, check || last)) return e;
+        iters = k;
+        if (last) break;
+        if (check) {
+          ++g_launches;
+          reduce_max_kernel<<<1, 256, 0, S.st>>>(S.F(L.res), (int)pr.B, S.F(L.scratch));
+          CK(cudaGetLastError());
+          float hmax = 0.f;
+          int hstatus = 0;
+          CK(cudaMemcpyAsync(&hmax, S.F(L.scratch), 4, cudaMemcpyDeviceToHost, S.st));
+          CK(cudaMemcpyAsync(&hstatus, status, 4, cudaMemcpyDeviceToHost, S.st));
+          CK(cudaStreamSynchronize(S.st));
+          double gmax = (hstatus != 0) ? NAN : (double)hmax;
+          if (g_reducer) gmax = g_reducer(gmax, g_reducer_user);
+          if (hstatus != 0) break;
+          if (gmax <= op.tolerance) break;   // converged: g2[cur] = log_v_k, f2 = log_u_k
+        }
+        cur ^= 1;
+      }
+      return 0;
+    };
+    // Without a stopping test the loop has no host decision: a repeated solve
+    // (same workspace, cost and shape) replays it as one CUDA graph, so its
+    // ~2 launches per iteration cannot stall behind the host.
+    FusedGraph* fg = nullptr;
+    if (!checks && g_reducer == nullptr && !g_no_graph)
+      fg = fused_graph_slot(FusedGraphKey{ws, cost, pr.B, pr.d1, pr.d2, pr.cost_kind, op.lambda,
+                                          op.max_iters, S.di.dev});
+    if (fg != nullptr && fg->seen && fg->exec == nullptr) {   // second sighting: capture
+      static thread_local cudaStream_t cs = nullptr;
+      if (cs == nullptr) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      const unsigned long long l0 = g_launches;
+      S.st = cs;
+      CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      const int e = fused_loop();
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+      S.st = st;
+      if (e) return e;
+      CK(ce);
+      CK(cudaGraphInstantiate(&fg->exec, graph, 0));
+      CK(cudaGraphDestroy(graph));
+      fg->launches = g_launches - l0;
+      fg->iters = iters;
+      fg->cur = cur;
+      g_launches = l0;
     }
-    cur = 1;
-    for (int k = 1; k <= op.max_iters; ++k) {
-      const bool last = (k == op.max_iters);
-      const bool check = checks && (k % op.check_interval == 0) && !last;
-      if (check || last) {
-        if (int e = S.zero_res()) return e;
-      }
-      if (int e = S.fused_iteration(cur, check || last, check || last)) return e;
-      iters = k;
-      if (last) break;
-      if (check) {
-        ++g_launches;
-        reduce_max_kernel<<<1, 256, 0, st>>>(S.F(L.res), (int)pr.B, S.F(L.scratch));
-        CK(cudaGetLastError());
-        float hmax = 0.f;
-        int hstatus = 0;
-        CK(cudaMemcpyAsync(&hmax, S.F(L.scratch), 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&hstatus, status, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        double gmax = (hstatus != 0) ? NAN : (double)hmax;
-        if (g_reducer) gmax = g_reducer(gmax, g_reducer_user);
-        if (hstatus != 0) break;
-        if (gmax <= op.tolerance) break;   // converged: g2[cur] = log_v_k, f2 = log_u_k
-      }
-      cur ^= 1;
+    if (fg != nullptr && fg->exec != nullptr) {
+      CK(cudaGraphLaunch(fg->exec, st));
+      g_launches += fg->launches;
+      iters = fg->iters;
+      cur = fg->cur;
+    } else {
+      if (fg != nullptr) fg->seen = true;
+      if (int e = fused_loop()) return e;
     }
   }
   for (int k = 1; !persist && !small && !L.fused && k <= op.max_iters; ++k) {

@@ -408,3 +408,31 @@ def test_fused_pass_ragged_shapes_against_oracle(B, d1, d2, tol, cuda):
     assert np.abs(lu[fu] - ref.log_u[fu]).max() <= 1e-3 * max(1.0, np.abs(ref.log_u[fu]).max())
     res_r = res.residuals.double().cpu().numpy()
     assert np.allclose(res_r, ref.residuals, atol=2e-6), (res_r[:4], ref.residuals[:4])
+
+
+@pytest.mark.parametrize("kind", ["shared", "per_sample"])
+def test_repeated_fused_solve_replays_the_same_result(kind, cuda):
+    """Tolerance-0 fused solves: the first runs eagerly, the second captures the
+    iteration loop as a CUDA graph and replays it, the third replays it again.
+    All three give bitwise the same potentials and costs."""
+    skb = _skb()
+    from oracle import sinkhorn_oracle as orc
+
+    rng = np.random.default_rng(5)
+    B, d = 40, 96
+    mu = torch.tensor(orc.fp32_exact(orc.random_histogram_batch(B, d, rng)), device=cuda)
+    nu = torch.tensor(orc.fp32_exact(orc.random_histogram_batch(B, d, rng)), device=cuda)
+    shape = (d, d) if kind == "shared" else (B, d, d)
+    cost = torch.tensor(orc.fp32_exact(rng.random(shape)), dtype=torch.float32, device=cuda)
+    runs = [skb.solve(mu, nu, cost, 0.1, 30, 0.0, 10, tiled_only=True) for _ in range(3)]
+    assert all(r.path == "fused" for r in runs)
+    for r in runs[1:]:
+        assert torch.equal(r.cost_e0, runs[0].cost_e0)
+        assert torch.equal(r.log_u, runs[0].log_u) and torch.equal(r.log_v, runs[0].log_v)
+        assert r.iterations_run == runs[0].iterations_run == 30
+    # the input changes between replays: the graph reads the current buffers
+    mu2 = torch.tensor(orc.fp32_exact(orc.random_histogram_batch(B, d, rng)), device=cuda)
+    a = skb.solve(mu2, nu, cost, 0.1, 30, 0.0, 10, tiled_only=True)
+    ref = skb.solve(mu2, nu, cost, 0.1, 30, 0.0, 10, tiled_only=True, fused=False)
+    rel = ((a.cost_e0 - ref.cost_e0).abs() / ref.cost_e0).max().item()
+    assert rel <= 2e-6
