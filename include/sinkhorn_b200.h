@@ -126,6 +126,26 @@ int32_t sinkhorn_forward_device_v1(const sinkhorn_problem_v1* prob,
                                    float* out_residuals, void* workspace,
                                    size_t workspace_bytes, void* stream);
 
+/* float64 parity mode: the reference's float64 iteration
+ * (batch.py:264-349) on the device, in natural log, reaching the
+ * reference's default tolerance 1e-9 (core.py:85) that an fp32 solve cannot.
+ * Same problem / options / statuses as sinkhorn_forward_device_v1, with
+ * double device buffers and its own workspace size.  Slower than the fp32
+ * paths: one warp per output, exact two-pass log-sum-exp in double. */
+size_t sinkhorn_workspace_bytes_f64_v1(const sinkhorn_problem_v1* prob);
+int32_t sinkhorn_forward_f64_device_v1(const sinkhorn_problem_v1* prob,
+                                       const sinkhorn_options_v1* opt, const double* mu,
+                                       const double* nu, const double* cost, double* out_cost,
+                                       double* out_log_u, double* out_log_v,
+                                       int32_t* out_iterations, double* out_residuals,
+                                       void* workspace, size_t workspace_bytes, void* stream);
+/* batch_backward in float64 over device buffers (the fp64 mode's backward). */
+int32_t sinkhorn_backward_f64_device_v1(int64_t B, int64_t d1, int64_t d2, double lambda,
+                                        const double* log_u, const double* log_v,
+                                        const double* upstream, double* out_grad_mu,
+                                        double* out_grad_nu, int32_t* out_zero_mass_lane,
+                                        void* workspace, size_t workspace_bytes, void* stream);
+
 /* Warm start (the reference has no such API, batch.py:295
  * always starts from log_u = 0 on the support): as sinkhorn_forward_device_v1,
  * but the iteration starts from init_log_u (B, d1) natural log, device fp32,

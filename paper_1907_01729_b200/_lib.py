@@ -45,6 +45,9 @@ EXPORTED_SYMBOLS = (
     "sinkhorn_forward_device_v1",
     "sinkhorn_forward_warm_device_v1",
     "sinkhorn_backward_device_v1",
+    "sinkhorn_workspace_bytes_f64_v1",
+    "sinkhorn_forward_f64_device_v1",
+    "sinkhorn_backward_f64_device_v1",
     "sinkhorn_half_sweep_workspace_bytes_v1",
     "sinkhorn_half_sweep_device_v1",
     "sinkhorn_plan_grad_device_v1",
@@ -116,6 +119,12 @@ def _declare(lib):
             i32, [ctypes.POINTER(Problem), ctypes.POINTER(Options), P, P, P, P, P, P, P,
                   ctypes.POINTER(ctypes.c_int32), P, P, sz, P]),
         "sinkhorn_backward_device_v1": (
+            i32, [i64, i64, i64, f64, P, P, P, P, P, ctypes.POINTER(ctypes.c_int32), P, sz, P]),
+        "sinkhorn_workspace_bytes_f64_v1": (sz, [ctypes.POINTER(Problem)]),
+        "sinkhorn_forward_f64_device_v1": (
+            i32, [ctypes.POINTER(Problem), ctypes.POINTER(Options), P, P, P, P, P, P,
+                  ctypes.POINTER(ctypes.c_int32), P, P, sz, P]),
+        "sinkhorn_backward_f64_device_v1": (
             i32, [i64, i64, i64, f64, P, P, P, P, P, ctypes.POINTER(ctypes.c_int32), P, sz, P]),
         "sinkhorn_half_sweep_workspace_bytes_v1": (sz, [i64, i64, i64]),
         "sinkhorn_half_sweep_device_v1": (i32, [i64, i64, i64, f64, P, P, P, P, P, P, P, sz, P]),

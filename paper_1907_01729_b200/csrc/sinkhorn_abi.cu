@@ -28,6 +28,7 @@
 #include "sweep_small.cuh"
 #include "sweep_sep.cuh"
 #include "sweep_fused.cuh"
+#include "sweep_f64.cuh"
 
 using namespace skb;
 
@@ -1558,11 +1559,13 @@ int32_t sinkhorn_forward_warm_device_v1(const sinkhorn_problem_v1* prob,
 }
 
 
-int32_t sinkhorn_backward_device_v1(int64_t B, int64_t d1, int64_t d2, double lambda,
-                                    const float* log_u, const float* log_v,
-                                    const float* upstream, float* out_grad_mu,
-                                    float* out_grad_nu, int32_t* out_zero_mass_lane,
-                                    void* workspace, size_t workspace_bytes, void* stream) {
+extern "C++" {
+namespace {
+template <typename T>
+int backward_device(int64_t B, int64_t d1, int64_t d2, double lambda, const T* log_u,
+                    const T* log_v, const T* upstream, T* out_grad_mu, T* out_grad_nu,
+                    int32_t* out_zero_mass_lane, void* workspace, size_t workspace_bytes,
+                    void* stream) {
   if (B < 0 || d1 < 0 || d2 < 0) return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "negative extent");
   if (B == 0) return 0;
   if (!log_u || !log_v || !upstream || !out_grad_mu || !out_grad_nu || !workspace)
@@ -1574,7 +1577,7 @@ int32_t sinkhorn_backward_device_v1(int64_t B, int64_t d1, int64_t d2, double la
   CK(cudaMemsetAsync(status, 0, 4, st));
   CK(cudaMemsetAsync(bad, 0x7f, 4, st));
   ++g_launches;
-  backward_kernel<float><<<dim3((unsigned)B, 2), 256, 0, st>>>(
+  backward_kernel<T><<<dim3((unsigned)B, 2), 256, 0, st>>>(
       log_u, log_v, (int)d1, (int)d2, lambda, upstream, out_grad_mu, out_grad_nu, status, bad);
   CK(cudaGetLastError());
   int h[2] = {0, 0};
@@ -1585,6 +1588,198 @@ int32_t sinkhorn_backward_device_v1(int64_t B, int64_t d1, int64_t d2, double la
     return fail(SINKHORN_STATUS_ZERO_MASS_LANE, "zero-mass bin in lane " + std::to_string(h[1]));
   }
   return h[0];
+}
+
+// ---- float64 parity mode (sweep_f64.cuh) ----------------------------------
+struct F64Layout {
+  size_t a = 0, at = 0, lmu = 0, lnu = 0, u = 0, v = 0, rrow = 0, rcol = 0, e0 = 0, res = 0;
+  size_t status = 0, total = 0;
+};
+
+F64Layout f64_layout(const sinkhorn_problem_v1& pr) {
+  F64Layout L;
+  Carver c;
+  const size_t lanes = pr.cost_kind == SINKHORN_COST_PER_SAMPLE ? (size_t)pr.B : 1;
+  const size_t n1 = (size_t)pr.B * pr.d1 * 8, n2 = (size_t)pr.B * pr.d2 * 8;
+  L.a = c.take(lanes * pr.d1 * pr.d2 * 8);
+  L.at = c.take(lanes * pr.d1 * pr.d2 * 8);
+  L.lmu = c.take(n1);
+  L.u = c.take(n1);
+  L.rrow = c.take(n1);
+  L.lnu = c.take(n2);
+  L.v = c.take(n2);
+  L.rcol = c.take(n2);
+  L.e0 = c.take(n2);
+  L.res = c.take((size_t)pr.B * 8);
+  L.status = c.take(8);
+  L.total = c.off;
+  return L;
+}
+
+int forward_f64_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, const double* mu,
+                     const double* nu, const double* cost, double* out_cost, double* out_log_u,
+                     double* out_log_v, int32_t* out_iterations, double* out_residuals, void* ws,
+                     size_t ws_bytes, cudaStream_t st) {
+  const F64Layout L = f64_layout(pr);
+  if (ws == nullptr || ws_bytes < L.total) return fail(SINKHORN_STATUS_WORKSPACE, "workspace too small");
+  auto D = [&](size_t off) { return at<double>(ws, off); };
+  int* status = at<int>(ws, L.status);
+  int* badrow = status + 1;
+  const int B = (int)pr.B, d1 = (int)pr.d1, d2 = (int)pr.d2;
+  const bool per_sample = pr.cost_kind == SINKHORN_COST_PER_SAMPLE;
+  g_last_path = "fp64";
+  CK(cudaMemsetAsync(status, 0, 4, st));
+  CK(cudaMemsetAsync(badrow, 0x7f, 4, st));
+  if (!(op.flags & SINKHORN_FLAG_SKIP_VALIDATION)) {
+    ++g_launches;
+    validate_rows_kernel<double><<<(unsigned)B, 256, 0, st>>>(mu, d1, status, badrow);
+    ++g_launches;
+    validate_rows_kernel<double><<<(unsigned)B, 256, 0, st>>>(nu, d2, status, badrow);
+  }
+  ++g_launches;
+  f64_prep_kernel<<<grid_for((size_t)B * (d1 + d2)), 256, 0, st>>>(mu, nu, B, d1, d2, D(L.lmu),
+                                                                    D(L.lnu), D(L.u), D(L.v));
+  {
+    dim3 g((unsigned)((d2 + 31) / 32), (unsigned)((d1 + 31) / 32), per_sample ? (unsigned)B : 1u);
+    ++g_launches;
+    f64_cost_kernel<<<g, 256, 0, st>>>(pr.cost_kind == SINKHORN_COST_GRID2D ? nullptr : cost,
+                                       per_sample ? B : 1, d1, d2, op.lambda, (int)pr.grid_nx,
+                                       (double)pr.grid_hx * pr.grid_hx,
+                                       (double)pr.grid_hy * pr.grid_hy, D(L.a), D(L.at), status);
+  }
+  CK(cudaGetLastError());
+  const long long lane_cells = per_sample ? (long long)d1 * d2 : 0;
+  auto sweep = [&](int mode, bool col, double* out, const double* pot, const double* marg) -> int {
+    F64SweepParams p = {};
+    p.B = B;
+    p.P = col ? d2 : d1;
+    p.Q = col ? d1 : d2;
+    p.G = col ? D(L.at) : D(L.a);
+    p.g_lane = lane_cells;
+    p.x = col ? D(L.u) : D(L.v);
+    p.target = col ? D(L.lnu) : D(L.lmu);
+    p.out = out;
+    p.pot = pot;
+    p.marg = marg;
+    p.lam = op.lambda;
+    p.status = status;
+    dim3 g((unsigned)((p.P + 7) / 8), (unsigned)B);
+    ++g_launches;
+    if (mode == kF64Update) f64_sweep_kernel<kF64Update><<<g, 256, 0, st>>>(p);
+    else if (mode == kF64Residual) f64_sweep_kernel<kF64Residual><<<g, 256, 0, st>>>(p);
+    else f64_sweep_kernel<kF64E0><<<g, 256, 0, st>>>(p);
+    CK(cudaGetLastError());
+    return 0;
+  };
+  // lane_residuals (batch.py:303-309): row term with A, column term with A^T
+  auto residuals = [&]() -> int {
+    if (int e = sweep(kF64Residual, false, D(L.rrow), D(L.u), mu)) return e;
+    if (int e = sweep(kF64Residual, true, D(L.rcol), D(L.v), nu)) return e;
+    ++g_launches;
+    f64_lane_reduce_kernel<<<(unsigned)((B + 7) / 8), 256, 0, st>>>(D(L.rrow), d1, D(L.rcol), d2, B,
+                                                                    D(L.res), 0);
+    CK(cudaGetLastError());
+    return 0;
+  };
+  // ---- lockstep iteration (batch.py:314-324) ----
+  int iters = 0;
+  bool have_res = false, converged = false;
+  std::vector<double> hres((size_t)B);
+  for (int k = 1; k <= op.max_iters; ++k) {
+    if (int e = sweep(kF64Update, true, D(L.v), nullptr, nullptr)) return e;    // v first
+    if (int e = sweep(kF64Update, false, D(L.u), nullptr, nullptr)) return e;   // then u
+    iters = k;
+    if (op.tolerance > 0 && k % op.check_interval == 0) {
+      if (int e = residuals()) return e;
+      have_res = true;
+      int hstatus = 0;
+      CK(cudaMemcpyAsync(hres.data(), D(L.res), (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&hstatus, status, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      double gmax = 0.0;
+      for (double r : hres) gmax = (r != r || gmax != gmax) ? NAN : std::max(gmax, r);
+      if (hstatus != 0) gmax = NAN;
+      if (g_reducer) gmax = g_reducer(gmax, g_reducer_user);
+      if (hstatus != 0) break;
+      if (gmax <= op.tolerance) {
+        converged = true;
+        break;
+      }
+    }
+  }
+  if (!have_res || !converged) {
+    if (int e = residuals()) return e;
+  }
+  ++g_launches;
+  f64_nan_kernel<<<grid_for((size_t)B * (d1 + d2)), 256, 0, st>>>(D(L.u), (size_t)B * d1, D(L.v),
+                                                                  (size_t)B * d2, status);
+  // stable E0 (batch.py:329-337)
+  if (int e = sweep(kF64E0, true, D(L.e0), D(L.v), nullptr)) return e;
+  ++g_launches;
+  f64_lane_reduce_kernel<<<(unsigned)((B + 7) / 8), 256, 0, st>>>(D(L.e0), d2, nullptr, 0, B,
+                                                                  out_cost, 1);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out_log_u, D(L.u), (size_t)B * d1 * 8, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(out_log_v, D(L.v), (size_t)B * d2 * 8, cudaMemcpyDeviceToDevice, st));
+  if (out_residuals)
+    CK(cudaMemcpyAsync(out_residuals, D(L.res), (size_t)B * 8, cudaMemcpyDeviceToDevice, st));
+  if (out_iterations) *out_iterations = iters;
+  int h[2] = {0, 0};
+  CK(cudaMemcpyAsync(h, status, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h[0] == SINKHORN_STATUS_INVALID_HISTOGRAM)
+    return fail(h[0], "invalid histogram (row " + std::to_string(h[1]) + ")");
+  if (h[0] == SINKHORN_STATUS_INVALID_COST) return fail(h[0], "cost must be finite and >= 0");
+  if (h[0] == SINKHORN_STATUS_NON_FINITE_OUTPUT) return fail(h[0], "NaN in batched solver state");
+  return h[0];
+}
+}  // namespace
+}  // extern "C++"
+
+int32_t sinkhorn_backward_device_v1(int64_t B, int64_t d1, int64_t d2, double lambda,
+                                    const float* log_u, const float* log_v,
+                                    const float* upstream, float* out_grad_mu,
+                                    float* out_grad_nu, int32_t* out_zero_mass_lane,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  return backward_device<float>(B, d1, d2, lambda, log_u, log_v, upstream, out_grad_mu,
+                                out_grad_nu, out_zero_mass_lane, workspace, workspace_bytes, stream);
+}
+
+int32_t sinkhorn_backward_f64_device_v1(int64_t B, int64_t d1, int64_t d2, double lambda,
+                                        const double* log_u, const double* log_v,
+                                        const double* upstream, double* out_grad_mu,
+                                        double* out_grad_nu, int32_t* out_zero_mass_lane,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+  return backward_device<double>(B, d1, d2, lambda, log_u, log_v, upstream, out_grad_mu,
+                                 out_grad_nu, out_zero_mass_lane, workspace, workspace_bytes,
+                                 stream);
+}
+
+size_t sinkhorn_workspace_bytes_f64_v1(const sinkhorn_problem_v1* prob) {
+  if (check_problem(prob) != 0) return 0;
+  return f64_layout(*prob).total;
+}
+
+int32_t sinkhorn_forward_f64_device_v1(const sinkhorn_problem_v1* prob,
+                                       const sinkhorn_options_v1* opt, const double* mu,
+                                       const double* nu, const double* cost, double* out_cost,
+                                       double* out_log_u, double* out_log_v,
+                                       int32_t* out_iterations, double* out_residuals,
+                                       void* workspace, size_t workspace_bytes, void* stream) {
+  if (int e = check_problem(prob)) return e;
+  if (prob->B == 0) {   // ffi.ts:107-109
+    if (out_iterations) *out_iterations = 0;
+    return 0;
+  }
+  if (prob->d1 == 0 || prob->d2 == 0)
+    return fail(SINKHORN_STATUS_INVALID_HISTOGRAM, "empty histogram cannot sum to 1");
+  if (int e = check_options(opt)) return e;
+  if (!mu || !nu || !out_cost || !out_log_u || !out_log_v ||
+      (prob->cost_kind != SINKHORN_COST_GRID2D && !cost))
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
+  return forward_f64_impl(*prob, *opt, mu, nu, cost, out_cost, out_log_u, out_log_v,
+                          out_iterations, out_residuals, workspace, workspace_bytes,
+                          static_cast<cudaStream_t>(stream));
 }
 
 size_t sinkhorn_half_sweep_workspace_bytes_v1(int64_t B, int64_t d1, int64_t d2) {

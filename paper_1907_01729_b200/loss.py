@@ -137,7 +137,8 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
           check_interval: int = 10, validate: bool = True, time_loop: bool = False,
           exact_max: bool = False, mufu_only: bool = False,
           persistent: bool = False, tiled_only: bool = False,
-          dense_grid: bool = False, init_log_u=None, fused: bool = True) -> SolveResult:
+          dense_grid: bool = False, init_log_u=None, fused: bool = True,
+          fp64: bool = False) -> SolveResult:
     """batch_forward (batch.py:264-349) on the GPU.
 
     mu (B, d1), nu (B, d2) histograms; cost a (d1, d2) tensor shared by all
@@ -147,8 +148,12 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
     ``init_log_u`` (B, d1) warm-starts the iteration from a previous solve's
     log_u instead of 0 on the support (no reference API; batch.py:295).
     ``fused=False`` runs shared costs as two half-sweeps per iteration instead
-    of the fused row->column pass (sweep_fused.cuh).
+    of the fused row->column pass (sweep_fused.cuh).  ``fp64=True`` runs the
+    reference's float64 iteration on the device (sweep_f64.cuh): float64
+    outputs, reaches the reference's default tolerance 1e-9; path "fp64".
     """
+    if fp64:
+        return _solve_f64(mu, nu, cost, lam, max_iters, tolerance, check_interval, validate)
     mu, nu = torch.as_tensor(mu), torch.as_tensor(nu)
     if not isinstance(cost, GridCost):
         cost = torch.as_tensor(cost)
@@ -198,10 +203,47 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
                        path)
 
 
+def _solve_f64(mu, nu, cost, lam, max_iters, tolerance, check_interval, validate) -> SolveResult:
+    """The float64 parity mode: sinkhorn_forward_f64_device_v1 (sweep_f64.cuh)."""
+    mu, nu = torch.as_tensor(mu), torch.as_tensor(nu)
+    if not isinstance(cost, GridCost):
+        cost = torch.as_tensor(cost)
+    B, d1, d2 = _check_shapes(mu, nu, cost)
+    dev = mu.device if mu.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    f64 = dict(device=dev, dtype=torch.float64)
+    mu, nu = mu.to(**f64).contiguous(), nu.to(**f64).contiguous()
+    if not isinstance(cost, GridCost):
+        cost = cost.to(**f64).contiguous()
+    lib = _lib.load()
+    pr = _problem(B, d1, d2, cost)
+    op = _lib.Options()
+    op.lam, op.max_iters, op.check_interval, op.tolerance = float(lam), int(max_iters), \
+        int(check_interval), float(tolerance)
+    op.flags = 0 if validate else _lib.FLAG_SKIP_VALIDATION
+    out_cost = torch.empty(B, **f64)
+    log_u = torch.empty(B, d1, **f64)
+    log_v = torch.empty(B, d2, **f64)
+    residuals = torch.empty(B, **f64)
+    iters = ctypes.c_int32(0)
+    with torch.cuda.device(dev):
+        ws = _workspace(dev, lib.sinkhorn_workspace_bytes_f64_v1(ctypes.byref(pr)))
+        st = lib.sinkhorn_forward_f64_device_v1(
+            ctypes.byref(pr), ctypes.byref(op), _ptr(mu), _ptr(nu),
+            None if isinstance(cost, GridCost) else _ptr(cost), _ptr(out_cost), _ptr(log_u),
+            _ptr(log_v), ctypes.byref(iters), _ptr(residuals), _ptr(ws), ws.numel(),
+            _stream_handle(dev))
+    raise_for_status(st, "sinkhorn_forward_f64_device_v1")
+    return SolveResult(out_cost, log_u, log_v, float(lam), int(iters.value), residuals, -1.0,
+                       lib.sinkhorn_last_path_v1().decode())
+
+
 def potentials_backward(log_u: torch.Tensor, log_v: torch.Tensor, lam: float,
                         upstream: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
-    """batch_backward (batch.py:352-375): up[b] * lam * (x - mean_i x)."""
+    """batch_backward (batch.py:352-375): up[b] * lam * (x - mean_i x).
+    float64 potentials (the fp64 mode) are differentiated in float64."""
     dev = log_u.device
+    if log_u.dtype == torch.float64:
+        return _potentials_backward_f64(log_u, log_v, lam, upstream)
     log_u = _as_f32_cuda(log_u, dev)
     log_v = _as_f32_cuda(log_v, dev)
     up = _as_f32_cuda(upstream, dev).reshape(-1)
@@ -222,6 +264,30 @@ def potentials_backward(log_u: torch.Tensor, log_v: torch.Tensor, lam: float,
                                              ctypes.byref(lane), _ptr(ws), ws.numel(),
                                              _stream_handle(dev))
     raise_for_status(st, "sinkhorn_backward_device_v1", lane=lane.value)
+    return g_mu, g_nu
+
+
+def _potentials_backward_f64(log_u, log_v, lam, upstream):
+    dev = log_u.device
+    f64 = dict(device=dev, dtype=torch.float64)
+    log_u, log_v = log_u.to(**f64).contiguous(), log_v.to(**f64).contiguous()
+    up = torch.as_tensor(upstream).to(**f64).reshape(-1).contiguous()
+    B, d1 = log_u.shape
+    d2 = log_v.shape[1]
+    if log_v.shape[0] != B or up.numel() != B:
+        raise ShapeMismatch(f"upstream must have shape ({B},), got {tuple(up.shape)}")
+    g_mu, g_nu = torch.empty_like(log_u), torch.empty_like(log_v)
+    if B == 0:
+        return g_mu, g_nu
+    lib = _lib.load()
+    ws = torch.empty(64, device=dev, dtype=torch.uint8)
+    lane = ctypes.c_int32(-1)
+    with torch.cuda.device(dev):
+        st = lib.sinkhorn_backward_f64_device_v1(B, d1, d2, float(lam), _ptr(log_u), _ptr(log_v),
+                                                 _ptr(up), _ptr(g_mu), _ptr(g_nu),
+                                                 ctypes.byref(lane), _ptr(ws), ws.numel(),
+                                                 _stream_handle(dev))
+    raise_for_status(st, "sinkhorn_backward_f64_device_v1", lane=lane.value)
     return g_mu, g_nu
 
 

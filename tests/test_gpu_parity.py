@@ -436,3 +436,56 @@ def test_repeated_fused_solve_replays_the_same_result(kind, cuda):
     ref = skb.solve(mu2, nu, cost, 0.1, 30, 0.0, 10, tiled_only=True, fused=False)
     rel = ((a.cost_e0 - ref.cost_e0).abs() / ref.cost_e0).max().item()
     assert rel <= 2e-6
+
+
+# ---------------------------------------------------------------------------
+# float64 parity mode
+
+@pytest.mark.parametrize("name", ["closed_form_2x2", "config1", "config1_tol", "lockstep",
+                                  "zero_mass", "rect_37x53", "stability", "config4_subset"])
+def test_fp64_mode_matches_reference_to_float64_precision(name, cuda):
+    """solve(fp64=True) runs the reference's float64 iteration on the device:
+    costs to 1e-9 relative, potentials to 1e-8 (relative to their scale),
+    identical iteration counts and -inf patterns."""
+    skb = _skb()
+    g = load_golden(name)
+    c = torch.tensor(golden_cost(g), dtype=torch.float64, device=cuda)
+    res = skb.solve(torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
+                    float(g["lam"]), int(g["max_iters"]), float(g["tol"]),
+                    int(g["check_interval"]), fp64=True)
+    assert res.path == "fp64" and res.cost_e0.dtype == torch.float64
+    assert res.iterations_run == int(g["iterations_run"])
+    rel = np.abs(res.cost_e0.cpu().numpy() - g["cost_e0"]) / np.abs(g["cost_e0"])
+    assert rel.max() <= 1e-9, rel.max()
+    for got, want in ((res.log_u, g["log_u"]), (res.log_v, g["log_v"])):
+        got = got.cpu().numpy()
+        assert np.array_equal(np.isneginf(got), np.isneginf(want))
+        fin = np.isfinite(want)
+        scale = max(1.0, np.abs(want[fin]).max())
+        assert np.abs(got[fin] - want[fin]).max() <= 1e-8 * scale
+    assert np.abs(res.residuals.cpu().numpy() - g["residuals"]).max() <= 1e-10
+
+
+def test_fp64_mode_reaches_the_reference_default_tolerance(cuda):
+    """tolerance 1e-9 (core.py:85): the fp64 mode stops at the reference's
+    iteration with residuals <= 1e-9, and its backward matches in float64."""
+    skb = _skb()
+    from oracle import sinkhorn_oracle as orc
+
+    rng = np.random.default_rng(21)
+    B, d1, d2, lam = 6, 30, 41, 0.2
+    mu = orc.random_histogram_batch(B, d1, rng)
+    nu = orc.random_histogram_batch(B, d2, rng)
+    c = rng.random((d1, d2))
+    ref = orc.batch_forward(mu, nu, c, lam, max_iters=2000, tolerance=1e-9, check_interval=10)
+    res = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda),
+                    torch.tensor(c, device=cuda), lam, 2000, 1e-9, 10, fp64=True)
+    assert res.iterations_run == ref.iterations_run < 2000
+    assert float(res.residuals.max()) <= 1e-9
+    assert np.abs(res.cost_e0.cpu().numpy() - ref.cost_e0).max() <= 1e-12
+    up = rng.normal(size=B)
+    gm_ref, gn_ref = orc.batch_backward(ref.log_u, ref.log_v, lam, up)
+    gm, gn = skb.potentials_backward(res.log_u, res.log_v, lam, torch.tensor(up, device=cuda))
+    assert gm.dtype == torch.float64
+    assert np.abs(gm.cpu().numpy() - gm_ref).max() <= 1e-10
+    assert np.abs(gn.cpu().numpy() - gn_ref).max() <= 1e-10
