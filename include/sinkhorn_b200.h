@@ -99,6 +99,10 @@ typedef struct sinkhorn_problem_v1 {
 #define SINKHORN_FLAG_DENSE_GRID 128u    /* grid costs: dense on-the-fly sweeps, not separable */
 #define SINKHORN_FLAG_NO_FUSED 256u      /* shared costs: two half-sweeps per iteration, not the
                                             fused row->column pass (sweep_fused.cuh) */
+#define SINKHORN_FLAG_NO_GEMM 512u       /* large shared costs: tiled half-sweeps, not the two
+                                            fp32 GEMMs per iteration (sweep_gemm.cuh) */
+#define SINKHORN_FLAG_FORCE_GEMM 1024u   /* shared costs: the GEMM path even where the fused
+                                            pass applies (d <= 1024) */
 
 typedef struct sinkhorn_options_v1 {
   double lambda;          /* > 0, finite */

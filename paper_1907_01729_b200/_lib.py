@@ -36,6 +36,8 @@ FLAG_PERSISTENT = 32
 FLAG_TILED_ONLY = 64
 FLAG_DENSE_GRID = 128
 FLAG_NO_FUSED = 256
+FLAG_NO_GEMM = 512
+FLAG_FORCE_GEMM = 1024
 
 # every symbol include/sinkhorn_b200.h declares
 EXPORTED_SYMBOLS = (

@@ -6,9 +6,11 @@
 // synchronises when the reference's semantics need a host decision (the
 // convergence test every check_interval iterations when tolerance > 0) and once
 // at the end to report the status word.
+#include <cublas_v2.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -29,6 +31,7 @@
 #include "sweep_sep.cuh"
 #include "sweep_fused.cuh"
 #include "sweep_f64.cuh"
+#include "sweep_gemm.cuh"
 
 using namespace skb;
 
@@ -179,6 +182,8 @@ struct Layout {
   int lane_nsplit = 1, lane_nj = 1, lane_vec = 4;
   bool fused = false;             // shared cost, one fused row->column pass per iteration
   int fused_nct = 0, fused_maxseg = 0;
+  bool gemm = false;              // large shared cost: two fp32 GEMMs per iteration
+  size_t kc = 0, gx = 0, gs = 0, gt = 0, ga = 0, gvmax = 0, gvmax0 = 0, gfall = 0;
 };
 
 // Fused passes (sweep_fused.cuh): shared stored cost, both padded extents
@@ -197,17 +202,46 @@ bool fused_eligible(const sinkhorn_problem_v1& pr) {
 // Grid costs run the separable sweeps on lane-major buffers unless the dense
 // on-the-fly tiled sweeps are requested (SINKHORN_FLAG_DENSE_GRID).
 Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = false,
-                   bool fused = false) {
+                   bool fused = false, bool gemm = false) {
   Layout L;
   L.B = pr.B;
   L.d1 = pr.d1;
   L.d2 = pr.d2;
-  L.fused = fused && fused_eligible(pr);
+  L.gemm = gemm && pr.cost_kind == SINKHORN_COST_SHARED;
+  L.fused = !L.gemm && fused && fused_eligible(pr);
   L.sep = pr.cost_kind == SINKHORN_COST_GRID2D && !dense_grid;
-  L.tiled = !L.fused && (pr.cost_kind == SINKHORN_COST_SHARED ||
-                         (pr.cost_kind == SINKHORN_COST_GRID2D && dense_grid));
+  L.tiled = !L.fused && !L.gemm && (pr.cost_kind == SINKHORN_COST_SHARED ||
+                                    (pr.cost_kind == SINKHORN_COST_GRID2D && dense_grid));
   Carver c;
-  if (L.fused) {
+  if (L.gemm) {
+    // exact extents, lane-major: the GEMMs read K / KC row-major [d1][d2]
+    L.Bp = (int)pr.B;
+    L.D1p = (int)pr.d1;
+    L.D2p = (int)pr.d2;
+    L.sb1 = L.D1p;
+    L.si1 = 1;
+    L.sb2 = L.D2p;
+    L.si2 = 1;
+    L.kmat = c.take((size_t)pr.d1 * pr.d2 * 4);
+    L.kc = c.take((size_t)pr.d1 * pr.d2 * 4);
+    const size_t n1 = (size_t)L.B * L.D1p * 4, n2 = (size_t)L.B * L.D2p * 4;
+    L.f2 = c.take(n1);
+    L.g2[0] = c.take(n2);
+    L.g2[1] = c.take(n2);
+    L.l2mu = c.take(n1);
+    L.l2nu = c.take(n2);
+    L.mu = c.take(n1);
+    L.nu = c.take(n2);
+    L.gx = c.take(n2);
+    L.gt = c.take(n2);
+    L.gs = c.take(n1);
+    L.ga = c.take(n1);
+    L.gvmax = c.take((size_t)L.B * 4);
+    L.gvmax0 = c.take((size_t)L.B * 4);
+    L.gfall = c.take((size_t)L.B * L.D1p * 4);
+    L.e0 = c.take(64);
+    L.counter_count = 1;
+  } else if (L.fused) {
     // lane-major potentials [B][Dp], Dp = the cost rows' padded length
     L.Bp = (int)pr.B;
     L.D1p = (int)round_up(pr.d1, TILE_PAD);
@@ -316,6 +350,7 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
 size_t workspace_total(const sinkhorn_problem_v1& pr, int sms) {
   size_t t = make_layout(pr, sms).total;
   if (fused_eligible(pr)) t = std::max(t, make_layout(pr, sms, false, true).total);
+  if (pr.cost_kind == SINKHORN_COST_SHARED) t = std::max(t, make_layout(pr, sms, false, false, true).total);
   if (pr.cost_kind == SINKHORN_COST_GRID2D) t = std::max(t, make_layout(pr, sms, true).total);
   return t;
 }
@@ -472,6 +507,52 @@ int launch_tiled(const Layout& L, void* ws, const DeviceInfo& di, const TiledArg
                  const sinkhorn_problem_v1& pr, float lam, cudaStream_t st) {
   return pick_bt(pr.B) == 128 ? launch_tiled_pt<128, 64, kGrid, kMode>(L, ws, di, a, pr, lam, st)
                                : launch_tiled_pt<64, 64, kGrid, kMode>(L, ws, di, a, pr, lam, st);
+}
+
+// ---- cuBLAS, resolved at run time ---------------------------------------------
+// The GEMM path calls cublasSgemm (plain fp32 GEMMs).  The library is opened
+// on first use, so the C ABI has no link-time cuBLAS dependency and shares the
+// copy a host process (e.g. PyTorch) has already loaded.
+struct CublasApi {
+  decltype(&cublasCreate_v2) create = nullptr;
+  decltype(&cublasSetStream_v2) set_stream = nullptr;
+  decltype(&cublasSgemm_v2) sgemm = nullptr;
+  decltype(&cublasSetMathMode) set_math = nullptr;
+  bool ok = false;
+};
+
+const CublasApi& cublas_api() {
+  static CublasApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = nullptr;
+    for (const char* name : {"libcublas.so.12", "/usr/local/cuda/lib64/libcublas.so.12",
+                             "libcublas.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return;
+    api.create = reinterpret_cast<decltype(api.create)>(dlsym(h, "cublasCreate_v2"));
+    api.set_stream = reinterpret_cast<decltype(api.set_stream)>(dlsym(h, "cublasSetStream_v2"));
+    api.sgemm = reinterpret_cast<decltype(api.sgemm)>(dlsym(h, "cublasSgemm_v2"));
+    api.set_math = reinterpret_cast<decltype(api.set_math)>(dlsym(h, "cublasSetMathMode"));
+    api.ok = api.create && api.set_stream && api.sgemm;
+  });
+  return api;
+}
+
+cublasHandle_t cublas_handle(int dev) {
+  static thread_local cublasHandle_t handles[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!handles[dev]) {
+    const CublasApi& api = cublas_api();
+    if (!api.ok || api.create(&handles[dev]) != CUBLAS_STATUS_SUCCESS) return nullptr;
+    // full-precision fp32 products (SKB_GEMM_MATH=tf32 is a diagnostic, not parity-safe)
+    static const char* mm = getenv("SKB_GEMM_MATH");
+    if (api.set_math && mm && std::string(mm) == "tf32")
+      api.set_math(handles[dev], CUBLAS_TF32_TENSOR_OP_MATH);
+  }
+  return handles[dev];
 }
 
 // ---- the solver --------------------------------------------------------------
@@ -766,6 +847,94 @@ struct Solve {
     ++g_launches;
     CK(launch_pdl(&fused_merge_kernel, dim3((unsigned)((L.D2p + 511) / 512), (unsigned)pr.B),
                   dim3(256), 0, st, mp));
+    return 0;
+  }
+
+  // ---- GEMM path (sweep_gemm.cuh) ---------------------------------------------
+  // C (m x n, col-major) = op(A) B with A = K or KC stored row-major [d1][d2]
+  // (col-major d2 x d1).  rows: C = A X (m = d1, k = d2); cols: C = A^T a.
+  int gemm(bool rows, const float* A, const float* Bm, float* C) {
+    const CublasApi& api = cublas_api();
+    cublasHandle_t h = cublas_handle(di.dev);
+    if (!h) return fail(SINKHORN_STATUS_CUDA_ERROR, "cuBLAS unavailable for the GEMM path");
+    api.set_stream(h, st);
+    const float one = 1.f, zero = 0.f;
+    const int d1 = (int)pr.d1, d2 = (int)pr.d2, B = (int)pr.B;
+    cublasStatus_t e = rows ? api.sgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, d1, B, d2, &one, A, d2, Bm,
+                                        d2, &zero, C, d1)
+                            : api.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, d2, B, d1, &one, A, d2, Bm,
+                                        d1, &zero, C, d2);
+    g_launches += 1;
+    if (e != CUBLAS_STATUS_SUCCESS)
+      return fail(SINKHORN_STATUS_CUDA_ERROR, "cublasSgemm failed: " + std::to_string((int)e));
+    return 0;
+  }
+  int gemm_col(const float* vmax, const float* v_old, float* v_new, bool res) {
+    GemmColParams cp = {};
+    cp.B = (int)pr.B;
+    cp.d2 = (int)pr.d2;
+    cp.T = F(L.gt);
+    cp.vmax = vmax;
+    cp.v_old = v_old;
+    cp.v_new = v_new;
+    cp.l2nu = F(L.l2nu);
+    cp.nu = F(L.nu);
+    cp.res = res ? F(L.res) : nullptr;
+    cp.est_fail = est_fail;
+    cp.status = at<int>(ws, L.status);
+    ++g_launches;
+    gemm_col_kernel<<<grid_for((size_t)pr.B * pr.d2), 256, 0, st>>>(cp);
+    CK(cudaGetLastError());
+    return 0;
+  }
+  // the first column sweep: v_1 = l2nu - LSE_i(A2 + u_0), u_0 = 0 on the support
+  int gemm_first() {
+    ++g_launches;
+    gemm_first_a_kernel<<<grid_for((size_t)pr.B * pr.d1), 256, 0, st>>>(F(L.mu),
+                                                                       (size_t)pr.B * pr.d1, F(L.ga));
+    CK(cudaMemsetAsync(F(L.gvmax0), 0, (size_t)pr.B * 4, st));
+    if (int e = gemm(false, F(L.kmat), F(L.ga), F(L.gt))) return e;
+    return gemm_col(F(L.gvmax0), nullptr, F(L.g2[1]), false);
+  }
+  // iteration k from v_k = g2[cur]: X, S = K X, u and a, T = K^T a, v_{k+1}
+  int gemm_iteration(int cur, bool res) {
+    ++g_launches;
+    gemm_scale_kernel<<<(unsigned)pr.B, 1024, 0, st>>>(F(L.g2[cur]), (int)pr.d2, F(L.gx),
+                                                        F(L.gvmax));
+    CK(cudaGetLastError());
+    if (int e = gemm(true, F(L.kmat), F(L.gx), F(L.gs))) return e;
+    int* nfall = at<int>(ws, L.counters);
+    CK(cudaMemsetAsync(nfall, 0, 4, st));
+    GemmRowParams rp = {};
+    rp.B = (int)pr.B;
+    rp.d1 = (int)pr.d1;
+    rp.d2 = (int)pr.d2;
+    rp.S = F(L.gs);
+    rp.vmax = F(L.gvmax);
+    rp.l2mu = F(L.l2mu);
+    rp.mu = F(L.mu);
+    rp.u = F(L.f2);
+    rp.a = F(L.ga);
+    rp.nfall = nfall;
+    rp.fall = at<int>(ws, L.gfall);
+    rp.res = res ? F(L.res) : nullptr;
+    rp.status = at<int>(ws, L.status);
+    ++g_launches;
+    gemm_row_kernel<<<grid_for((size_t)pr.B * pr.d1), 256, 0, st>>>(rp);
+    ++g_launches;
+    gemm_row_fallback_kernel<<<(unsigned)di.sms, 256, 0, st>>>(rp, cost, F(L.g2[cur]),
+                                                                -kLog2e / lam);
+    CK(cudaGetLastError());
+    if (int e = gemm(false, F(L.kmat), F(L.ga), F(L.gt))) return e;
+    return gemm_col(F(L.gvmax), F(L.g2[cur]), F(L.g2[cur ^ 1]), res);
+  }
+  // E0 from the last iteration's X and a: sum_i a_i ((K o C) X)_i
+  int gemm_e0(float* out_cost) {
+    if (int e = gemm(true, F(L.kc), F(L.gx), F(L.gs))) return e;
+    ++g_launches;
+    gemm_e0_kernel<<<(unsigned)pr.B, 256, 0, st>>>(F(L.ga), F(L.gs), (int)pr.d1, out_cost,
+                                                   at<int>(ws, L.status));
+    CK(cudaGetLastError());
     return 0;
   }
 
@@ -1180,7 +1349,8 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   // one fused row->column pass per iteration for shared costs, unless the
   // problem takes the single-launch small solver (or this is the exact rerun)
   const bool cost_aligned = (reinterpret_cast<uintptr_t>(cost) & 15) == 0;
-  if (allow_est && !(op.flags & SINKHORN_FLAG_NO_FUSED) && fused_eligible(pr) &&
+  if (allow_est && !(op.flags & (SINKHORN_FLAG_NO_FUSED | SINKHORN_FLAG_FORCE_GEMM)) &&
+      fused_eligible(pr) &&
       (pr.cost_kind != SINKHORN_COST_PER_SAMPLE || cost_aligned)) {
     SmallParams sp0;
     int g0 = 0;
@@ -1188,6 +1358,17 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     bool small0 = false;
     if (int e = S.plan_small(sp0, g0, sm0, &small0)) return e;
     if (!small0) S.L = make_layout(pr, S.di.sms, false, true);
+  }
+  // large shared costs (and on request any shared cost): two GEMMs per iteration
+  if (allow_est && pr.cost_kind == SINKHORN_COST_SHARED && !S.L.fused &&
+      !(op.flags & SINKHORN_FLAG_NO_GEMM) &&
+      ((op.flags & SINKHORN_FLAG_FORCE_GEMM) || !fused_eligible(pr))) {
+    SmallParams sp0;
+    int g0 = 0;
+    size_t sm0 = 0;
+    bool small0 = false;
+    if (int e = S.plan_small(sp0, g0, sm0, &small0)) return e;
+    if (!small0) S.L = make_layout(pr, S.di.sms, false, false, true);
   }
   const Layout& L = S.L;
   if (ws_bytes < L.total || ws == nullptr)
@@ -1234,7 +1415,13 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     mask_potential_kernel<<<grid_for(n1), 256, 0, st>>>(S.F(L.f2), S.F(L.mu), n1);
     CK(cudaGetLastError());
   }
-  if (pr.cost_kind == SINKHORN_COST_SHARED) {
+  if (L.gemm) {
+    const size_t nk = (size_t)pr.d1 * pr.d2;
+    ++g_launches;
+    gemm_kernel_matrices<<<grid_for(nk), 256, 0, st>>>(cost, nk, (float)(-kLog2e / op.lambda),
+                                                        S.F(L.kmat), S.F(L.kc), status);
+    CK(cudaGetLastError());
+  } else if (pr.cost_kind == SINKHORN_COST_SHARED) {
     dim3 g((unsigned)((L.D2p + 31) / 32), (unsigned)((L.D1p + 31) / 32));
     ++g_launches;
     prep_cost_kernel<<<g, 256, 0, st>>>(cost, (int)pr.d1, (int)pr.d2, L.D1p, L.D2p,
@@ -1302,6 +1489,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   g_last_path = small     ? "small"
                 : persist ? "persistent"
                 : L.fused ? "fused"
+                : L.gemm  ? "gemm"
                 : L.tiled ? "tiled"
                 : L.sep   ? "separable"
                           : "lane";
@@ -1377,7 +1565,36 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
       if (int e = fused_loop()) return e;
     }
   }
-  for (int k = 1; !persist && !small && !L.fused && k <= op.max_iters; ++k) {
+  if (L.gemm && !small) {
+    if (int e = S.gemm_first()) return e;
+    cur = 1;
+    for (int k = 1; k <= op.max_iters; ++k) {
+      const bool last = (k == op.max_iters);
+      const bool check = checks && (k % op.check_interval == 0) && !last;
+      if (check || last) {
+        if (int e = S.zero_res()) return e;
+      }
+      if (int e = S.gemm_iteration(cur, check || last)) return e;
+      iters = k;
+      if (last) break;
+      if (check) {
+        ++g_launches;
+        reduce_max_kernel<<<1, 256, 0, st>>>(S.F(L.res), (int)pr.B, S.F(L.scratch));
+        CK(cudaGetLastError());
+        float hmax = 0.f;
+        int hstatus = 0;
+        CK(cudaMemcpyAsync(&hmax, S.F(L.scratch), 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&hstatus, status, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        double gmax = (hstatus != 0) ? NAN : (double)hmax;
+        if (g_reducer) gmax = g_reducer(gmax, g_reducer_user);
+        if (hstatus != 0) break;
+        if (gmax <= op.tolerance) break;   // converged: g2[cur] = log_v_k, X and a of iteration k
+      }
+      cur ^= 1;
+    }
+  }
+  for (int k = 1; !persist && !small && !L.fused && !L.gemm && k <= op.max_iters; ++k) {
     // estimate mode once the potentials have settled past the first sweeps
     S.est = allow_est && k >= kEstFromIter;
     if (!have_next) {
@@ -1417,7 +1634,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   if (timed) CK(cudaEventRecord(ev1, st));
   // ---- tail: residual + stable E0 in one column pass (batch.py:323-337) ----
   S.est = allow_est && iters >= kEstFromIter;
-  if (!small && !L.fused) {   // the fused passes already produced the tail terms
+  if (!small && !L.fused && !L.gemm) {   // the fused / GEMM passes produced the tail terms
     if (int e = S.tail(cur)) return e;
   }
   if (small) {
@@ -1428,7 +1645,9 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     const int nb = (int)((pr.B + 31) / 32);
     const long long sb = L.tiled ? 1 : L.D2p, sj = L.tiled ? L.Bp : 1;
     ++g_launches;
-    if (L.fused)   // per-row E0 terms of the fused passes
+    if (L.gemm) {
+      if (int e = S.gemm_e0(out_cost)) return e;
+    } else if (L.fused)   // per-row E0 terms of the fused passes
       e0_rows_finalize_kernel<<<(unsigned)((pr.B + 7) / 8), 256, 0, st>>>(
           S.F(L.e0), (int)pr.B, (int)pr.d1, L.D1p, out_cost, status);
     else           // per-column E0 terms of the tail pass
@@ -1451,7 +1670,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   int hstatus = 0;
   if (int e = S.read_status(&hstatus)) return e;
   static const bool no_rerun = getenv("SKB_NO_RERUN") != nullptr;   // diagnostics
-  if (allow_est && (L.tiled || L.fused) && !no_rerun) {
+  if (allow_est && (L.tiled || L.fused || L.gemm) && !no_rerun) {
     int hfail = 0;
     CK(cudaMemcpy(&hfail, S.est_fail, 4, cudaMemcpyDeviceToHost));
     if (hfail) {   // an estimate overshot: recompute the whole solve exactly

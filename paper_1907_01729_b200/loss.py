@@ -138,7 +138,7 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
           exact_max: bool = False, mufu_only: bool = False,
           persistent: bool = False, tiled_only: bool = False,
           dense_grid: bool = False, init_log_u=None, fused: bool = True,
-          fp64: bool = False) -> SolveResult:
+          fp64: bool = False, gemm: bool | None = None) -> SolveResult:
     """batch_forward (batch.py:264-349) on the GPU.
 
     mu (B, d1), nu (B, d2) histograms; cost a (d1, d2) tensor shared by all
@@ -151,6 +151,9 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
     of the fused row->column pass (sweep_fused.cuh).  ``fp64=True`` runs the
     reference's float64 iteration on the device (sweep_f64.cuh): float64
     outputs, reaches the reference's default tolerance 1e-9; path "fp64".
+    ``gemm``: None (default) takes the two-GEMM iteration (sweep_gemm.cuh) for
+    shared costs larger than the fused pass handles; True forces it for any
+    shared cost, False never takes it.
     """
     if fp64:
         return _solve_f64(mu, nu, cost, lam, max_iters, tolerance, check_interval, validate)
@@ -172,7 +175,8 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
         (_lib.FLAG_TIME_LOOP if time_loop else 0) | (_lib.FLAG_EXACT_MAX if exact_max else 0) | \
         (_lib.FLAG_MUFU_ONLY if mufu_only else 0) | (_lib.FLAG_PERSISTENT if persistent else 0) | \
         (_lib.FLAG_TILED_ONLY if tiled_only else 0) | (_lib.FLAG_DENSE_GRID if dense_grid else 0) | \
-        (0 if fused else _lib.FLAG_NO_FUSED)
+        (0 if fused else _lib.FLAG_NO_FUSED) | \
+        (_lib.FLAG_FORCE_GEMM if gemm else 0) | (_lib.FLAG_NO_GEMM if gemm is False else 0)
     out_cost = torch.empty(B, device=dev, dtype=torch.float32)
     log_u = torch.empty(B, d1, device=dev, dtype=torch.float32)
     log_v = torch.empty(B, d2, device=dev, dtype=torch.float32)

@@ -44,8 +44,9 @@ def _run_golden(name, cuda, cost=None, **kw):
 # (sweep_fused.cuh, shared costs with d <= 1024) or, with fused=False, the
 # stream-K tiled half-sweeps.  All of them must match.
 PATHS = [pytest.param({}, id="auto"),
-         pytest.param({"tiled_only": True, "fused": False}, id="tiled"),
-         pytest.param({"tiled_only": True}, id="fused")]
+         pytest.param({"tiled_only": True, "fused": False, "gemm": False}, id="tiled"),
+         pytest.param({"tiled_only": True}, id="fused"),
+         pytest.param({"tiled_only": True, "gemm": True}, id="gemm")]
 
 
 def _check_loss_and_grads(g, res, loss_rtol=LOSS_RTOL, grad_atol=GRAD_ATOL):
@@ -260,8 +261,8 @@ def test_estimate_mode_matches_exact_two_pass(name, cuda):
     c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
     args = (torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
             float(g["lam"]), int(g["max_iters"]), float(g["tol"]), int(g["check_interval"]))
-    fast = skb.solve(*args, tiled_only=True, fused=False)
-    exact = skb.solve(*args, exact_max=True, tiled_only=True, fused=False)
+    fast = skb.solve(*args, tiled_only=True, fused=False, gemm=False)
+    exact = skb.solve(*args, exact_max=True, tiled_only=True, fused=False, gemm=False)
     assert fast.iterations_run == exact.iterations_run
     rel = (fast.cost_e0.double() - exact.cost_e0.double()).abs() / exact.cost_e0.double().abs()
     assert float(rel.max()) <= 2e-6
@@ -365,7 +366,7 @@ def test_fused_pass_is_the_shared_cost_path_and_matches_tiled(cuda):
     args = (torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
             float(g["lam"]), int(g["max_iters"]), float(g["tol"]), int(g["check_interval"]))
     fused = skb.solve(*args, tiled_only=True)
-    tiled = skb.solve(*args, tiled_only=True, fused=False)
+    tiled = skb.solve(*args, tiled_only=True, fused=False, gemm=False)
     assert fused.path == "fused" and tiled.path == "tiled"
     _check_loss_and_grads(g, fused)
     rel = (fused.cost_e0.double() - tiled.cost_e0.double()).abs() / tiled.cost_e0.double()
@@ -489,3 +490,33 @@ def test_fp64_mode_reaches_the_reference_default_tolerance(cuda):
     assert gm.dtype == torch.float64
     assert np.abs(gm.cpu().numpy() - gm_ref).max() <= 1e-10
     assert np.abs(gn.cpu().numpy() - gn_ref).max() <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["config2_subset", "config5_pin4096", "config5_pin16384"])
+def test_gemm_path_matches_reference_and_tiled(name, cuda):
+    """Large shared costs run as two fp32 GEMMs per iteration (sweep_gemm.cuh):
+    parity with the reference and with the log-domain tiled half-sweeps."""
+    skb = _skb()
+    g = load_golden(name)
+    c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
+    args = (torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
+            float(g["lam"]), int(g["max_iters"]), float(g["tol"]), int(g["check_interval"]))
+    res = skb.solve(*args, tiled_only=True, gemm=True)
+    assert res.path == "gemm"
+    _check_loss_and_grads(g, res)
+    tiled = skb.solve(*args, tiled_only=True, fused=False, gemm=False)
+    rel = ((res.cost_e0.double() - tiled.cost_e0.double()).abs() / tiled.cost_e0.double()).max()
+    assert float(rel) <= 2e-6
+
+
+def test_gemm_path_underflowing_rows_fall_back_exactly(cuda):
+    """c/lambda >= 5000 (test_acceptance.py:175-201): K = 2^A2 underflows, so
+    rows fall back to the log domain (or the solve reruns exactly); the result
+    still matches the reference."""
+    skb = _skb()
+    g = load_golden("stability")
+    c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
+    res = skb.solve(torch.tensor(g["mu"], device=cuda), torch.tensor(g["nu"], device=cuda), c,
+                    float(g["lam"]), int(g["max_iters"]), float(g["tol"]),
+                    int(g["check_interval"]), tiled_only=True, gemm=True)
+    _check_loss_and_grads(g, res)

@@ -20,6 +20,7 @@ ap.add_argument("--dense-grid", action="store_true")
 ap.add_argument("--tiled-only", action="store_true")
 ap.add_argument("--mufu-only", action="store_true")
 ap.add_argument("--no-fused", action="store_true")
+ap.add_argument("--gemm", choices=["auto", "on", "off"], default="auto")
 ap.add_argument("--B", type=int, default=None, help="override the config's batch")
 a = ap.parse_args()
 cfg = dict(CONFIGS[a.config])
@@ -35,7 +36,8 @@ for _ in range(a.reps):
     t0 = time.perf_counter()
     r = skb.solve(mu, nu, cost, cfg["lam"], a.iters or cfg["iters"], 0.0, 10,
                   dense_grid=a.dense_grid, tiled_only=a.tiled_only, time_loop=True,
-                  mufu_only=a.mufu_only, fused=not a.no_fused)
+                  mufu_only=a.mufu_only, fused=not a.no_fused,
+                  gemm={"auto": None, "on": True, "off": False}[a.gemm])
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     skb.potentials_backward(r.log_u, r.log_v, cfg["lam"], up)
