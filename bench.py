@@ -198,6 +198,7 @@ def work_units(cfg: dict) -> float:
 KERNEL_OF_PATH = {
     "fused": "fused_pass_kernel + fused_merge_kernel (one fused row->column pass per iteration: "
              "row LSE, plan column partials, column update)",
+    "gemm": "cublasSgemm x2 (S = K X, T = K^T a) + gemm_scale/row/col kernels (one iteration)",
     "tiled": "tiled_sweep_kernel (stream-K online-LSE half-sweep)",
     "small": "small_solve_kernel (whole solve in one launch, cost in shared memory)",
     "persistent": "persistent_solve_kernel (cooperative whole loop)",
@@ -236,6 +237,21 @@ def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
     sms = 148
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
+    if path == "gemm":
+        # one launch group = one iteration = two fp32 GEMMs of 2*B*d1*d2 FLOP
+        # (S = K X, T = K^T a; sweep_gemm.cuh), run by cuBLAS SGEMM on the
+        # fp32 FMA pipe: 148 SM x 128 FFMA/clk x 2 FLOP (nominal, no measured figure)
+        flop = 4 * cells
+        achieved = flop / (sweep_ms * 1e-3) / 1e12
+        peak = sms * 128 * 2 * fmax * 1e6 / 1e12
+        out = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+               "frac": achieved / peak, "traffic": traffic,
+               "kernel": KERNEL_OF_PATH["gemm"],
+               "algorithmic_per_launch": f"{flop:.4g} FLOP (2 GEMMs of 2*B*d1*d2 per iteration)",
+               "peak_source": f"nominal: 148 SM x 128 FFMA/clk x 2 x sm_max_mhz {fmax:.0f}",
+               "ex2_equivalent_frac": 2 * cells / (sweep_ms * 1e-3) /
+               (sms * MUFU_PER_SM_CLK * fmax * 1e6)}
+        return out
     ex2 = cells                                            # one ex2 per cell per sweep
     if path == "fused":
         # one launch = one whole iteration; SURVEY 8(d) counts 2 ex2 per
@@ -451,7 +467,8 @@ def run_ours(args, cfg, world, rank, local):
     ms = sum(step_ms) / len(step_ms)
     step_stats = {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)}
     # row sharding has no per-solve loop timer: its half-sweep share is the step's
-    launches_per_iter = 1 if path == "fused" else 2   # fused: one pass (+ merge) per iteration
+    # fused: one pass (+ merge) per iteration; gemm: one GEMM pair per iteration
+    launches_per_iter = 1 if path in ("fused", "gemm") else 2
     sweep_ms = (statistics.median(loop_ms) if not row else statistics.median(step_ms)) / (
         launches_per_iter * iters)
     t = torch.tensor([ms, sweep_ms], device=dev, dtype=torch.float64)
