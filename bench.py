@@ -204,6 +204,8 @@ KERNEL_OF_PATH = {
     "persistent": "persistent_solve_kernel (cooperative whole loop)",
     "lane": "lane_col_kernel / lane_row_kernel (per-sample sweep)",
     "separable": "sep_sweep_kernel (separable grid LSE: two nested 1-D LSE-GEMMs per sweep)",
+    "row-sharded-gemm": "cuBLAS SGEMMs on this rank's kernel-matrix rows (K_r X, K_r^T a); "
+                        "whole step incl. the NCCL (max, sum) merge per column sweep",
     "row-sharded": "tiled_sweep_kernel through the half-sweep C ABI (this rank's cost rows; "
                    "whole step incl. NCCL merges per half-sweep)",
 }
@@ -237,7 +239,7 @@ def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
     sms = 148
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
-    if path == "gemm":
+    if path in ("gemm", "row-sharded-gemm"):
         # one launch group = one iteration = two fp32 GEMMs of 2*B*d1*d2 FLOP
         # (S = K X, T = K^T a; sweep_gemm.cuh), run by cuBLAS SGEMM on the
         # fp32 FMA pipe: 148 SM x 128 FFMA/clk x 2 FLOP (nominal, no measured figure)
@@ -246,7 +248,7 @@ def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
         peak = sms * 128 * 2 * fmax * 1e6 / 1e12
         out = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                "frac": achieved / peak, "traffic": traffic,
-               "kernel": KERNEL_OF_PATH["gemm"],
+               "kernel": KERNEL_OF_PATH[path],
                "algorithmic_per_launch": f"{flop:.4g} FLOP (2 GEMMs of 2*B*d1*d2 per iteration)",
                "peak_source": f"nominal: 148 SM x 128 FFMA/clk x 2 x sm_max_mhz {fmax:.0f}",
                "ex2_equivalent_frac": 2 * cells / (sweep_ms * 1e-3) /
@@ -420,7 +422,8 @@ def run_ours(args, cfg, world, rank, local):
         r0 = rank * rows
         cost = index_cost_rows(d, r0, rows, dev)
         mu_l = mu[:, r0:r0 + rows].contiguous()
-        backend = D.CudaShardBackend(cost)
+        backend = (D.CudaGemmShardBackend(cost) if args.row_backend == "gemm"
+                   else D.CudaShardBackend(cost))
     else:
         mu, nu, cost = make_inputs(cfg, dev, seed=1234 + rank)
     up = torch.ones(B, device=dev)
@@ -431,7 +434,8 @@ def run_ours(args, cfg, world, rank, local):
         if row:
             res = D.row_sharded_solve(mu_l, nu, backend, lam, iters, 0.0, 10, d1_total=d)
             D.row_sharded_backward(res.log_u, res.log_v, lam, up, d1_total=d)
-            res.loop_ms, res.path = -1.0, "row-sharded"
+            res.loop_ms, res.path = -1.0, ("row-sharded-gemm" if args.row_backend == "gemm"
+                                           else "row-sharded")
             return res
         res = skb.solve(mu, nu, cost, lam, iters, 0.0, 10, validate=True, time_loop=True)
         gm, gn = skb.potentials_backward(res.log_u, res.log_v, lam, up)
@@ -468,7 +472,7 @@ def run_ours(args, cfg, world, rank, local):
     step_stats = {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)}
     # row sharding has no per-solve loop timer: its half-sweep share is the step's
     # fused: one pass (+ merge) per iteration; gemm: one GEMM pair per iteration
-    launches_per_iter = 1 if path in ("fused", "gemm") else 2
+    launches_per_iter = 1 if path in ("fused", "gemm", "row-sharded-gemm") else 2
     sweep_ms = (statistics.median(loop_ms) if not row else statistics.median(step_ms)) / (
         launches_per_iter * iters)
     t = torch.tensor([ms, sweep_ms], device=dev, dtype=torch.float64)
@@ -629,6 +633,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--clock-interval-ms", type=int, default=500)
+    ap.add_argument("--row-backend", choices=["gemm", "lse"], default="gemm",
+                    help="row sharding: local fp32 GEMMs (default) or log-domain half-sweeps")
     ap.add_argument("--sharding", choices=["batch", "row"], default=None,
                     help="multi-GPU split (default: row for config 5 on N>1, else batch)")
     args = ap.parse_args()

@@ -121,6 +121,71 @@ class CudaShardBackend:
         return self._batch.e0_partial_log2(log_u_l, log_v, self.c, lam)
 
 
+class CudaGemmShardBackend:
+    """Per-shard arithmetic as fp32 GEMMs on the local rows' kernel matrix
+    (the GEMM iteration of csrc/sweep_gemm.cuh, restricted to rows I_r).
+
+    K_r = 2^(-c_r log2e / lam) <= 1 and, per lane, X_j = 2^(v_j - vmax):
+      row update:   u_i = log_mu_i - (vmax + log2 (K_r X)_i)          (local)
+      col partial:  (max, sum) = (umax_r, (K_r^T 2^(u - umax_r))_j)   (per lane shift)
+    so the cross-rank merge of the column sums is the same (max, sum-exp)
+    merge as the log-domain shards, with the max agreed once per lane.  A
+    call whose sums fall below 2^-60 (terms may have flushed) is redone by the
+    exact log-domain backend.  The GEMMs are cuBLAS SGEMMs through torch.
+    """
+
+    MIN = 2.0 ** -60
+
+    def __init__(self, cost_local: torch.Tensor):
+        self.c = cost_local.float().contiguous()
+        self._lam = None
+        self._exact = None
+
+    def _kernel(self, lam):
+        if self._lam != lam:
+            self.K = torch.exp2(self.c * (-1.0 / (lam * LN2)))
+            self.KC = self.K * self.c
+            self._lam = lam
+        return self.K
+
+    def exact(self):
+        if self._exact is None:
+            self._exact = CudaShardBackend(self.c)
+        return self._exact
+
+    def col_partial(self, log_u_l, lam):
+        K = self._kernel(lam)
+        u2 = log_u_l.float() / LN2
+        umax = torch.clamp(u2.amax(dim=1, keepdim=True), min=NEG_BIG)
+        a = torch.exp2(u2 - umax)
+        T = a @ K                                   # (B, d2) = sum_i a_i K_ij
+        if bool((T < self.MIN).any()):
+            return self.exact().col_partial(log_u_l, lam)
+        return umax.expand_as(T), T
+
+    def row_update(self, log_v, lam, log_mu_l):
+        K = self._kernel(lam)
+        v2 = log_v.float() / LN2
+        vmax = torch.clamp(v2.amax(dim=1, keepdim=True), min=NEG_BIG)
+        X = torch.exp2(v2 - vmax)
+        S = X @ K.t()                               # (B, d1_r) = sum_j K_ij X_j
+        if bool(((S < self.MIN) & ~torch.isneginf(log_mu_l)).any()):
+            return self.exact().row_update(log_v, lam, log_mu_l)
+        lse = (vmax + torch.log2(S)) * LN2
+        return torch.where(torch.isneginf(log_mu_l), log_mu_l, log_mu_l - lse)
+
+    def e0_partial(self, log_u_l, log_v, lam):
+        """Per lane log2 sum_{i local, j} P_ij c_ij = log2 sum_i a_i (KC X)_i."""
+        self._kernel(lam)
+        v2 = log_v.float() / LN2
+        vmax = torch.clamp(v2.amax(dim=1, keepdim=True), min=NEG_BIG)
+        X = torch.exp2(v2 - vmax)
+        SE = X @ self.KC.t()                        # (B, d1_r)
+        w = torch.exp2(log_u_l.float() / LN2 + vmax)  # a_i = 2^(u_i + vmax)
+        tot = (w * SE).double().sum(dim=1)
+        return torch.where(tot > 0, torch.log2(tot), torch.full_like(tot, -math.inf)).float()
+
+
 def _merge_lse(m: torch.Tensor, s: torch.Tensor, group) -> torch.Tensor:
     """All-rank OnlineLseAccumulator.merge of (max, sum) pairs in log base 2 -> natural LSE."""
     M = m.clone()
@@ -215,7 +280,7 @@ def row_sharded_backward(log_u_local, log_v, lam: float, upstream, group=None,
 
 
 __all__ = [
-    "CudaShardBackend", "batch_sharded_solve", "gather_lane_values", "global_max",
+    "CudaGemmShardBackend", "CudaShardBackend", "batch_sharded_solve", "gather_lane_values", "global_max",
     "global_residual_reducer",
     "row_sharded_backward", "row_sharded_solve",
 ]

@@ -91,7 +91,7 @@ def _problem(seed=3, B=3, d1=20, d2=15):
     return mu, nu, c
 
 
-def _row_sharded(rank, world, tol=0.0, iters=40, lam=0.3, zero=False):
+def _row_sharded(rank, world, tol=0.0, iters=40, lam=0.3, zero=False, gemm=False):
     from paper_1907_01729_b200 import distributed as D
 
     mu, nu, c = _problem()
@@ -101,7 +101,8 @@ def _row_sharded(rank, world, tol=0.0, iters=40, lam=0.3, zero=False):
     d1 = mu.shape[1]
     lo, hi = rank * d1 // world, (rank + 1) * d1 // world
     res = D.row_sharded_solve(torch.from_numpy(mu[:, lo:hi].copy()), torch.from_numpy(nu),
-                              OracleShardBackend(c[lo:hi]), lam, iters, tol, 10)
+                              D.CudaGemmShardBackend(torch.from_numpy(c[lo:hi].copy())) if gemm
+                              else OracleShardBackend(c[lo:hi]), lam, iters, tol, 10)
     out = {"cost": res.cost_e0.numpy(), "log_u": res.log_u.numpy(), "log_v": res.log_v.numpy(),
            "iters": res.iterations_run, "res": res.residuals.numpy(), "lo": lo}
     up = torch.from_numpy(np.array([0.5, -1.0, 2.0]))
@@ -171,3 +172,20 @@ def test_batch_sharded_collectives():
         np.testing.assert_array_equal(vals, [0, 1, 2, 10, 11, 12, 13])
         assert gmax == 1.5
         assert nanmax == math.inf     # NaN on any rank never converges
+
+
+def _row_sharded_gemm(rank, world):
+    return _row_sharded(rank, world, gemm=True)
+
+
+def test_row_sharded_gemm_shards_match_unsharded_oracle():
+    """CudaGemmShardBackend's arithmetic (plain torch fp32 GEMMs, here on CPU
+    tensors) through the same two-rank collective logic: fp32 parity."""
+    outs = _spawn(_row_sharded_gemm)
+    mu, nu, c = _problem()
+    ref = orc.batch_forward(mu, nu, c, 0.3, 40, 0.0)
+    log_u, r0, r1 = _assemble(outs)
+    np.testing.assert_allclose(r0["cost"], ref.cost_e0, rtol=1e-5)
+    np.testing.assert_allclose(r1["cost"], ref.cost_e0, rtol=1e-5)
+    np.testing.assert_allclose(log_u, ref.log_u, atol=1e-4)
+    np.testing.assert_allclose(r0["log_v"], ref.log_v, atol=1e-4)

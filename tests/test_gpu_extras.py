@@ -86,16 +86,19 @@ def nccl_world1(cuda):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["config5_pin4096", "rect_37x53", "config1_tol"])
-def test_row_sharded_solve_on_the_device(name, nccl_world1, cuda):
-    """row_sharded_solve + CudaShardBackend (NCCL, one rank) against the reference."""
+@pytest.mark.parametrize("backend", ["lse", "gemm"])
+@pytest.mark.parametrize("name", ["config5_pin4096", "rect_37x53", "config1_tol", "stability"])
+def test_row_sharded_solve_on_the_device(name, backend, nccl_world1, cuda):
+    """row_sharded_solve (NCCL, one rank) with the log-domain half-sweep shards
+    and with the GEMM shards, against the reference."""
     from paper_1907_01729_b200 import distributed as D
 
     g = load_golden(name)
     c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
     mu = torch.tensor(g["mu"], dtype=torch.float32, device=cuda)
     nu = torch.tensor(g["nu"], dtype=torch.float32, device=cuda)
-    res = D.row_sharded_solve(mu, nu, D.CudaShardBackend(c), float(g["lam"]), int(g["max_iters"]),
+    shard = D.CudaGemmShardBackend(c) if backend == "gemm" else D.CudaShardBackend(c)
+    res = D.row_sharded_solve(mu, nu, shard, float(g["lam"]), int(g["max_iters"]),
                               float(g["tol"]), int(g["check_interval"]))
     assert res.iterations_run == int(g["iterations_run"])
     rel = np.abs(res.cost_e0.double().cpu().numpy() - g["cost_e0"]) / g["cost_e0"]
