@@ -176,10 +176,13 @@ class CudaGemmShardBackend:
 
     def e0_partial(self, log_u_l, log_v, lam):
         """Per lane log2 sum_{i local, j} P_ij c_ij = log2 sum_i a_i (KC X)_i."""
-        self._kernel(lam)
+        K = self._kernel(lam)
         v2 = log_v.float() / LN2
         vmax = torch.clamp(v2.amax(dim=1, keepdim=True), min=NEG_BIG)
         X = torch.exp2(v2 - vmax)
+        # rows whose terms may have flushed: the exact log-domain partial
+        if bool(((X @ K.t() < self.MIN) & ~torch.isneginf(log_u_l)).any()):
+            return self.exact().e0_partial(log_u_l, log_v, lam)
         SE = X @ self.KC.t()                        # (B, d1_r)
         w = torch.exp2(log_u_l.float() / LN2 + vmax)  # a_i = 2^(u_i + vmax)
         tot = (w * SE).double().sum(dim=1)
