@@ -42,6 +42,9 @@ thread_local unsigned long long g_launches = 0;   // kernels this thread launche
 thread_local float g_last_loop_ms = -1.f;         // last timed iteration loop (ms)
 thread_local const char* g_last_path = "none";    // solver path of the last forward
 thread_local unsigned long long g_exact_reruns = 0;  // solves redone without estimates
+// non-check fused iterations of shared costs as the two-GEMM block pass
+// (SKB_FUSED_ROWS=1: the warp-per-row linear pass instead; diagnostics / A-B)
+const bool g_use_fgemm = getenv("SKB_FUSED_ROWS") == nullptr;
 // Optional cross-rank agreement on the stopping test (batch-sharded solves).
 thread_local sinkhorn_residual_reducer_v1 g_reducer = nullptr;
 thread_local void* g_reducer_user = nullptr;
@@ -182,6 +185,7 @@ struct Layout {
   int lane_nsplit = 1, lane_nj = 1, lane_vec = 4;
   bool fused = false;             // shared cost, one fused row->column pass per iteration
   int fused_nct = 0, fused_maxseg = 0;
+  int fg_nct = 0, fg_maxseg = 0;  // the two-GEMM block pass (units: 16 lanes x 16 rows)
   bool gemm = false;              // large shared cost: two fp32 GEMMs per iteration
   size_t kc = 0, gx = 0, gs = 0, gt = 0, ga = 0, gvmax = 0, gvmax0 = 0, gfall = 0;
 };
@@ -275,6 +279,14 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     const long long per = (U + L.fused_nct - 1) / L.fused_nct;
     L.fused_maxseg = (int)((per - 1) / pr.d1 + 2);
     L.part_bytes = (size_t)L.fused_nct * L.fused_maxseg * nw * L.D2p * 4;
+    if (pr.cost_kind == SINKHORN_COST_SHARED) {   // fgemm_pass_kernel's pieces
+      const long long Ufg = ((pr.B + kFgLanes - 1) / kFgLanes) * (L.D1p / kFgRows);
+      L.fg_nct = (int)std::max<long long>(1, std::min<long long>(sms, Ufg));
+      const long long pfg = (Ufg + L.fg_nct - 1) / L.fg_nct;
+      L.fg_maxseg = (int)((pfg - 1) / (L.D1p / kFgRows) + 2);
+      L.part_bytes = std::max(L.part_bytes,
+                              (size_t)L.fg_nct * L.fg_maxseg * kFgLanes * L.D2p * 4);
+    }
     L.part = c.take(L.part_bytes);
     L.counter_count = 1;
   } else if (L.tiled) {
@@ -770,6 +782,24 @@ struct Solve {
       return fp.e0 != nullptr ? launch_fused_ps_t<NQ, true>(fp) : launch_fused_ps_t<NQ, false>(fp);
     }
   }
+  template <int NQ>
+  int launch_fgemm(const FusedParams& fp, int nrb) {
+    if constexpr (NQ > kFusedMaxChunks) {
+      return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
+    } else {
+      if (fp.nq != NQ) return launch_fgemm<NQ + 1>(fp, nrb);
+      auto kern = &fgemm_pass_kernel<NQ>;
+      static bool attr = false;
+      const size_t smem = fg_smem_bytes<NQ>();
+      if (!attr) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+      }
+      ++g_launches;
+      CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(kFgThreads), smem, st, fp, nrb));
+      return 0;
+    }
+  }
   template <bool kRowOnly>
   int launch_fused(const FusedParams& fp) {
     return launch_fused_nq<1, kRowOnly>(fp);
@@ -824,16 +854,28 @@ struct Solve {
     fp.part = F(L.part);
     fp.res = (res || e0) ? F(L.res) : nullptr;   // kTail: residual and E0 together
     fp.e0 = (res || e0) ? F(L.e0) : nullptr;
-    if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE) {
+    // non-check iterations of shared costs: the two-GEMM block pass (units are
+    // 16 lanes x 16 rows; the merge walks the same unit space)
+    const bool fg = pr.cost_kind == SINKHORN_COST_SHARED && !(res || e0) && g_use_fgemm;
+    int merge_nw = nw, merge_rows = (int)pr.d1;
+    if (fg) {
+      const int nrb = L.D1p / kFgRows;
+      fp.U = ((pr.B + kFgLanes - 1) / kFgLanes) * (long long)nrb;
+      fp.nct = L.fg_nct;
+      fp.maxseg = L.fg_maxseg;
+      merge_nw = kFgLanes;
+      merge_rows = nrb;
+      if (int e = launch_fgemm<1>(fp, nrb)) return e;
+    } else if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE) {
       if (int e = launch_fused_ps<1>(fp)) return e;
     } else {
       if (int e = launch_fused<false>(fp)) return e;
     }
     FusedMergeParams mp = {};
     mp.B = (int)pr.B;
-    mp.nrows = (int)pr.d1;
+    mp.nrows = merge_rows;
     mp.rowlen = L.D2p;
-    mp.nw = nw;
+    mp.nw = merge_nw;
     mp.U = fp.U;
     mp.nct = fp.nct;
     mp.maxseg = fp.maxseg;

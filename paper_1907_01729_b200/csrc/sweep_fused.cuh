@@ -719,6 +719,192 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
   pdl_launch_dependents();
 }
 
+// ---------------------------------------------------------------------------
+// The linear rows as two register-blocked GEMMs per block of 16 cost rows
+// (fgemm_pass_kernel, the default for the non-check iterations of shared
+// costs with d <= 1024).  A CTA owns 16 lanes (b) and walks blocks of 16 rows
+// (i) of K = 2^A2, staged in shared memory (cp.async.bulk, double buffered):
+//   S[i][b] = sum_j K[i][j] X[b][j]      16 x 16 outputs, the j range split
+//                                        over 16 thread slices (4x4 blocking)
+//   u, a[i][b] = mu / S                   one thread per output
+//   T[b][j] += sum_i K[i][j] a[i][b]      every thread 4 lanes x NQ columns,
+//                                        held in registers for the segment
+// X[b][j] T[b][j] = sum_i P_ij is the plan column partial the merge kernel
+// sums, exactly as the warp-per-row pass writes it.  There are no per-row shuffle reductions, so
+// the loop is a plain FFMA2 / LDS.128 stream.  A row block with any S below
+// 2^-60 (terms may have flushed) flags the solve for the exact rerun.
+constexpr int kFgRows = 16;     // cost rows per block
+constexpr int kFgLanes = 16;    // lanes per CTA
+constexpr int kFgThreads = 256;
+
+__host__ __device__ constexpr int fg_stride(int nq) { return nq * 64 + 4; }   // padded row (banks)
+
+template <int NQ>
+__host__ __device__ constexpr size_t fg_smem_bytes() {
+  return (size_t)(3 * kFgRows * fg_stride(NQ)            // X (16 lanes) + two K blocks
+                  + 16 * kFgRows * kFgLanes               // GEMM-1 slice partials
+                  + kFgRows * kFgLanes + kFgLanes) * 4     // a, vmax
+         + 2 * 8;                                         // mbarriers
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedParams p, int nrb) {
+  extern __shared__ __align__(128) unsigned char fsm[];
+  constexpr int STR = fg_stride(NQ);
+  constexpr int DP = NQ * 64;
+  float* Xs = reinterpret_cast<float*>(fsm);               // [16 lanes][STR]
+  float* Ks = Xs + kFgLanes * STR;                          // [2][16 rows][STR]
+  float* Sred = Ks + 2 * kFgRows * STR;                     // [16 slices][256]
+  float* As = Sred + 16 * kFgRows * kFgLanes;               // [16 rows][16 lanes]
+  float* Vm = As + kFgRows * kFgLanes;                      // [16]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Vm + kFgLanes);
+  const int t = threadIdx.x, warp = warp_id(), lane = lane_id();
+  const long long u0 = fused_seg_start(p.U, p.nct, blockIdx.x);
+  const long long u1 = fused_seg_start(p.U, p.nct, blockIdx.x + 1);
+  const int n = (int)(u1 - u0);
+  const uint32_t row_bytes = DP * 4u;
+
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  // stream position k -> row block (u0 + k) % nrb; thread 0 issues its 16 row copies
+  auto issue = [&](int k) {
+    const int rb = (int)((u0 + k) % nrb);
+    const int st = k & 1;
+    mbar_arrive_expect_tx(&bar[st], kFgRows * row_bytes);
+    for (int r = 0; r < kFgRows; ++r)
+      bulk_g2s(Ks + (st * kFgRows + r) * STR, p.a2 + (size_t)(rb * kFgRows + r) * DP, row_bytes,
+               &bar[st]);
+  };
+  if (t == 0) {
+    issue(0);
+    if (n > 1) issue(1);
+  }
+  pdl_wait();
+  const bool dead = p.status != nullptr && *p.status != 0;
+
+  // GEMM-1 roles: slice of the j range, 4 rows, 4 lanes
+  const int ks = t >> 4, rq = (t >> 2) & 3, lq = t & 3;
+  // GEMM-2 roles: 4 lanes, columns jc + 64 k
+  const int l4 = t >> 6, jc = t & 63;
+  int k = 0;   // stream position
+  long long u = u0;
+  const int g_first = (int)(u0 / nrb);
+  while (u < u1) {
+    const int g = (int)(u / nrb);
+    const long long seg_end = (long long)(g + 1) * nrb < u1 ? (long long)(g + 1) * nrb : u1;
+    const int b0 = g * kFgLanes;
+    // this group's potentials as X = 2^(v - vmax) (warp w: lanes 2w, 2w+1)
+    __syncthreads();
+    for (int h = 0; h < 2; ++h) {
+      const int l = warp * 2 + h, b = b0 + l;
+      const float* v = p.x + (size_t)b * DP;
+      float m = kNegBig;
+      if (b < p.B)
+        for (int j = lane; j < DP; j += 32) m = fmaxf(m, v[j]);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+      for (int j = lane; j < DP; j += 32) Xs[l * STR + j] = b < p.B ? ex2(v[j] - m) : 0.f;
+      if (lane == 0) Vm[l] = m;
+    }
+    uint64_t T[2][NQ];   // [lane pair][column k]: lanes 4 l4 + {0,1} and {2,3}
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) T[0][q] = T[1][q] = 0ull;
+    __syncthreads();
+
+    for (; u < seg_end; ++u, ++k) {
+      const int st = k & 1;
+      const int rb = (int)(u - (long long)g * nrb);
+      mbar_wait(&bar[st], (uint32_t)((k >> 1) & 1));
+      const float* Kb = Ks + st * kFgRows * STR;
+      // ---- GEMM 1: partial S over this thread's j slice, 4 rows x 4 lanes
+      float acc[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc[r][l] = 0.f;
+      const int j0 = ks * (DP / 16);
+#pragma unroll
+      for (int jj = 0; jj < DP / 16; jj += 4) {
+        float4 kr[4], xl[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          kr[r] = *reinterpret_cast<const float4*>(Kb + (rq * 4 + r) * STR + j0 + jj);
+#pragma unroll
+        for (int l = 0; l < 4; ++l)
+          xl[l] = *reinterpret_cast<const float4*>(Xs + (lq * 4 + l) * STR + j0 + jj);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            acc[r][l] = fmaf(kr[r].x, xl[l].x, acc[r][l]);
+            acc[r][l] = fmaf(kr[r].y, xl[l].y, acc[r][l]);
+            acc[r][l] = fmaf(kr[r].z, xl[l].z, acc[r][l]);
+            acc[r][l] = fmaf(kr[r].w, xl[l].w, acc[r][l]);
+          }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) Sred[ks * 256 + (rq * 4 + r) * 16 + lq * 4 + l] = acc[r][l];
+      __syncthreads();
+      // ---- row epilogue: thread t -> (row i, lane b)
+      {
+        const int r = t >> 4, l = t & 15;
+        float S = 0.f;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) S += Sred[q * 256 + t];   // ascending slices
+        const int i = rb * kFgRows + r, b = b0 + l;
+        float a = 0.f;
+        if (i < p.nrows && b < p.B && !dead) {
+          const size_t o = (size_t)b * p.ldo + i;
+          const float mg = p.marg[o];
+          if (mg > 0.f && !(S >= kFusedEstLo)) *p.est_fail = 1;   // flushed terms: exact rerun
+          p.out[o] = sweep_out(p.target[o], Vm[l] + lg2(S));
+          a = mg > 0.f ? mg * rcp_approx(S) : 0.f;
+        }
+        As[r * 16 + l] = a;
+      }
+      __syncthreads();
+      // ---- GEMM 2: T[lane][j] += sum_r K[r][j] a[r][lane]
+#pragma unroll 4
+      for (int r = 0; r < kFgRows; ++r) {
+        const float4 a4 = *reinterpret_cast<const float4*>(As + r * 16 + l4 * 4);
+        const uint64_t a01 = pk2(a4.x, a4.y), a23 = pk2(a4.z, a4.w);
+        const float* kr = Kb + r * STR + jc;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const float kv = kr[64 * q];
+          const uint64_t kk = pk2(kv, kv);
+          ffma2_acc(T[0][q], kk, a01);
+          ffma2_acc(T[1][q], kk, a23);
+        }
+      }
+      __syncthreads();   // every thread is done with this K block and with As / Sred
+      if (t == 0 && k + 2 < n) {
+        fence_proxy_async();
+        issue(k + 2);
+      }
+    }
+    // plan column partials of this segment, part[cta][seg][lane][j] =
+    // X[lane][j] * T[lane][j] = sum_i a_i K_ij X_j (the plan entries' sum)
+    float* dst = p.part + ((size_t)blockIdx.x * p.maxseg + (g - g_first)) * kFgLanes * (size_t)DP;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int j = jc + 64 * q;
+      const int l = l4 * 4;
+      dst[(size_t)(l + 0) * DP + j] = lo2(T[0][q]) * Xs[(l + 0) * STR + j];
+      dst[(size_t)(l + 1) * DP + j] = hi2(T[0][q]) * Xs[(l + 1) * STR + j];
+      dst[(size_t)(l + 2) * DP + j] = lo2(T[1][q]) * Xs[(l + 2) * STR + j];
+      dst[(size_t)(l + 3) * DP + j] = hi2(T[1][q]) * Xs[(l + 3) * STR + j];
+    }
+  }
+  pdl_launch_dependents();
+}
+
 // Column update from the plan partials: colsum_j = sum over the CTAs that
 // covered lane b's group (ascending), v'_j = v_j + l2nu_j - log2(colsum_j),
 // column residual |colsum_j - nu_j|.  grid (ceil(rowlen / 256), B).
