@@ -741,7 +741,8 @@ __host__ __device__ constexpr int fg_stride(int nq) { return nq * 64 + 4; }   //
 
 template <int NQ>
 __host__ __device__ constexpr size_t fg_smem_bytes() {
-  return (size_t)(3 * kFgRows * fg_stride(NQ)            // X (16 lanes) + two K blocks
+  return (size_t)(kFgLanes / 2 * (2 * NQ * 64 + 4)       // X: 8 interleaved lane pairs
+                  + 2 * kFgRows * fg_stride(NQ)            // two K blocks
                   + 16 * kFgRows * kFgLanes               // GEMM-1 slice partials
                   + kFgRows * kFgLanes + kFgLanes) * 4     // a, vmax
          + 2 * 8;                                         // mbarriers
@@ -751,9 +752,10 @@ template <int NQ>
 __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedParams p, int nrb) {
   extern __shared__ __align__(128) unsigned char fsm[];
   constexpr int STR = fg_stride(NQ);
+  constexpr int XSTR = 2 * NQ * 64 + 4;   // a lane pair's interleaved row (+4: banks)
   constexpr int DP = NQ * 64;
   float* Xs = reinterpret_cast<float*>(fsm);               // [16 lanes][STR]
-  float* Ks = Xs + kFgLanes * STR;                          // [2][16 rows][STR]
+  float* Ks = Xs + kFgLanes / 2 * XSTR;                     // [2][16 rows][STR]
   float* Sred = Ks + 2 * kFgRows * STR;                     // [16 slices][256]
   float* As = Sred + 16 * kFgRows * kFgLanes;               // [16 rows][16 lanes]
   float* Vm = As + kFgRows * kFgLanes;                      // [16]
@@ -807,7 +809,10 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
         for (int j = lane; j < DP; j += 32) m = fmaxf(m, v[j]);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-      for (int j = lane; j < DP; j += 32) Xs[l * STR + j] = b < p.B ? ex2(v[j] - m) : 0.f;
+      // lane pairs interleaved: Xs[l / 2][j][l % 2], so GEMM 1 multiplies a K value
+      // into two lanes with one FFMA2
+      for (int j = lane; j < DP; j += 32)
+        Xs[(l >> 1) * XSTR + 2 * j + (l & 1)] = b < p.B ? ex2(v[j] - m) : 0.f;
       if (lane == 0) Vm[l] = m;
     }
     uint64_t T[2][NQ];   // [lane pair][column k]: lanes 4 l4 + {0,1} and {2,3}
@@ -820,36 +825,43 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
       const int rb = (int)(u - (long long)g * nrb);
       mbar_wait(&bar[st], (uint32_t)((k >> 1) & 1));
       const float* Kb = Ks + st * kFgRows * STR;
-      // ---- GEMM 1: partial S over this thread's j slice, 4 rows x 4 lanes
-      float acc[4][4];
+      // ---- GEMM 1: partial S over this thread's j slice, 4 rows x 2 lane pairs
+      uint64_t acc[4][2];
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int l = 0; l < 4; ++l) acc[r][l] = 0.f;
+      for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = 0ull;
       const int j0 = ks * (DP / 16);
+      const float* xp0 = Xs + (lq * 2) * XSTR + 2 * j0;       // lanes 4 lq, 4 lq + 1
+      const float* xp1 = Xs + (lq * 2 + 1) * XSTR + 2 * j0;   // lanes 4 lq + 2, 4 lq + 3
 #pragma unroll
       for (int jj = 0; jj < DP / 16; jj += 4) {
-        float4 kr[4], xl[4];
+        float4 kr[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
           kr[r] = *reinterpret_cast<const float4*>(Kb + (rq * 4 + r) * STR + j0 + jj);
+        // (x_l(j), x_l+1(j)) pairs for j = jj .. jj + 3
+        const float4 xa = *reinterpret_cast<const float4*>(xp0 + 2 * jj);
+        const float4 xb = *reinterpret_cast<const float4*>(xp0 + 2 * jj + 4);
+        const float4 xc = *reinterpret_cast<const float4*>(xp1 + 2 * jj);
+        const float4 xd = *reinterpret_cast<const float4*>(xp1 + 2 * jj + 4);
+        const uint64_t p0[4] = {pk2(xa.x, xa.y), pk2(xa.z, xa.w), pk2(xb.x, xb.y), pk2(xb.z, xb.w)};
+        const uint64_t p1[4] = {pk2(xc.x, xc.y), pk2(xc.z, xc.w), pk2(xd.x, xd.y), pk2(xd.z, xd.w)};
 #pragma unroll
-        for (int l = 0; l < 4; ++l)
-          xl[l] = *reinterpret_cast<const float4*>(Xs + (lq * 4 + l) * STR + j0 + jj);
+        for (int r = 0; r < 4; ++r) {
+          const float kv[4] = {kr[r].x, kr[r].y, kr[r].z, kr[r].w};
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int l = 0; l < 4; ++l) {
-            acc[r][l] = fmaf(kr[r].x, xl[l].x, acc[r][l]);
-            acc[r][l] = fmaf(kr[r].y, xl[l].y, acc[r][l]);
-            acc[r][l] = fmaf(kr[r].z, xl[l].z, acc[r][l]);
-            acc[r][l] = fmaf(kr[r].w, xl[l].w, acc[r][l]);
+          for (int e = 0; e < 4; ++e) {
+            const uint64_t kk = pk2(kv[e], kv[e]);
+            ffma2_acc(acc[r][0], kk, p0[e]);
+            ffma2_acc(acc[r][1], kk, p1[e]);
           }
+        }
       }
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int l = 0; l < 4; ++l) Sred[ks * 256 + (rq * 4 + r) * 16 + lq * 4 + l] = acc[r][l];
+      for (int r = 0; r < 4; ++r) {
+        float* o = Sred + ks * 256 + (rq * 4 + r) * 16 + lq * 4;
+        *reinterpret_cast<float4*>(o) = make_float4(lo2(acc[r][0]), hi2(acc[r][0]), lo2(acc[r][1]),
+                                                    hi2(acc[r][1]));
+      }
       __syncthreads();
       // ---- row epilogue: thread t -> (row i, lane b)
       {
@@ -896,10 +908,12 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
     for (int q = 0; q < NQ; ++q) {
       const int j = jc + 64 * q;
       const int l = l4 * 4;
-      dst[(size_t)(l + 0) * DP + j] = lo2(T[0][q]) * Xs[(l + 0) * STR + j];
-      dst[(size_t)(l + 1) * DP + j] = hi2(T[0][q]) * Xs[(l + 1) * STR + j];
-      dst[(size_t)(l + 2) * DP + j] = lo2(T[1][q]) * Xs[(l + 2) * STR + j];
-      dst[(size_t)(l + 3) * DP + j] = hi2(T[1][q]) * Xs[(l + 3) * STR + j];
+      const float2 x01 = *reinterpret_cast<const float2*>(Xs + (l >> 1) * XSTR + 2 * j);
+      const float2 x23 = *reinterpret_cast<const float2*>(Xs + ((l >> 1) + 1) * XSTR + 2 * j);
+      dst[(size_t)(l + 0) * DP + j] = lo2(T[0][q]) * x01.x;
+      dst[(size_t)(l + 1) * DP + j] = hi2(T[0][q]) * x01.y;
+      dst[(size_t)(l + 2) * DP + j] = lo2(T[1][q]) * x23.x;
+      dst[(size_t)(l + 3) * DP + j] = hi2(T[1][q]) * x23.y;
     }
   }
   pdl_launch_dependents();
