@@ -788,12 +788,12 @@ struct Solve {
       return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
     } else {
       if (fp.nq != NQ) return launch_fgemm<NQ + 1>(fp, nrb);
-      auto kern = &fgemm_pass_kernel<NQ>;
-      static bool attr = false;
+      auto kern = fp.e0 != nullptr ? &fgemm_pass_kernel<NQ, true> : &fgemm_pass_kernel<NQ, false>;
+      static bool attr[2] = {false, false};
       const size_t smem = fg_smem_bytes<NQ>();
-      if (!attr) {
+      if (!attr[fp.e0 != nullptr]) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+        attr[fp.e0 != nullptr] = true;
       }
       ++g_launches;
       CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(kFgThreads), smem, st, fp, nrb));
@@ -856,13 +856,14 @@ struct Solve {
     fp.e0 = (res || e0) ? F(L.e0) : nullptr;
     // non-check iterations of shared costs: the two-GEMM block pass (units are
     // 16 lanes x 16 rows; the merge walks the same unit space)
-    const bool fg = pr.cost_kind == SINKHORN_COST_SHARED && !(res || e0) && g_use_fgemm;
+    const bool fg = pr.cost_kind == SINKHORN_COST_SHARED && g_use_fgemm;
     int merge_nw = nw, merge_rows = (int)pr.d1;
     if (fg) {
       const int nrb = L.D1p / kFgRows;
       fp.U = ((pr.B + kFgLanes - 1) / kFgLanes) * (long long)nrb;
       fp.nct = L.fg_nct;
       fp.maxseg = L.fg_maxseg;
+      fp.a2 = F(L.kmat);   // the block pass streams K (its tail recovers c from K)
       merge_nw = kFgLanes;
       merge_rows = nrb;
       if (int e = launch_fgemm<1>(fp, nrb)) return e;

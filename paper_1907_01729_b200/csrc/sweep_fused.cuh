@@ -741,14 +741,17 @@ __host__ __device__ constexpr int fg_stride(int nq) { return nq * 64 + 4; }   //
 
 template <int NQ>
 __host__ __device__ constexpr size_t fg_smem_bytes() {
-  return (size_t)(kFgLanes / 2 * (2 * NQ * 64 + 4)       // X: 8 interleaved lane pairs
+  return (size_t)(kFgLanes / 2 * (2 * NQ * 64 + 4)        // X: 8 interleaved lane pairs
                   + 2 * kFgRows * fg_stride(NQ)            // two K blocks
                   + 16 * kFgRows * kFgLanes               // GEMM-1 slice partials
                   + kFgRows * kFgLanes + kFgLanes) * 4     // a, vmax
          + 2 * 8;                                         // mbarriers
 }
 
-template <int NQ>
+// kTail (check and last iterations): GEMM 1 also accumulates
+// SE = (K o C) X with c = -log2(K) * lambda ln2 recovered per cell, and the
+// epilogue writes the row residual and the E0 row term a_i SE_i.
+template <int NQ, bool kTail>
 __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedParams p, int nrb) {
   extern __shared__ __align__(128) unsigned char fsm[];
   constexpr int STR = fg_stride(NQ);
@@ -826,9 +829,9 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
       mbar_wait(&bar[st], (uint32_t)((k >> 1) & 1));
       const float* Kb = Ks + st * kFgRows * STR;
       // ---- GEMM 1: partial S over this thread's j slice, 4 rows x 2 lane pairs
-      uint64_t acc[4][2];
+      uint64_t acc[4][2], ace[4][2];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = 0ull;
+      for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = ace[r][0] = ace[r][1] = 0ull;
       const int j0 = ks * (DP / 16);
       const float* xp0 = Xs + (lq * 2) * XSTR + 2 * j0;       // lanes 4 lq, 4 lq + 1
       const float* xp1 = Xs + (lq * 2 + 1) * XSTR + 2 * j0;   // lanes 4 lq + 2, 4 lq + 3
@@ -853,6 +856,12 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
             const uint64_t kk = pk2(kv[e], kv[e]);
             ffma2_acc(acc[r][0], kk, p0[e]);
             ffma2_acc(acc[r][1], kk, p1[e]);
+            if constexpr (kTail) {   // K c / (lambda ln2) = -K log2 K (0 where K flushed)
+              const float kc = kv[e] > 0.f ? -kv[e] * lg2(kv[e]) : 0.f;
+              const uint64_t kck = pk2(kc, kc);
+              ffma2_acc(ace[r][0], kck, p0[e]);
+              ffma2_acc(ace[r][1], kck, p1[e]);
+            }
           }
         }
       }
@@ -862,6 +871,16 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
         *reinterpret_cast<float4*>(o) = make_float4(lo2(acc[r][0]), hi2(acc[r][0]), lo2(acc[r][1]),
                                                     hi2(acc[r][1]));
       }
+      float se_part[4][4];
+      if constexpr (kTail) {   // the SE partials go through Sred after the S sums are read
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          se_part[r][0] = lo2(ace[r][0]);
+          se_part[r][1] = hi2(ace[r][0]);
+          se_part[r][2] = lo2(ace[r][1]);
+          se_part[r][3] = hi2(ace[r][1]);
+        }
+      }
       __syncthreads();
       // ---- row epilogue: thread t -> (row i, lane b)
       {
@@ -869,14 +888,34 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
         float S = 0.f;
 #pragma unroll
         for (int q = 0; q < 16; ++q) S += Sred[q * 256 + t];   // ascending slices
+        float SE = 0.f;
+        if constexpr (kTail) {
+          __syncthreads();   // every S is read: reuse Sred for the SE partials
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) {
+            float* o = Sred + ks * 256 + (rq * 4 + rr) * 16 + lq * 4;
+            *reinterpret_cast<float4*>(o) =
+                make_float4(se_part[rr][0], se_part[rr][1], se_part[rr][2], se_part[rr][3]);
+          }
+          __syncthreads();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) SE += Sred[q * 256 + t];
+        }
         const int i = rb * kFgRows + r, b = b0 + l;
         float a = 0.f;
         if (i < p.nrows && b < p.B && !dead) {
           const size_t o = (size_t)b * p.ldo + i;
           const float mg = p.marg[o];
           if (mg > 0.f && !(S >= kFusedEstLo)) *p.est_fail = 1;   // flushed terms: exact rerun
-          p.out[o] = sweep_out(p.target[o], Vm[l] + lg2(S));
+          const float lse = Vm[l] + lg2(S);
+          const float u = sweep_out(p.target[o], lse);
+          p.out[o] = u;
           a = mg > 0.f ? mg * rcp_approx(S) : 0.f;
+          if constexpr (kTail) {
+            atomic_max_nonneg(&p.res[b], fabsf(exp2f(u + lse) - mg));
+            // E0 row term a_i SE_i lambda ln2, log2 for e0_rows_finalize_kernel
+            p.e0[o] = (a > 0.f && SE > 0.f) ? log2f(a) + log2f(SE) + p.e0_log2scale : neg_inf();
+          }
         }
         As[r * 16 + l] = a;
       }
@@ -946,7 +985,18 @@ __global__ void __launch_bounds__(256) fused_merge_kernel(const FusedMergeParams
     const int np = s_n;
     float2 cs = make_float2(0.f, 0.f);
     int k = 0;
-    for (; k + 4 <= np; k += 4) {   // four loads in flight, summed in ascending order
+    for (; k + 8 <= np; k += 8) {   // eight loads in flight, summed in ascending order
+      float2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = __ldcg(reinterpret_cast<const float2*>(p.part + (size_t)s_off[k + u] * p.rowlen + j));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        cs.x += v[u].x;
+        cs.y += v[u].y;
+      }
+    }
+    for (; k + 4 <= np; k += 4) {
       float2 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
