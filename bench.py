@@ -66,80 +66,119 @@ def load_peaks() -> dict:
 # clocks during the timed region (B200_PROFILING.md "clocks" line)
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region.
+    """Clock and throttle-reason sampling during the timed region.
 
-    Sampling every 100 ms contends with the driver while the solver enqueues
-    its ~200 launches per step, so the interval defaults to 500 ms."""
+    In-process NVML queries from a background thread (ctypes calls release the
+    GIL): unlike an ``nvidia-smi -lms`` child, which re-enumerates the devices
+    on every sample and can hold the driver lock for tens of milliseconds
+    while the solver enqueues its launches.  Falls back to nvidia-smi when
+    NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap,timestamp")
+    REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu_index: int, interval_ms: int = 500):
-        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
-        self.proc = None
         self.gpu = gpu_index
         self.interval_ms = interval_ms
         self.window = None   # wall-clock (start, end) of the timed region
+        self.rows = []       # (ts, sm_mhz, sm_max_mhz, {reason: active})
+        self._stop = None
+        self._thread = None
+        self._proc = None
+        self._path = None
 
     def mark(self, t0: float, t1: float) -> None:
         """The timed region; samples within one interval of it are reported.
-        (The sampler itself starts before the warm-up steps, so nvidia-smi's own
-        start-up never lands inside the timed steps.)"""
+        (Sampling starts before the warm-up steps.)"""
         self.window = (t0, t1)
 
-    def __enter__(self):
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
         try:
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", str(self.interval_ms)],
-                stdout=self.fh, stderr=subprocess.DEVNULL)
+            prop = torch.cuda.get_device_properties(self.gpu)
+            bus = f"{prop.pci_domain_id:08X}:{prop.pci_bus_id:02X}:{prop.pci_device_id:02X}.0"
+            return pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+
+    def _loop(self, h):
+        import pynvml
+
+        bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+        while not self._stop.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((time.time(), float(sm), float(smax),
+                                  {n: bool(mask & b) for n, b in zip(self.REASONS, bits)}))
+            except Exception:
+                pass
+            self._stop.wait(self.interval_ms * 1e-3)
+
+    def __enter__(self):
+        import threading
+
+        try:
+            h = self._nvml_handle()
+            self._stop = threading.Event()
+            self._thread = threading.Thread(target=self._loop, args=(h,), daemon=True)
+            self._thread.start()
+            return self
+        except Exception:
+            pass
+        try:   # fallback: an nvidia-smi child process
+            self._path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+            self._fh = open(self._path, "w")
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits",
+                 "-lms", str(self.interval_ms)], stdout=self._fh, stderr=subprocess.DEVNULL)
             time.sleep(0.3)
         except (OSError, FileNotFoundError):
-            self.proc = None
+            self._proc = None
         return self
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=5)
+        if self._proc is not None:
+            self._proc.terminate()
             try:
-                self.proc.wait(timeout=5)
+                self._proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
-                self.proc.kill()
-            self.fh.close()
+                self._proc.kill()
+            self._fh.close()
+            try:   # no timestamps from this fallback: every row counts
+                with open(self._path) as f:
+                    for line in f:
+                        v = [x.strip() for x in line.split(",")]
+                        if len(v) >= 6 and v[0].replace(".", "").isdigit():
+                            self.rows.append((None, float(v[0]), float(v[1]),
+                                              {n: v[2 + k] == "Active"
+                                               for k, n in enumerate(self.REASONS)}))
+            except OSError:
+                pass
 
     def summary(self) -> dict:
-        import datetime
-
-        rows = []
-        try:
-            with open(self.path) as f:
-                for line in f:
-                    parts = [p.strip() for p in line.split(",")]
-                    if len(parts) >= 8:
-                        rows.append(parts)
-        except OSError:
-            pass
+        rows = self.rows
         if self.window is not None and rows:
             pad = self.interval_ms * 1e-3
             t0, t1 = self.window[0] - pad, self.window[1] + pad
-            near = []
-            for r in rows:
-                try:
-                    ts = datetime.datetime.strptime(r[7], "%Y/%m/%d %H:%M:%S.%f").timestamp()
-                except ValueError:
-                    continue
-                if t0 <= ts <= t1:
-                    near.append(r)
+            near = [r for r in rows if r[0] is None or t0 <= r[0] <= t1]
             rows = near or rows[-1:]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        smax = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
-        load = [s for s in sm if s > 0.5 * smax] or sm
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k] == "Active"})
+        smax = max(r[2] for r in rows)
+        sm = [r[1] for r in rows]
+        load = [x for x in sm if x > 0.5 * smax] or sm
+        reasons = sorted({n for r in rows for n, on in r[3].items() if on})
         return {"sm_mhz": statistics.median(load), "sm_max_mhz": smax, "reasons": reasons,
                 "samples": len(rows)}
 
@@ -632,7 +671,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--clock-interval-ms", type=int, default=500)
+    ap.add_argument("--clock-interval-ms", type=int, default=100)
     ap.add_argument("--row-backend", choices=["gemm", "lse"], default="gemm",
                     help="row sharding: local fp32 GEMMs (default) or log-domain half-sweeps")
     ap.add_argument("--sharding", choices=["batch", "row"], default=None,
