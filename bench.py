@@ -602,11 +602,16 @@ def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
     if cfg["cost"] in ("index", "grid_stored") and d <= 8192:
         # the reference-facing C ABI: sinkhorn_forward_v1 / sinkhorn_backward_v1 (ffi.ts:80-191)
         lib = _lib.load()
-        h_mu = mu.double().cpu().numpy()
-        h_nu = nu.double().cpu().numpy()
-        h_c = cost.double().cpu().numpy()
-        o_cost, o_lu, o_lv = np.empty(B), np.empty((B, d)), np.empty((B, d))
-        up, g_mu, g_nu = np.ones(B), np.empty((B, d)), np.empty((B, d))
+
+        def pinned(shape, src=None):   # numpy views of page-locked host memory
+            t = torch.empty(shape, dtype=torch.float64).pin_memory()
+            if src is not None:
+                t.copy_(src.double().cpu())
+            return t.numpy()
+        h_mu, h_nu, h_c = pinned((B, d), mu), pinned((B, d), nu), pinned((d, d), cost)
+        o_cost, o_lu, o_lv = pinned((B,)), pinned((B, d)), pinned((B, d))
+        up, g_mu, g_nu = pinned((B,)), pinned((B, d)), pinned((B, d))
+        up[:] = 1.0
 
         def view(a):
             v = _lib.View()
@@ -630,7 +635,8 @@ def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
             assert st == 0, (st, _lib.last_error())
         h2d = 8 * (2 * B * d + d * d) + 8 * (2 * B * d + B)
         d2h = 8 * (B + 2 * B * d) + 8 * (2 * B * d)
-        path = "C ABI sinkhorn_forward_v1 + sinkhorn_backward_v1, host float64 views"
+        path = ("C ABI sinkhorn_forward_v1 + sinkhorn_backward_v1, host float64 views in "
+                "pinned memory")
     else:
         h_mu = mu.cpu().pin_memory()
         h_nu = nu.cpu().pin_memory()
