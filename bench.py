@@ -657,7 +657,7 @@ def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
             h_gm.copy_(gm, non_blocking=True)
             h_gn.copy_(gn, non_blocking=True)
             torch.cuda.synchronize()
-        h2d = 4 * (2 * B * d + (0 if grid else B * d * d))
+        h2d = 4 * (2 * B * d + (0 if grid else cost.numel()))
         d2h = 4 * (B + 2 * B * d)
         path = "torch API solve()+potentials_backward() from pinned host tensors"
     one()
