@@ -318,6 +318,12 @@ def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
                           "(MEASURED_PEAKS.json)"}
     if clocks.get("sm_mhz"):
         out["frac_at_measured_clock"] = achieved / (sms * MUFU_PER_SM_CLK * clocks["sm_mhz"] * 1e-6)
+    if path == "fused":
+        # what bounds the block pass itself: two GEMMs (2 FMA = 4 FLOP per cell-iteration)
+        # on the fp32 FMA pipe, 148 SM x 128 FFMA/clk x 2 FLOP (nominal)
+        tf = 4 * cells / (sweep_ms * 1e-3) / 1e12
+        out["fp32_pipe"] = {"achieved_tflops": tf, "peak_tflops": sms * 128 * 2 * fmax * 1e-6,
+                            "frac": tf / (sms * 128 * 2 * fmax * 1e-6)}
     return out
 
 
