@@ -737,11 +737,15 @@ constexpr int kFgRows = 16;     // cost rows per block
 constexpr int kFgLanes = 16;    // lanes per CTA
 constexpr int kFgThreads = 256;
 
-__host__ __device__ constexpr int fg_stride(int nq) { return nq * 64 + 4; }   // padded row (banks)
+// Shared-memory strides chosen so the LDS.128s of a warp hit 8 distinct 16-byte
+// bank groups: K rows padded by 8 floats (a thread's 4 rows interleaved by 4),
+// X lane-pair rows carry a 4-float gap after every j slice plus 4 floats of pad.
+__host__ __device__ constexpr int fg_stride(int nq) { return nq * 64 + 8; }
+__host__ __device__ constexpr int fg_xstride(int nq) { return 2 * nq * 64 + 4 * 16 + 4; }
 
 template <int NQ>
 __host__ __device__ constexpr size_t fg_smem_bytes() {
-  return (size_t)(kFgLanes / 2 * (2 * NQ * 64 + 4)        // X: 8 interleaved lane pairs
+  return (size_t)(kFgLanes / 2 * fg_xstride(NQ)            // X: 8 interleaved lane pairs
                   + 2 * kFgRows * fg_stride(NQ)            // two K blocks
                   + 16 * kFgRows * kFgLanes               // GEMM-1 slice partials
                   + kFgRows * kFgLanes + kFgLanes) * 4     // a, vmax
@@ -755,9 +759,12 @@ template <int NQ, bool kTail>
 __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedParams p, int nrb) {
   extern __shared__ __align__(128) unsigned char fsm[];
   constexpr int STR = fg_stride(NQ);
-  constexpr int XSTR = 2 * NQ * 64 + 4;   // a lane pair's interleaved row (+4: banks)
+  constexpr int XSTR = fg_xstride(NQ);    // a lane pair's interleaved row
+  constexpr int SL = NQ * 4;              // j slice length (DP / 16)
+  // X position of column j in a pair row: 2 j plus a 4-float gap per slice
+  auto xpos = [](int j) { return 2 * j + 4 * (j / SL); };
   constexpr int DP = NQ * 64;
-  float* Xs = reinterpret_cast<float*>(fsm);               // [16 lanes][STR]
+  float* Xs = reinterpret_cast<float*>(fsm);               // [8 lane pairs][XSTR]
   float* Ks = Xs + kFgLanes / 2 * XSTR;                     // [2][16 rows][STR]
   float* Sred = Ks + 2 * kFgRows * STR;                     // [16 slices][256]
   float* As = Sred + 16 * kFgRows * kFgLanes;               // [16 rows][16 lanes]
@@ -815,7 +822,7 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
       // lane pairs interleaved: Xs[l / 2][j][l % 2], so GEMM 1 multiplies a K value
       // into two lanes with one FFMA2
       for (int j = lane; j < DP; j += 32)
-        Xs[(l >> 1) * XSTR + 2 * j + (l & 1)] = b < p.B ? ex2(v[j] - m) : 0.f;
+        Xs[(l >> 1) * XSTR + xpos(j) + (l & 1)] = b < p.B ? ex2(v[j] - m) : 0.f;
       if (lane == 0) Vm[l] = m;
     }
     uint64_t T[2][NQ];   // [lane pair][column k]: lanes 4 l4 + {0,1} and {2,3}
@@ -833,14 +840,14 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = ace[r][0] = ace[r][1] = 0ull;
       const int j0 = ks * (DP / 16);
-      const float* xp0 = Xs + (lq * 2) * XSTR + 2 * j0;       // lanes 4 lq, 4 lq + 1
-      const float* xp1 = Xs + (lq * 2 + 1) * XSTR + 2 * j0;   // lanes 4 lq + 2, 4 lq + 3
+      const float* xp0 = Xs + (lq * 2) * XSTR + 2 * j0 + 4 * ks;       // lanes 4 lq, 4 lq + 1
+      const float* xp1 = Xs + (lq * 2 + 1) * XSTR + 2 * j0 + 4 * ks;   // lanes 4 lq + 2, + 3
 #pragma unroll
       for (int jj = 0; jj < DP / 16; jj += 4) {
         float4 kr[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
-          kr[r] = *reinterpret_cast<const float4*>(Kb + (rq * 4 + r) * STR + j0 + jj);
+          kr[r] = *reinterpret_cast<const float4*>(Kb + (rq + 4 * r) * STR + j0 + jj);
         // (x_l(j), x_l+1(j)) pairs for j = jj .. jj + 3
         const float4 xa = *reinterpret_cast<const float4*>(xp0 + 2 * jj);
         const float4 xb = *reinterpret_cast<const float4*>(xp0 + 2 * jj + 4);
@@ -867,7 +874,7 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        float* o = Sred + ks * 256 + (rq * 4 + r) * 16 + lq * 4;
+        float* o = Sred + ks * 256 + (rq + 4 * r) * 16 + lq * 4;
         *reinterpret_cast<float4*>(o) = make_float4(lo2(acc[r][0]), hi2(acc[r][0]), lo2(acc[r][1]),
                                                     hi2(acc[r][1]));
       }
@@ -893,7 +900,7 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
           __syncthreads();   // every S is read: reuse Sred for the SE partials
 #pragma unroll
           for (int rr = 0; rr < 4; ++rr) {
-            float* o = Sred + ks * 256 + (rq * 4 + rr) * 16 + lq * 4;
+            float* o = Sred + ks * 256 + (rq + 4 * rr) * 16 + lq * 4;
             *reinterpret_cast<float4*>(o) =
                 make_float4(se_part[rr][0], se_part[rr][1], se_part[rr][2], se_part[rr][3]);
           }
@@ -947,8 +954,8 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
     for (int q = 0; q < NQ; ++q) {
       const int j = jc + 64 * q;
       const int l = l4 * 4;
-      const float2 x01 = *reinterpret_cast<const float2*>(Xs + (l >> 1) * XSTR + 2 * j);
-      const float2 x23 = *reinterpret_cast<const float2*>(Xs + ((l >> 1) + 1) * XSTR + 2 * j);
+      const float2 x01 = *reinterpret_cast<const float2*>(Xs + (l >> 1) * XSTR + xpos(j));
+      const float2 x23 = *reinterpret_cast<const float2*>(Xs + ((l >> 1) + 1) * XSTR + xpos(j));
       dst[(size_t)(l + 0) * DP + j] = lo2(T[0][q]) * x01.x;
       dst[(size_t)(l + 1) * DP + j] = hi2(T[0][q]) * x01.y;
       dst[(size_t)(l + 2) * DP + j] = lo2(T[1][q]) * x23.x;
