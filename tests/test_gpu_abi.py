@@ -161,3 +161,36 @@ def test_device_api_raises_the_reference_exceptions(cuda):
     c_bad[1, 1] = -1.0
     with pytest.raises(skb.InvalidCost):
         skb.solve(t(mu), t(nu), t(c_bad), 0.1, 10)
+
+
+@pytest.mark.parametrize("path", ["fused", "gemm", "per_sample", "per_sample_fused", "fp64"])
+def test_every_path_reports_invalid_inputs(path, cuda):
+    """Status 11 (histogram) and 15 (cost) on the fused block pass, the GEMM
+    iteration, the fused per-sample pass and the float64 mode, each raised as
+    the reference's exception type before any result is returned."""
+    import torch
+
+    import paper_1907_01729_b200 as skb
+
+    mu, nu, c = _base()
+    if path == "per_sample_fused":   # d2 = 12: rows of whole 16-byte units (the fused pass)
+        from oracle import sinkhorn_oracle as orc
+
+        nu = orc.random_histogram_batch(4, 12, np.random.default_rng(9))
+        c = orc.fp32_exact(np.random.default_rng(9).random((12, 12)))
+    B, d1, d2 = mu.shape[0], mu.shape[1], nu.shape[1]
+    dt = torch.float64 if path == "fp64" else torch.float32
+    t = lambda a: torch.tensor(a, dtype=dt, device=cuda)   # noqa: E731
+    kw = {"tiled_only": True, "gemm": path == "gemm", "fp64": path == "fp64"}
+    cost = np.repeat(c[None], B, axis=0) if path.startswith("per_sample") else c
+    res = skb.solve(t(mu), t(nu), t(cost), 0.1, 20, **kw)
+    # (d2 = 9 is not a multiple of 4: per-sample costs take the lane kernels here)
+    assert res.path == {"per_sample": "lane", "per_sample_fused": "fused"}.get(path, path)
+    bad = mu.copy()
+    bad[1, 3] += 1e-3
+    with pytest.raises(skb.InvalidHistogram):
+        skb.solve(t(bad), t(nu), t(cost), 0.1, 20, **kw)
+    c_bad = cost.copy()
+    c_bad[..., 2, 2] = -1.0
+    with pytest.raises(skb.InvalidCost):
+        skb.solve(t(mu), t(nu), t(c_bad), 0.1, 20, **kw)
