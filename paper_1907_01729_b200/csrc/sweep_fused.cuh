@@ -833,6 +833,12 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
     for (; u < seg_end; ++u, ++k) {
       const int st = k & 1;
       const int rb = (int)(u - (long long)g * nrb);
+      // this thread's epilogue scalars, requested now so the L2 latency hides under GEMM 1
+      const int e_i = rb * kFgRows + (t >> 4), e_b = b0 + (t & 15);
+      const bool e_ok = e_i < p.nrows && e_b < p.B && !dead;
+      const size_t e_o = (size_t)e_b * p.ldo + e_i;
+      const float e_mg = e_ok ? __ldg(p.marg + e_o) : 0.f;
+      const float e_tg = e_ok ? __ldg(p.target + e_o) : 0.f;
       mbar_wait(&bar[st], (uint32_t)((k >> 1) & 1));
       const float* Kb = Ks + st * kFgRows * STR;
       // ---- GEMM 1: partial S over this thread's j slice, 4 rows x 2 lane pairs
@@ -908,14 +914,14 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
 #pragma unroll
           for (int q = 0; q < 16; ++q) SE += Sred[q * 256 + t];
         }
-        const int i = rb * kFgRows + r, b = b0 + l;
+        const int b = b0 + l;
         float a = 0.f;
-        if (i < p.nrows && b < p.B && !dead) {
-          const size_t o = (size_t)b * p.ldo + i;
-          const float mg = p.marg[o];
+        if (e_ok) {
+          const size_t o = e_o;
+          const float mg = e_mg;
           if (mg > 0.f && !(S >= kFusedEstLo)) *p.est_fail = 1;   // flushed terms: exact rerun
           const float lse = Vm[l] + lg2(S);
-          const float u = sweep_out(p.target[o], lse);
+          const float u = sweep_out(e_tg, lse);
           p.out[o] = u;
           a = mg > 0.f ? mg * rcp_approx(S) : 0.f;
           if constexpr (kTail) {
