@@ -814,15 +814,21 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
     for (int h = 0; h < 2; ++h) {
       const int l = warp * 2 + h, b = b0 + l;
       const float* v = p.x + (size_t)b * DP;
+      float vr[DP / 32];   // the lane's potentials, one load each, all in flight
+#pragma unroll
+      for (int q = 0; q < DP / 32; ++q) vr[q] = b < p.B ? __ldg(v + lane + 32 * q) : neg_inf();
       float m = kNegBig;
-      if (b < p.B)
-        for (int j = lane; j < DP; j += 32) m = fmaxf(m, v[j]);
+#pragma unroll
+      for (int q = 0; q < DP / 32; ++q) m = fmaxf(m, vr[q]);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
       // lane pairs interleaved: Xs[l / 2][j][l % 2], so GEMM 1 multiplies a K value
       // into two lanes with one FFMA2
-      for (int j = lane; j < DP; j += 32)
-        Xs[(l >> 1) * XSTR + xpos(j) + (l & 1)] = b < p.B ? ex2(v[j] - m) : 0.f;
+#pragma unroll
+      for (int q = 0; q < DP / 32; ++q) {
+        const int j = lane + 32 * q;
+        Xs[(l >> 1) * XSTR + xpos(j) + (l & 1)] = ex2(vr[q] - m);
+      }
       if (lane == 0) Vm[l] = m;
     }
     uint64_t T[2][NQ];   // [lane pair][column k]: lanes 4 l4 + {0,1} and {2,3}
