@@ -788,12 +788,14 @@ struct Solve {
       return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
     } else {
       if (fp.nq != NQ) return launch_fgemm<NQ + 1>(fp, nrb);
-      auto kern = fp.e0 != nullptr ? &fgemm_pass_kernel<NQ, true> : &fgemm_pass_kernel<NQ, false>;
-      static bool attr[2] = {false, false};
+      const int mode = fp.vmax_out != nullptr ? 2 : fp.e0 != nullptr ? 1 : 0;
+      auto kern = mode == 2 ? &fgemm_pass_kernel<NQ, 2>
+                  : mode == 1 ? &fgemm_pass_kernel<NQ, 1> : &fgemm_pass_kernel<NQ, 0>;
+      static bool attr[3] = {false, false, false};
       const size_t smem = fg_smem_bytes<NQ>();
-      if (!attr[fp.e0 != nullptr]) {
+      if (!attr[mode]) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr[fp.e0 != nullptr] = true;
+        attr[mode] = true;
       }
       ++g_launches;
       CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(kFgThreads), smem, st, fp, nrb));
@@ -832,7 +834,7 @@ struct Solve {
   }
   // iteration k: u_k from v_k = g2[cur] (row sweep), then v_{k+1} into
   // g2[cur ^ 1] from the plan's column marginal; residuals / E0 row terms on request
-  int fused_iteration(int cur, bool res, bool e0) {
+  int fused_iteration(int cur, bool res, bool e0, bool first = false) {
     FusedParams fp = fused_common();
     const int nw = fused_warps(L.D2p / 64);
     const long long groups = (pr.B + nw - 1) / nw;
@@ -864,6 +866,7 @@ struct Solve {
       fp.nct = L.fg_nct;
       fp.maxseg = L.fg_maxseg;
       fp.a2 = F(L.kmat);   // the block pass streams K (its tail recovers c from K)
+      if (first) fp.vmax_out = F(L.g2[cur]);   // v := umax_b, then the merge writes v_1
       merge_nw = kFgLanes;
       merge_rows = nrb;
       if (int e = launch_fgemm<1>(fp, nrb)) return e;
@@ -1541,6 +1544,8 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     auto fused_loop = [&]() -> int {
       if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE) {
         if (int e = S.lane_col(kModeUpdate, S.F(L.g2[1]), S.F(L.g2[0]), kResNone)) return e;
+      } else if (g_use_fgemm) {   // the block pass from u0 (cur = 0), merged into g2[1]
+        if (int e = S.fused_iteration(0, false, false, true)) return e;
       } else {
         if (int e = S.fused_row_only(1)) return e;
       }

@@ -75,6 +75,7 @@ struct FusedParams {
   float e0_log2scale;     // log2(lambda * ln2): c = -A2 * lambda * ln2
   const int* status;      // abort if validation failed
   int* est_fail;          // kLin: more fallback rows than a warp can queue -> exact rerun
+  float* vmax_out;        // block pass, first sweep: [B][rowlen] filled with -(the lane's max log u0)
 };
 
 struct FusedMergeParams {
@@ -755,8 +756,14 @@ __host__ __device__ constexpr size_t fg_smem_bytes() {
 // kTail (check and last iterations): GEMM 1 also accumulates
 // SE = (K o C) X with c = -log2(K) * lambda ln2 recovered per cell, and the
 // epilogue writes the row residual and the E0 row term a_i SE_i.
-template <int NQ, bool kTail>
+// kMode 0: an iteration; 1: a check / last iteration (kTail); 2: the first
+// column sweep from u0 (kFirst): no GEMM 1, a_i = 2^(u0_i - umax_b) on the
+// support, T = K^T a = 2^(-umax_b) sum_i K_ij 2^(u0_i), and -umax_b written to
+// vmax_out so the merge's v' = v + l2nu - log2(T) starts from v = -umax_b.
+template <int NQ, int kMode>
 __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedParams p, int nrb) {
+  constexpr bool kTail = kMode == 1;
+  constexpr bool kFirst = kMode == 2;
   extern __shared__ __align__(128) unsigned char fsm[];
   constexpr int STR = fg_stride(NQ);
   constexpr int XSTR = fg_xstride(NQ);    // a lane pair's interleaved row
@@ -811,6 +818,21 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
     const int b0 = g * kFgLanes;
     // this group's potentials as X = 2^(v - vmax) (warp w: lanes 2w, 2w+1)
     __syncthreads();
+    if constexpr (kFirst) {   // umax_b over log u0; X = 1 (the partials are T itself)
+      for (int h = 0; h < 2; ++h) {
+        const int l = warp * 2 + h, b = b0 + l;
+        float m = kNegBig;
+        if (b < p.B)
+          for (int i = lane; i < p.nrows; i += 32) m = fmaxf(m, p.out[(size_t)b * p.ldo + i]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+        for (int j = lane; j < DP; j += 32) Xs[(l >> 1) * XSTR + xpos(j) + (l & 1)] = 1.f;
+        if (lane == 0) Vm[l] = m;
+        // the group's CTA holding row block 0 publishes -umax as the merge's v
+        if (b < p.B && (u - (long long)g * nrb) == 0)
+          for (int j = lane; j < DP; j += 32) p.vmax_out[(size_t)b * DP + j] = -m;
+      }
+    } else
     for (int h = 0; h < 2; ++h) {
       const int l = warp * 2 + h, b = b0 + l;
       const float* v = p.x + (size_t)b * DP;
@@ -844,9 +866,11 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
       const bool e_ok = e_i < p.nrows && e_b < p.B && !dead;
       const size_t e_o = (size_t)e_b * p.ldo + e_i;
       const float e_mg = e_ok ? __ldg(p.marg + e_o) : 0.f;
-      const float e_tg = e_ok ? __ldg(p.target + e_o) : 0.f;
+      const float e_tg = e_ok ? (kFirst ? p.out[e_o] : __ldg(p.target + e_o)) : 0.f;   // kFirst: u0
       mbar_wait(&bar[st], (uint32_t)((k >> 1) & 1));
       const float* Kb = Ks + st * kFgRows * STR;
+      float se_part[4][4];   // kTail: this thread's SE partials
+      if constexpr (!kFirst) {
       // ---- GEMM 1: partial S over this thread's j slice, 4 rows x 2 lane pairs
       uint64_t acc[4][2], ace[4][2];
 #pragma unroll
@@ -890,7 +914,6 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
         *reinterpret_cast<float4*>(o) = make_float4(lo2(acc[r][0]), hi2(acc[r][0]), lo2(acc[r][1]),
                                                     hi2(acc[r][1]));
       }
-      float se_part[4][4];
       if constexpr (kTail) {   // the SE partials go through Sred after the S sums are read
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -901,8 +924,12 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
         }
       }
       __syncthreads();
+      }
       // ---- row epilogue: thread t -> (row i, lane b)
-      {
+      if constexpr (kFirst) {
+        const int r = t >> 4, l = t & 15;
+        As[r * 16 + l] = (e_ok && e_mg > 0.f) ? ex2(e_tg - Vm[l]) : 0.f;   // 2^(u0 - umax)
+      } else {
         const int r = t >> 4, l = t & 15;
         float S = 0.f;
 #pragma unroll
