@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
       }
       __syncthreads();
       // ---- GEMM 2: T[lane][j] += sum_r K[r][j] a[r][lane]
-#pragma unroll 4
+#pragma unroll 8
       for (int r = 0; r < kFgRows; ++r) {
         const float4 a4 = *reinterpret_cast<const float4*>(As + r * 16 + l4 * 4);
         const uint64_t a01 = pk2(a4.x, a4.y), a23 = pk2(a4.z, a4.w);
