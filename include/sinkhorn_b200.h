@@ -200,7 +200,10 @@ int32_t sinkhorn_e0_partial_device_v1(int64_t B, int64_t d1, int64_t d2, double 
 /* Cross-process agreement on the stopping test (batch-sharded lockstep,
  * batch.py:318-322): when set (per thread), every convergence check calls
  * fn(local max residual, user) and stops iff the returned global max <= tol.
- * All ranks call it the same number of times.  NULL restores local checks. */
+ * All ranks call it the same number of times: once per check, plus once at
+ * the end of a solve's first attempt with local_max = 1 if this rank's
+ * estimate-mode sweeps need the exact rerun (else 0), so that the ranks rerun
+ * together or not at all.  NULL restores local checks. */
 typedef double (*sinkhorn_residual_reducer_v1)(double local_max, void* user);
 void sinkhorn_set_residual_reducer_v1(sinkhorn_residual_reducer_v1 fn, void* user);
 

@@ -7,6 +7,7 @@ The CUDA runtime is linked statically so the .so travels with the repo.
 
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
@@ -17,9 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB_NAME = "libsinkhorn_b200.so"
 SOURCES = ["sinkhorn_abi.cu"]
-HEADERS = ["common.cuh", "sweep_tiled.cuh", "sweep_lane.cuh", "sweep_small.cuh", "sweep_sep.cuh",
-           "persistent.cuh",
-           "aux_kernels.cuh"]
+HEADERS = sorted(os.path.basename(f) for f in glob.glob(os.path.join(CSRC, "*.cuh")))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

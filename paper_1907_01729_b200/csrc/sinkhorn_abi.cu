@@ -6,11 +6,9 @@
 // synchronises when the reference's semantics need a host decision (the
 // convergence test every check_interval iterations when tolerance > 0) and once
 // at the end to report the status word.
-#include <cublas_v2.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
-#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -32,6 +30,7 @@
 #include "sweep_fused.cuh"
 #include "sweep_f64.cuh"
 #include "sweep_gemm.cuh"
+#include "sweep_umma.cuh"
 
 using namespace skb;
 
@@ -140,6 +139,23 @@ bool make_tmap(CUtensorMap* m, const float* base, size_t rows, size_t cols, int 
   return r == CUDA_SUCCESS;
 }
 
+// Operand map of the tensor-core contractions: [rows][cols] fp32 with row pitch
+// `pitch` elements, box 32 (one 128-byte swizzle row) x box_rows, SWIZZLE_128B;
+// elements past `cols` / `rows` read as 0.
+bool make_tmap_sw128(CUtensorMap* m, const float* base, size_t rows, size_t cols, size_t pitch,
+                     int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch * sizeof(float)};
+  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // ---- launch helpers ----------------------------------------------------------
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -188,6 +204,8 @@ struct Layout {
   int fg_nct = 0, fg_maxseg = 0;  // the two-GEMM block pass (units: 16 lanes x 16 rows)
   bool gemm = false;              // large shared cost: two fp32 GEMMs per iteration
   size_t kc = 0, gx = 0, gs = 0, gt = 0, ga = 0, gvmax = 0, gvmax0 = 0, gfall = 0;
+  size_t kmatT = 0, gxh = 0, gxl = 0, gah = 0, gal = 0, um_part = 0;
+  int ldk1 = 0, ldk2 = 0;
 };
 
 // Fused passes (sweep_fused.cuh): shared stored cost, both padded extents
@@ -226,9 +244,21 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     L.si1 = 1;
     L.sb2 = L.D2p;
     L.si2 = 1;
-    L.kmat = c.take((size_t)pr.d1 * pr.d2 * 4);
-    L.kc = c.take((size_t)pr.d1 * pr.d2 * 4);
+    // K and K o C row-major [d1][ldk2], K^T [d2][ldk1] (the column sweep's A
+    // operand, so both contractions read a K-major tile), row pitch a 16-byte
+    // multiple for TMA
+    L.ldk1 = (int)round_up(pr.d1, 4);
+    L.ldk2 = (int)round_up(pr.d2, 4);
+    L.kmat = c.take((size_t)pr.d1 * L.ldk2 * 4);
+    L.kc = c.take((size_t)pr.d1 * L.ldk2 * 4);
+    L.kmatT = c.take((size_t)pr.d2 * L.ldk1 * 4);
     const size_t n1 = (size_t)L.B * L.D1p * 4, n2 = (size_t)L.B * L.D2p * 4;
+    // tf32 hi / lo planes of X [B][ldk2] and a [B][ldk1] (the MMAs' B operands)
+    L.gxh = c.take((size_t)L.B * L.ldk2 * 4);
+    L.gxl = c.take((size_t)L.B * L.ldk2 * 4);
+    L.gah = c.take((size_t)L.B * L.ldk1 * 4);
+    L.gal = c.take((size_t)L.B * L.ldk1 * 4);
+    L.um_part = c.take((size_t)sms * 2 * kUmBN * kUmBM * 4);
     L.f2 = c.take(n1);
     L.g2[0] = c.take(n2);
     L.g2[1] = c.take(n2);
@@ -370,6 +400,27 @@ size_t workspace_total(const sinkhorn_problem_v1& pr, int sms) {
 template <typename T>
 T* at(void* ws, size_t off) {
   return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+// Dynamic shared-memory opt-in for a kernel on the current device.  The
+// attribute is per (function, device), so the cache is keyed on both: a thread
+// that solves on a second GPU sets it there too.
+int set_max_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, size_t>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : done)
+    if (e.first.first == fn && e.first.second == dev && e.second >= bytes) return 0;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess)
+    return fail(SINKHORN_STATUS_CUDA_ERROR,
+                std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  for (auto& x : done)
+    if (x.first.first == fn && x.first.second == dev) { x.second = bytes; return 0; }
+  done.push_back({{fn, dev}, bytes});
+  return 0;
 }
 
 // Resident CTAs per SM for a kernel; the attribute set + occupancy query cost
@@ -521,52 +572,6 @@ int launch_tiled(const Layout& L, void* ws, const DeviceInfo& di, const TiledArg
                                : launch_tiled_pt<64, 64, kGrid, kMode>(L, ws, di, a, pr, lam, st);
 }
 
-// ---- cuBLAS, resolved at run time ---------------------------------------------
-// The GEMM path calls cublasSgemm (plain fp32 GEMMs).  The library is opened
-// on first use, so the C ABI has no link-time cuBLAS dependency and shares the
-// copy a host process (e.g. PyTorch) has already loaded.
-struct CublasApi {
-  decltype(&cublasCreate_v2) create = nullptr;
-  decltype(&cublasSetStream_v2) set_stream = nullptr;
-  decltype(&cublasSgemm_v2) sgemm = nullptr;
-  decltype(&cublasSetMathMode) set_math = nullptr;
-  bool ok = false;
-};
-
-const CublasApi& cublas_api() {
-  static CublasApi api;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* h = nullptr;
-    for (const char* name : {"libcublas.so.12", "/usr/local/cuda/lib64/libcublas.so.12",
-                             "libcublas.so"}) {
-      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
-      if (h) break;
-    }
-    if (!h) return;
-    api.create = reinterpret_cast<decltype(api.create)>(dlsym(h, "cublasCreate_v2"));
-    api.set_stream = reinterpret_cast<decltype(api.set_stream)>(dlsym(h, "cublasSetStream_v2"));
-    api.sgemm = reinterpret_cast<decltype(api.sgemm)>(dlsym(h, "cublasSgemm_v2"));
-    api.set_math = reinterpret_cast<decltype(api.set_math)>(dlsym(h, "cublasSetMathMode"));
-    api.ok = api.create && api.set_stream && api.sgemm;
-  });
-  return api;
-}
-
-cublasHandle_t cublas_handle(int dev) {
-  static thread_local cublasHandle_t handles[64] = {};
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!handles[dev]) {
-    const CublasApi& api = cublas_api();
-    if (!api.ok || api.create(&handles[dev]) != CUBLAS_STATUS_SUCCESS) return nullptr;
-    // full-precision fp32 products (SKB_GEMM_MATH=tf32 is a diagnostic, not parity-safe)
-    static const char* mm = getenv("SKB_GEMM_MATH");
-    if (api.set_math && mm && std::string(mm) == "tf32")
-      api.set_math(handles[dev], CUBLAS_TF32_TENSOR_OP_MATH);
-  }
-  return handles[dev];
-}
-
 // ---- the solver --------------------------------------------------------------
 struct Solve {
   sinkhorn_problem_v1 pr;
@@ -638,11 +643,7 @@ struct Solve {
     const bool tail = mode == kModeTail;
     const size_t smem = sep_smem_floats<SepS>(p.nx, p.ny, tail) * 4;
     auto kern = tail ? &sep_sweep_kernel<SepS, kModeTail> : &sep_sweep_kernel<SepS, kModeUpdate>;
-    static size_t attr_bytes[2] = {0, 0};
-    if (attr_bytes[tail] < smem) {
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_bytes[tail] = smem;
-    }
+    if (int e = set_max_smem(reinterpret_cast<const void*>(kern), smem)) return e;
     dim3 grid((unsigned)p.nblk, (unsigned)pr.B);
     // diagnostics (SKB_SEP_TIMELINE=n): per-CTA start / staged / end stamps of the n-th sweep
     static const long long tl_at = getenv("SKB_SEP_TIMELINE") ? atoll(getenv("SKB_SEP_TIMELINE")) : -1;
@@ -737,12 +738,7 @@ struct Solve {
   template <int NQ, bool kRowOnly, bool kTail, bool kLin>
   int launch_fused_t(const FusedParams& fp) {
     auto kern = &fused_pass_kernel<NQ, kRowOnly, kTail, kLin>;
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)fused_smem_bytes<NQ>()));
-      attr = true;
-    }
+    if (int e = set_max_smem(reinterpret_cast<const void*>(kern), fused_smem_bytes<NQ>())) return e;
     const size_t smem = (size_t)kFusedStages * fp.rowlen * 4 + kFusedStages * 8;
     ++g_launches;
     CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(fused_warps(NQ) * 32), smem, st, fp));
@@ -762,12 +758,8 @@ struct Solve {
   template <int NQ, bool kTail>
   int launch_fused_ps_t(const FusedParams& fp) {
     auto kern = &fused_ps_kernel<NQ, kTail>;
-    static bool attr = false;
     const size_t smem = fused_ps_smem_bytes<NQ>();
-    if (!attr) {
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    if (int e = set_max_smem(reinterpret_cast<const void*>(kern), smem)) return e;
     ++g_launches;
     CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(fused_warps(NQ) * 32), smem, st, fp, cost,
                   (int)pr.d2, (float)(-kLog2e / lam)));
@@ -791,12 +783,8 @@ struct Solve {
       const int mode = fp.vmax_out != nullptr ? 2 : fp.e0 != nullptr ? 1 : 0;
       auto kern = mode == 2 ? &fgemm_pass_kernel<NQ, 2>
                   : mode == 1 ? &fgemm_pass_kernel<NQ, 1> : &fgemm_pass_kernel<NQ, 0>;
-      static bool attr[3] = {false, false, false};
       const size_t smem = fg_smem_bytes<NQ>();
-      if (!attr[mode]) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr[mode] = true;
-      }
+      if (int e = set_max_smem(reinterpret_cast<const void*>(kern), smem)) return e;
       ++g_launches;
       CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(kFgThreads), smem, st, fp, nrb));
       return 0;
@@ -896,23 +884,48 @@ struct Solve {
     return 0;
   }
 
-  // ---- GEMM path (sweep_gemm.cuh) ---------------------------------------------
-  // C (m x n, col-major) = op(A) B with A = K or KC stored row-major [d1][d2]
-  // (col-major d2 x d1).  rows: C = A X (m = d1, k = d2); cols: C = A^T a.
-  int gemm(bool rows, const float* A, const float* Bm, float* C) {
-    const CublasApi& api = cublas_api();
-    cublasHandle_t h = cublas_handle(di.dev);
-    if (!h) return fail(SINKHORN_STATUS_CUDA_ERROR, "cuBLAS unavailable for the GEMM path");
-    api.set_stream(h, st);
-    const float one = 1.f, zero = 0.f;
-    const int d1 = (int)pr.d1, d2 = (int)pr.d2, B = (int)pr.B;
-    cublasStatus_t e = rows ? api.sgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, d1, B, d2, &one, A, d2, Bm,
-                                        d2, &zero, C, d1)
-                            : api.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, d2, B, d1, &one, A, d2, Bm,
-                                        d1, &zero, C, d2);
-    g_launches += 1;
-    if (e != CUBLAS_STATUS_SUCCESS)
-      return fail(SINKHORN_STATUS_CUDA_ERROR, "cublasSgemm failed: " + std::to_string((int)e));
+  // ---- GEMM path (sweep_gemm.cuh, contractions in sweep_umma.cuh) -------------
+  // rows: S[b][i] = sum_j K[i][j] X[b][j]  (A = K or K o C, B operand = X)
+  // cols: T[b][j] = sum_i K^T[j][i] a[b][i] (A = K^T, B operand = a)
+  CUtensorMap tm_k, tm_kt, tm_kc, tm_xh, tm_xl, tm_ah, tm_al;
+  int setup_umma_maps() {
+    if (!L.gemm) return 0;
+    const size_t d1 = (size_t)pr.d1, d2 = (size_t)pr.d2, B = (size_t)pr.B;
+    bool ok = make_tmap_sw128(&tm_k, F(L.kmat), d1, d2, L.ldk2, kUmBM);
+    ok &= make_tmap_sw128(&tm_kc, F(L.kc), d1, d2, L.ldk2, kUmBM);
+    ok &= make_tmap_sw128(&tm_kt, F(L.kmatT), d2, d1, L.ldk1, kUmBM);
+    ok &= make_tmap_sw128(&tm_xh, F(L.gxh), B, d2, L.ldk2, kUmBN);
+    ok &= make_tmap_sw128(&tm_xl, F(L.gxl), B, d2, L.ldk2, kUmBN);
+    ok &= make_tmap_sw128(&tm_ah, F(L.gah), B, d1, L.ldk1, kUmBN);
+    ok &= make_tmap_sw128(&tm_al, F(L.gal), B, d1, L.ldk1, kUmBN);
+    return ok ? 0 : fail(SINKHORN_STATUS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (umma)");
+  }
+  // the lane operand's tf32 planes from its lane-major fp32 array
+  int umma_split(const float* x, int d, int ld, float* hi, float* lo) {
+    ++g_launches;
+    umma_split_kernel<<<grid_for((size_t)pr.B * ld), 256, 0, st>>>(x, pr.B, d, ld, hi, lo);
+    CK(cudaGetLastError());
+    return 0;
+  }
+  int gemm(bool rows, const CUtensorMap& tA, float* C) {
+    UmmaParams p = {};
+    p.M = (int)(rows ? pr.d1 : pr.d2);
+    p.K = (int)(rows ? pr.d2 : pr.d1);
+    p.N = (int)pr.B;
+    p.MT = (p.M + kUmBM - 1) / kUmBM;
+    p.NT = (p.N + kUmBN - 1) / kUmBN;
+    p.KCH = (p.K + kUmBK - 1) / kUmBK;
+    p.units = (long long)p.MT * p.NT * p.KCH;
+    p.G = (int)std::min<long long>(di.sms, p.units);
+    p.out = C;
+    p.ldo = p.M;
+    p.part = F(L.um_part);
+    p.status = at<int>(ws, L.status);
+    if (int e = set_max_smem(reinterpret_cast<const void*>(&umma_gemm_kernel), kUmSmemBytes))
+      return e;
+    CK(launch_pdl(umma_gemm_kernel, dim3(p.G), dim3(kUmThreads), kUmSmemBytes, st, tA,
+                  rows ? tm_xh : tm_ah, rows ? tm_xl : tm_al, p));
+    CK(launch_pdl(umma_fixup_kernel, dim3((unsigned)(p.MT * p.NT)), dim3(256), 0, st, p));
     return 0;
   }
   int gemm_col(const float* vmax, const float* v_old, float* v_new, bool res) {
@@ -939,7 +952,8 @@ struct Solve {
     gemm_first_a_kernel<<<grid_for((size_t)pr.B * pr.d1), 256, 0, st>>>(F(L.mu),
                                                                        (size_t)pr.B * pr.d1, F(L.ga));
     CK(cudaMemsetAsync(F(L.gvmax0), 0, (size_t)pr.B * 4, st));
-    if (int e = gemm(false, F(L.kmat), F(L.ga), F(L.gt))) return e;
+    if (int e = umma_split(F(L.ga), (int)pr.d1, L.ldk1, F(L.gah), F(L.gal))) return e;
+    if (int e = gemm(false, tm_kt, F(L.gt))) return e;
     return gemm_col(F(L.gvmax0), nullptr, F(L.g2[1]), false);
   }
   // iteration k from v_k = g2[cur]: X, S = K X, u and a, T = K^T a, v_{k+1}
@@ -948,7 +962,8 @@ struct Solve {
     gemm_scale_kernel<<<(unsigned)pr.B, 1024, 0, st>>>(F(L.g2[cur]), (int)pr.d2, F(L.gx),
                                                         F(L.gvmax));
     CK(cudaGetLastError());
-    if (int e = gemm(true, F(L.kmat), F(L.gx), F(L.gs))) return e;
+    if (int e = umma_split(F(L.gx), (int)pr.d2, L.ldk2, F(L.gxh), F(L.gxl))) return e;
+    if (int e = gemm(true, tm_k, F(L.gs))) return e;
     int* nfall = at<int>(ws, L.counters);
     CK(cudaMemsetAsync(nfall, 0, 4, st));
     GemmRowParams rp = {};
@@ -971,12 +986,13 @@ struct Solve {
     gemm_row_fallback_kernel<<<(unsigned)di.sms, 256, 0, st>>>(rp, cost, F(L.g2[cur]),
                                                                 -kLog2e / lam);
     CK(cudaGetLastError());
-    if (int e = gemm(false, F(L.kmat), F(L.ga), F(L.gt))) return e;
+    if (int e = umma_split(F(L.ga), (int)pr.d1, L.ldk1, F(L.gah), F(L.gal))) return e;
+    if (int e = gemm(false, tm_kt, F(L.gt))) return e;
     return gemm_col(F(L.gvmax), F(L.g2[cur]), F(L.g2[cur ^ 1]), res);
   }
   // E0 from the last iteration's X and a: sum_i a_i ((K o C) X)_i
   int gemm_e0(float* out_cost) {
-    if (int e = gemm(true, F(L.kc), F(L.gx), F(L.gs))) return e;
+    if (int e = gemm(true, tm_kc, F(L.gs))) return e;
     ++g_launches;
     gemm_e0_kernel<<<(unsigned)pr.B, 256, 0, st>>>(F(L.ga), F(L.gs), (int)pr.d1, out_cost,
                                                    at<int>(ws, L.status));
@@ -1031,13 +1047,7 @@ struct Solve {
     using K = TiledK<BT, PT, kGrid, kModeUpdate>;
     auto kern = &persistent_solve_kernel<BT, PT, QC, RB, RP, NSTAGE, kGrid>;
     const size_t smem = K::S::SMEM_BYTES;
-    static bool attr_set[2] = {false, false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!attr_set[kGrid ? 1 : 0]) {
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_set[kGrid ? 1 : 0] = true;
-    }
+    if (int e = set_max_smem(reinterpret_cast<const void*>(kern), smem)) return e;
     // every CTA must own >= 1 row of both sweep orientations
     const long long G = std::min<long long>(
         di.sms, std::min(tiled_chunks<BT, PT>(L, (int)pr.d2, (int)pr.d1),
@@ -1087,7 +1097,6 @@ struct Solve {
     CK(cudaStreamSynchronize(st));
     *iters = h[0];
     *cur = h[1];
-    (void)dev;
     return 0;
   }
 
@@ -1130,19 +1139,18 @@ struct Solve {
     if (!(L.tiled || L.sep) || g_reducer != nullptr || (op.flags & SINKHORN_FLAG_TILED_ONLY))
       return 0;
     if (pr.cost_kind != SINKHORN_COST_SHARED && pr.cost_kind != SINKHORN_COST_GRID2D) return 0;
-    static int smem_optin = 0;
-    if (smem_optin == 0)
-      cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, di.dev);
+    int smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, di.dev);
     const long long d1 = pr.d1, d2 = pr.d2, B = pr.B;
-    static bool attr_set = false;
     auto kern = &small_solve_kernel<kSmallNT>;
-    if (!attr_set) {
+    {
       cudaFuncAttributes fa = {};
       CK(cudaFuncGetAttributes(&fa, kern));
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              smem_optin - (int)fa.sharedSizeBytes));
+      if (int e = set_max_smem(reinterpret_cast<const void*>(kern),
+                               (size_t)(smem_optin - (int)fa.sharedSizeBytes)))
+        return e;
+      // a function attribute, also per device; cheap enough to set every call
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      attr_set = true;
     }
     for (int occ = 4; occ >= 1; --occ) {
       const int Lc = (int)((B + (long long)di.sms * occ - 1) / ((long long)di.sms * occ));
@@ -1462,10 +1470,11 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     CK(cudaGetLastError());
   }
   if (L.gemm) {
-    const size_t nk = (size_t)pr.d1 * pr.d2;
+    dim3 g((unsigned)((pr.d2 + 31) / 32), (unsigned)((pr.d1 + 31) / 32));
     ++g_launches;
-    gemm_kernel_matrices<<<grid_for(nk), 256, 0, st>>>(cost, nk, (float)(-kLog2e / op.lambda),
-                                                        S.F(L.kmat), S.F(L.kc), status);
+    umma_kernel_matrices<<<g, 256, 0, st>>>(cost, (int)pr.d1, (int)pr.d2, L.ldk1, L.ldk2,
+                                            (float)(-kLog2e / op.lambda), S.F(L.kmat),
+                                            S.F(L.kc), S.F(L.kmatT), status);
     CK(cudaGetLastError());
   } else if (pr.cost_kind == SINKHORN_COST_SHARED) {
     dim3 g((unsigned)((L.D2p + 31) / 32), (unsigned)((L.D1p + 31) / 32));
@@ -1505,6 +1514,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   if (int e = S.plan_small(sp, small_grid, small_smem, &small)) return e;
   if (!small) {
     if (int e = S.setup_maps()) return e;
+    if (int e = S.setup_umma_maps()) return e;
   }
 
   // ---- lockstep iteration (batch.py:314-324) ----
@@ -1585,7 +1595,11 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
       fg = fused_graph_slot(FusedGraphKey{ws, cost, pr.B, pr.d1, pr.d2, pr.cost_kind, op.lambda,
                                           op.max_iters, S.di.dev});
     if (fg != nullptr && fg->seen && fg->exec == nullptr) {   // second sighting: capture
-      static thread_local cudaStream_t cs = nullptr;
+      // a capture stream per (thread, device): a stream belongs to the device
+      // that was current when it was created
+      static thread_local cudaStream_t cs_dev[64] = {};
+      if (S.di.dev < 0 || S.di.dev >= 64) return fail(SINKHORN_STATUS_CUDA_ERROR, "device ordinal");
+      cudaStream_t& cs = cs_dev[S.di.dev];
       if (cs == nullptr) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
       const unsigned long long l0 = g_launches;
       S.st = cs;
@@ -1718,9 +1732,15 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   int hstatus = 0;
   if (int e = S.read_status(&hstatus)) return e;
   static const bool no_rerun = getenv("SKB_NO_RERUN") != nullptr;   // diagnostics
-  if (allow_est && (L.tiled || L.fused || L.gemm) && !no_rerun) {
+  if (allow_est) {
     int hfail = 0;
-    CK(cudaMemcpy(&hfail, S.est_fail, 4, cudaMemcpyDeviceToHost));
+    if ((L.tiled || L.fused || L.gemm) && !no_rerun)
+      CK(cudaMemcpy(&hfail, S.est_fail, 4, cudaMemcpyDeviceToHost));
+    // With a reducer installed (batch-sharded solves) the rerun is decided
+    // across ranks: every rank's first attempt calls the reducer here once,
+    // whatever its path, and all ranks rerun if any rank's estimate failed --
+    // the reruns' stopping tests then call the reducer in step on every rank.
+    if (g_reducer) hfail = g_reducer(hfail ? 1.0 : 0.0, g_reducer_user) > 0.0 ? 1 : 0;
     if (hfail) {   // an estimate overshot: recompute the whole solve exactly
       ++g_exact_reruns;
       if (timed) {

@@ -9,8 +9,9 @@
 //     v'_j = l2nu_j + vmax_b - log2 T_j
 // which is the reference's iteration (batch.py:314-316) with the log-sum-exps
 // shifted by vmax_b, a valid shift (no term exceeds 1).  The two contractions
-// over the whole (B, d1, d2) space are plain GEMMs, run by cuBLAS in fp32
-// (BF16x9 emulation on the tensor cores where cuBLAS picks it).  Range
+// over the whole (B, d1, d2) space run on the tcgen05 tensor cores in 3xTF32
+// (sweep_umma.cuh: K and its stored transpose streamed once per contraction,
+// fp32-accurate products, promoted fp32 accumulation).  Range
 // guards: a row with S_i < 2^-60 (its terms may have flushed to zero) is
 // redone exactly in the log domain from the caller's cost; a column with
 // T_j < 2^-60 or a non-finite update flags the solve for the exact rerun.
@@ -150,21 +151,6 @@ __global__ void gemm_col_kernel(const GemmColParams p) {
       atomic_max_nonneg(&p.res[b], fabsf(exp2f(p.v_old[k] - p.vmax[b] + lt) - p.nu[k]));
     p.v_new[k] = vn;
   }
-}
-
-// K = 2^(c * kscale) and KC = K * c (E0), from the caller's cost.
-__global__ void gemm_kernel_matrices(const float* __restrict__ c, size_t n, float kscale,
-                                     float* __restrict__ K, float* __restrict__ KC, int* status) {
-  bool bad = false;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const float cv = c[i];
-    if (!(cv >= 0.f) || isinf(cv)) bad = true;
-    const float k = ex2(cv * kscale);
-    K[i] = k;
-    KC[i] = k * cv;
-  }
-  if (__any_sync(0xffffffffu, bad) && lane_id() == 0) set_status(status, 15);
 }
 
 // a0 = 1 on the support of mu (u0 = 0 there), 0 off it (batch.py:295).
