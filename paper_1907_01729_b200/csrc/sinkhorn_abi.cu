@@ -244,20 +244,23 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     L.si1 = 1;
     L.sb2 = L.D2p;
     L.si2 = 1;
-    // K and K o C row-major [d1][ldk2], K^T [d2][ldk1] (the column sweep's A
-    // operand, so both contractions read a K-major tile), row pitch a 16-byte
-    // multiple for TMA
-    L.ldk1 = (int)round_up(pr.d1, 4);
-    L.ldk2 = (int)round_up(pr.d2, 4);
-    L.kmat = c.take((size_t)pr.d1 * L.ldk2 * 4);
-    L.kc = c.take((size_t)pr.d1 * L.ldk2 * 4);
-    L.kmatT = c.take((size_t)pr.d2 * L.ldk1 * 4);
+    // K and K o C over (d1 rows, d2 reduction), K^T over (d2 rows, d1
+    // reduction) -- the column sweep's A operand, so both contractions read
+    // K-major tiles -- in the tile-major operand layout of sweep_umma.cuh
+    // (extents padded to 128 rows x 32-column chunks)
+    L.ldk1 = (int)round_up(pr.d1, 128);   // padded row / reduction extents
+    L.ldk2 = (int)round_up(pr.d2, 128);
+    L.kmat = c.take((size_t)L.ldk1 * L.ldk2 * 4);
+    L.kc = c.take((size_t)L.ldk1 * L.ldk2 * 4);
+    L.kmatT = c.take((size_t)L.ldk2 * L.ldk1 * 4);
     const size_t n1 = (size_t)L.B * L.D1p * 4, n2 = (size_t)L.B * L.D2p * 4;
-    // tf32 hi / lo planes of X [B][ldk2] and a [B][ldk1] (the MMAs' B operands)
-    L.gxh = c.take((size_t)L.B * L.ldk2 * 4);
-    L.gxl = c.take((size_t)L.B * L.ldk2 * 4);
-    L.gah = c.take((size_t)L.B * L.ldk1 * 4);
-    L.gal = c.take((size_t)L.B * L.ldk1 * 4);
+    // tf32 hi / lo planes of X (reduction d2) and a (reduction d1): the MMAs'
+    // B operands, tiled [B/64][chunks][64][32]
+    const size_t bpad = round_up(pr.B, kUmBN);
+    L.gxh = c.take(bpad * L.ldk2 * 4);
+    L.gxl = c.take(bpad * L.ldk2 * 4);
+    L.gah = c.take(bpad * L.ldk1 * 4);
+    L.gal = c.take(bpad * L.ldk1 * 4);
     L.um_part = c.take((size_t)sms * 2 * kUmBN * kUmBM * 4);
     L.f2 = c.take(n1);
     L.g2[0] = c.take(n2);
@@ -890,20 +893,26 @@ struct Solve {
   CUtensorMap tm_k, tm_kt, tm_kc, tm_xh, tm_xl, tm_ah, tm_al;
   int setup_umma_maps() {
     if (!L.gemm) return 0;
-    const size_t d1 = (size_t)pr.d1, d2 = (size_t)pr.d2, B = (size_t)pr.B;
-    bool ok = make_tmap_sw128(&tm_k, F(L.kmat), d1, d2, L.ldk2, kUmBM);
-    ok &= make_tmap_sw128(&tm_kc, F(L.kc), d1, d2, L.ldk2, kUmBM);
-    ok &= make_tmap_sw128(&tm_kt, F(L.kmatT), d2, d1, L.ldk1, kUmBM);
-    ok &= make_tmap_sw128(&tm_xh, F(L.gxh), B, d2, L.ldk2, kUmBN);
-    ok &= make_tmap_sw128(&tm_xl, F(L.gxl), B, d2, L.ldk2, kUmBN);
-    ok &= make_tmap_sw128(&tm_ah, F(L.gah), B, d1, L.ldk1, kUmBN);
-    ok &= make_tmap_sw128(&tm_al, F(L.gal), B, d1, L.ldk1, kUmBN);
+    // tiled operands: 2-D [tiles * chunks * sub-blocks * rows][32] maps, pitch 128 B
+    const size_t k1 = (size_t)(pr.d1 + kUmBK - 1) / kUmBK * kUmSub;   // 32-wide sub-blocks
+    const size_t k2 = (size_t)(pr.d2 + kUmBK - 1) / kUmBK * kUmSub;
+    const size_t mt1 = (size_t)L.ldk1 / kUmBM, mt2 = (size_t)L.ldk2 / kUmBM;
+    const size_t nt = (size_t)(pr.B + kUmBN - 1) / kUmBN;
+    bool ok = make_tmap_sw128(&tm_k, F(L.kmat), mt1 * k2 * kUmBM, 32, 32, kUmBM);
+    ok &= make_tmap_sw128(&tm_kc, F(L.kc), mt1 * k2 * kUmBM, 32, 32, kUmBM);
+    ok &= make_tmap_sw128(&tm_kt, F(L.kmatT), mt2 * k1 * kUmBM, 32, 32, kUmBM);
+    ok &= make_tmap_sw128(&tm_xh, F(L.gxh), nt * k2 * kUmBN, 32, 32, kUmBN);
+    ok &= make_tmap_sw128(&tm_xl, F(L.gxl), nt * k2 * kUmBN, 32, 32, kUmBN);
+    ok &= make_tmap_sw128(&tm_ah, F(L.gah), nt * k1 * kUmBN, 32, 32, kUmBN);
+    ok &= make_tmap_sw128(&tm_al, F(L.gal), nt * k1 * kUmBN, 32, 32, kUmBN);
     return ok ? 0 : fail(SINKHORN_STATUS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (umma)");
   }
-  // the lane operand's tf32 planes from its lane-major fp32 array
-  int umma_split(const float* x, int d, int ld, float* hi, float* lo) {
+  // the lane operand's tf32 planes (tiled) from its lane-major fp32 array
+  int umma_split(const float* x, int d, float* hi, float* lo) {
+    const long long kch = (d + kUmBK - 1) / kUmBK;
     ++g_launches;
-    umma_split_kernel<<<grid_for((size_t)pr.B * ld), 256, 0, st>>>(x, pr.B, d, ld, hi, lo);
+    umma_split_kernel<<<grid_for((size_t)round_up(pr.B, kUmBN) * kch * kUmBK), 256, 0, st>>>(
+        x, (int)pr.B, d, kch, hi, lo);
     CK(cudaGetLastError());
     return 0;
   }
@@ -952,7 +961,7 @@ struct Solve {
     gemm_first_a_kernel<<<grid_for((size_t)pr.B * pr.d1), 256, 0, st>>>(F(L.mu),
                                                                        (size_t)pr.B * pr.d1, F(L.ga));
     CK(cudaMemsetAsync(F(L.gvmax0), 0, (size_t)pr.B * 4, st));
-    if (int e = umma_split(F(L.ga), (int)pr.d1, L.ldk1, F(L.gah), F(L.gal))) return e;
+    if (int e = umma_split(F(L.ga), (int)pr.d1, F(L.gah), F(L.gal))) return e;
     if (int e = gemm(false, tm_kt, F(L.gt))) return e;
     return gemm_col(F(L.gvmax0), nullptr, F(L.g2[1]), false);
   }
@@ -962,7 +971,7 @@ struct Solve {
     gemm_scale_kernel<<<(unsigned)pr.B, 1024, 0, st>>>(F(L.g2[cur]), (int)pr.d2, F(L.gx),
                                                         F(L.gvmax));
     CK(cudaGetLastError());
-    if (int e = umma_split(F(L.gx), (int)pr.d2, L.ldk2, F(L.gxh), F(L.gxl))) return e;
+    if (int e = umma_split(F(L.gx), (int)pr.d2, F(L.gxh), F(L.gxl))) return e;
     if (int e = gemm(true, tm_k, F(L.gs))) return e;
     int* nfall = at<int>(ws, L.counters);
     CK(cudaMemsetAsync(nfall, 0, 4, st));
@@ -986,7 +995,7 @@ struct Solve {
     gemm_row_fallback_kernel<<<(unsigned)di.sms, 256, 0, st>>>(rp, cost, F(L.g2[cur]),
                                                                 -kLog2e / lam);
     CK(cudaGetLastError());
-    if (int e = umma_split(F(L.ga), (int)pr.d1, L.ldk1, F(L.gah), F(L.gal))) return e;
+    if (int e = umma_split(F(L.ga), (int)pr.d1, F(L.gah), F(L.gal))) return e;
     if (int e = gemm(false, tm_kt, F(L.gt))) return e;
     return gemm_col(F(L.gvmax), F(L.g2[cur]), F(L.g2[cur ^ 1]), res);
   }
@@ -1470,9 +1479,9 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     CK(cudaGetLastError());
   }
   if (L.gemm) {
-    dim3 g((unsigned)((pr.d2 + 31) / 32), (unsigned)((pr.d1 + 31) / 32));
+    dim3 g((unsigned)(L.ldk2 / 32), (unsigned)(L.ldk1 / 32));
     ++g_launches;
-    umma_kernel_matrices<<<g, 256, 0, st>>>(cost, (int)pr.d1, (int)pr.d2, L.ldk1, L.ldk2,
+    umma_kernel_matrices<<<g, 256, 0, st>>>(cost, (int)pr.d1, (int)pr.d2,
                                             (float)(-kLog2e / op.lambda), S.F(L.kmat),
                                             S.F(L.kc), S.F(L.kmatT), status);
     CK(cudaGetLastError());

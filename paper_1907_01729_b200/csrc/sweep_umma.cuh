@@ -22,7 +22,8 @@
 // (tile, k-chunk) units, split tiles merged in ascending CTA order by
 // umma_fixup_kernel -- deterministic, like the reference's ascending span
 // merge, batch.py:198-201):
-//   warp 0      TMA producer: A tile [128][32] + B hi/lo tiles [64][32], SW128
+//   warp 0      TMA producer, A ring: tile [128][32] (evict-first), SW128
+//   warp 3      TMA producer, B ring: hi / lo tiles [64][32] (evict-last)
 //   warp 1      MMA issuer (one thread): 12 kind::tf32 MMAs per chunk, A from TMEM
 //   warp 2      TMEM allocator
 //   warps 4-7   splitters: A tile rows smem -> registers -> hi / lo -> TMEM
@@ -38,17 +39,42 @@ namespace skb {
 
 constexpr int kUmBM = 128;       // MMA M (rows of A per tile)
 constexpr int kUmBN = 64;        // MMA N (lanes per tile)
-constexpr int kUmBK = 32;        // reduction indices per chunk (one 128-byte swizzle row)
-constexpr int kUmStages = 4;     // shared-memory stages
-constexpr int kUmAStages = 3;    // TMEM A stages (hi + lo, 64 columns each)
-constexpr int kUmSlots = 4;      // TMEM accumulator slots (64 columns each)
+#ifndef SKB_UM_SUB
+#define SKB_UM_SUB 2
+#endif
+constexpr int kUmSub = SKB_UM_SUB;   // 32-wide sub-blocks (one 128-byte swizzle row) per chunk
+constexpr int kUmBK = 32 * kUmSub;   // reduction indices per chunk
+#ifndef SKB_UM_ASM
+#define SKB_UM_ASM (8 / SKB_UM_SUB)
+#endif
+#ifndef SKB_UM_BSM
+#define SKB_UM_BSM (6 / SKB_UM_SUB)
+#endif
+#ifndef SKB_UM_ATM
+#define SKB_UM_ATM (4 / SKB_UM_SUB)
+#endif
+#ifndef SKB_UM_SLOTS
+#define SKB_UM_SLOTS 2
+#endif
+#ifndef SKB_UM_PROMO
+#define SKB_UM_PROMO 1
+#endif
+constexpr int kUmAStagesSm = SKB_UM_ASM;   // shared-memory A tile ring
+constexpr int kUmBStagesSm = SKB_UM_BSM;   // shared-memory B hi/lo ring
+constexpr int kUmAStages = SKB_UM_ATM;     // TMEM A stages (hi | lo, 2 * kUmBK columns each)
+constexpr int kUmSlots = SKB_UM_SLOTS;     // TMEM accumulator slot sets
+constexpr int kUmPromo = SKB_UM_PROMO;     // chunks accumulated in TMEM per promotion
+constexpr int kUmSlotCols = 2 * kUmBN;     // [hi*hi + lo*hi | hi*lo]
+constexpr int kUmACols = 2 * kUmBK;
+static_assert(kUmSlots * kUmSlotCols + kUmAStages * kUmACols <= 512, "TMEM budget");
 constexpr int kUmThreads = 384;
 constexpr uint32_t kUmTmemCols = 512;
-constexpr uint32_t kUmABase = kUmSlots * kUmBN;   // A stages after the accumulator slots
-constexpr int kUmATileBytes = kUmBM * kUmBK * 4;  // 16 KB
-constexpr int kUmBTileBytes = kUmBN * kUmBK * 4;  // 8 KB
-constexpr int kUmStageBytes = kUmATileBytes + 2 * kUmBTileBytes;
-constexpr int kUmSmemBytes = kUmStages * kUmStageBytes + 1024;
+constexpr uint32_t kUmABase = kUmSlots * kUmSlotCols;   // A stages after the accumulators
+constexpr int kUmASubBytes = kUmBM * 32 * 4;            // 16 KB: one [128][32] box
+constexpr int kUmBSubBytes = kUmBN * 32 * 4;            // 8 KB: one [64][32] box (one plane)
+constexpr int kUmATileBytes = kUmSub * kUmASubBytes;
+constexpr int kUmBStageBytes = kUmSub * 2 * kUmBSubBytes;   // per sub-block: hi rows, then lo rows
+constexpr int kUmSmemBytes = kUmAStagesSm * kUmATileBytes + kUmBStagesSm * kUmBStageBytes + 1024;
 
 struct UmmaParams {
   int M, N, K;          // D is M x N, reduction length K
@@ -79,16 +105,23 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   extern __shared__ uint8_t um_smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(um_smem_raw) + 1023) &
                                            ~uintptr_t(1023));
-  __shared__ uint64_t full[kUmStages], kfree[kUmStages];
+  __shared__ uint64_t afull_sm[kUmAStagesSm], afree_sm[kUmAStagesSm];
+  __shared__ uint64_t bfull_sm[kUmBStagesSm], bfree_sm[kUmBStagesSm];
   __shared__ uint64_t afull[kUmAStages], aempty[kUmAStages];
   __shared__ uint64_t cfull[kUmSlots], cempty[kUmSlots];
   __shared__ uint32_t tmem_base_sh;
+  uint8_t* smA = sm;
+  uint8_t* smB = sm + kUmAStagesSm * kUmATileBytes;
 
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kUmStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&kfree[s], 4 + 1);   // 4 splitter warps (A) + the MMA commit (B)
+    for (int s = 0; s < kUmAStagesSm; ++s) {
+      mbar_init(&afull_sm[s], 1);
+      mbar_init(&afree_sm[s], 4);    // the 4 splitter warps
+    }
+    for (int s = 0; s < kUmBStagesSm; ++s) {
+      mbar_init(&bfull_sm[s], 1);
+      mbar_init(&bfree_sm[s], 1);    // the MMA commit
     }
     for (int a = 0; a < kUmAStages; ++a) {
       mbar_init(&afull[a], 4);
@@ -112,55 +145,103 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   const uint32_t tbase = tmem_base_sh;
 
   pdl_wait();
+#ifdef SKB_UM_DBG_CLOCK
+  const long long dbg_t0 = clock64();
+#endif
   const bool skip = p.status != nullptr && *p.status != 0;
   const long long u0 = um_start(p.units, p.G, blockIdx.x);
   const long long u1 = um_start(p.units, p.G, blockIdx.x + 1);
 
   if (!skip && warp == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA producer, A ring (the streamed kernel matrix) ----------------
     if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
       int s = 0;
       uint32_t ph = 0;
       for (long long u = u0; u < u1; ++u) {
         const long long tile = u / p.KCH;
         const int kc = (int)(u % p.KCH);
-        const int nt = (int)(tile % p.NT), mt = (int)(tile / p.NT);
-        mbar_wait(&kfree[s], ph ^ 1);
-        uint8_t* st = sm + (size_t)s * kUmStageBytes;
-        mbar_arrive_expect_tx(&full[s], kUmStageBytes);
-        tma_load_2d(st, &tmA, kc * kUmBK, mt * kUmBM, &full[s]);
-        tma_load_2d(st + kUmATileBytes, &tmBh, kc * kUmBK, nt * kUmBN, &full[s]);
-        tma_load_2d(st + kUmATileBytes + kUmBTileBytes, &tmBl, kc * kUmBK, nt * kUmBN, &full[s]);
-        if (++s == kUmStages) { s = 0; ph ^= 1; }
+        const int mt = (int)(tile / p.NT);
+        mbar_wait(&afree_sm[s], ph ^ 1);
+        mbar_arrive_expect_tx(&afull_sm[s], kUmATileBytes);
+        const int arow = (int)(((long long)mt * p.KCH + kc) * kUmSub * kUmBM);
+#pragma unroll
+        for (int sb = 0; sb < kUmSub; ++sb)
+          tma_load_2d_hint(smA + (size_t)s * kUmATileBytes + sb * kUmASubBytes, &tmA, 0,
+                           arow + sb * kUmBM, &afull_sm[s], pol);
+        if (++s == kUmAStagesSm) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (!skip && warp == 3) {
+    // ---------------- TMA producer, B ring (the lanes' tf32 planes) ----------------
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_last();
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long u = u0; u < u1; ++u) {
+        const long long tile = u / p.KCH;
+        const int kc = (int)(u % p.KCH);
+        const int nt = (int)(tile % p.NT);
+        mbar_wait(&bfree_sm[s], ph ^ 1);
+        uint8_t* st = smB + (size_t)s * kUmBStageBytes;
+        mbar_arrive_expect_tx(&bfull_sm[s], kUmBStageBytes);
+        const int brow = (int)(((long long)nt * p.KCH + kc) * kUmSub * kUmBN);
+#pragma unroll
+        for (int sb = 0; sb < kUmSub; ++sb) {
+          tma_load_2d_hint(st + sb * 2 * kUmBSubBytes, &tmBh, 0, brow + sb * kUmBN, &bfull_sm[s], pol);
+          tma_load_2d_hint(st + sb * 2 * kUmBSubBytes + kUmBSubBytes, &tmBl, 0, brow + sb * kUmBN,
+                           &bfull_sm[s], pol);
+        }
+        if (++s == kUmBStagesSm) { s = 0; ph ^= 1; }
       }
     }
   } else if (!skip && warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_tf32(kUmBM, kUmBN);
+      const uint32_t idesc2 = umma_idesc_tf32(kUmBM, 2 * kUmBN);
       int s = 0, a = 0, r = 0;
       uint32_t ph = 0, aph = 0, rph = 0;
+      long long span0 = u0;   // first chunk of the current promotion span
       for (long long u = u0; u < u1; ++u) {
-        mbar_wait(&cempty[r], rph ^ 1);
-        mbar_wait(&full[s], ph);
+        const long long piece0 = u0 > (u / p.KCH) * p.KCH ? u0 : (u / p.KCH) * p.KCH;
+        const bool first = (u - piece0) % kUmPromo == 0;
+        const bool last = (u - piece0) % kUmPromo == kUmPromo - 1 || u + 1 == u1 ||
+                          (u + 1) % p.KCH == 0;
+        if (first) {
+          span0 = u;
+          mbar_wait(&cempty[r], rph ^ 1);
+        }
+        mbar_wait(&bfull_sm[s], ph);
         mbar_wait(&afull[a], aph);
         tc_fence_after();
-        const uint32_t sb = smem_u32(sm + (size_t)s * kUmStageBytes);
-        const uint32_t bh = sb + kUmATileBytes, bl = bh + kUmBTileBytes;
-        const uint32_t ahi = tbase + kUmABase + 64 * a, alo = ahi + 32;
-        const uint32_t d = tbase + r * kUmBN;
+        const uint32_t bst = smem_u32(smB + (size_t)s * kUmBStageBytes);
+        const uint32_t ahi = tbase + kUmABase + kUmACols * a, alo = ahi + kUmBK;
+        // per k-step two MMAs: hi x [B hi ; B lo] as one N = 128 MMA (the two
+        // planes are adjacent 64-row halves of the sub-block, one 1024-byte-
+        // strided operand) into the slot set's columns [0, 128), then lo x B hi
+        // (N = 64) accumulated onto the hi x B hi columns [0, 64).  An N = 64
+        // MMA costs ~45 cycles, an N = 128 one 64 (tools/micro/umma_rate.cu).
+        const uint32_t d = tbase + r * kUmSlotCols;
+        const uint32_t acc = (u > span0) ? 1u : 0u;
+#ifdef SKB_UM_DBG_NOMMA
+        if (false)
+#endif
 #pragma unroll
         for (int k = 0; k < kUmBK / 8; ++k) {
-          umma_tf32_ts(d, ahi + 8 * k, umma_sdesc_sw128(bh + 32 * k), idesc, k > 0);
-          umma_tf32_ts(d, ahi + 8 * k, umma_sdesc_sw128(bl + 32 * k), idesc, 1);
-          umma_tf32_ts(d, alo + 8 * k, umma_sdesc_sw128(bh + 32 * k), idesc, 1);
+          const uint32_t ak = k > 0 ? 1u : acc;
+          const uint64_t bd = umma_sdesc_sw128(bst + (k / 4) * 2 * kUmBSubBytes + 32 * (k % 4));
+          umma_tf32_ts(d, ahi + 8 * k, bd, idesc2, ak);
+          umma_tf32_ts(d, alo + 8 * k, bd, idesc, 1);
         }
-        umma_commit(&kfree[s]);
+        umma_commit(&bfree_sm[s]);
         umma_commit(&aempty[a]);
-        umma_commit(&cfull[r]);
-        if (++s == kUmStages) { s = 0; ph ^= 1; }
+        if (++s == kUmBStagesSm) { s = 0; ph ^= 1; }
         if (++a == kUmAStages) { a = 0; aph ^= 1; }
-        if (++r == kUmSlots) { r = 0; rph ^= 1; }
+        if (last) {
+          umma_commit(&cfull[r]);
+          if (++r == kUmSlots) { r = 0; rph ^= 1; }
+        }
       }
     }
   } else if (!skip && warp >= 4 && warp < 8) {
@@ -170,33 +251,43 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     int s = 0, a = 0;
     uint32_t ph = 0, aph = 0;
     for (long long u = u0; u < u1; ++u) {
-      mbar_wait(&full[s], ph);
-      const float4* rowp =
-          reinterpret_cast<const float4*>(sm + (size_t)s * kUmStageBytes + row * 128);
-      uint32_t hi[32], lo[32];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 v = rowp[q ^ (row & 7)];
-        const float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float h = tf32_hi(x[e]);
-          hi[4 * q + e] = __float_as_uint(h);
-          lo[4 * q + e] = __float_as_uint(x[e] - h);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&kfree[s])) : "memory");
+      mbar_wait(&afull_sm[s], ph);
       mbar_wait(&aempty[a], aph ^ 1);
       tc_fence_after();
-      const uint32_t ahi = tbase + lane_off + kUmABase + 64 * a;
-      tmem_st32(ahi, hi);
-      tmem_st32(ahi + 32, lo);
+      const uint32_t ahi = tbase + lane_off + kUmABase + kUmACols * a;
+#pragma unroll
+      for (int sb = 0; sb < kUmSub; ++sb) {
+        const float4* rowp = reinterpret_cast<const float4*>(smA + (size_t)s * kUmATileBytes +
+                                                             sb * kUmASubBytes + row * 128);
+        uint32_t hi[32], lo[32];
+#if defined(SKB_UM_DBG_NOSPLIT) || defined(SKB_UM_DBG_NOLDS)
+        if (false)
+#endif
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 v = rowp[q ^ (row & 7)];
+          const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float h = tf32_hi(x[e]);
+            hi[4 * q + e] = __float_as_uint(h);
+            lo[4 * q + e] = __float_as_uint(x[e] - h);
+          }
+        }
+#ifndef SKB_UM_DBG_NOSPLIT
+        tmem_st32(ahi + 32 * sb, hi);
+        tmem_st32(ahi + kUmBK + 32 * sb, lo);
+#endif
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&afree_sm[s])) : "memory");
+#ifndef SKB_UM_DBG_NOSPLIT
       tmem_st_wait();
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&afull[a])) : "memory");
-      if (++s == kUmStages) { s = 0; ph ^= 1; }
+      if (++s == kUmAStagesSm) { s = 0; ph ^= 1; }
       if (++a == kUmAStages) { a = 0; aph ^= 1; }
     }
   } else if (!skip && warp >= 8) {
@@ -214,16 +305,21 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       float acc[kUmBN];
 #pragma unroll
       for (int n = 0; n < kUmBN; ++n) acc[n] = 0.f;
-      for (int kc = k0; kc < k1; ++kc) {
+      for (int kc = k0; kc < k1; kc += kUmPromo) {
         mbar_wait(&cfull[r], rph);
         tc_fence_after();
+#ifdef SKB_UM_DBG_NOEPI
+        if (false)
+#endif
 #pragma unroll
         for (int h = 0; h < kUmBN / 32; ++h) {
-          uint32_t v[32];
-          tmem_ld32(tbase + lane_off + r * kUmBN + 32 * h, v);
+          uint32_t v0[32], v1[32];
+          const uint32_t t = tbase + lane_off + r * kUmSlotCols + 32 * h;
+          tmem_ld32(t, v0);
+          tmem_ld32(t + kUmBN, v1);
           tmem_ld_wait();
 #pragma unroll
-          for (int n = 0; n < 32; ++n) acc[32 * h + n] += __uint_as_float(v[n]);
+          for (int n = 0; n < 32; ++n) acc[32 * h + n] += __uint_as_float(v1[n]) + __uint_as_float(v0[n]);
         }
         tc_fence_before();
         __syncwarp();
@@ -250,6 +346,13 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+#ifdef SKB_UM_DBG_CLOCK
+  if (threadIdx.x == 0) {
+    extern __device__ unsigned long long g_um_dbg_cycles[2];
+    atomicAdd(&g_um_dbg_cycles[0], (unsigned long long)(clock64() - dbg_t0));
+    atomicAdd(&g_um_dbg_cycles[1], (unsigned long long)(u1 - u0));
+  }
+#endif
   pdl_launch_dependents();
   if (warp == 2) {
     tc_fence_after();
@@ -282,54 +385,78 @@ __global__ void __launch_bounds__(256) umma_fixup_kernel(const UmmaParams p) {
   }
 }
 
-// hi / lo tf32 planes [rows][ld] of a lane-major [rows][cols] fp32 array (ld >=
-// cols; the padding columns are written as 0).
-__global__ void umma_split_kernel(const float* __restrict__ x, long long rows, int cols, int ld,
+// Operand layout.  Every operand is stored tile-major,
+// [tile][chunk][sub-block][row][32]: an R x 32 sub-block (R = 128 or 64) is one
+// contiguous 16 / 8 KB run, so each TMA box is a single sequential read, and a
+// CTA's stream-K range (consecutive chunks of consecutive tiles) is one
+// contiguous stretch of HBM.  Element (r, k) of an operand with R-row tiles
+// and kch chunks of kUmBK sits at
+//   ((r / R) * kch + k / kUmBK) * R * kUmBK + ((k % kUmBK) / 32) * R * 32 + (r % R) * 32 + k % 32.
+__host__ __device__ __forceinline__ long long um_tiled_index(long long r, long long k, int R,
+                                                             long long kch) {
+  return ((r / R) * kch + k / kUmBK) * R * kUmBK + ((k % kUmBK) / 32) * R * 32 + (r % R) * 32 +
+         (k % 32);
+}
+
+// hi / lo tf32 planes of a lane-major [rows][cols] fp32 array in the tiled
+// B-operand layout (64-row tiles, kch chunks; the padding reads as 0).
+// grid-stride over the padded [NT*64][kch*32] index space.
+__global__ void umma_split_kernel(const float* __restrict__ x, int rows, int cols, long long kch,
                                   float* __restrict__ hi, float* __restrict__ lo) {
-  const long long n = rows * ld;
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
-       k += (long long)gridDim.x * blockDim.x) {
-    const long long b = k / ld;
-    const int j = (int)(k - b * ld);
-    const float v = j < cols ? x[b * cols + j] : 0.f;
+  const int nt = (rows + kUmBN - 1) / kUmBN;
+  const long long n = (long long)nt * kUmBN * kch * kUmBK;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    // e enumerates the tiled array itself (coalesced stores)
+    const long long blk = e / (kUmBN * kUmBK);        // (tile, chunk)
+    const int within = (int)(e % (kUmBN * kUmBK));
+    const int sb = within / (kUmBN * 32), w2 = within % (kUmBN * 32);
+    const int r = (int)((blk / kch) * kUmBN + w2 / 32);
+    const long long k = (blk % kch) * kUmBK + sb * 32 + w2 % 32;
+    const float v = (r < rows && k < cols) ? x[(long long)r * cols + k] : 0.f;
     const float h = tf32_hi(v);
-    hi[k] = h;
-    lo[k] = v - h;
+    hi[e] = h;
+    lo[e] = v - h;
   }
 }
 
-// K = 2^(c * kscale), K o C (E0) row-major [d1][ldk2] and K^T [d2][ldk1] from
-// the caller's cost (validated: finite, >= 0, status 15), 32 x 32 tiles
-// through shared memory so both the row-major and the transposed stores are
-// coalesced.  grid (ceil(d2/32), ceil(d1/32)), block 256.
+// K = 2^(c * kscale) and K o C (E0) as tiled A operands over (d1 rows, d2
+// reduction), and K^T over (d2 rows, d1 reduction), from the caller's cost
+// (validated: finite, >= 0, status 15).  One block per 32 x 32 cost block
+// through shared memory: in the tiled layout a 32 x 32 block is one
+// contiguous 4 KB run for both orientations.  The padded extents are
+// covered too (zeros).  grid (ceil(D2p/32), ceil(D1p/32)) with D1p, D2p the
+// extents rounded up to 128; block 256.
 __global__ void __launch_bounds__(256) umma_kernel_matrices(const float* __restrict__ c, int d1,
-                                                            int d2, int ldk1, int ldk2, float kscale,
+                                                            int d2, float kscale,
                                                             float* __restrict__ K, float* __restrict__ KC,
                                                             float* __restrict__ KT, int* status) {
   __shared__ float tile[32][33];
   const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  const long long kch1 = (d1 + kUmBK - 1) / kUmBK, kch2 = (d2 + kUmBK - 1) / kUmBK;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const bool in_k = i0 < ((d1 + kUmBM - 1) / kUmBM) * kUmBM && j0 < kch2 * kUmBK;    // K / KC rows
+  const bool in_kt = j0 < ((d2 + kUmBM - 1) / kUmBM) * kUmBM && i0 < kch1 * kUmBK;   // K^T rows
   bool bad = false;
   for (int r = ty; r < 32; r += 8) {
     const int i = i0 + r, j = j0 + tx;
-    float k = 0.f;
+    float k = 0.f, kc = 0.f;
     if (i < d1 && j < d2) {
       const float cv = c[(size_t)i * d2 + j];
       if (!(cv >= 0.f) || isinf(cv)) bad = true;
       k = ex2(cv * kscale);
-      K[(size_t)i * ldk2 + j] = k;
-      KC[(size_t)i * ldk2 + j] = k * cv;
-    } else if (i < d1 && j < ldk2) {
-      K[(size_t)i * ldk2 + j] = 0.f;
-      KC[(size_t)i * ldk2 + j] = 0.f;
+      kc = k * cv;
+    }
+    if (in_k) {
+      const long long o = um_tiled_index(i, j, kUmBM, kch2);
+      K[o] = k;
+      KC[o] = kc;
     }
     tile[r][tx] = k;
   }
   __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int j = j0 + r, i = i0 + tx;
-    if (j < d2 && i < ldk1) KT[(size_t)j * ldk1 + i] = i < d1 ? tile[tx][r] : 0.f;
-  }
+  if (in_kt)
+    for (int r = ty; r < 32; r += 8) KT[um_tiled_index(j0 + r, i0 + tx, kUmBM, kch1)] = tile[tx][r];
   if (__any_sync(0xffffffffu, bad) && lane_id() == 0) set_status(status, 15);
 }
 

@@ -22,10 +22,13 @@ ap.add_argument("--mufu-only", action="store_true")
 ap.add_argument("--no-fused", action="store_true")
 ap.add_argument("--gemm", choices=["auto", "on", "off"], default="auto")
 ap.add_argument("--B", type=int, default=None, help="override the config's batch")
+ap.add_argument("--d", type=int, default=None, help="override the config's support size")
 a = ap.parse_args()
 cfg = dict(CONFIGS[a.config])
 if a.B:
     cfg["B"] = a.B
+if a.d:
+    cfg["d"] = a.d
 dev = torch.device("cuda", 0)
 mu, nu, cost = make_inputs(cfg, dev, 1)
 import time  # noqa: E402
