@@ -907,6 +907,11 @@ struct Solve {
     ok &= make_tmap_sw128(&tm_al, F(L.gal), nt * k1 * kUmBN, 32, 32, kUmBN);
     return ok ? 0 : fail(SINKHORN_STATUS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (umma)");
   }
+  // (x: blocks over a lane's d elements, y: lanes) for the lane-wise epilogues
+  dim3 lane_grid(int64_t d) const {
+    const int64_t per_lane = std::max<int64_t>(1, (int64_t)di.sms * 8 / std::max<int64_t>(pr.B, 1));
+    return dim3((unsigned)std::min<int64_t>((d + 255) / 256, per_lane), (unsigned)pr.B);
+  }
   // the lane operand's tf32 planes (tiled) from its lane-major fp32 array
   int umma_split(const float* x, int d, float* hi, float* lo) {
     const long long kch = (d + kUmBK - 1) / kUmBK;
@@ -934,7 +939,7 @@ struct Solve {
       return e;
     CK(launch_pdl(umma_gemm_kernel, dim3(p.G), dim3(kUmThreads), kUmSmemBytes, st, tA,
                   rows ? tm_xh : tm_ah, rows ? tm_xl : tm_al, p));
-    CK(launch_pdl(umma_fixup_kernel, dim3((unsigned)(p.MT * p.NT)), dim3(256), 0, st, p));
+    CK(launch_pdl(umma_fixup_kernel, dim3((unsigned)p.G), dim3(256), 0, st, p));
     return 0;
   }
   int gemm_col(const float* vmax, const float* v_old, float* v_new, bool res) {
@@ -951,7 +956,7 @@ struct Solve {
     cp.est_fail = est_fail;
     cp.status = at<int>(ws, L.status);
     ++g_launches;
-    gemm_col_kernel<<<grid_for((size_t)pr.B * pr.d2), 256, 0, st>>>(cp);
+    gemm_col_kernel<<<lane_grid(pr.d2), 256, 0, st>>>(cp);
     CK(cudaGetLastError());
     return 0;
   }
@@ -990,7 +995,7 @@ struct Solve {
     rp.res = res ? F(L.res) : nullptr;
     rp.status = at<int>(ws, L.status);
     ++g_launches;
-    gemm_row_kernel<<<grid_for((size_t)pr.B * pr.d1), 256, 0, st>>>(rp);
+    gemm_row_kernel<<<lane_grid(pr.d1), 256, 0, st>>>(rp);
     ++g_launches;
     gemm_row_fallback_kernel<<<(unsigned)di.sms, 256, 0, st>>>(rp, cost, F(L.g2[cur]),
                                                                 -kLog2e / lam);

@@ -65,13 +65,12 @@ struct GemmRowParams {
   const int* status;
 };
 
-// u_i and a_i from the GEMM row sums; grid-stride over B*d1.
+// u_i and a_i from the GEMM row sums; grid (x: grid-stride over d1, y: lane b).
 __global__ void gemm_row_kernel(const GemmRowParams p) {
   if (p.status != nullptr && *p.status != 0) return;
-  const size_t n = (size_t)p.B * p.d1;
-  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
-       k += (size_t)gridDim.x * blockDim.x) {
-    const int b = (int)(k / p.d1);
+  const int b = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.d1; i += gridDim.x * blockDim.x) {
+    const size_t k = (size_t)b * p.d1 + i;
     const float S = p.S[k];
     const float m = p.mu[k];
     if (!(S >= kGemmMin) || !(S < 3.0e38f)) {
@@ -133,12 +132,12 @@ struct GemmColParams {
 };
 
 // v'_j = l2nu_j + vmax_b - log2 T_j, column residual |2^(v_j - vmax + log2 T_j) - nu_j|.
+// grid (x: grid-stride over d2, y: lane b).
 __global__ void gemm_col_kernel(const GemmColParams p) {
   if (p.status != nullptr && *p.status != 0) return;
-  const size_t n = (size_t)p.B * p.d2;
-  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
-       k += (size_t)gridDim.x * blockDim.x) {
-    const int b = (int)(k / p.d2);
+  const int b = blockIdx.y;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.d2; j += gridDim.x * blockDim.x) {
+    const size_t k = (size_t)b * p.d2 + j;
     const float T = p.T[k];
     const float tgt = p.l2nu[k];
     const float lt = log2f(T);

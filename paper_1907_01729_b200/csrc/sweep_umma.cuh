@@ -360,28 +360,55 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   }
 }
 
-// Split tiles: sum the pieces in ascending CTA order into out.  grid = tiles,
-// block 256; unsplit tiles return at once.
+// Split tiles: sum the pieces in ascending CTA order into out.  grid = G
+// blocks, block 256: block c owns the tile holding its range's first unit when
+// that tile is split there and no earlier boundary falls inside it.
 __global__ void __launch_bounds__(256) umma_fixup_kernel(const UmmaParams p) {
   pdl_wait();
   if (p.status != nullptr && *p.status != 0) return;
-  const long long t = blockIdx.x;
-  const long long uf = t * p.KCH, ul = uf + p.KCH - 1;
-  const int c0 = um_owner(p.units, p.G, uf), c1 = um_owner(p.units, p.G, ul);
-  if (c0 == c1) return;
+  __shared__ int cs[2];
+  const int c = blockIdx.x;
+  if (threadIdx.x == 0) {
+    cs[0] = cs[1] = -1;
+    const long long uc = um_start(p.units, p.G, c);
+    const long long t = uc / p.KCH;
+    bool mine = c > 0 && uc < p.units && uc % p.KCH != 0 && um_start(p.units, p.G, c + 1) > uc;
+    if (mine) {   // an earlier non-empty range starting inside t owns it instead
+      for (int e = c - 1; e >= 1; --e) {
+        const long long ue = um_start(p.units, p.G, e);
+        if (ue / p.KCH != t) break;
+        if (ue % p.KCH != 0 && um_start(p.units, p.G, e + 1) > ue) { mine = false; break; }
+      }
+    }
+    if (mine) {
+      cs[0] = um_owner(p.units, p.G, t * p.KCH);
+      cs[1] = um_owner(p.units, p.G, (t + 1) * p.KCH - 1);
+    }
+  }
+  __syncthreads();
+  const int c0 = cs[0], c1 = cs[1];
+  if (c0 < 0) return;
+  const long long t = um_start(p.units, p.G, c) / p.KCH;
   const int nt = (int)(t % p.NT), mt = (int)(t / p.NT);
   const int nmax = min(kUmBN, p.N - nt * kUmBN);
-  for (int e = threadIdx.x; e < kUmBM * kUmBN; e += 256) {
-    const int n = e / kUmBM, row = e % kUmBM;
-    const int m = mt * kUmBM + row;
-    float s = 0.f;
-    for (int c = c0; c <= c1; ++c) {
-      const long long uc = um_start(p.units, p.G, c);
-      if (um_start(p.units, p.G, c + 1) == uc) continue;   // empty range
-      const int slot = (uc / p.KCH == t) ? 0 : 1;
-      s += p.part[((size_t)(c * 2 + slot) * kUmBN + n) * kUmBM + row];
+  for (int e = threadIdx.x; e < kUmBM * kUmBN / 4; e += 256) {
+    const int n = e / (kUmBM / 4), row = 4 * (e % (kUmBM / 4));
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int cc = c0; cc <= c1; ++cc) {
+      const long long u = um_start(p.units, p.G, cc);
+      if (um_start(p.units, p.G, cc + 1) == u) continue;   // empty range
+      const int slot = (u / p.KCH == t) ? 0 : 1;
+      const float4 v = *reinterpret_cast<const float4*>(
+          p.part + ((size_t)(cc * 2 + slot) * kUmBN + n) * kUmBM + row);
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
     }
-    if (n < nmax && m < p.M) p.out[(long long)(nt * kUmBN + n) * p.ldo + m] = s;
+    if (n < nmax) {
+      const float vals[4] = {s.x, s.y, s.z, s.w};
+      float* o = p.out + (long long)(nt * kUmBN + n) * p.ldo + mt * kUmBM + row;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (mt * kUmBM + row + q < p.M) o[q] = vals[q];
+    }
   }
 }
 
