@@ -2,17 +2,21 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl ours|reference]
 
-Default workload (N=1) is BASELINE.json configs[1] ("config 2"): 28x28 grid
-histograms (d=784), B=256 lanes per GPU, shared stored squared-Euclidean cost,
-lambda=0.05, 100 iterations (tolerance 0, like the reference's own bench,
-cli.py:293-297), forward + backward.  Synthetic inputs, generated on the device.
-A "step" is one forward (100 iterations + the fused residual/E0 tail) plus the
-analytic backward over the batch.  Multi-GPU (torchrun): the batch is sharded
-(weak scaling, 256 lanes per GPU) with one final NCCL all-gather of the
-per-lane losses per step.
+Default workload (N=1): BASELINE.json configs[3] ("config 4") -- the config the
+metric is quoted on at 1/2/4/8 B200 that fits one GPU: per-sample U[0,1) cost
+matrices d1=d2=1024, B=1024 lanes per GPU (4.3 GB of costs streamed from HBM
+every iteration), lambda=0.05, 100 iterations, tolerance 0 (like the
+reference's own bench, cli.py:293-297), forward + analytic backward.
+Synthetic inputs generated on the device.  A "step" is one forward (100
+iterations + the fused residual/E0 tail) plus the backward over the batch.
+`--gpus N` runs N ranks (it launches torchrun itself when not already under
+it): the batch is sharded (weak scaling, B lanes per GPU) with one final NCCL
+all-gather of the per-lane losses per step; config 5 is row-sharded.
 
-Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle port
-of the reference (oracle/, kind "port") on the same workload instead.
+Prints ONE JSON line (rank 0).  `--impl reference` times the reference
+implementation itself (the `sinkloss` package installed in baseline/_ref,
+kind "reference") on the host cores instead; the CPU oracle port (oracle/,
+kind "port") stands in only when baseline/_ref is absent.
 """
 
 from __future__ import annotations
@@ -235,171 +239,274 @@ def work_units(cfg: dict) -> float:
 
 
 KERNEL_OF_PATH = {
-    "fused": "fused_pass_kernel + fused_merge_kernel (one fused row->column pass per iteration: "
-             "row LSE, plan column partials, column update)",
-    "gemm": "cublasSgemm x2 (S = K X, T = K^T a) + gemm_scale/row/col kernels (one iteration)",
+    "fused": "fused_ps_kernel (per-sample: one fused row->column pass per iteration, C_b read "
+             "once) / fgemm_pass_kernel (shared: two register-blocked fp32 GEMMs per 16-row block)",
+    "gemm": "umma_gemm_kernel (tcgen05 3xTF32 contraction streaming K or K^T from HBM; two per "
+            "iteration, S = K X and T = K^T a)",
     "tiled": "tiled_sweep_kernel (stream-K online-LSE half-sweep)",
     "small": "small_solve_kernel (whole solve in one launch, cost in shared memory)",
     "persistent": "persistent_solve_kernel (cooperative whole loop)",
     "lane": "lane_col_kernel / lane_row_kernel (per-sample sweep)",
     "separable": "sep_sweep_kernel (separable grid LSE: two nested 1-D LSE-GEMMs per sweep)",
-    "row-sharded-gemm": "cuBLAS SGEMMs on this rank's kernel-matrix rows (K_r X, K_r^T a); "
-                        "whole step incl. the NCCL (max, sum) merge per column sweep",
-    "row-sharded": "tiled_sweep_kernel through the half-sweep C ABI (this rank's cost rows; "
-                   "whole step incl. NCCL merges per half-sweep)",
+    "row-sharded-gemm": "umma_gemm_kernel on this rank's kernel-matrix rows (whole step incl. "
+                        "the NCCL all-reduce of the column sums)",
 }
 
 
-def roofline(cfg: dict, sweep_ms: float, peaks: dict, clocks: dict, traffic,
-             path: str = "tiled", share: float = 1.0) -> dict:
-    """Dominant kernel = the half-sweep (2*iters per step; one launch each on the
-    tiled path, all inside one launch on the small path), or on the fused path
-    the fused pass (iters per step: the column half-sweep is an FFMA on the row
-    sweep's plan entries, so one launch does a whole iteration's work)."""
-    cells = float(cfg["B"]) * cfg["d"] * cfg["d"] * share  # cells per sweep launch (this GPU)
-    if cfg["cost"] == "per_sample":
-        # SURVEY 8(d): 4 B of C per cell per half-sweep.  A fused launch is a
-        # whole iteration (8 B per cell algorithmic) that reads C_b once.
-        per_cell = 8 if path == "fused" else 4
-        achieved = cells * per_cell / (sweep_ms * 1e-3) / 1e9
-        peak = float(peaks.get("hbm_gbs", 6650.0))
-        out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-               "frac": achieved / peak, "traffic": traffic}
-        if path == "fused":   # what the fused kernel actually streams: C_b once
-            read = cells * 4 / (sweep_ms * 1e-3) / 1e9
-            out.update({"achieved_read": read, "frac_read": read / peak})
-        return {**out,
-                "kernel": ("fused_ps_kernel + fused_merge_kernel (one read of C_b per iteration)"
-                           if path == "fused" else
-                           "lane_col_kernel / lane_row_kernel (per-sample sweep)"),
-                "algorithmic_per_launch": (f"{cells * per_cell:.4g} B ({per_cell} B per cell"
-                                           + (", 2 half-sweeps; 4 B actually read)" if path == "fused"
-                                              else ")")),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
-    sms = 148
+def roofline(cfg: dict, kernel_ms: float, peaks: dict, clocks: dict, traffic, path: str,
+             share: float = 1.0) -> dict:
+    """Roofline of the dominant kernel from its measured average launch time
+    (CUDA events around each launch, SINKHORN_FLAG_TIME_KERNEL) and the
+    ALGORITHMIC work one launch does (DESIGN.md section 4 states both):
+
+    * per-sample fused pass: reads C_b once per iteration, 4 B per cell
+      (bound hbm); the survey's 8 B per cell-iteration (two half-sweeps that
+      each read C) is reported beside it;
+    * GEMM iteration: one contraction streams the d1 x d2 kernel matrix once,
+      4 B per matrix element (bound hbm); its 3xTF32 tensor work is reported
+      beside it;
+    * shared fused block pass: two fp32 GEMMs, 4 FLOP per cell (bound fp32
+      FMA pipe);
+    * tiled / separable / small: ex2 per cell (bound mufu).
+    """
+    B, d = float(cfg["B"]), float(cfg["d"])
+    cells = B * d * d * share          # cells one launch covers (this GPU)
+    t = kernel_ms * 1e-3
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = 148
+    hbm_src = ("MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
+               else "fallback 6650 GB/s (B200_PROFILING.md)")
+    base = {"traffic": traffic, "kernel": KERNEL_OF_PATH.get(path, path),
+            "kernel_ms_per_launch": kernel_ms}
+    if cfg["cost"] == "per_sample" and path == "fused":
+        read = 4 * cells
+        a = read / t / 1e9
+        return {"bound": "hbm", "achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm, **base,
+                "algorithmic_per_launch": f"{read:.4g} B (C_b read once per iteration: 4 B per cell)",
+                "peak_source": hbm_src,
+                "survey_8B_per_cell": {"achieved": 2 * a, "frac": 2 * a / hbm,
+                                       "note": "SURVEY 8(d) counts two half-sweeps that each read "
+                                               "C_b (8 B per cell-iteration); the fused pass reads "
+                                               "it once"}}
     if path in ("gemm", "row-sharded-gemm"):
-        # one launch group = one iteration = two fp32 GEMMs of 2*B*d1*d2 FLOP
-        # (S = K X, T = K^T a; sweep_gemm.cuh), run by cuBLAS SGEMM on the
-        # fp32 FMA pipe: 148 SM x 128 FFMA/clk x 2 FLOP (nominal, no measured figure)
+        mat = d * d * share                              # kernel-matrix elements per launch
+        read = 4 * mat
+        a = read / t / 1e9
+        tf = 6 * B * mat / t / 1e12                      # 3 tf32 products x 2 FLOP
+        tf_peak = float(peaks.get("bf16_tflops", 1606.6)) / 2
+        return {"bound": "hbm", "achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm, **base,
+                "algorithmic_per_launch": f"{read:.4g} B (the d1 x d2 kernel matrix, 4 B per "
+                                          "element, streamed once per contraction)",
+                "peak_source": hbm_src,
+                "tensor_tf32": {"achieved_tflops": tf, "peak_tflops": tf_peak,
+                                "frac": tf / tf_peak,
+                                "note": "3xTF32: 3 MMA products x 2 FLOP per B-lane x element; "
+                                        "peak = measured bf16 / 2 (tf32 runs at half the bf16 rate)"}}
+    if path == "fused":
         flop = 4 * cells
-        achieved = flop / (sweep_ms * 1e-3) / 1e12
+        a = flop / t / 1e12
         peak = sms * 128 * 2 * fmax * 1e6 / 1e12
-        out = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-               "frac": achieved / peak, "traffic": traffic,
-               "kernel": KERNEL_OF_PATH[path],
-               "algorithmic_per_launch": f"{flop:.4g} FLOP (2 GEMMs of 2*B*d1*d2 per iteration)",
-               "peak_source": f"nominal: 148 SM x 128 FFMA/clk x 2 x sm_max_mhz {fmax:.0f}",
-               "ex2_equivalent_frac": 2 * cells / (sweep_ms * 1e-3) /
-               (sms * MUFU_PER_SM_CLK * fmax * 1e6)}
-        return out
-    ex2 = cells                                            # one ex2 per cell per sweep
-    if path == "fused":
-        # one launch = one whole iteration; SURVEY 8(d) counts 2 ex2 per
-        # cell-iteration (one per half-sweep).  The fused linear pass itself
-        # evaluates no per-cell exponential (K = 2^A2 is precomputed), so this
-        # fraction can exceed 1: it is the exp-pipe roofline of the direct method.
-        ex2 = 2 * cells
+        return {"bound": "fp32", "achieved": a, "peak": peak, "unit": "TFLOP/s", "frac": a / peak,
+                **base, "algorithmic_per_launch": f"{flop:.4g} FLOP (two GEMMs, 4 FLOP per cell "
+                                                  "per iteration)",
+                "peak_source": f"nominal 148 SM x 128 FFMA/clk x 2 x sm_max_mhz {fmax:.0f}",
+                "ex2_equivalent": {"frac": 2 * cells / t / (sms * MUFU_PER_SM_CLK * fmax * 1e6),
+                                   "note": "the direct log-domain method's 2 ex2 per "
+                                           "cell-iteration (SURVEY 8(d)) vs the MUFU peak; the "
+                                           "block pass evaluates none per cell"}}
     if path == "separable":
-        # nested 1-D LSEs: B * (nx*ny) * (nx + ny) exponentials per sweep
-        ex2 = float(cfg["B"]) * cfg["d"] * (2 * cfg["nx"])
-    achieved = ex2 / (sweep_ms * 1e-3) / 1e12
+        ex2 = B * d * (2 * cfg["nx"])                    # nested 1-D LSEs per sweep
+        what = f"{ex2:.4g} ex2 (B*d*(nx+ny), separable)"
+    elif path == "small":
+        ex2 = cells * 2 * cfg["iters"]                   # the whole solve in one launch
+        what = f"{ex2:.4g} ex2 (whole solve: 2 per cell-iteration)"
+    else:
+        ex2 = cells
+        what = f"{ex2:.4g} ex2 (1 per cell per half-sweep)"
+    a = ex2 / t / 1e12
     peak = sms * MUFU_PER_SM_CLK * fmax * 1e6 / 1e12
-    out = {"bound": "mufu", "achieved": achieved, "peak": peak, "unit": "Tex2/s",
-           "frac": achieved / peak, "traffic": traffic,
-           "kernel": KERNEL_OF_PATH.get(path, path),
-           "algorithmic_per_launch": (f"{ex2:.4g} ex2 (B*d*(nx+ny), separable)"
-                                      if path == "separable" else
-                                      f"{2 * cells:.4g} ex2-equivalent (2 per cell-iteration, "
-                                      "SURVEY 8(d); the fused pass computes K_ij*2^(v_j-vmax) "
-                                      "products, no per-cell ex2)" if path == "fused"
-                                      else f"{cells:.4g} ex2 (1 per cell)"),
-           "peak_source": f"148 SM x {MUFU_PER_SM_CLK} ex2/clk x sm_max_mhz {fmax:.0f} "
-                          "(MEASURED_PEAKS.json)"}
+    out = {"bound": "mufu", "achieved": a, "peak": peak, "unit": "Tex2/s", "frac": a / peak, **base,
+           "algorithmic_per_launch": what,
+           "peak_source": f"148 SM x {MUFU_PER_SM_CLK} ex2/clk x sm_max_mhz {fmax:.0f}"}
     if clocks.get("sm_mhz"):
-        out["frac_at_measured_clock"] = achieved / (sms * MUFU_PER_SM_CLK * clocks["sm_mhz"] * 1e-6)
-    if path == "fused":
-        # what bounds the block pass itself: two GEMMs (2 FMA = 4 FLOP per cell-iteration)
-        # on the fp32 FMA pipe, 148 SM x 128 FFMA/clk x 2 FLOP (nominal)
-        tf = 4 * cells / (sweep_ms * 1e-3) / 1e12
-        out["fp32_pipe"] = {"achieved_tflops": tf, "peak_tflops": sms * 128 * 2 * fmax * 1e-6,
-                            "frac": tf / (sms * 128 * 2 * fmax * 1e-6)}
+        out["frac_at_measured_clock"] = a / (sms * MUFU_PER_SM_CLK * clocks["sm_mhz"] * 1e-6)
     return out
 
 
-def load_traffic(cfg_id: int):
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+def load_traffic(cfg_id: int, path: str):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu capture of this config and solver path (profiles/), or None."""
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             data = json.load(f)
-        v = data.get(f"config{cfg_id}", {}).get("dram_bytes_per_sweep_launch")
-        return v
     except (OSError, ValueError):
         return None
+    entry = data.get(f"config{cfg_id}", {})
+    if entry.get("path") == path:
+        return entry.get("dram_bytes_per_sweep_launch")
+    return entry.get(f"{path}_path", {}).get("dram_bytes_per_sweep_launch")
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port of the reference (oracle/), bounded sample
+# CPU baseline: the reference itself (baseline/_ref), bounded samples
 
-def cpu_reference_sample(cfg: dict, seed: int = 0) -> dict:
-    """Time the reference algorithm (oracle port, float64) on host cores.
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
-    Lanes are independent at tolerance 0 and every iteration costs the same
-    (test_batch.py:46-63), so a run of k1 and k2 iterations gives the
-    per-iteration slope and the fixed tail (final residual + E0); the rate is
-    extrapolated to the configured iteration count.
+
+def reference_package():
+    """The reference's own `sinkloss` package installed in baseline/_ref
+    (pip --target), or None when it is absent."""
+    if not os.path.isfile(os.path.join(REF_DIR, "sinkloss", "batch.py")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import sinkloss  # noqa: F401
+
+    return sinkloss
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _ref_hist(rng, d):
+    """random_histogram (oracle.py:152-155): U(0.5, 1.5) normalised."""
+    m = rng.uniform(0.5, 1.5, d)
+    return m / m.sum()
+
+
+def _ref_lane_job(args):
+    """One per-sample lane through the reference's public API: batch_forward
+    with B = 1 and the lane's own cost (the reference has no per-sample API,
+    SPEC.md:323; lanes are independent at tolerance 0, test_batch.py:46-63),
+    then batch_backward.  Returns the solve's seconds."""
+    seed, lane, d, lam, iters = args
+    reference_package()
+    from sinkloss import batch, core
+
+    rng = np.random.default_rng([seed, lane])
+    mu, nu = _ref_hist(rng, d), _ref_hist(rng, d)
+    c = rng.random((d, d), dtype=np.float32).astype(np.float64)
+    cfg = core.SinkhornConfig(lam=lam, max_iters=iters, tolerance=0.0)
+    hb = batch.validate_histogram_batch
+    t0 = time.perf_counter()
+    r = batch.batch_forward(hb(mu[None]), hb(nu[None]), core.CostMatrix(c), cfg, workers=1)
+    batch.batch_backward(r, np.ones(1))
+    return time.perf_counter() - t0
+
+
+def _ref_shared_cost(cfg, d):
+    from sinkloss import core, oracle
+
+    if cfg["cost"] == "index":
+        return oracle.index_grid_cost(d, power=2)
+    n = int(math.isqrt(d))   # 2-D grids (configs 2, 3): coordinates (col, row)/(n-1)
+    k = np.arange(n * n)
+    x, y = (k % n) / max(n - 1, 1), (k // n) / max(n - 1, 1)
+    return core.CostMatrix(cost=(x[:, None] - x[None, :]) ** 2 + (y[:, None] - y[None, :]) ** 2)
+
+
+def reference_cpu_sample(cfg: dict, seed: int = 0, runs: int = 3, light: bool = False) -> dict:
+    """Time the reference implementation (baseline/_ref sinkloss) on the host cores.
+
+    Forward (batch_forward, workers = os.cpu_count()) + batch_backward at k1
+    and k2 iterations, median of `runs` runs each (cli.py:299-306 with fewer
+    repetitions); the per-iteration slope and the fixed tail (final residual
+    + E0) extrapolate to the configured iteration count (lanes independent at
+    tolerance 0, every iteration costs the same).  Per-sample costs (config 4)
+    run one lane per process over a pool of os.cpu_count() processes.
     """
+    sl = reference_package()
+    if sl is None:
+        return port_cpu_sample(cfg, seed)
+    from sinkloss import batch, core
+
+    threads = os.cpu_count() or 1
+    B, d, lam, iters = cfg["B"], cfg["d"], cfg["lam"], cfg["iters"]
+    k1, k2 = (2, 4) if light else (5, 10)
+    if cfg["cost"] == "per_sample":
+        from concurrent.futures import ProcessPoolExecutor
+
+        lanes = threads
+        with ProcessPoolExecutor(max_workers=threads) as ex:
+            list(ex.map(_ref_lane_job, [(seed, b, d, lam, 1) for b in range(lanes)]))  # warm
+
+            def run(k):
+                ts = list(ex.map(_ref_lane_job, [(seed, b, d, lam, k) for b in range(lanes)]))
+                return max(ts)     # the lanes run concurrently, one per process
+            t1 = statistics.median(run(k1) for _ in range(runs))
+            t2 = statistics.median(run(k2) for _ in range(runs))
+        cells = float(lanes) * d * d
+        sample = (f"reference sinkloss.batch_forward(B=1)+batch_backward, {lanes} per-sample lanes "
+                  f"d={d} on {threads} processes, {k1} and {k2} iterations, median of {runs}")
+    else:
+        dd = min(d, 4096)
+        Bs = B if dd == d and B * dd * dd <= 256 * 784 * 784 else min(B, 16 if dd >= 4096 else B)
+        rng = np.random.default_rng(seed)
+        hb = batch.validate_histogram_batch
+        mu = hb(np.stack([_ref_hist(rng, dd) for _ in range(Bs)]))
+        nu = hb(np.stack([_ref_hist(rng, dd) for _ in range(Bs)]))
+        c = _ref_shared_cost(cfg, dd)
+        if d <= 100:
+            k1, k2 = iters // 2, iters
+
+        def one(k):
+            conf = core.SinkhornConfig(lam=lam, max_iters=k, tolerance=0.0)
+            t0 = time.perf_counter()
+            r = batch.batch_forward(mu, nu, c, conf, workers=threads)
+            batch.batch_backward(r, np.ones(Bs))
+            return time.perf_counter() - t0
+        one(1)
+        t1 = statistics.median(one(k1) for _ in range(runs))
+        t2 = statistics.median(one(k2) for _ in range(runs))
+        cells = float(Bs) * dd * dd
+        sample = (f"reference sinkloss.batch_forward+batch_backward, workers={threads}, B={Bs} "
+                  f"d={dd}, {k1} and {k2} iterations, median of {runs}"
+                  + (f"; per-cell rate extrapolated to d={d} (the reference's fp64 copies of "
+                     f"a d={d} cost exceed host RAM)" if dd != d else ""))
+    per_iter = max((t2 - t1) / (k2 - k1), 1e-9)
+    tail = max(t1 - k1 * per_iter, 0.0)
+    t_full = tail + iters * per_iter
+    rate = cells * iters / t_full
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": sample + f"; extrapolated to {iters} iterations (slope + fixed tail)",
+            "cpu": cpu_model(), "seconds_per_iteration": per_iter, "tail_seconds": tail,
+            "ms_per_step_full": t_full * 1e3 * (float(B) * d * d / cells)}
+
+
+def port_cpu_sample(cfg: dict, seed: int = 0) -> dict:
+    """Fallback when baseline/_ref is absent: the oracle port (oracle/, kind "port")."""
     from oracle import sinkhorn_oracle as orc
 
     rng = np.random.default_rng(seed)
     B, d, lam, iters = cfg["B"], cfg["d"], cfg["lam"], cfg["iters"]
     threads = os.cpu_count() or 1
-    kind = cfg["cost"]
-    if kind in ("index", "grid_stored") and d <= 1024:
-        Bs = B
-        mu = orc.random_histogram_batch(Bs, d, rng)
-        nu = orc.random_histogram_batch(Bs, d, rng)
-        c = orc.index_grid_cost(d) if kind == "index" else orc.grid2d_cost(cfg["nx"])
+    dd = min(d, 1024)
+    mu = orc.random_histogram_batch(1, dd, rng)[0]
+    nu = orc.random_histogram_batch(1, dd, rng)[0]
+    c = (orc.per_sample_cost(1, 0, dd, dd).astype(np.float64) if cfg["cost"] == "per_sample"
+         else orc.index_grid_cost(dd))
 
-        def run(k):
-            t0 = time.perf_counter()
-            r = orc.batch_forward(mu, nu, c, lam, k, 0.0, workers=threads)
-            orc.batch_backward(r.log_u, r.log_v, lam, np.ones(Bs))
-            return time.perf_counter() - t0
-        k1, k2 = 1, 2
-        sample = f"streaming port (batch.py structure), B={Bs} d={d}, {k1} and {k2} iterations"
-        cores = threads
-    else:
-        # dense single-lane restatement (core.py:305-357) on a lane subset
-        Bs = 1
-        dd = min(d, 4096)
-        mu = orc.random_histogram_batch(1, dd, rng)[0]
-        nu = orc.random_histogram_batch(1, dd, rng)[0]
-        if kind == "per_sample":
-            c = orc.per_sample_cost(1, 0, dd, dd).astype(np.float64)
-        elif kind == "grid_fly" or kind == "grid_stored":
-            c = orc.grid2d_cost(int(math.isqrt(dd)))
-        else:
-            c = orc.index_grid_cost(dd)
-
-        def run(k):
-            t0 = time.perf_counter()
-            r = orc.dense_forward(mu, nu, c, lam, k)
-            orc.batch_backward(r.log_u, r.log_v, lam, np.ones(1))
-            return time.perf_counter() - t0
-        k1, k2 = 1, 2
-        sample = (f"dense single-lane port (core.py:305-357), 1 lane of d={dd}, {k1} and {k2} "
-                  "iterations" + (f"; per-cell rate extrapolated to d={d}" if dd != d else ""))
-        cores = 1
-    t1, t2 = run(k1), run(k2)
-    per_iter = max((t2 - t1) / (k2 - k1), 1e-9)
-    tail = max(t1 - k1 * per_iter, 0.0)
-    cells_sample = float(Bs) * mu.shape[-1] * mu.shape[-1]
-    t_full = tail + iters * per_iter                     # extrapolated full forward+backward
-    rate = cells_sample * iters / t_full
-    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": sample + f"; extrapolated to {iters} iterations (slope + fixed tail)",
-            "seconds": t1 + t2, "ms_per_step_full": t_full * 1e3 * (B / Bs)}
+    def run(k):
+        t0 = time.perf_counter()
+        r = orc.dense_forward(mu, nu, c, lam, k)
+        orc.batch_backward(r.log_u, r.log_v, lam, np.ones(1))
+        return time.perf_counter() - t0
+    t1, t2 = run(1), run(2)
+    per_iter = max(t2 - t1, 1e-9)
+    tail = max(t1 - per_iter, 0.0)
+    t_full = tail + iters * per_iter
+    return {"value": float(dd) * dd * iters / t_full, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle port dense single lane d={dd}, 1 and 2 iterations (baseline/_ref absent)",
+            "cpu": cpu_model(), "ms_per_step_full": t_full * 1e3 * B * (d / dd) ** 2}
 
 
 # ---------------------------------------------------------------------------
@@ -411,27 +518,47 @@ def init_dist():
     return world, rank, local
 
 
+def config_dict(cfg: dict, world: int, row: bool, path: str | None = None) -> dict:
+    """The `config` object both arms print (same keys, same values)."""
+    jobs = 1 if row else world
+    out = {"workload": cfg["workload"], "B_per_gpu": cfg["B"], "global_batch": cfg["B"] * jobs,
+           "d1": cfg["d"], "d2": cfg["d"], "iters": cfg["iters"], "lambda": cfg["lam"],
+           "tolerance": 0.0,
+           "parallelism": (f"row-sharded cost over {world} GPU(s), one NCCL all-reduce of the "
+                           "column sums per iteration") if row else f"batch-sharded dp{world}",
+           "l2": ("flushed between steps (256 MiB write outside the timed events); config-4 / "
+                  "config-5 inputs (4.3 / 17.2 GB) also exceed L2")}
+    if path is not None:
+        out["solver_path"] = path
+    return out
+
+
 def run_reference(args, cfg, world, rank):
+    """`--impl reference`: the reference's own CPU implementation on this
+    host's cores, rank 0 only (the other ranks exit without work)."""
     if rank != 0:
         return
+    heavy = cfg["cost"] != "per_sample" and cfg["d"] > 100
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_reference_sample(dict(cfg, iters=cfg["iters"]), seed=1)
-    vals, ms = [], []
+        reference_cpu_sample(cfg, seed=99, runs=1, light=True)
+    vals, ms, r = [], [], None
     for s in range(args.steps):
-        r = cpu_reference_sample(cfg, seed=s)
+        r = reference_cpu_sample(cfg, seed=s, runs=1, light=heavy)
         vals.append(r["value"])
         ms.append(r["ms_per_step_full"])
-    r["value"] = statistics.median(vals)
+    value = statistics.median(vals)
+    row = args.config == 5 and world > 1
     line = {
-        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": statistics.median(ms), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "B": cfg["B"], "d1": cfg["d"], "d2": cfg["d"],
-                   "iters": cfg["iters"], "lambda": cfg["lam"]},
-        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(ms), "higher_is_better": True,
+        "scaling": "strong" if row else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": config_dict(cfg, world, row),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+                         "sample": r["sample"] + f"; one sample per step, median of {args.steps}",
+                         "cpu": r["cpu"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -498,6 +625,7 @@ def run_ours(args, cfg, world, rank, local):
         if world > 1:
             dist.barrier()
         launches0 = lib.sinkhorn_launch_count_v1()
+        reruns0 = lib.sinkhorn_exact_reruns_v1()
         torch.cuda.synchronize()
         t_wall0 = time.time()
         for s in range(args.steps):
@@ -510,20 +638,25 @@ def run_ours(args, cfg, world, rank, local):
         torch.cuda.synchronize()
         clk.mark(t_wall0, time.time())
     launches = lib.sinkhorn_launch_count_v1() - launches0
+    reruns = lib.sinkhorn_exact_reruns_v1() - reruns0
+    # the dominant kernel's average launch time: one more solve (untimed by the
+    # step clock) with CUDA events around each of its launches
+    if row:
+        kernel_ms = None
+    else:
+        kr = skb.solve(mu, nu, cost, lam, iters, 0.0, 10, validate=True, time_kernel=True)
+        kernel_ms = kr.kernel_ms / max(kr.kernel_launches, 1)
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     ms = sum(step_ms) / len(step_ms)
     step_stats = {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)}
-    # row sharding has no per-solve loop timer: its half-sweep share is the step's
-    # fused: one pass (+ merge) per iteration; gemm: one GEMM pair per iteration
-    launches_per_iter = 1 if path in ("fused", "gemm", "row-sharded-gemm") else 2
-    sweep_ms = (statistics.median(loop_ms) if not row else statistics.median(step_ms)) / (
-        launches_per_iter * iters)
-    t = torch.tensor([ms, sweep_ms], device=dev, dtype=torch.float64)
+    if kernel_ms is None:   # row sharding: the step's share per contraction (2 per iteration)
+        kernel_ms = statistics.median(step_ms) / (2 * iters)
+    t = torch.tensor([ms, kernel_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, sweep_ms = float(t[0]), float(t[1])
+    ms, kernel_ms = float(t[0]), float(t[1])
     # batch sharding: every rank solves its own B lanes (weak scaling);
     # row sharding: the ranks share one B x d x d problem (strong scaling)
     jobs = 1 if row else world
@@ -546,24 +679,20 @@ def run_ours(args, cfg, world, rank, local):
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong" if row else "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "B_per_gpu": B, "global_batch": B * jobs,
-                   "d1": d, "d2": d, "iters": iters, "lambda": lam, "tolerance": 0.0,
-                   "parallelism": (f"row-sharded cost over {world} GPU(s), NCCL (max, sum-exp) "
-                                   "all-reduce per column sweep") if row
-                   else f"batch-sharded dp{world}",
-                   "solver_path": path,
-                   "l2": "flushed between steps (256 MiB write outside the timed events)"},
-        "roofline": roofline(cfg, sweep_ms, peaks, clocks, load_traffic(args.config), path,
+        "config": config_dict(cfg, world, row, path),
+        "roofline": roofline(cfg, kernel_ms, peaks, clocks, load_traffic(args.config, path), path,
                              share=(1.0 / world) if row else 1.0),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
                 "d2h_bytes_per_step": e2e["d2h"], "path": e2e["path"]},
         "gpu_launches": int(launches),
+        "exact_reruns": int(reruns),
         "clocks": clocks,
         "step_ms_stats": step_stats,
+        "loop_ms_median": statistics.median(loop_ms) if not row else None,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference_sample(cfg)
-        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cb = reference_cpu_sample(cfg, runs=1, light=cfg["cost"] != "per_sample" and d > 100)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
@@ -647,17 +776,19 @@ def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
         h_mu = mu.cpu().pin_memory()
         h_nu = nu.cpu().pin_memory()
         grid = isinstance(cost, skb.GridCost)
-        big = (not grid) and cost.numel() * 4 > (4 << 30)   # > 4 GiB: pageable, not pinned
+        big = (not grid) and cost.numel() * 4 > (8 << 30)   # > 8 GiB: pageable, not pinned
         h_c = None if grid else (cost.cpu() if big else cost.cpu().pin_memory())
         h_loss = torch.empty(B).pin_memory()
         h_gm = torch.empty(B, d).pin_memory()
         h_gn = torch.empty(B, d).pin_memory()
+        per_sample = (not grid) and cost.dim() == 3
+        chunks = args.e2e_chunks if per_sample else 1
 
         def one():
-            m = h_mu.to(dev, non_blocking=True)
-            n = h_nu.to(dev, non_blocking=True)
-            c = cost if grid else h_c.to(dev, non_blocking=True)
-            res = skb.solve(m, n, c, lam, iters, 0.0)
+            # solve_streamed: lane groups of histograms (+ per-sample costs) are
+            # uploaded on a copy stream while the previous group solves
+            res = skb.solve_streamed(h_mu, h_nu, cost if grid else h_c, lam, iters, 0.0,
+                                     chunks=chunks, device=dev)
             gm, gn = skb.potentials_backward(res.log_u, res.log_v, lam, torch.ones(B, device=dev))
             h_loss.copy_(res.cost_e0, non_blocking=True)
             h_gm.copy_(gm, non_blocking=True)
@@ -665,7 +796,8 @@ def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
             torch.cuda.synchronize()
         h2d = 4 * (2 * B * d + (0 if grid else cost.numel()))
         d2h = 4 * (B + 2 * B * d)
-        path = "torch API solve()+potentials_backward() from pinned host tensors"
+        path = (f"torch API solve_streamed(chunks={chunks})+potentials_backward() from pinned "
+                "host tensors (uploads overlap the solve)")
     one()
     t0 = time.perf_counter()
     for _ in range(steps):
@@ -680,7 +812,7 @@ def main():
     ap.add_argument("--steps", type=int, default=None,
                     help="timed steps (default per config: ~0.3-1 s of timed work, 3 for config 5)")
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--clock-interval-ms", type=int, default=100)
@@ -688,14 +820,44 @@ def main():
                     help="row sharding: local fp32 GEMMs (default) or log-domain half-sweeps")
     ap.add_argument("--sharding", choices=["batch", "row"], default=None,
                     help="multi-GPU split (default: row for config 5 on N>1, else batch)")
+    ap.add_argument("--probe-ranks", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--e2e-chunks", type=int, default=8,
+                    help="e2e leg, per-sample costs: lane groups whose upload overlaps the solve")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: relaunch under torchrun (the driver's own launch
+        # sets WORLD_SIZE and lands in the branch below instead)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}: "
+                         "launch N ranks for --gpus N")
     if args.steps is None:
         # enough steps that a rare host-side stall (seen on the boxes: one
         # step in ~100 takes 5-100 ms longer, with or without our sampler)
         # does not dominate the mean
         args.steps = {1: 50, 2: 30, 3: 30, 4: 10, 5: 3}[args.config]
     world, rank, local = init_dist()
+    if args.probe_ranks:   # launcher check (tests/test_bench_cpu.py): gloo, no GPU work
+        import torch
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        if rank == 0:
+            print(json.dumps({"probe": "ranks", "world": world, "ranks_seen": int(t.item()),
+                              "gpus_arg": args.gpus}), flush=True)
+        dist.destroy_process_group()
+        return
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
     else:

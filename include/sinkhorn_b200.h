@@ -103,6 +103,8 @@ typedef struct sinkhorn_problem_v1 {
                                             fp32 GEMMs per iteration (sweep_gemm.cuh) */
 #define SINKHORN_FLAG_FORCE_GEMM 1024u   /* shared costs: the GEMM path even where the fused
                                             pass applies (d <= 1024) */
+#define SINKHORN_FLAG_TIME_KERNEL 2048u  /* CUDA events around each launch of the solve's
+                                            dominant kernel (sinkhorn_last_kernel_ms_v1) */
 
 typedef struct sinkhorn_options_v1 {
   double lambda;          /* > 0, finite */
@@ -232,6 +234,12 @@ unsigned long long sinkhorn_launch_count_v1(void);
  * estimate overshot the result (estimate mode). */
 unsigned long long sinkhorn_exact_reruns_v1(void);
 float sinkhorn_last_loop_ms_v1(void);
+/* Total milliseconds (CUDA events) and launch count of the dominant kernel's
+ * launches in this thread's last forward run with SINKHORN_FLAG_TIME_KERNEL:
+ * umma_gemm_kernel (GEMM path), fused_ps_kernel / fgemm_pass_kernel /
+ * fused_pass_kernel (fused passes), tiled_sweep_kernel, sep_sweep_kernel,
+ * small_solve_kernel.  -1 ms if none. */
+float sinkhorn_last_kernel_ms_v1(int32_t* launches);
 /* Solver path of this thread's last forward: "small" (one-launch solve,
  * cost in shared memory), "tiled" (stream-K sweeps), "persistent" (opt-in
  * cooperative loop) or "lane" (per-sample costs). */

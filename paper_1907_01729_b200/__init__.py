@@ -34,7 +34,7 @@ from .errors import (
     ZeroMassGradient,
 )
 from .loss import GridCost, SinkhornLossFunction, SolveResult, plan_gradient, \
-    potentials_backward, sinkhorn_loss, solve
+    potentials_backward, sinkhorn_loss, solve, solve_streamed
 
 __version__ = "0.1.0"
 
@@ -43,5 +43,5 @@ __all__ = [
     "InvalidHistogram", "NaNProduced", "ShapeMismatch", "SinkhornConfig",
     "SinkhornLossFunction", "SinklossError", "SolveResult", "ZeroMassGradient",
     "batch_backward", "batch_forward", "fused_log_reduction", "partial_log_reduction",
-    "plan_gradient", "potentials_backward", "sinkhorn_loss", "solve",
+    "plan_gradient", "potentials_backward", "sinkhorn_loss", "solve", "solve_streamed",
 ]

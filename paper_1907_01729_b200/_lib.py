@@ -38,6 +38,7 @@ FLAG_DENSE_GRID = 128
 FLAG_NO_FUSED = 256
 FLAG_NO_GEMM = 512
 FLAG_FORCE_GEMM = 1024
+FLAG_TIME_KERNEL = 2048
 
 # every symbol include/sinkhorn_b200.h declares
 EXPORTED_SYMBOLS = (
@@ -60,6 +61,7 @@ EXPORTED_SYMBOLS = (
     "sinkhorn_launch_count_v1",
     "sinkhorn_exact_reruns_v1",
     "sinkhorn_last_loop_ms_v1",
+    "sinkhorn_last_kernel_ms_v1",
     "sinkhorn_last_path_v1",
 )
 
@@ -138,6 +140,7 @@ def _declare(lib):
         "sinkhorn_launch_count_v1": (ctypes.c_ulonglong, []),
         "sinkhorn_exact_reruns_v1": (ctypes.c_ulonglong, []),
         "sinkhorn_last_loop_ms_v1": (ctypes.c_float, []),
+        "sinkhorn_last_kernel_ms_v1": (ctypes.c_float, [ctypes.POINTER(ctypes.c_int32)]),
         "sinkhorn_last_path_v1": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():

@@ -39,6 +39,23 @@ namespace {
 thread_local std::string g_last_error;
 thread_local unsigned long long g_launches = 0;   // kernels this thread launched
 thread_local float g_last_loop_ms = -1.f;         // last timed iteration loop (ms)
+// SINKHORN_FLAG_TIME_KERNEL: CUDA events around every launch of the solve's
+// dominant kernel (the per-iteration sweep / contraction), for the roofline.
+struct KernelTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;   // begin / end pairs
+  float last_ms = -1.f;
+  int last_launches = 0;
+};
+thread_local KernelTimer g_kt;
+inline void kt_mark(cudaStream_t st) {
+  if (!g_kt.on) return;
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) == cudaSuccess) {
+    cudaEventRecord(e, st);
+    g_kt.ev.push_back(e);
+  }
+}
 thread_local const char* g_last_path = "none";    // solver path of the last forward
 thread_local unsigned long long g_exact_reruns = 0;  // solves redone without estimates
 // non-check fused iterations of shared costs as the two-GEMM block pass
@@ -530,7 +547,9 @@ int launch_tiled_pt(const Layout& L, void* ws, const DeviceInfo& di, const Tiled
     p.dbg = tl_buf;
   }
   auto kern = &tiled_sweep_kernel<BT, PT, QC, RB, RP, NSTAGE, kGrid, kMode>;
+  kt_mark(st);
   CK(launch_pdl(kern, dim3(p.G), dim3(K::S::NT), smem, st, *a.tg, *a.tx, p));
+  kt_mark(st);
   // merge + epilogue of the tiles the stream-K split cut between CTAs
   const unsigned nfix = (unsigned)(p.ntile_b * p.ntile_p * (K::S::NT * 4 / 256));
   CK(launch_pdl(&tiled_fixup_kernel<BT, PT, QC, RB, RP, kMode>, dim3(nfix), dim3(256), 0, st, p));
@@ -658,7 +677,9 @@ struct Solve {
       if (!tl_buf) CK(cudaMalloc(&tl_buf, 8 * 4096 * 8));
       p.dbg = tl_buf;
     }
+    kt_mark(st);
     CK(launch_pdl(kern, grid, dim3(SepS::NT), smem, st, p));
+    kt_mark(st);
     if (tl) {
       std::vector<unsigned long long> h(8 * 4096);
       CK(cudaMemcpyAsync(h.data(), tl_buf, 8 * 4096 * 8, cudaMemcpyDeviceToHost, st));
@@ -744,7 +765,9 @@ struct Solve {
     if (int e = set_max_smem(reinterpret_cast<const void*>(kern), fused_smem_bytes<NQ>())) return e;
     const size_t smem = (size_t)kFusedStages * fp.rowlen * 4 + kFusedStages * 8;
     ++g_launches;
+    kt_mark(st);
     CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(fused_warps(NQ) * 32), smem, st, fp));
+    kt_mark(st);
     return 0;
   }
   template <int NQ, bool kRowOnly>
@@ -764,8 +787,10 @@ struct Solve {
     const size_t smem = fused_ps_smem_bytes<NQ>();
     if (int e = set_max_smem(reinterpret_cast<const void*>(kern), smem)) return e;
     ++g_launches;
+    kt_mark(st);
     CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(fused_warps(NQ) * 32), smem, st, fp, cost,
                   (int)pr.d2, (float)(-kLog2e / lam)));
+    kt_mark(st);
     return 0;
   }
   template <int NQ>
@@ -789,7 +814,9 @@ struct Solve {
       const size_t smem = fg_smem_bytes<NQ>();
       if (int e = set_max_smem(reinterpret_cast<const void*>(kern), smem)) return e;
       ++g_launches;
+      kt_mark(st);
       CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(kFgThreads), smem, st, fp, nrb));
+      kt_mark(st);
       return 0;
     }
   }
@@ -937,8 +964,10 @@ struct Solve {
     p.status = at<int>(ws, L.status);
     if (int e = set_max_smem(reinterpret_cast<const void*>(&umma_gemm_kernel), kUmSmemBytes))
       return e;
+    kt_mark(st);
     CK(launch_pdl(umma_gemm_kernel, dim3(p.G), dim3(kUmThreads), kUmSmemBytes, st, tA,
                   rows ? tm_xh : tm_ah, rows ? tm_xl : tm_al, p));
+    kt_mark(st);
     CK(launch_pdl(umma_fixup_kernel, dim3((unsigned)p.G), dim3(256), 0, st, p));
     return 0;
   }
@@ -1284,7 +1313,9 @@ struct Solve {
       sp.dbg = tl_buf;
     }
     ++g_launches;
+    kt_mark(st);
     CK(cudaLaunchKernelEx(&cfg, &small_solve_kernel<kSmallNT>, sp));
+    kt_mark(st);
     if (tl) {
       unsigned long long h[64];
       CK(cudaMemcpyAsync(h, tl_buf, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -1403,6 +1434,9 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
                  float* out_log_v, int32_t* out_iterations, float* out_residuals, void* ws,
                  size_t ws_bytes, cudaStream_t st, bool allow_est = true,
                  const float* init_log_u = nullptr) {
+  for (cudaEvent_t e : g_kt.ev) cudaEventDestroy(e);
+  g_kt.ev.clear();
+  g_kt.on = (op.flags & SINKHORN_FLAG_TIME_KERNEL) != 0;
   Solve S;
   S.pr = pr;
   S.op = op;
@@ -1778,6 +1812,18 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
   }
+  if (g_kt.on) {   // the stream was synchronised by read_status
+    float tot = 0.f;
+    for (size_t k = 0; k + 1 < g_kt.ev.size(); k += 2) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, g_kt.ev[k], g_kt.ev[k + 1]) == cudaSuccess) tot += ms;
+    }
+    g_kt.last_ms = tot;
+    g_kt.last_launches = (int)(g_kt.ev.size() / 2);
+    for (cudaEvent_t e : g_kt.ev) cudaEventDestroy(e);
+    g_kt.ev.clear();
+    g_kt.on = false;
+  }
   if (hstatus == 11) {
     int row = 0;
     cudaMemcpy(&row, badrow, 4, cudaMemcpyDeviceToHost);
@@ -1804,6 +1850,10 @@ unsigned long long sinkhorn_launch_count_v1(void) { return g_launches; }
 unsigned long long sinkhorn_exact_reruns_v1(void) { return g_exact_reruns; }
 
 float sinkhorn_last_loop_ms_v1(void) { return g_last_loop_ms; }
+float sinkhorn_last_kernel_ms_v1(int32_t* launches) {
+  if (launches) *launches = g_kt.last_launches;
+  return g_kt.last_ms;
+}
 
 const char* sinkhorn_last_path_v1(void) { return g_last_path; }
 

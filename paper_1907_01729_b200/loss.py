@@ -66,6 +66,8 @@ class SolveResult:
     residuals: torch.Tensor   # (B,)
     loop_ms: float = -1.0     # iteration-loop time (CUDA events) when solve(time_loop=True)
     path: str = ""            # solver path taken ("small", "tiled", "persistent", "lane")
+    kernel_ms: float = -1.0   # dominant kernel's launches (CUDA events), solve(time_kernel=True)
+    kernel_launches: int = 0
 
 
 def _stream_handle(device: torch.device) -> int:
@@ -138,7 +140,8 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
           exact_max: bool = False, mufu_only: bool = False,
           persistent: bool = False, tiled_only: bool = False,
           dense_grid: bool = False, init_log_u=None, fused: bool = True,
-          fp64: bool = False, gemm: bool | None = None) -> SolveResult:
+          fp64: bool = False, gemm: bool | None = None,
+          time_kernel: bool = False) -> SolveResult:
     """batch_forward (batch.py:264-349) on the GPU.
 
     mu (B, d1), nu (B, d2) histograms; cost a (d1, d2) tensor shared by all
@@ -153,7 +156,10 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
     outputs, reaches the reference's default tolerance 1e-9; path "fp64".
     ``gemm``: None (default) takes the two-GEMM iteration (sweep_gemm.cuh) for
     shared costs larger than the fused pass handles; True forces it for any
-    shared cost, False never takes it.
+    shared cost, False never takes it.  ``time_kernel`` records CUDA events
+    around every launch of the solve's dominant kernel (``kernel_ms``,
+    ``kernel_launches``; measurement only -- the events break the launch
+    overlap).
     """
     if fp64:
         return _solve_f64(mu, nu, cost, lam, max_iters, tolerance, check_interval, validate)
@@ -176,7 +182,8 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
         (_lib.FLAG_MUFU_ONLY if mufu_only else 0) | (_lib.FLAG_PERSISTENT if persistent else 0) | \
         (_lib.FLAG_TILED_ONLY if tiled_only else 0) | (_lib.FLAG_DENSE_GRID if dense_grid else 0) | \
         (0 if fused else _lib.FLAG_NO_FUSED) | \
-        (_lib.FLAG_FORCE_GEMM if gemm else 0) | (_lib.FLAG_NO_GEMM if gemm is False else 0)
+        (_lib.FLAG_FORCE_GEMM if gemm else 0) | (_lib.FLAG_NO_GEMM if gemm is False else 0) | \
+        (_lib.FLAG_TIME_KERNEL if time_kernel else 0)
     out_cost = torch.empty(B, device=dev, dtype=torch.float32)
     log_u = torch.empty(B, d1, device=dev, dtype=torch.float32)
     log_v = torch.empty(B, d2, device=dev, dtype=torch.float32)
@@ -203,8 +210,88 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
     raise_for_status(st, "sinkhorn_forward_device_v1")
     loop_ms = float(lib.sinkhorn_last_loop_ms_v1()) if time_loop else -1.0
     path = lib.sinkhorn_last_path_v1().decode()
+    kms, kn = -1.0, 0
+    if time_kernel:
+        n = ctypes.c_int32(0)
+        kms, kn = float(lib.sinkhorn_last_kernel_ms_v1(ctypes.byref(n))), int(n.value)
     return SolveResult(out_cost, log_u, log_v, float(lam), int(iters.value), residuals, loop_ms,
-                       path)
+                       path, kms, kn)
+
+
+def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.0,
+                   check_interval: int = 10, chunks: int = 8, device=None,
+                   validate: bool = True) -> SolveResult:
+    """``solve`` from host tensors, overlapping the host->device upload with the solve.
+
+    mu (B, d1), nu (B, d2) and cost -- shared (d1, d2), per-sample (B, d1, d2)
+    or a GridCost -- in host memory (pin it for full PCIe bandwidth).  At
+    tolerance 0 the lanes are independent (test_batch.py:46-63), so the batch
+    is solved in ``chunks`` lane groups: while group k solves on the current
+    stream, group k+1's histograms and per-sample costs are copied on a
+    second stream into the other of two device buffers.  With tolerance > 0
+    the lockstep stopping rule couples every lane (batch.py:318-322), so the
+    batch is one group.  Results are device tensors, as from ``solve``.
+    """
+    mu, nu = torch.as_tensor(mu), torch.as_tensor(nu)
+    grid = isinstance(cost, GridCost)
+    if not grid:
+        cost = torch.as_tensor(cost)
+    B, d1, d2 = _check_shapes(mu, nu, cost)
+    dev = torch.device(device) if device is not None else \
+        torch.device("cuda", torch.cuda.current_device())
+    per_sample = (not grid) and cost.dim() == 3
+    if tolerance > 0 or B == 0:
+        chunks = 1
+    chunks = max(1, min(int(chunks), B if B else 1))
+    bounds = [(B * k // chunks, B * (k + 1) // chunks) for k in range(chunks)]
+    gmax = max(hi - lo for lo, hi in bounds) if B else 0
+    compute = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    f32 = dict(device=dev, dtype=torch.float32)
+    bufs = [(torch.empty(gmax, d1, **f32), torch.empty(gmax, d2, **f32),
+             torch.empty(gmax, d1, d2, **f32) if per_sample else None) for _ in range(2)]
+    shared = None if (grid or per_sample) else cost.to(**f32, non_blocking=True)
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    out_cost = torch.empty(B, **f32)
+    log_u = torch.empty(B, d1, **f32)
+    log_v = torch.empty(B, d2, **f32)
+    residuals = torch.empty(B, **f32)
+
+    def upload(k):
+        lo, hi = bounds[k]
+        m, n, c = bufs[k % 2]
+        with torch.cuda.stream(copy):
+            if k >= 2:
+                copy.wait_event(free[k % 2])      # group k-2 has finished with the buffer
+            m[: hi - lo].copy_(mu[lo:hi], non_blocking=True)
+            n[: hi - lo].copy_(nu[lo:hi], non_blocking=True)
+            if c is not None:
+                c[: hi - lo].copy_(cost[lo:hi], non_blocking=True)
+            ready[k % 2].record(copy)
+
+    iters = 0
+    with torch.cuda.device(dev):
+        upload(0)
+        if chunks > 1:
+            upload(1)
+        for k, (lo, hi) in enumerate(bounds):
+            m, n, c = bufs[k % 2]
+            compute.wait_event(ready[k % 2])
+            g = hi - lo
+            cg = cost if grid else (c[:g] if per_sample else shared)
+            r = solve(m[:g], n[:g], cg, lam, max_iters, tolerance, check_interval,
+                      validate=validate)
+            out_cost[lo:hi] = r.cost_e0
+            log_u[lo:hi] = r.log_u
+            log_v[lo:hi] = r.log_v
+            residuals[lo:hi] = r.residuals
+            iters = max(iters, r.iterations_run)
+            free[k % 2].record(compute)
+            if k + 2 < chunks:
+                upload(k + 2)
+    return SolveResult(out_cost, log_u, log_v, float(lam), iters, residuals, -1.0,
+                       _lib.load().sinkhorn_last_path_v1().decode())
 
 
 def _solve_f64(mu, nu, cost, lam, max_iters, tolerance, check_interval, validate) -> SolveResult:
