@@ -1639,7 +1639,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     // (same workspace, cost and shape) replays it as one CUDA graph, so its
     // ~2 launches per iteration cannot stall behind the host.
     FusedGraph* fg = nullptr;
-    if (!checks && g_reducer == nullptr && !g_no_graph)
+    if (!checks && g_reducer == nullptr && !g_no_graph && !g_kt.on)
       fg = fused_graph_slot(FusedGraphKey{ws, cost, pr.B, pr.d1, pr.d2, pr.cost_kind, op.lambda,
                                           op.max_iters, S.di.dev});
     if (fg != nullptr && fg->seen && fg->exec == nullptr) {   // second sighting: capture

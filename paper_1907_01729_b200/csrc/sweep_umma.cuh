@@ -252,14 +252,13 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     uint32_t ph = 0, aph = 0;
     for (long long u = u0; u < u1; ++u) {
       mbar_wait(&afull_sm[s], ph);
-      mbar_wait(&aempty[a], aph ^ 1);
-      tc_fence_after();
-      const uint32_t ahi = tbase + lane_off + kUmABase + kUmACols * a;
+      // split from shared memory first (overlaps the MMAs still reading the
+      // TMEM stage), then wait for the stage and store both planes
+      uint32_t hi[kUmBK], lo[kUmBK];
 #pragma unroll
       for (int sb = 0; sb < kUmSub; ++sb) {
         const float4* rowp = reinterpret_cast<const float4*>(smA + (size_t)s * kUmATileBytes +
                                                              sb * kUmASubBytes + row * 128);
-        uint32_t hi[32], lo[32];
 #if defined(SKB_UM_DBG_NOSPLIT) || defined(SKB_UM_DBG_NOLDS)
         if (false)
 #endif
@@ -268,20 +267,26 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           const float4 v = rowp[q ^ (row & 7)];
           const float x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float h = tf32_hi(x[e]);
-            hi[4 * q + e] = __float_as_uint(h);
-            lo[4 * q + e] = __float_as_uint(x[e] - h);
+          for (int e = 0; e < 4; e += 2) {   // lo = x - hi on packed pairs (FADD2)
+            const int c = 32 * sb + 4 * q + e;
+            const float h0 = tf32_hi(x[e]), h1 = tf32_hi(x[e + 1]);
+            hi[c] = __float_as_uint(h0);
+            hi[c + 1] = __float_as_uint(h1);
+            const uint64_t d2 = fadd2(pk2(x[e], x[e + 1]), pk2(-h0, -h1));
+            lo[c] = __float_as_uint(lo2(d2));
+            lo[c + 1] = __float_as_uint(hi2(d2));
           }
         }
-#ifndef SKB_UM_DBG_NOSPLIT
-        tmem_st32(ahi + 32 * sb, hi);
-        tmem_st32(ahi + kUmBK + 32 * sb, lo);
-#endif
       }
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&afree_sm[s])) : "memory");
+      mbar_wait(&aempty[a], aph ^ 1);
+      tc_fence_after();
+      const uint32_t ahi = tbase + lane_off + kUmABase + kUmACols * a;
 #ifndef SKB_UM_DBG_NOSPLIT
+      static_assert(kUmBK == 64, "the splitter stores 64-column planes");
+      tmem_st64(ahi, hi);
+      tmem_st64(ahi + kUmBK, lo);
       tmem_st_wait();
 #endif
       tc_fence_before();
@@ -302,9 +307,9 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       const long long tile = u / p.KCH;
       const int k0 = (int)(u % p.KCH);
       const int k1 = (int)(k0 + (u1 - u) < p.KCH ? k0 + (u1 - u) : p.KCH);
-      float acc[kUmBN];
+      uint64_t acc2[kUmBN / 2];   // packed pairs: FADD2 promotion
 #pragma unroll
-      for (int n = 0; n < kUmBN; ++n) acc[n] = 0.f;
+      for (int n = 0; n < kUmBN / 2; ++n) acc2[n] = 0ull;
       for (int kc = k0; kc < k1; kc += kUmPromo) {
         mbar_wait(&cfull[r], rph);
         tc_fence_after();
@@ -315,16 +320,26 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         for (int h = 0; h < kUmBN / 32; ++h) {
           uint32_t v0[32], v1[32];
           const uint32_t t = tbase + lane_off + r * kUmSlotCols + 32 * h;
-          tmem_ld32(t, v0);
-          tmem_ld32(t + kUmBN, v1);
+          tmem_ld32(t, v0);            // hi*hi + lo*hi
+          tmem_ld32(t + kUmBN, v1);    // hi*lo
           tmem_ld_wait();
 #pragma unroll
-          for (int n = 0; n < 32; ++n) acc[32 * h + n] += __uint_as_float(v1[n]) + __uint_as_float(v0[n]);
+          for (int n = 0; n < 16; ++n) {
+            const uint64_t s0 = fadd2(pk2(__uint_as_float(v0[2 * n]), __uint_as_float(v0[2 * n + 1])),
+                                      pk2(__uint_as_float(v1[2 * n]), __uint_as_float(v1[2 * n + 1])));
+            fadd2_acc(acc2[16 * h + n], s0);
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&cempty[r])) : "memory");
         if (++r == kUmSlots) { r = 0; rph ^= 1; }
+      }
+      float acc[kUmBN];
+#pragma unroll
+      for (int n = 0; n < kUmBN / 2; ++n) {
+        acc[2 * n] = lo2(acc2[n]);
+        acc[2 * n + 1] = hi2(acc2[n]);
       }
       const int nt = (int)(tile % p.NT), mt = (int)(tile / p.NT);
       const int m = mt * kUmBM + row;

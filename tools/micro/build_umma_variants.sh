@@ -8,6 +8,5 @@ F="-gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I$I -lcuda"
 build() { nvcc $F "$@" -o "umv_$(echo "$@" | tr -d ' =-' | tr 'D' '_')" umma_gemm_bench.cu & }
 build -DSKB_UM_SUB=2
 build -DSKB_UM_SUB=2 -DSKB_UM_DBG_NOSPLIT
-build -DSKB_UM_SUB=2 -DSKB_UM_DBG_NOLDS
 wait
 ls umv_*
