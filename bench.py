@@ -594,8 +594,7 @@ def run_ours(args, cfg, world, rank, local):
         r0 = rank * rows
         cost = index_cost_rows(d, r0, rows, dev)
         mu_l = mu[:, r0:r0 + rows].contiguous()
-        backend = (D.CudaGemmShardBackend(cost) if args.row_backend == "gemm"
-                   else D.CudaShardBackend(cost))
+        backend = None if args.row_backend == "gemm" else D.CudaShardBackend(cost)
     else:
         mu, nu, cost = make_inputs(cfg, dev, seed=1234 + rank)
     up = torch.ones(B, device=dev)
@@ -604,10 +603,13 @@ def run_ours(args, cfg, world, rank, local):
 
     def step():
         if row:
-            res = D.row_sharded_solve(mu_l, nu, backend, lam, iters, 0.0, 10, d1_total=d)
+            if backend is None:   # the library's loop: one NCCL sum per column sweep
+                res = D.row_sharded_solve_device(mu_l, nu, cost, lam, iters, 0.0, 10,
+                                                 time_loop=True)
+            else:
+                res = D.row_sharded_solve(mu_l, nu, backend, lam, iters, 0.0, 10, d1_total=d)
+                res.loop_ms, res.path = -1.0, "row-sharded"
             D.row_sharded_backward(res.log_u, res.log_v, lam, up, d1_total=d)
-            res.loop_ms, res.path = -1.0, ("row-sharded-gemm" if args.row_backend == "gemm"
-                                           else "row-sharded")
             return res
         res = skb.solve(mu, nu, cost, lam, iters, 0.0, 10, validate=True, time_loop=True)
         gm, gn = skb.potentials_backward(res.log_u, res.log_v, lam, up)
@@ -641,7 +643,10 @@ def run_ours(args, cfg, world, rank, local):
     reruns = lib.sinkhorn_exact_reruns_v1() - reruns0
     # the dominant kernel's average launch time: one more solve (untimed by the
     # step clock) with CUDA events around each of its launches
-    if row:
+    if row and backend is None:
+        kr = D.row_sharded_solve_device(mu_l, nu, cost, lam, iters, 0.0, 10, time_kernel=True)
+        kernel_ms = kr.kernel_ms / max(kr.kernel_launches, 1)
+    elif row:
         kernel_ms = None
     else:
         kr = skb.solve(mu, nu, cost, lam, iters, 0.0, 10, validate=True, time_kernel=True)
@@ -688,7 +693,7 @@ def run_ours(args, cfg, world, rank, local):
         "exact_reruns": int(reruns),
         "clocks": clocks,
         "step_ms_stats": step_stats,
-        "loop_ms_median": statistics.median(loop_ms) if not row else None,
+        "loop_ms_median": statistics.median(loop_ms) if loop_ms and loop_ms[0] > 0 else None,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = reference_cpu_sample(cfg, runs=1, light=cfg["cost"] != "per_sample" and d > 100)
@@ -817,7 +822,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--clock-interval-ms", type=int, default=100)
     ap.add_argument("--row-backend", choices=["gemm", "lse"], default="gemm",
-                    help="row sharding: local fp32 GEMMs (default) or log-domain half-sweeps")
+                    help="row sharding: the library's GEMM loop (default) or the exact "
+                         "log-domain half-sweep shards")
     ap.add_argument("--sharding", choices=["batch", "row"], default=None,
                     help="multi-GPU split (default: row for config 5 on N>1, else batch)")
     ap.add_argument("--probe-ranks", action="store_true", help=argparse.SUPPRESS)

@@ -43,6 +43,7 @@ extern "C" {
 #define SINKHORN_STATUS_INVALID_COST 15     /* core.py:53-63 ValueError */
 #define SINKHORN_STATUS_BAD_ARGUMENT 16     /* null pointer / unsupported descriptor */
 #define SINKHORN_STATUS_WORKSPACE 17        /* workspace too small */
+#define SINKHORN_STATUS_EXACT_NEEDED 18     /* row-sharded GEMM solve: rerun exactly (see below) */
 #define SINKHORN_STATUS_CUDA_ERROR 20       /* CUDA runtime error (message: sinkhorn_last_error) */
 
 /* ---- layer 1: host float64 views (ffi.ts:14-19 TensorView) ------------- */
@@ -208,6 +209,33 @@ int32_t sinkhorn_e0_partial_device_v1(int64_t B, int64_t d1, int64_t d2, double 
  * together or not at all.  NULL restores local checks. */
 typedef double (*sinkhorn_residual_reducer_v1)(double local_max, void* user);
 void sinkhorn_set_residual_reducer_v1(sinkhorn_residual_reducer_v1 fn, void* user);
+
+/* Row-sharded solves (BASELINE config 5 across GPUs).  Rank r
+ * owns rows I_r of the shared cost and of mu / log u; every rank holds the
+ * full nu and log v.  The library runs the GEMM iteration (sweep_gemm.cuh,
+ * contractions on the tensor cores) on the rank's rows and calls `allreduce`
+ * -- enqueue-only, on `stream`, no host synchronisation -- once per column
+ * sweep to sum the ranks' column partials (B*d2 floats), and once for the
+ * per-lane E0 partials (B floats).  With a common per-lane shift (every rank
+ * holds log v) the (max, sum-exp) merge of batch.py:116-130 reduces to that
+ * one sum.  Convergence checks (tolerance > 0) and the estimate-guard
+ * decision go through the residual reducer (sinkhorn_set_residual_reducer_v1),
+ * which the caller sets to a MAX over ranks.  prob->d1 is the rank's row
+ * count; mu_rows (B, d1), cost_rows (d1, d2); out_log_u_rows (B, d1).  The
+ * caller validates the histograms globally (a slice of mu does not sum to 1).
+ * Status 18 (SINKHORN_STATUS_EXACT_NEEDED, on every rank together): a range
+ * guard fired (sums below 2^-60); rerun the solve with the exact log-domain
+ * half-sweeps (sinkhorn_half_sweep_device_v1). */
+#define SINKHORN_REDUCE_SUM 0
+typedef void (*sinkhorn_allreduce_v1)(float* data, int64_t count, int32_t op, void* stream,
+                                      void* user);
+int32_t sinkhorn_forward_rows_device_v1(const sinkhorn_problem_v1* prob,
+                                        const sinkhorn_options_v1* opt, const float* mu_rows,
+                                        const float* nu, const float* cost_rows,
+                                        float* out_cost, float* out_log_u_rows, float* out_log_v,
+                                        int32_t* out_iterations, float* out_residuals,
+                                        sinkhorn_allreduce_v1 allreduce, void* user,
+                                        void* workspace, size_t workspace_bytes, void* stream);
 
 /* Transport-plan gradient w.r.t. the cost (north-star item 4, core.py:363-368):
  * SHARED:     dC[i,j]   = sum_b upstream[b] * P_b[i,j]

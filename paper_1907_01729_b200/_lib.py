@@ -22,6 +22,7 @@ STATUS_INVALID_CONFIG = 14
 STATUS_INVALID_COST = 15
 STATUS_BAD_ARGUMENT = 16
 STATUS_WORKSPACE = 17
+STATUS_EXACT_NEEDED = 18
 STATUS_CUDA_ERROR = 20
 
 COST_SHARED = 0
@@ -56,6 +57,7 @@ EXPORTED_SYMBOLS = (
     "sinkhorn_plan_grad_device_v1",
     "sinkhorn_e0_partial_device_v1",
     "sinkhorn_set_residual_reducer_v1",
+    "sinkhorn_forward_rows_device_v1",
     "sinkhorn_last_error",
     "sinkhorn_version",
     "sinkhorn_launch_count_v1",
@@ -102,6 +104,10 @@ class Options(ctypes.Structure):
 
 # double (*)(double local_max, void* user)
 REDUCER = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
+# void (*)(float* data, int64_t count, int32_t op, void* stream, void* user)
+ALLREDUCE = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                             ctypes.c_void_p, ctypes.c_void_p)
+REDUCE_SUM = 0
 
 _lock = threading.Lock()
 _lib = None
@@ -135,6 +141,9 @@ def _declare(lib):
         "sinkhorn_plan_grad_device_v1": (i32, [ctypes.POINTER(Problem), f64, P, P, P, P, P, P]),
         "sinkhorn_e0_partial_device_v1": (i32, [i64, i64, i64, f64, P, P, P, P, P, sz, P]),
         "sinkhorn_set_residual_reducer_v1": (None, [REDUCER, P]),
+        "sinkhorn_forward_rows_device_v1": (
+            i32, [ctypes.POINTER(Problem), ctypes.POINTER(Options), P, P, P, P, P, P,
+                  ctypes.POINTER(ctypes.c_int32), P, ALLREDUCE, P, P, sz, P]),
         "sinkhorn_last_error": (ctypes.c_char_p, []),
         "sinkhorn_version": (ctypes.c_char_p, []),
         "sinkhorn_launch_count_v1": (ctypes.c_ulonglong, []),

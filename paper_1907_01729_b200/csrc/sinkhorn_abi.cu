@@ -64,6 +64,11 @@ const bool g_use_fgemm = getenv("SKB_FUSED_ROWS") == nullptr;
 // Optional cross-rank agreement on the stopping test (batch-sharded solves).
 thread_local sinkhorn_residual_reducer_v1 g_reducer = nullptr;
 thread_local void* g_reducer_user = nullptr;
+// Row-sharded GEMM solves (sinkhorn_forward_rows_device_v1): the caller's
+// collective, enqueued on the solve's stream after every partial column
+// contraction (T = K_r^T a, summed over the ranks) and after the E0 partials.
+thread_local sinkhorn_allreduce_v1 g_allreduce = nullptr;
+thread_local void* g_allreduce_user = nullptr;
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -997,6 +1002,7 @@ struct Solve {
     CK(cudaMemsetAsync(F(L.gvmax0), 0, (size_t)pr.B * 4, st));
     if (int e = umma_split(F(L.ga), (int)pr.d1, F(L.gah), F(L.gal))) return e;
     if (int e = gemm(false, tm_kt, F(L.gt))) return e;
+    if (int e = sum_over_ranks(F(L.gt), pr.B * pr.d2)) return e;
     return gemm_col(F(L.gvmax0), nullptr, F(L.g2[1]), false);
   }
   // iteration k from v_k = g2[cur]: X, S = K X, u and a, T = K^T a, v_{k+1}
@@ -1031,6 +1037,7 @@ struct Solve {
     CK(cudaGetLastError());
     if (int e = umma_split(F(L.ga), (int)pr.d1, F(L.gah), F(L.gal))) return e;
     if (int e = gemm(false, tm_kt, F(L.gt))) return e;
+    if (int e = sum_over_ranks(F(L.gt), pr.B * pr.d2)) return e;
     return gemm_col(F(L.gvmax), F(L.g2[cur]), F(L.g2[cur ^ 1]), res);
   }
   // E0 from the last iteration's X and a: sum_i a_i ((K o C) X)_i
@@ -1039,6 +1046,17 @@ struct Solve {
     ++g_launches;
     gemm_e0_kernel<<<(unsigned)pr.B, 256, 0, st>>>(F(L.ga), F(L.gs), (int)pr.d1, out_cost,
                                                    at<int>(ws, L.status));
+    CK(cudaGetLastError());
+    return sum_over_ranks(out_cost, pr.B);   // row shards: E0 = sum of the ranks' row partials
+  }
+  // Row-sharded solves: the column sums of the local rows become the global
+  // ones.  In the linear domain every rank's partial carries the same shift
+  // (vmax_b: all ranks hold the full v), so the (max, sum-exp) merge of
+  // OnlineLseAccumulator.merge (batch.py:116-130) needs no max exchange: it is
+  // one sum all-reduce of the partial sums, enqueued on the solve's stream.
+  int sum_over_ranks(float* data, int64_t count) {
+    if (!g_allreduce) return 0;
+    g_allreduce(data, count, SINKHORN_REDUCE_SUM, st, g_allreduce_user);
     CK(cudaGetLastError());
     return 0;
   }
@@ -1789,6 +1807,14 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     // whatever its path, and all ranks rerun if any rank's estimate failed --
     // the reruns' stopping tests then call the reducer in step on every rank.
     if (g_reducer) hfail = g_reducer(hfail ? 1.0 : 0.0, g_reducer_user) > 0.0 ? 1 : 0;
+    if (hfail && g_allreduce) {   // row shards: the caller reruns the exact log-domain shards
+      if (timed) {
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+      }
+      return fail(SINKHORN_STATUS_EXACT_NEEDED,
+                  "row-sharded GEMM solve: a guard fired (sums below 2^-60); rerun exactly");
+    }
     if (hfail) {   // an estimate overshot: recompute the whole solve exactly
       ++g_exact_reruns;
       if (timed) {
@@ -1883,6 +1909,39 @@ int32_t sinkhorn_forward_device_v1(const sinkhorn_problem_v1* prob,
                       out_residuals, workspace, workspace_bytes,
                       static_cast<cudaStream_t>(stream),
                       (opt->flags & SINKHORN_FLAG_EXACT_MAX) == 0);
+}
+
+int32_t sinkhorn_forward_rows_device_v1(const sinkhorn_problem_v1* prob,
+                                        const sinkhorn_options_v1* opt, const float* mu_rows,
+                                        const float* nu, const float* cost_rows,
+                                        float* out_cost, float* out_log_u_rows, float* out_log_v,
+                                        int32_t* out_iterations, float* out_residuals,
+                                        sinkhorn_allreduce_v1 allreduce, void* user,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+  if (int e = check_problem(prob)) return e;
+  if (prob->cost_kind != SINKHORN_COST_SHARED)
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "row sharding needs a stored shared cost");
+  if (prob->B == 0) {
+    if (out_iterations) *out_iterations = 0;
+    return 0;
+  }
+  if (prob->d2 == 0) return fail(SINKHORN_STATUS_INVALID_HISTOGRAM, "empty histogram");
+  if (int e = check_options(opt)) return e;
+  if (!mu_rows || !nu || !cost_rows || !out_cost || !out_log_u_rows || !out_log_v || !allreduce)
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
+  sinkhorn_options_v1 op = *opt;
+  // the GEMM iteration, no single-launch solver; the caller validates the
+  // histograms globally (a rank's slice of mu does not sum to 1)
+  op.flags |= SINKHORN_FLAG_FORCE_GEMM | SINKHORN_FLAG_TILED_ONLY | SINKHORN_FLAG_SKIP_VALIDATION;
+  op.flags &= ~(SINKHORN_FLAG_NO_GEMM | SINKHORN_FLAG_EXACT_MAX);
+  g_allreduce = allreduce;
+  g_allreduce_user = user;
+  const int rc = forward_impl(*prob, op, mu_rows, nu, cost_rows, out_cost, out_log_u_rows,
+                              out_log_v, out_iterations, out_residuals, workspace, workspace_bytes,
+                              static_cast<cudaStream_t>(stream), true);
+  g_allreduce = nullptr;
+  g_allreduce_user = nullptr;
+  return rc;
 }
 
 int32_t sinkhorn_forward_warm_device_v1(const sinkhorn_problem_v1* prob,

@@ -11,15 +11,22 @@ runs on gloo/CPU tensors in the tests).
   The only other collective is the final all-gather of the per-lane losses.
 
 * Row sharding -- for supports too large for one GPU, rank r owns rows
-  I_r of the cost and of mu / log_u.  The column sweep becomes a local
-  partial (max, sum) reduction over I_r followed by the cross-GPU merge of
-  OnlineLseAccumulator.merge (batch.py:116-130): all-reduce(MAX) of the maxima,
-  local rescale, all-reduce(SUM) of the sums.  The row sweep is local.  E0 and
-  the backward's means merge the same way.
+  I_r of the cost and of mu / log_u.  ``row_sharded_solve_device`` runs the
+  whole lockstep loop in the library (sinkhorn_forward_rows_device_v1: the
+  GEMM iteration on the tensor cores over the rank's rows) and only hands
+  back a stream-ordered collective: per column sweep one all-reduce(SUM) of
+  the B x d2 column sums.  That sum *is* the (max, sum-exp) merge of
+  OnlineLseAccumulator.merge (batch.py:116-130): every rank's partial sums
+  carry the same per-lane shift vmax_b (all ranks hold the full log v), so the
+  max half of the merge is known in advance.  No host synchronisation per
+  iteration (tolerance 0); checks all-reduce one MAX.  A range guard (sums
+  below 2^-60) makes every rank rerun through ``row_sharded_solve`` with the
+  exact log-domain half-sweep shards (``CudaShardBackend``).
 
-The per-shard arithmetic goes through a *backend* (the CUDA library in
-production; tests inject the CPU oracle) so the collective logic is the same
-code in both.
+``row_sharded_solve`` is the backend-driven restatement used for that exact
+fallback and, with the CPU oracle as backend, by the gloo tests; there the
+column merge is all-reduce(MAX) of the maxima, a local rescale and
+all-reduce(SUM) of the sums.
 """
 
 from __future__ import annotations
@@ -32,7 +39,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .loss import SolveResult, potentials_backward, solve
+from .loss import SolveResult, solve
 
 LN2 = math.log(2.0)
 NEG_BIG = -1.0e30
@@ -121,74 +128,6 @@ class CudaShardBackend:
         return self._batch.e0_partial_log2(log_u_l, log_v, self.c, lam)
 
 
-class CudaGemmShardBackend:
-    """Per-shard arithmetic as fp32 GEMMs on the local rows' kernel matrix
-    (the GEMM iteration of csrc/sweep_gemm.cuh, restricted to rows I_r).
-
-    K_r = 2^(-c_r log2e / lam) <= 1 and, per lane, X_j = 2^(v_j - vmax):
-      row update:   u_i = log_mu_i - (vmax + log2 (K_r X)_i)          (local)
-      col partial:  (max, sum) = (umax_r, (K_r^T 2^(u - umax_r))_j)   (per lane shift)
-    so the cross-rank merge of the column sums is the same (max, sum-exp)
-    merge as the log-domain shards, with the max agreed once per lane.  A
-    call whose sums fall below 2^-60 (terms may have flushed) is redone by the
-    exact log-domain backend.  The GEMMs are cuBLAS SGEMMs through torch.
-    """
-
-    MIN = 2.0 ** -60
-
-    def __init__(self, cost_local: torch.Tensor):
-        self.c = cost_local.float().contiguous()
-        self._lam = None
-        self._exact = None
-
-    def _kernel(self, lam):
-        if self._lam != lam:
-            self.K = torch.exp2(self.c * (-1.0 / (lam * LN2)))
-            self.KC = self.K * self.c
-            self._lam = lam
-        return self.K
-
-    def exact(self):
-        if self._exact is None:
-            self._exact = CudaShardBackend(self.c)
-        return self._exact
-
-    def col_partial(self, log_u_l, lam):
-        K = self._kernel(lam)
-        u2 = log_u_l.float() / LN2
-        umax = torch.clamp(u2.amax(dim=1, keepdim=True), min=NEG_BIG)
-        a = torch.exp2(u2 - umax)
-        T = a @ K                                   # (B, d2) = sum_i a_i K_ij
-        if bool((T < self.MIN).any()):
-            return self.exact().col_partial(log_u_l, lam)
-        return umax.expand_as(T), T
-
-    def row_update(self, log_v, lam, log_mu_l):
-        K = self._kernel(lam)
-        v2 = log_v.float() / LN2
-        vmax = torch.clamp(v2.amax(dim=1, keepdim=True), min=NEG_BIG)
-        X = torch.exp2(v2 - vmax)
-        S = X @ K.t()                               # (B, d1_r) = sum_j K_ij X_j
-        if bool(((S < self.MIN) & ~torch.isneginf(log_mu_l)).any()):
-            return self.exact().row_update(log_v, lam, log_mu_l)
-        lse = (vmax + torch.log2(S)) * LN2
-        return torch.where(torch.isneginf(log_mu_l), log_mu_l, log_mu_l - lse)
-
-    def e0_partial(self, log_u_l, log_v, lam):
-        """Per lane log2 sum_{i local, j} P_ij c_ij = log2 sum_i a_i (KC X)_i."""
-        K = self._kernel(lam)
-        v2 = log_v.float() / LN2
-        vmax = torch.clamp(v2.amax(dim=1, keepdim=True), min=NEG_BIG)
-        X = torch.exp2(v2 - vmax)
-        # rows whose terms may have flushed: the exact log-domain partial
-        if bool(((X @ K.t() < self.MIN) & ~torch.isneginf(log_u_l)).any()):
-            return self.exact().e0_partial(log_u_l, log_v, lam)
-        SE = X @ self.KC.t()                        # (B, d1_r)
-        w = torch.exp2(log_u_l.float() / LN2 + vmax)  # a_i = 2^(u_i + vmax)
-        tot = (w * SE).double().sum(dim=1)
-        return torch.where(tot > 0, torch.log2(tot), torch.full_like(tot, -math.inf)).float()
-
-
 def _merge_lse(m: torch.Tensor, s: torch.Tensor, group) -> torch.Tensor:
     """All-rank OnlineLseAccumulator.merge of (max, sum) pairs in log base 2 -> natural LSE."""
     M = m.clone()
@@ -257,6 +196,124 @@ def row_sharded_solve(mu_local, nu, backend, lam: float, max_iters: int,
     return SolveResult(cost, log_u, log_v, float(lam), iters, res)
 
 
+class _CudaArrayView:
+    """A raw float32 device buffer as a zero-copy torch tensor (CUDA array interface)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f4",
+                                         "data": (int(ptr), False), "version": 3}
+
+
+class _SumOverRanks:
+    """The library's allreduce callback: sum a float32 buffer over the group on
+    the current stream (NCCL enqueues; nothing waits on the host)."""
+
+    def __init__(self, group, device):
+        self.group, self.device = group, device
+        self.error = None
+        self.calls = 0
+        self.fn = _lib.ALLREDUCE(self._call)
+
+    def _call(self, ptr, count, op, stream, user):
+        try:
+            if op != _lib.REDUCE_SUM:
+                raise ValueError(f"unsupported reduction {op}")
+            self.calls += 1
+            if count == 0:
+                return
+            if self.device.type == "cuda":
+                t = torch.as_tensor(_CudaArrayView(ptr, count), device=self.device)
+            else:   # host buffers (the gloo tests drive the callback directly)
+                import numpy as np
+
+                t = torch.from_numpy(np.ctypeslib.as_array(
+                    (ctypes.c_float * int(count)).from_address(int(ptr))))
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        except Exception as err:   # never unwind through the C ABI
+            self.error = err
+
+
+def _check_row_histograms(mu_local, nu, group):
+    """validate_histogram (core.py:143-160) on row-sharded mu: finite and >= 0
+    per shard, |sum - 1| <= 1e-6 over the shards' partial sums (ffi.ts:111-115)."""
+    from .errors import InvalidHistogram
+
+    part = mu_local.double().sum(dim=1)
+    bad = (~torch.isfinite(mu_local).all(dim=1) | (mu_local < 0).any(dim=1)).double()
+    dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(bad, op=dist.ReduceOp.MAX, group=group)
+    badnu = ~torch.isfinite(nu).all(dim=1) | (nu < 0).any(dim=1) | \
+        ((nu.double().sum(dim=1) - 1.0).abs() > 1e-6)
+    rows = (bad > 0) | ((part - 1.0).abs() > 1e-6) | badnu
+    if bool(rows.any()):
+        raise InvalidHistogram(f"invalid histogram in row {int(torch.nonzero(rows)[0])}")
+
+
+def row_sharded_solve_device(mu_local, nu, cost_local, lam: float, max_iters: int,
+                             tolerance: float = 0.0, check_interval: int = 10, group=None,
+                             validate: bool = True, time_loop: bool = False,
+                             time_kernel: bool = False) -> SolveResult:
+    """Row-sharded lockstep solve with the whole loop in the library.
+
+    mu_local (B, d1_r) and cost_local (d1_r, d2): this rank's rows; nu (B, d2)
+    replicated.  Returns log_u for the local rows, the full log_v, the global
+    E0 per lane, the global iteration count and residuals -- batch.py:264-349
+    semantics, sharded.  Falls back to the exact log-domain shards when the
+    library reports a fired range guard (status 18, on every rank together).
+    """
+    from .errors import raise_for_status
+    from .loss import _as_f32_cuda, _problem, _stream_handle, _workspace
+
+    mu_local = _as_f32_cuda(mu_local)
+    dev = mu_local.device
+    nu = _as_f32_cuda(nu, dev)
+    cost_local = _as_f32_cuda(cost_local, dev)
+    B, d1 = mu_local.shape
+    d2 = nu.shape[1]
+    if nu.shape[0] != B or tuple(cost_local.shape) != (d1, d2):
+        from .errors import ShapeMismatch
+
+        raise ShapeMismatch(f"mu rows {tuple(mu_local.shape)}, nu {tuple(nu.shape)}, "
+                            f"cost rows {tuple(cost_local.shape)}")
+    if validate:
+        _check_row_histograms(mu_local, nu, group)
+    lib = _lib.load()
+    pr = _problem(B, d1, d2, cost_local)
+    op = _lib.Options()
+    op.lam, op.max_iters, op.check_interval, op.tolerance = float(lam), int(max_iters), \
+        int(check_interval), float(tolerance)
+    op.flags = (_lib.FLAG_TIME_LOOP if time_loop else 0) | \
+        (_lib.FLAG_TIME_KERNEL if time_kernel else 0)
+    out_cost = torch.empty(B, device=dev, dtype=torch.float32)
+    log_u = torch.empty(B, d1, device=dev, dtype=torch.float32)
+    log_v = torch.empty(B, d2, device=dev, dtype=torch.float32)
+    residuals = torch.empty(B, device=dev, dtype=torch.float32)
+    iters = ctypes.c_int32(0)
+    summer = _SumOverRanks(group, dev)
+    with torch.cuda.device(dev), global_residual_reducer(group):
+        ws = _workspace(dev, lib.sinkhorn_workspace_bytes_v1(ctypes.byref(pr)))
+        st = lib.sinkhorn_forward_rows_device_v1(
+            ctypes.byref(pr), ctypes.byref(op), mu_local.data_ptr(), nu.data_ptr(),
+            cost_local.data_ptr(), out_cost.data_ptr(), log_u.data_ptr(), log_v.data_ptr(),
+            ctypes.byref(iters), residuals.data_ptr(), summer.fn, None, ws.data_ptr(),
+            ws.numel(), _stream_handle(dev))
+    if summer.error is not None:
+        raise summer.error
+    if st == _lib.STATUS_EXACT_NEEDED:
+        return row_sharded_solve(mu_local, nu, CudaShardBackend(cost_local), lam, max_iters,
+                                 tolerance, check_interval, group)
+    raise_for_status(st, "sinkhorn_forward_rows_device_v1")
+    # row residuals are per shard: the lane maximum over the ranks
+    dist.all_reduce(residuals, op=dist.ReduceOp.MAX, group=group)
+    kms, kn = -1.0, 0
+    if time_kernel:
+        n = ctypes.c_int32(0)
+        kms, kn = float(lib.sinkhorn_last_kernel_ms_v1(ctypes.byref(n))), int(n.value)
+    return SolveResult(out_cost, log_u, log_v, float(lam), int(iters.value), residuals,
+                       float(lib.sinkhorn_last_loop_ms_v1()) if time_loop else -1.0,
+                       "row-sharded-gemm", kms, kn)
+
+
 def row_sharded_backward(log_u_local, log_v, lam: float, upstream, group=None,
                          d1_total: int | None = None):
     """batch_backward (batch.py:352-375) with log_u's rows sharded: the lane
@@ -283,9 +340,7 @@ def row_sharded_backward(log_u_local, log_v, lam: float, upstream, group=None,
 
 
 __all__ = [
-    "CudaGemmShardBackend", "CudaShardBackend", "batch_sharded_solve", "gather_lane_values", "global_max",
-    "global_residual_reducer",
-    "row_sharded_backward", "row_sharded_solve",
+    "CudaShardBackend", "batch_sharded_solve", "gather_lane_values", "global_max",
+    "global_residual_reducer", "row_sharded_backward", "row_sharded_solve",
+    "row_sharded_solve_device",
 ]
-
-_ = (ctypes, potentials_backward)

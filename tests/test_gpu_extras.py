@@ -90,16 +90,19 @@ def nccl_world1(cuda):
 @pytest.mark.parametrize("name", ["config5_pin4096", "rect_37x53", "config1_tol", "stability"])
 def test_row_sharded_solve_on_the_device(name, backend, nccl_world1, cuda):
     """row_sharded_solve (NCCL, one rank) with the log-domain half-sweep shards
-    and with the GEMM shards, against the reference."""
+    and with the library's row-sharded GEMM loop, against the reference."""
     from paper_1907_01729_b200 import distributed as D
 
     g = load_golden(name)
     c = torch.tensor(golden_cost(g), dtype=torch.float32, device=cuda)
     mu = torch.tensor(g["mu"], dtype=torch.float32, device=cuda)
     nu = torch.tensor(g["nu"], dtype=torch.float32, device=cuda)
-    shard = D.CudaGemmShardBackend(c) if backend == "gemm" else D.CudaShardBackend(c)
-    res = D.row_sharded_solve(mu, nu, shard, float(g["lam"]), int(g["max_iters"]),
-                              float(g["tol"]), int(g["check_interval"]))
+    if backend == "gemm":   # the library's row-sharded loop (sinkhorn_forward_rows_device_v1)
+        res = D.row_sharded_solve_device(mu, nu, c, float(g["lam"]), int(g["max_iters"]),
+                                         float(g["tol"]), int(g["check_interval"]))
+    else:
+        res = D.row_sharded_solve(mu, nu, D.CudaShardBackend(c), float(g["lam"]),
+                                  int(g["max_iters"]), float(g["tol"]), int(g["check_interval"]))
     assert res.iterations_run == int(g["iterations_run"])
     rel = np.abs(res.cost_e0.double().cpu().numpy() - g["cost_e0"]) / g["cost_e0"]
     assert rel.max() <= LOSS_RTOL
@@ -215,11 +218,14 @@ def test_config5_full_support_against_float64(nccl_world1, cuda):
         runs[name] = (r.path, r.cost_e0.double().cpu(), r.log_u.double().cpu())
         del r
         release()
-    for name, backend in (("rows-lse", D.CudaShardBackend), ("rows-gemm", D.CudaGemmShardBackend)):
-        r = D.row_sharded_solve(mu, nu, backend(c), lam, iters, 0.0, d1_total=d)
-        runs[name] = (name, r.cost_e0.double().cpu(), r.log_u.double().cpu())
-        del r
-        release()
+    r = D.row_sharded_solve(mu, nu, D.CudaShardBackend(c), lam, iters, 0.0, d1_total=d)
+    runs["rows-lse"] = ("rows-lse", r.cost_e0.double().cpu(), r.log_u.double().cpu())
+    del r
+    release()
+    r = D.row_sharded_solve_device(mu, nu, c, lam, iters, 0.0)
+    runs["rows-gemm"] = ("rows-gemm", r.cost_e0.double().cpu(), r.log_u.double().cpu())
+    del r
+    release()
     assert runs["gemm"][0] == "gemm" and runs["tiled"][0] == "tiled"
     for name, (_, cost, log_u) in runs.items():
         rel = float(((cost - want_cost).abs() / want_cost).max())
