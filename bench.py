@@ -583,8 +583,16 @@ def run_ours(args, cfg, world, rank, local):
     if row:
         # BASELINE config 5: the cost's rows are sharded over the ranks; every
         # column sweep merges (max, sum-exp) pairs across ranks
-        if not dist.is_initialized():
-            dist.init_process_group("nccl", device_id=dev)   # also for a 1-rank run
+        if not dist.is_initialized():   # also for a 1-rank run outside torchrun
+            if "RANK" not in os.environ:
+                import socket
+
+                with socket.socket() as sk:
+                    sk.bind(("127.0.0.1", 0))
+                    os.environ.setdefault("MASTER_PORT", str(sk.getsockname()[1]))
+                os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("nccl", device_id=dev)
         from paper_1907_01729_b200 import distributed as D
 
         if d % world:
