@@ -189,7 +189,8 @@ __global__ void __launch_bounds__(256) export_potential_kernel(const float* __re
                                                                int B, int d, long long sb,
                                                                long long si,
                                                                float* __restrict__ out,
-                                                               int* status, float scale) {
+                                                               int* status, float scale,
+                                                               int strict = 1) {
   __shared__ float tile[32][33];
   const int i0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -207,7 +208,9 @@ __global__ void __launch_bounds__(256) export_potential_kernel(const float* __re
     const int b = b0 + r, i = i0 + tx;
     if (b < B && i < d) {
       const float v = tile[r][tx];
-      if (v != v) nan = true;
+      // solver state: NaN, +inf or sentinel-scale (common.cuh); the half-sweep
+      // API (fused_log_reduction) returns +inf like the reference and flags NaN only
+      if (strict ? broken_state(v) : (v != v)) nan = true;
       out[(size_t)b * d + i] = v * scale;
     }
   }

@@ -112,6 +112,15 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return r;
 }
 
+// A potential (log2 units) is a broken state when it is NaN or +inf -- or at
+// the scale of the finite -inf sentinel kNegBig, which only an empty
+// reduction produces.  That is the case where a target with positive mass has
+// no finite term in its reduction (every -c/lambda is -inf): the reference's
+// next half-sweep then evaluates -inf + inf = NaN and batch_forward raises
+// NaNProduced (batch.py:326-327), so the device reports status 12.
+constexpr float kStateMax = 1.0e29f;
+__device__ __forceinline__ bool broken_state(float v) { return !(v <= kStateMax); }
+
 // (m, s) -> log2-sum-exp; an empty accumulator (s == 0) is -inf (batch.py:132-138).
 __device__ __forceinline__ float lse_final(float m, float s) {
   return s > 0.0f ? m + log2f(s) : neg_inf();

@@ -2257,14 +2257,14 @@ int32_t sinkhorn_half_sweep_device_v1(int64_t B, int64_t d1, int64_t d2, double 
   if (partial) {
     ++g_launches;
     export_potential_kernel<<<gv, 256, 0, st>>>(S.F(L.g2[0]), (int)B, (int)d2, L.sb2, L.si2,
-                                                out_max, status, 1.0f);
+                                                out_max, status, 1.0f, 0);
     ++g_launches;
     export_potential_kernel<<<gv, 256, 0, st>>>(S.F(L.g2[1]), (int)B, (int)d2, L.sb2, L.si2,
-                                                out_sum, status, 1.0f);
+                                                out_sum, status, 1.0f, 0);
   } else {
     ++g_launches;
     export_potential_kernel<<<gv, 256, 0, st>>>(S.F(L.g2[0]), (int)B, (int)d2, L.sb2, L.si2,
-                                                out, status, kLn2);
+                                                out, status, kLn2, 0);
   }
   CK(cudaGetLastError());
   int h = 0;

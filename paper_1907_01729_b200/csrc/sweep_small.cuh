@@ -375,16 +375,16 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
     bool nan = false;
     for (int e = tid; e < nl * p.d1; e += NT) {
       const float v = sm.f[e];
-      nan |= (v != v);
+      nan |= broken_state(v);
       p.out_log_u[(size_t)b0 * p.d1 + e] = v * kLn2;
     }
     const float* gv = sm.g(cur);
     for (int e = tid; e < nl * p.d2; e += NT) {
       const float v = gv[e];
-      nan |= (v != v);
+      nan |= broken_state(v);
       p.out_log_v[(size_t)b0 * p.d2 + e] = v * kLn2;
     }
-    if (nan) set_status(p.status, 12);   // batch.py:326-327 NaNProduced
+    if (nan) set_status(p.status, 12);   // batch.py:326-327 NaNProduced (see broken_state)
   }
   if (blockIdx.x == 0 && tid == 0) p.result[0] = iters;
 }

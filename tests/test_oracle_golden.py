@@ -9,6 +9,8 @@ reference's closed-form known answers.  Runs on CPU.
 from __future__ import annotations
 
 import math
+import os
+import sys
 
 import numpy as np
 import pytest
@@ -173,3 +175,30 @@ def test_ffi_status_semantics():
     assert st == orc.STATUS_INVALID_CONFIG
     st, *_ = orc.forward_v1([[0.5, 0.5]], [[0.5, 0.5]], -c2, 0.5, 10, 0)
     assert st == orc.STATUS_INVALID_COST
+
+
+def test_nan_state_instance_raises_in_reference_and_oracle():
+    """The status-12 instance of tests/test_gpu_batch_props.py: c = 1e30,
+    lambda = 1e-300 makes A = -c/lambda = -inf, the state turns NaN and the
+    reference raises NaNProduced (batch.py:326-327); the oracle agrees."""
+    import warnings
+
+    from oracle import sinkhorn_oracle as orc
+
+    rng = np.random.default_rng(6)
+    mu = orc.random_histogram_batch(3, 64, rng)
+    nu = orc.random_histogram_batch(3, 64, rng)
+    c = np.full((64, 64), 1.0e30)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        with pytest.raises(orc.OracleError, match="NaNProduced"):
+            orc.batch_forward(mu, nu, c, 1e-300, 20, 0.0)
+        ref_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                               "baseline", "_ref")
+        if os.path.isfile(os.path.join(ref_dir, "sinkloss", "batch.py")):
+            sys.path.insert(0, ref_dir)
+            import sinkloss as sk
+
+            with pytest.raises(sk.NaNProduced):
+                sk.batch_forward(sk.HistogramBatch(mu), sk.HistogramBatch(nu), sk.CostMatrix(c),
+                                 sk.SinkhornConfig(lam=1e-300, max_iters=20, tolerance=0.0))

@@ -1,0 +1,46 @@
+"""Where the linear-domain fast path of shared costs stops applying.
+
+Config 2's shape (B=256, 28x28 grid cost, 100 iterations) at decreasing
+lambda: the solver path, the exact reruns its range guards trigger
+(sinkhorn_exact_reruns_v1), the loop time, and parity of 4 lanes against the
+float64 oracle.  Prints one JSON object (committed under profiles/).
+
+    python tools/lambda_sweep.py > profiles/r02_lambda_sweep.json
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1907_01729_b200 as skb  # noqa: E402
+from oracle import sinkhorn_oracle as orc  # noqa: E402
+from paper_1907_01729_b200 import _lib  # noqa: E402
+
+dev = torch.device("cuda", 0)
+lib = _lib.load()
+rng = np.random.default_rng(0)
+B, iters = 256, 100
+mu = orc.fp32_exact(orc.random_histogram_batch(B, 784, rng))
+nu = orc.fp32_exact(orc.random_histogram_batch(B, 784, rng))
+c = orc.fp32_exact(orc.grid2d_cost(28))
+tm, tn, tc = (torch.tensor(x, dtype=torch.float32, device=dev) for x in (mu, nu, c))
+rows = []
+for lam in (0.1, 0.05, 0.02, 0.01, 0.005, 0.002, 0.001):
+    skb.solve(tm, tn, tc, lam, iters, 0.0, time_loop=True)       # warm
+    r0 = lib.sinkhorn_exact_reruns_v1()
+    t0 = time.perf_counter()
+    res = skb.solve(tm, tn, tc, lam, iters, 0.0, time_loop=True)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    reruns = lib.sinkhorn_exact_reruns_v1() - r0
+    ref = orc.batch_forward(mu[:4], nu[:4], c, lam, iters, 0.0, workers=os.cpu_count() or 1)
+    rel = float(np.max(np.abs(res.cost_e0[:4].double().cpu().numpy() - ref.cost_e0) / ref.cost_e0))
+    rows.append({"lambda": lam, "path": res.path, "exact_reruns": int(reruns),
+                 "loop_ms": res.loop_ms, "solve_wall_ms": wall * 1e3,
+                 "loss_rel_err_4_lanes": rel, "max_c_over_lambda": float(c.max() / lam)})
+print(json.dumps({"workload": "config2 shape: B=256, 28x28 grid cost, 100 iterations, tol 0",
+                  "rows": rows}, indent=1))
