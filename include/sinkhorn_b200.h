@@ -106,6 +106,8 @@ typedef struct sinkhorn_problem_v1 {
                                             pass applies (d <= 1024) */
 #define SINKHORN_FLAG_TIME_KERNEL 2048u  /* CUDA events around each launch of the solve's
                                             dominant kernel (sinkhorn_last_kernel_ms_v1) */
+#define SINKHORN_FLAG_FORCE_RERUN 4096u  /* diagnostics: behave as if an estimate guard fired
+                                            (exercises the exact rerun, sync and async) */
 
 typedef struct sinkhorn_options_v1 {
   double lambda;          /* > 0, finite */
@@ -209,6 +211,24 @@ int32_t sinkhorn_e0_partial_device_v1(int64_t B, int64_t d1, int64_t d2, double 
  * together or not at all.  NULL restores local checks. */
 typedef double (*sinkhorn_residual_reducer_v1)(double local_max, void* user);
 void sinkhorn_set_residual_reducer_v1(sinkhorn_residual_reducer_v1 fn, void* user);
+
+/* Asynchronous forward (tolerance 0 only; SPEC.md:515-516 reentrancy, no host
+ * synchronisation -- SURVEY 8(b) "none with tol=0").  Same arguments as
+ * sinkhorn_forward_device_v1 minus out_iterations (= max_iters), plus a device
+ * int32 the library writes the final status to, in stream order: the call
+ * returns once the solve is enqueued.  Host-detectable errors (shapes,
+ * config, null pointers, workspace) are still returned.  Device-detected
+ * statuses (11 histogram, 12 non-finite, 15 cost) land in *device_status.  The
+ * estimate-guard rerun is decided on the device: a conditional graph node runs
+ * the exact solve (captured once per pointers/problem and replayed) only when
+ * a guard fired.  Workspace and outputs must stay alive until the stream
+ * reaches the solve's end. */
+int32_t sinkhorn_forward_async_device_v1(const sinkhorn_problem_v1* prob,
+                                         const sinkhorn_options_v1* opt, const float* mu,
+                                         const float* nu, const float* cost, float* out_cost,
+                                         float* out_log_u, float* out_log_v,
+                                         float* out_residuals, int32_t* device_status,
+                                         void* workspace, size_t workspace_bytes, void* stream);
 
 /* Row-sharded solves (BASELINE config 5 across GPUs).  Rank r
  * owns rows I_r of the shared cost and of mu / log u; every rank holds the

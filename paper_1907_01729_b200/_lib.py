@@ -40,6 +40,7 @@ FLAG_NO_FUSED = 256
 FLAG_NO_GEMM = 512
 FLAG_FORCE_GEMM = 1024
 FLAG_TIME_KERNEL = 2048
+FLAG_FORCE_RERUN = 4096
 
 # every symbol include/sinkhorn_b200.h declares
 EXPORTED_SYMBOLS = (
@@ -58,6 +59,7 @@ EXPORTED_SYMBOLS = (
     "sinkhorn_e0_partial_device_v1",
     "sinkhorn_set_residual_reducer_v1",
     "sinkhorn_forward_rows_device_v1",
+    "sinkhorn_forward_async_device_v1",
     "sinkhorn_last_error",
     "sinkhorn_version",
     "sinkhorn_launch_count_v1",
@@ -141,6 +143,9 @@ def _declare(lib):
         "sinkhorn_plan_grad_device_v1": (i32, [ctypes.POINTER(Problem), f64, P, P, P, P, P, P]),
         "sinkhorn_e0_partial_device_v1": (i32, [i64, i64, i64, f64, P, P, P, P, P, sz, P]),
         "sinkhorn_set_residual_reducer_v1": (None, [REDUCER, P]),
+        "sinkhorn_forward_async_device_v1": (
+            i32, [ctypes.POINTER(Problem), ctypes.POINTER(Options), P, P, P, P, P, P, P, P, P, sz,
+                  P]),
         "sinkhorn_forward_rows_device_v1": (
             i32, [ctypes.POINTER(Problem), ctypes.POINTER(Options), P, P, P, P, P, P,
                   ctypes.POINTER(ctypes.c_int32), P, ALLREDUCE, P, P, sz, P]),

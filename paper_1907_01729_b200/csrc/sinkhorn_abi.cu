@@ -1447,14 +1447,38 @@ FusedGraph* fused_graph_slot(const FusedGraphKey& k) {
   return &g_fused_graphs.back();
 }
 
+int enqueue_async_tail(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op,
+                       const float* mu, const float* nu, const float* cost, float* out_cost,
+                       float* out_log_u, float* out_log_v, float* out_residuals, void* ws,
+                       size_t ws_bytes, cudaStream_t st, const float* init_log_u,
+                       int32_t* device_status, const int* ws_status, const int* est_fail,
+                       bool can_fail);
+
+// capturing: enqueue only (the body of an asynchronous solve's rerun graph);
+// device_status != nullptr: asynchronous solve (tolerance 0) -- no host
+// synchronisation, the status and the rerun decision stay on the device.
+__global__ void fill_int_kernel(int* p, int n, int v) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = v;
+}
+// Asynchronous solves: the rerun decision on the device (a conditional graph
+// node reads est_fail), and the final status copied to the caller's word.
+__global__ void async_gate_kernel(cudaGraphConditionalHandle h, const int* est_fail,
+                                  const int* status) {
+  cudaGraphSetConditional(h, (*est_fail != 0 && *status == 0) ? 1u : 0u);
+}
+__global__ void async_status_kernel(const int* status, int32_t* out) { *out = *status; }
+
 int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, const float* mu,
                  const float* nu, const float* cost, float* out_cost, float* out_log_u,
                  float* out_log_v, int32_t* out_iterations, float* out_residuals, void* ws,
                  size_t ws_bytes, cudaStream_t st, bool allow_est = true,
-                 const float* init_log_u = nullptr) {
+                 const float* init_log_u = nullptr, int32_t* device_status = nullptr,
+                 bool capturing = false) {
+  const bool async_mode = device_status != nullptr;
+  const bool force_rerun_diag = (op.flags & SINKHORN_FLAG_FORCE_RERUN) != 0;
   for (cudaEvent_t e : g_kt.ev) cudaEventDestroy(e);
   g_kt.ev.clear();
-  g_kt.on = (op.flags & SINKHORN_FLAG_TIME_KERNEL) != 0;
+  g_kt.on = !async_mode && (op.flags & SINKHORN_FLAG_TIME_KERNEL) != 0;
   Solve S;
   S.pr = pr;
   S.op = op;
@@ -1587,7 +1611,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   // Optional: CUDA events on the caller's stream around the iteration loop, so
   // a benchmark can report the sweep kernels' average launch duration.
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  const bool timed = (op.flags & SINKHORN_FLAG_TIME_LOOP) != 0;
+  const bool timed = !async_mode && (op.flags & SINKHORN_FLAG_TIME_LOOP) != 0;
   if (timed) {
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
@@ -1657,7 +1681,7 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     // (same workspace, cost and shape) replays it as one CUDA graph, so its
     // ~2 launches per iteration cannot stall behind the host.
     FusedGraph* fg = nullptr;
-    if (!checks && g_reducer == nullptr && !g_no_graph && !g_kt.on)
+    if (!checks && g_reducer == nullptr && !g_no_graph && !g_kt.on && !capturing)
       fg = fused_graph_slot(FusedGraphKey{ws, cost, pr.B, pr.d1, pr.d2, pr.cost_kind, op.lambda,
                                           op.max_iters, S.di.dev});
     if (fg != nullptr && fg->seen && fg->exec == nullptr) {   // second sighting: capture
@@ -1795,6 +1819,22 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
                          st));
   }
   if (out_iterations) *out_iterations = iters;
+  if (force_rerun_diag && allow_est && (L.tiled || L.fused || L.gemm)) {   // diagnostics
+    ++g_launches;
+    fill_int_kernel<<<1, 32, 0, st>>>(S.est_fail, 1, 1);
+    CK(cudaGetLastError());
+  }
+  if (capturing) {   // the rerun body reports its own status word
+    ++g_launches;
+    async_status_kernel<<<1, 1, 0, st>>>(at<int>(ws, L.status), device_status);
+    CK(cudaGetLastError());
+    return 0;
+  }
+  if (device_status)
+    return enqueue_async_tail(pr, op, mu, nu, cost, out_cost, out_log_u, out_log_v,
+                              out_residuals, ws, ws_bytes, st, init_log_u, device_status,
+                              at<int>(ws, L.status), S.est_fail,
+                              allow_est && (L.tiled || L.fused || L.gemm));
   int hstatus = 0;
   if (int e = S.read_status(&hstatus)) return e;
   static const bool no_rerun = getenv("SKB_NO_RERUN") != nullptr;   // diagnostics
@@ -1859,6 +1899,157 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   return 0;
 }
 
+// ---- asynchronous solves (SINKHORN_FLAG_ASYNC, tolerance 0) ------------------
+// The tail of an asynchronous forward is one graph launch: a gate kernel sets
+// a conditional node from the estimate guard (est_fail) and the status word;
+// the node's body is the whole exact solve (allow_est = false), captured once
+// per (workspace, pointers, problem, options) and replayed; a last kernel
+// copies the status word to the caller's device int.  So the rerun decision
+// (batch.py semantics are unchanged: the exact solve replaces the estimate
+// one) never waits on the host.
+struct AsyncGraphKey {   // the slot: workspace + problem + options (pointers may change)
+  const void* ws;
+  int64_t B, d1, d2;
+  int32_t kind, max_iters, flags, dev;
+  double lambda;
+  size_t ws_bytes;
+  bool operator==(const AsyncGraphKey& o) const {
+    return ws == o.ws && B == o.B && d1 == o.d1 && d2 == o.d2 && kind == o.kind &&
+           max_iters == o.max_iters && flags == o.flags && dev == o.dev && lambda == o.lambda &&
+           ws_bytes == o.ws_bytes;
+  }
+};
+struct AsyncGraph {
+  AsyncGraphKey key;
+  const void* ptrs[9] = {};   // the buffers the captured rerun body reads / writes
+  cudaGraphExec_t exec = nullptr;
+  unsigned long long used = 0;
+};
+thread_local std::vector<AsyncGraph> g_async_graphs;
+thread_local unsigned long long g_async_clock = 0;
+
+// Parent graph of an asynchronous solve's tail: gate -> status copy ->
+// IF(guard fired) { exact solve }.
+int build_async_graph(cudaGraph_t* out, const sinkhorn_problem_v1& pr,
+                      const sinkhorn_options_v1& op, const float* mu, const float* nu,
+                      const float* cost, float* out_cost, float* out_log_u, float* out_log_v,
+                      float* out_residuals, void* ws, size_t ws_bytes, const float* init_log_u,
+                      int32_t* device_status, const int* ws_status, const int* est_fail,
+                      int dev) {
+  cudaGraph_t parent = nullptr;
+  CK(cudaGraphCreate(&parent, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, parent, 0, cudaGraphCondAssignDefault));
+  cudaGraphNode_t gate, fin, cond;
+  {
+    void* args[3] = {&h, const_cast<int**>(&est_fail), const_cast<int**>(&ws_status)};
+    cudaKernelNodeParams kp = {};
+    kp.func = reinterpret_cast<void*>(&async_gate_kernel);
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = args;
+    CK(cudaGraphAddKernelNode(&gate, parent, nullptr, 0, &kp));
+  }
+  {   // the fast solve's status first; a rerun overwrites it with its own
+    void* args[2] = {const_cast<int**>(&ws_status), &device_status};
+    cudaKernelNodeParams kp = {};
+    kp.func = reinterpret_cast<void*>(&async_status_kernel);
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = args;
+    CK(cudaGraphAddKernelNode(&fin, parent, &gate, 1, &kp));
+  }
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  CK(cudaGraphAddNode(&cond, parent, &fin, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  static thread_local cudaStream_t cs_dev[64] = {};
+  if (dev < 0 || dev >= 64) return fail(SINKHORN_STATUS_CUDA_ERROR, "device ordinal");
+  cudaStream_t& cs = cs_dev[dev];
+  if (cs == nullptr) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  const unsigned long long l0 = g_launches;
+  CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  sinkhorn_options_v1 exact = op;
+  exact.flags &= ~SINKHORN_FLAG_FORCE_RERUN;
+  int32_t it = 0;
+  const char* fast_path = g_last_path;   // the capture is not a solve of its own
+  const int e = forward_impl(pr, exact, mu, nu, cost, out_cost, out_log_u, out_log_v, &it,
+                             out_residuals, ws, ws_bytes, cs, false, init_log_u, device_status,
+                             true);
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(cs, &captured);
+  g_last_path = fast_path;
+  g_launches = l0;
+  if (e) return e;
+  CK(ce);
+  *out = parent;
+  return 0;
+}
+
+int enqueue_async_tail(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op,
+                       const float* mu, const float* nu, const float* cost, float* out_cost,
+                       float* out_log_u, float* out_log_v, float* out_residuals, void* ws,
+                       size_t ws_bytes, cudaStream_t st, const float* init_log_u,
+                       int32_t* device_status, const int* ws_status, const int* est_fail,
+                       bool can_fail) {
+  if (!can_fail) {   // no estimate guard on this path: only the status copy
+    ++g_launches;
+    async_status_kernel<<<1, 1, 0, st>>>(ws_status, device_status);
+    CK(cudaGetLastError());
+    return 0;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const AsyncGraphKey k = {ws, pr.B, pr.d1, pr.d2, pr.cost_kind, op.max_iters,
+                           (int32_t)op.flags, dev, op.lambda, ws_bytes};
+  const void* ptrs[9] = {mu, nu, cost, out_cost, out_log_u, out_log_v, out_residuals, init_log_u,
+                         device_status};
+  ++g_async_clock;
+  AsyncGraph* ag = nullptr;
+  for (auto& g : g_async_graphs)
+    if (g.key == k) ag = &g;
+  if (ag == nullptr) {
+    if (g_async_graphs.size() >= 8) {
+      auto it = std::min_element(g_async_graphs.begin(), g_async_graphs.end(),
+                                 [](const AsyncGraph& a, const AsyncGraph& b) { return a.used < b.used; });
+      if (it->exec) cudaGraphExecDestroy(it->exec);
+      g_async_graphs.erase(it);
+    }
+    g_async_graphs.push_back(AsyncGraph{});
+    ag = &g_async_graphs.back();
+    ag->key = k;
+  }
+  if (ag->exec == nullptr || !std::equal(ptrs, ptrs + 9, ag->ptrs)) {
+    // new buffers: re-capture the tail and update the executable graph in
+    // place (cheaper than instantiating; the topology is the same)
+    cudaGraph_t parent = nullptr;
+    if (int e = build_async_graph(&parent, pr, op, mu, nu, cost, out_cost, out_log_u, out_log_v,
+                                  out_residuals, ws, ws_bytes, init_log_u, device_status,
+                                  ws_status, est_fail, dev))
+      return e;
+    bool updated = false;
+    if (ag->exec != nullptr) {
+      cudaGraphExecUpdateResultInfo info = {};
+      updated = cudaGraphExecUpdate(ag->exec, parent, &info) == cudaSuccess;
+      if (!updated) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(ag->exec);
+        ag->exec = nullptr;
+      }
+    }
+    if (!updated) CK(cudaGraphInstantiate(&ag->exec, parent, 0));
+    CK(cudaGraphDestroy(parent));
+    std::copy(ptrs, ptrs + 9, ag->ptrs);
+  }
+  ag->used = g_async_clock;
+  CK(cudaGraphLaunch(ag->exec, st));
+  g_launches += 2;   // gate + status copy (the conditional body only runs when a guard fired)
+  return 0;
+}
+
 }  // namespace
 
 // =============================================================================
@@ -1909,6 +2100,36 @@ int32_t sinkhorn_forward_device_v1(const sinkhorn_problem_v1* prob,
                       out_residuals, workspace, workspace_bytes,
                       static_cast<cudaStream_t>(stream),
                       (opt->flags & SINKHORN_FLAG_EXACT_MAX) == 0);
+}
+
+int32_t sinkhorn_forward_async_device_v1(const sinkhorn_problem_v1* prob,
+                                         const sinkhorn_options_v1* opt, const float* mu,
+                                         const float* nu, const float* cost, float* out_cost,
+                                         float* out_log_u, float* out_log_v,
+                                         float* out_residuals, int32_t* device_status,
+                                         void* workspace, size_t workspace_bytes, void* stream) {
+  if (int e = check_problem(prob)) return e;
+  if (int e = check_options(opt)) return e;
+  if (opt->tolerance != 0.0)
+    return fail(SINKHORN_STATUS_INVALID_CONFIG,
+                "asynchronous solves need tolerance 0 (a stopping test is a host decision)");
+  if (!device_status) return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null device status");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (prob->B == 0) {   // ffi.ts:107-109
+    CK(cudaMemsetAsync(device_status, 0, 4, st));
+    return 0;
+  }
+  if (prob->d1 == 0 || prob->d2 == 0)
+    return fail(SINKHORN_STATUS_INVALID_HISTOGRAM, "empty histogram cannot sum to 1");
+  if (!mu || !nu || !out_cost || !out_log_u || !out_log_v ||
+      (prob->cost_kind != SINKHORN_COST_GRID2D && !cost))
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
+  sinkhorn_options_v1 op = *opt;
+  op.flags &= ~(SINKHORN_FLAG_TIME_LOOP | SINKHORN_FLAG_TIME_KERNEL | SINKHORN_FLAG_PERSISTENT);
+  int32_t iters = 0;
+  return forward_impl(*prob, op, mu, nu, cost, out_cost, out_log_u, out_log_v, &iters,
+                      out_residuals, workspace, workspace_bytes, st,
+                      (op.flags & SINKHORN_FLAG_EXACT_MAX) == 0, nullptr, device_status);
 }
 
 int32_t sinkhorn_forward_rows_device_v1(const sinkhorn_problem_v1* prob,

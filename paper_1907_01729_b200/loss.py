@@ -68,6 +68,19 @@ class SolveResult:
     path: str = ""            # solver path taken ("small", "tiled", "persistent", "lane")
     kernel_ms: float = -1.0   # dominant kernel's launches (CUDA events), solve(time_kernel=True)
     kernel_launches: int = 0
+    device_status: torch.Tensor | None = None   # solve(asynchronous=True): int32 on the device
+
+    def check(self) -> "SolveResult":
+        """An asynchronous solve's device status -> the reference's exception
+        (waits for the solve).  A no-op for synchronous solves."""
+        if self.device_status is not None:
+            st = int(self.device_status.item())
+            if st != 0:
+                _lib.load()
+                from .errors import _BY_STATUS, DeviceError
+
+                raise _BY_STATUS.get(st, DeviceError)(f"asynchronous solve: device status {st}")
+        return self
 
 
 def _stream_handle(device: torch.device) -> int:
@@ -141,7 +154,8 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
           persistent: bool = False, tiled_only: bool = False,
           dense_grid: bool = False, init_log_u=None, fused: bool = True,
           fp64: bool = False, gemm: bool | None = None,
-          time_kernel: bool = False) -> SolveResult:
+          time_kernel: bool = False, asynchronous: bool = False,
+          force_rerun: bool = False) -> SolveResult:
     """batch_forward (batch.py:264-349) on the GPU.
 
     mu (B, d1), nu (B, d2) histograms; cost a (d1, d2) tensor shared by all
@@ -159,7 +173,11 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
     shared cost, False never takes it.  ``time_kernel`` records CUDA events
     around every launch of the solve's dominant kernel (``kernel_ms``,
     ``kernel_launches``; measurement only -- the events break the launch
-    overlap).
+    overlap).  ``asynchronous=True`` (tolerance 0): the call returns once the
+    solve is enqueued on the current stream -- no host synchronisation; the
+    estimate-guard rerun is decided on the device; device-detected errors are
+    raised by ``result.check()`` (``iterations_run`` is ``max_iters``).
+    ``force_rerun`` (diagnostics) exercises the exact-rerun machinery.
     """
     if fp64:
         return _solve_f64(mu, nu, cost, lam, max_iters, tolerance, check_interval, validate)
@@ -183,7 +201,8 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
         (_lib.FLAG_TILED_ONLY if tiled_only else 0) | (_lib.FLAG_DENSE_GRID if dense_grid else 0) | \
         (0 if fused else _lib.FLAG_NO_FUSED) | \
         (_lib.FLAG_FORCE_GEMM if gemm else 0) | (_lib.FLAG_NO_GEMM if gemm is False else 0) | \
-        (_lib.FLAG_TIME_KERNEL if time_kernel else 0)
+        (_lib.FLAG_TIME_KERNEL if time_kernel else 0) | \
+        (_lib.FLAG_FORCE_RERUN if force_rerun else 0)
     out_cost = torch.empty(B, device=dev, dtype=torch.float32)
     log_u = torch.empty(B, d1, device=dev, dtype=torch.float32)
     log_v = torch.empty(B, d2, device=dev, dtype=torch.float32)
@@ -192,6 +211,18 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
         nbytes = lib.sinkhorn_workspace_bytes_v1(ctypes.byref(pr))
         ws = _workspace(dev, nbytes)
         iters = ctypes.c_int32(0)
+        if asynchronous:
+            if init_log_u is not None:
+                raise ValueError("asynchronous solves start from u = 0 (no warm start)")
+            dstat = torch.empty(1, device=dev, dtype=torch.int32)
+            st = lib.sinkhorn_forward_async_device_v1(
+                ctypes.byref(pr), ctypes.byref(op), _ptr(mu), _ptr(nu),
+                None if isinstance(cost, GridCost) else _ptr(cost), _ptr(out_cost), _ptr(log_u),
+                _ptr(log_v), _ptr(residuals), _ptr(dstat), _ptr(ws), ws.numel(),
+                _stream_handle(dev))
+            raise_for_status(st, "sinkhorn_forward_async_device_v1")
+            return SolveResult(out_cost, log_u, log_v, float(lam), int(max_iters), residuals,
+                               -1.0, lib.sinkhorn_last_path_v1().decode(), device_status=dstat)
         if init_log_u is not None:
             init = _as_f32_cuda(init_log_u, dev)
             if tuple(init.shape) != (B, d1):
