@@ -87,13 +87,14 @@ struct UmmaParams {
   const int* status;    // skip the work when an earlier kernel failed (nullable)
 };
 
+// First unit of CTA c's stream-K range (U units over G CTAs; U * G < 2^62).
 __device__ __forceinline__ long long um_start(long long U, int G, int c) {
-  return (long long)((__int128)U * c / G);
+  return U * c / G;
 }
 
 // The CTA whose unit range holds unit u.
 __device__ __forceinline__ int um_owner(long long U, int G, long long u) {
-  int c = (int)((__int128)u * G / U);
+  int c = (int)(u * G / U);
   while (c + 1 < G && um_start(U, G, c + 1) <= u) ++c;
   while (c > 0 && um_start(U, G, c) > u) --c;
   return c;
@@ -377,44 +378,48 @@ __global__ void __launch_bounds__(kUmThreads, 1)
 
 // Split tiles: sum the pieces in ascending CTA order into out.  grid = G
 // blocks, block 256: block c owns the tile holding its range's first unit when
-// that tile is split there and no earlier boundary falls inside it.
+// that tile is split there and no earlier boundary falls inside it.  The
+// contributing (CTA, slot) pieces are listed once per block in shared memory.
+constexpr int kUmFixMax = 256;
 __global__ void __launch_bounds__(256) umma_fixup_kernel(const UmmaParams p) {
   pdl_wait();
   if (p.status != nullptr && *p.status != 0) return;
-  __shared__ int cs[2];
+  __shared__ int s_n;
+  __shared__ int s_piece[kUmFixMax];   // part row offset (cta * 2 + slot)
   const int c = blockIdx.x;
+  const long long uc = um_start(p.units, p.G, c);
+  const long long t = uc / p.KCH;
   if (threadIdx.x == 0) {
-    cs[0] = cs[1] = -1;
-    const long long uc = um_start(p.units, p.G, c);
-    const long long t = uc / p.KCH;
+    s_n = 0;
     bool mine = c > 0 && uc < p.units && uc % p.KCH != 0 && um_start(p.units, p.G, c + 1) > uc;
-    if (mine) {   // an earlier non-empty range starting inside t owns it instead
-      for (int e = c - 1; e >= 1; --e) {
-        const long long ue = um_start(p.units, p.G, e);
-        if (ue / p.KCH != t) break;
-        if (ue % p.KCH != 0 && um_start(p.units, p.G, e + 1) > ue) { mine = false; break; }
-      }
+    for (int e = c - 1; mine && e >= 1; --e) {   // an earlier boundary inside t owns it
+      const long long ue = um_start(p.units, p.G, e);
+      if (ue / p.KCH != t) break;
+      if (ue % p.KCH != 0 && um_start(p.units, p.G, e + 1) > ue) mine = false;
     }
     if (mine) {
-      cs[0] = um_owner(p.units, p.G, t * p.KCH);
-      cs[1] = um_owner(p.units, p.G, (t + 1) * p.KCH - 1);
+      const int c0 = um_owner(p.units, p.G, t * p.KCH);
+      const int c1 = um_owner(p.units, p.G, (t + 1) * p.KCH - 1);
+      int n = 0;
+      for (int cc = c0; cc <= c1 && n < kUmFixMax; ++cc) {
+        const long long u = um_start(p.units, p.G, cc);
+        if (um_start(p.units, p.G, cc + 1) == u) continue;   // empty range
+        s_piece[n++] = cc * 2 + ((u / p.KCH == t) ? 0 : 1);
+      }
+      s_n = n;
     }
   }
   __syncthreads();
-  const int c0 = cs[0], c1 = cs[1];
-  if (c0 < 0) return;
-  const long long t = um_start(p.units, p.G, c) / p.KCH;
+  const int np = s_n;
+  if (np == 0) return;
   const int nt = (int)(t % p.NT), mt = (int)(t / p.NT);
   const int nmax = min(kUmBN, p.N - nt * kUmBN);
   for (int e = threadIdx.x; e < kUmBM * kUmBN / 4; e += 256) {
     const int n = e / (kUmBM / 4), row = 4 * (e % (kUmBM / 4));
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int cc = c0; cc <= c1; ++cc) {
-      const long long u = um_start(p.units, p.G, cc);
-      if (um_start(p.units, p.G, cc + 1) == u) continue;   // empty range
-      const int slot = (u / p.KCH == t) ? 0 : 1;
+    for (int k = 0; k < np; ++k) {
       const float4 v = *reinterpret_cast<const float4*>(
-          p.part + ((size_t)(cc * 2 + slot) * kUmBN + n) * kUmBM + row);
+          p.part + ((size_t)s_piece[k] * kUmBN + n) * kUmBM + row);
       s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
     }
     if (n < nmax) {
