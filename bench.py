@@ -432,6 +432,8 @@ def reference_cpu_sample(cfg: dict, seed: int = 0, runs: int = 3, light: bool = 
     threads = os.cpu_count() or 1
     B, d, lam, iters = cfg["B"], cfg["d"], cfg["lam"], cfg["iters"]
     k1, k2 = (2, 4) if light else (5, 10)
+    if cfg["cost"] != "per_sample" and min(cfg["d"], 4096) >= 4096:
+        k1, k2 = 1, 2   # ~4 s per iteration at d = 4096 on the reference's streaming loop
     if cfg["cost"] == "per_sample":
         from concurrent.futures import ProcessPoolExecutor
 
@@ -449,7 +451,7 @@ def reference_cpu_sample(cfg: dict, seed: int = 0, runs: int = 3, light: bool = 
                   f"d={d} on {threads} processes, {k1} and {k2} iterations, median of {runs}")
     else:
         dd = min(d, 4096)
-        Bs = B if dd == d and B * dd * dd <= 256 * 784 * 784 else min(B, 16 if dd >= 4096 else B)
+        Bs = B if dd == d and B * dd * dd <= 256 * 784 * 784 else min(B, 64)
         rng = np.random.default_rng(seed)
         hb = batch.validate_histogram_batch
         mu = hb(np.stack([_ref_hist(rng, dd) for _ in range(Bs)]))
@@ -542,10 +544,13 @@ def run_reference(args, cfg, world, rank):
     for _ in range(max(0, min(args.warmup, 1))):
         reference_cpu_sample(cfg, seed=99, runs=1, light=True)
     vals, ms, r = [], [], None
+    t0 = time.perf_counter()
     for s in range(args.steps):
         r = reference_cpu_sample(cfg, seed=s, runs=1, light=heavy)
         vals.append(r["value"])
         ms.append(r["ms_per_step_full"])
+        if time.perf_counter() - t0 > args.reference_budget_s:   # bounded CPU work
+            break
     value = statistics.median(vals)
     row = args.config == 5 and world > 1
     line = {
@@ -556,7 +561,9 @@ def run_reference(args, cfg, world, rank):
         "data": "synthetic",
         "config": config_dict(cfg, world, row),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
-                         "sample": r["sample"] + f"; one sample per step, median of {args.steps}",
+                         "sample": r["sample"] + f"; one sample per step, median of {len(vals)} "
+                                                 f"(of {args.steps} requested; CPU budget "
+                                                 f"{args.reference_budget_s:.0f} s)",
                          "cpu": r["cpu"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -704,7 +711,8 @@ def run_ours(args, cfg, world, rank, local):
         "loop_ms_median": statistics.median(loop_ms) if loop_ms and loop_ms[0] > 0 else None,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = reference_cpu_sample(cfg, runs=1, light=cfg["cost"] != "per_sample" and d > 100)
+        cb = reference_cpu_sample(cfg, runs=3 if cfg["cost"] == "per_sample" else 1,
+                                  light=cfg["cost"] != "per_sample" and d > 100)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu")}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -835,6 +843,8 @@ def main():
     ap.add_argument("--sharding", choices=["batch", "row"], default=None,
                     help="multi-GPU split (default: row for config 5 on N>1, else batch)")
     ap.add_argument("--probe-ranks", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--reference-budget-s", type=float, default=150.0,
+                    help="--impl reference: stop sampling after this many seconds of CPU work")
     ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="e2e leg, per-sample costs: lane groups whose upload overlaps the solve")
     args = ap.parse_args()
