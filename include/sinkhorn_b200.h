@@ -79,6 +79,10 @@ int32_t sinkhorn_backward_v1(const sinkhorn_view_v1* log_u, const sinkhorn_view_
 
 #define SINKHORN_COST_SHARED 0     /* one stored (d1,d2) cost for all lanes (the reference's case) */
 #define SINKHORN_COST_PER_SAMPLE 1 /* stored (B,d1,d2), one cost per lane (BASELINE config 4) */
+#define SINKHORN_COST_POINTS 3     /* squared Euclidean between point clouds x (d1, D), y (d2, D):
+                                      cost points to [x; y], (d1 + d2) x D fp32, D in grid_nx;
+                                      |x|^2 + |y|^2 - 2 x.y with the x.y contraction on the
+                                      tensor cores */
 #define SINKHORN_COST_GRID2D 2     /* squared Euclidean on an nx*ny grid, never materialised
                                       (BASELINE config 3); d1 = d2 = nx*ny,
                                       point k at ((k % nx)*hx, (k / nx)*hy) */

@@ -8,7 +8,8 @@ Public API (mirrors the reference's ``sinkhornLoss`` node and the
 * :func:`batch_forward`, :func:`batch_backward`, :func:`fused_log_reduction`,
   :class:`SinkhornConfig` -- the ``sinkloss.batch`` surface (batch.py);
 * :class:`GridCost` -- on-the-fly squared-Euclidean grid cost; a 3-D cost
-  tensor selects per-sample costs.
+  tensor selects per-sample costs; :class:`PointCloudCost` -- squared
+  Euclidean between point clouds (x.y on the tensor cores).
 
 All compute runs in the sm_100a library ``_lib/libsinkhorn_b200.so`` behind
 the C ABI declared in ``include/sinkhorn_b200.h``; importing this package
@@ -33,13 +34,13 @@ from .errors import (
     SinklossError,
     ZeroMassGradient,
 )
-from .loss import GridCost, SinkhornLossFunction, SolveResult, plan_gradient, \
+from .loss import GridCost, PointCloudCost, SinkhornLossFunction, SolveResult, plan_gradient, \
     potentials_backward, sinkhorn_loss, solve, solve_streamed
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BatchLossResult", "DeviceError", "GridCost", "InvalidConfig", "InvalidCost",
+    "BatchLossResult", "DeviceError", "GridCost", "InvalidConfig", "InvalidCost", "PointCloudCost",
     "InvalidHistogram", "NaNProduced", "ShapeMismatch", "SinkhornConfig",
     "SinkhornLossFunction", "SinklossError", "SolveResult", "ZeroMassGradient",
     "batch_backward", "batch_forward", "fused_log_reduction", "partial_log_reduction",

@@ -28,6 +28,7 @@ STATUS_CUDA_ERROR = 20
 COST_SHARED = 0
 COST_PER_SAMPLE = 1
 COST_GRID2D = 2
+COST_POINTS = 3
 
 FLAG_SKIP_VALIDATION = 1
 FLAG_TIME_LOOP = 4

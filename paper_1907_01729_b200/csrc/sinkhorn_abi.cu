@@ -414,7 +414,39 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
 
 // Workspace bytes for a problem under every option set (grid costs can take
 // either the separable or the dense tiled layout).
+// ---- point-cloud costs (SINKHORN_COST_POINTS) ---------------------------------
+// The cost is materialised once per solve at the front of the workspace --
+// the dot products on the tensor cores, then |x|^2 + |y|^2 - 2 x.y -- and the
+// solve proceeds as a shared stored cost on the rest of the workspace.
+struct PointLayout {
+  size_t cost = 0, ya = 0, xh = 0, xl = 0, nrm = 0, part = 0, total = 0;
+  long long kch = 0;
+};
+PointLayout point_layout(const sinkhorn_problem_v1& pr, int sms) {
+  PointLayout P;
+  Carver c;
+  const int D = pr.grid_nx;
+  P.kch = (D + kUmBK - 1) / kUmBK;
+  P.cost = c.take((size_t)pr.d1 * pr.d2 * 4);
+  P.ya = c.take((size_t)round_up(pr.d2, kUmBM) * P.kch * kUmBK * 4);
+  P.xh = c.take((size_t)round_up(pr.d1, kUmBN) * P.kch * kUmBK * 4);
+  P.xl = c.take((size_t)round_up(pr.d1, kUmBN) * P.kch * kUmBK * 4);
+  P.nrm = c.take((size_t)(pr.d1 + pr.d2) * 4);
+  P.part = c.take((size_t)sms * 2 * kUmBN * kUmBM * 4);
+  P.total = c.take(256);
+  return P;
+}
+sinkhorn_problem_v1 as_shared(const sinkhorn_problem_v1& pr) {
+  sinkhorn_problem_v1 q = pr;
+  q.cost_kind = SINKHORN_COST_SHARED;
+  q.grid_nx = q.grid_ny = 0;
+  q.grid_hx = q.grid_hy = 0.f;
+  return q;
+}
+
 size_t workspace_total(const sinkhorn_problem_v1& pr, int sms) {
+  if (pr.cost_kind == SINKHORN_COST_POINTS)
+    return point_layout(pr, sms).total + workspace_total(as_shared(pr), sms);
   size_t t = make_layout(pr, sms).total;
   if (fused_eligible(pr)) t = std::max(t, make_layout(pr, sms, false, true).total);
   if (pr.cost_kind == SINKHORN_COST_SHARED) t = std::max(t, make_layout(pr, sms, false, false, true).total);
@@ -1382,6 +1414,9 @@ int check_problem(const sinkhorn_problem_v1* pr) {
     if (!(std::isfinite(pr->grid_hx) && std::isfinite(pr->grid_hy) && pr->grid_hx >= 0 &&
           pr->grid_hy >= 0))
       return fail(SINKHORN_STATUS_INVALID_COST, "grid spacing must be finite and >= 0");
+  } else if (pr->cost_kind == SINKHORN_COST_POINTS) {
+    if (pr->grid_nx < 1 || pr->grid_nx > 4096)
+      return fail(SINKHORN_STATUS_SHAPE_MISMATCH, "point dimension (grid_nx) must be in 1..4096");
   } else if (pr->cost_kind != SINKHORN_COST_SHARED && pr->cost_kind != SINKHORN_COST_PER_SAMPLE) {
     return fail(SINKHORN_STATUS_BAD_ARGUMENT, "unknown cost_kind");
   }
@@ -1899,6 +1934,65 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
   return 0;
 }
 
+// Point clouds -> the materialised (d1, d2) cost at the front of the workspace.
+// Returns the cost pointer through *cost_out and the workspace after it.
+int materialize_points(const sinkhorn_problem_v1& pr, const float* pts, void* ws, size_t ws_bytes,
+                       cudaStream_t st, const float** cost_out, void** ws_rest,
+                       size_t* ws_rest_bytes) {
+  const DeviceInfo di = device_info();
+  const PointLayout P = point_layout(pr, di.sms);
+  if (ws == nullptr || ws_bytes < P.total) return fail(SINKHORN_STATUS_WORKSPACE, "workspace too small");
+  const int D = pr.grid_nx, d1 = (int)pr.d1, d2 = (int)pr.d2;
+  const float* x = pts;
+  const float* y = pts + (size_t)d1 * D;
+  float* C = at<float>(ws, P.cost);
+  float* nrm = at<float>(ws, P.nrm);
+  // a non-finite point makes its cost entries NaN, which the shared-cost
+  // solve's cost validation reports as status 15 (core.py:53-63)
+  ++g_launches;
+  points_norms_kernel<<<grid_for((size_t)(d1 + d2)), 256, 0, st>>>(pts, d1 + d2, D, nrm);
+  ++g_launches;
+  points_tile_a_kernel<<<grid_for((size_t)round_up(d2, kUmBM) * P.kch * kUmBK), 256, 0, st>>>(
+      y, d2, D, P.kch, at<float>(ws, P.ya));
+  ++g_launches;
+  umma_split_kernel<<<grid_for((size_t)round_up(d1, kUmBN) * P.kch * kUmBK), 256, 0, st>>>(
+      x, d1, D, P.kch, at<float>(ws, P.xh), at<float>(ws, P.xl));
+  CK(cudaGetLastError());
+  CUtensorMap ta, tbh, tbl;
+  const size_t mt = (size_t)round_up(d2, kUmBM) / kUmBM, nt = (size_t)round_up(d1, kUmBN) / kUmBN;
+  const size_t sub = (size_t)P.kch * kUmSub;
+  bool ok = make_tmap_sw128(&ta, at<float>(ws, P.ya), mt * sub * kUmBM, 32, 32, kUmBM);
+  ok &= make_tmap_sw128(&tbh, at<float>(ws, P.xh), nt * sub * kUmBN, 32, 32, kUmBN);
+  ok &= make_tmap_sw128(&tbl, at<float>(ws, P.xl), nt * sub * kUmBN, 32, 32, kUmBN);
+  if (!ok) return fail(SINKHORN_STATUS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (points)");
+  // dot[i][j] = y_j . x_i: M = d2 (rows of A = y), N = d1 (x as the lane operand),
+  // out[n * ldo + m] with ldo = d2 is the row-major (d1, d2) matrix
+  UmmaParams p = {};
+  p.M = d2;
+  p.N = d1;
+  p.K = D;
+  p.MT = (int)mt;
+  p.NT = (int)nt;
+  p.KCH = (int)P.kch;
+  p.units = (long long)p.MT * p.NT * p.KCH;
+  p.G = (int)std::min<long long>(di.sms, p.units);
+  p.out = C;
+  p.ldo = d2;
+  p.part = at<float>(ws, P.part);
+  p.status = nullptr;
+  if (int e = set_max_smem(reinterpret_cast<const void*>(&umma_gemm_kernel), kUmSmemBytes)) return e;
+  g_launches += 2;
+  CK(launch_pdl(umma_gemm_kernel, dim3(p.G), dim3(kUmThreads), kUmSmemBytes, st, ta, tbh, tbl, p));
+  CK(launch_pdl(umma_fixup_kernel, dim3((unsigned)p.G), dim3(256), 0, st, p));
+  ++g_launches;
+  points_cost_kernel<<<grid_for((size_t)d1 * d2), 256, 0, st>>>(C, nrm, nrm + d1, d1, d2);
+  CK(cudaGetLastError());
+  *cost_out = C;
+  *ws_rest = at<char>(ws, P.total);
+  *ws_rest_bytes = ws_bytes - P.total;
+  return 0;
+}
+
 // ---- asynchronous solves (SINKHORN_FLAG_ASYNC, tolerance 0) ------------------
 // The tail of an asynchronous forward is one graph launch: a gate kernel sets
 // a conditional node from the estimate guard (est_fail) and the status word;
@@ -2096,7 +2190,15 @@ int32_t sinkhorn_forward_device_v1(const sinkhorn_problem_v1* prob,
   if (!mu || !nu || !out_cost || !out_log_u || !out_log_v ||
       (prob->cost_kind != SINKHORN_COST_GRID2D && !cost))
     return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
-  return forward_impl(*prob, *opt, mu, nu, cost, out_cost, out_log_u, out_log_v, out_iterations,
+  sinkhorn_problem_v1 pr = *prob;
+  if (pr.cost_kind == SINKHORN_COST_POINTS) {   // materialise, then a shared stored cost
+    if (int e = materialize_points(pr, cost, workspace, workspace_bytes,
+                                   static_cast<cudaStream_t>(stream), &cost, &workspace,
+                                   &workspace_bytes))
+      return e;
+    pr = as_shared(pr);
+  }
+  return forward_impl(pr, *opt, mu, nu, cost, out_cost, out_log_u, out_log_v, out_iterations,
                       out_residuals, workspace, workspace_bytes,
                       static_cast<cudaStream_t>(stream),
                       (opt->flags & SINKHORN_FLAG_EXACT_MAX) == 0);
@@ -2127,7 +2229,14 @@ int32_t sinkhorn_forward_async_device_v1(const sinkhorn_problem_v1* prob,
   sinkhorn_options_v1 op = *opt;
   op.flags &= ~(SINKHORN_FLAG_TIME_LOOP | SINKHORN_FLAG_TIME_KERNEL | SINKHORN_FLAG_PERSISTENT);
   int32_t iters = 0;
-  return forward_impl(*prob, op, mu, nu, cost, out_cost, out_log_u, out_log_v, &iters,
+  sinkhorn_problem_v1 pr = *prob;
+  if (pr.cost_kind == SINKHORN_COST_POINTS) {
+    if (int e = materialize_points(pr, cost, workspace, workspace_bytes, st, &cost, &workspace,
+                                   &workspace_bytes))
+      return e;
+    pr = as_shared(pr);
+  }
+  return forward_impl(pr, op, mu, nu, cost, out_cost, out_log_u, out_log_v, &iters,
                       out_residuals, workspace, workspace_bytes, st,
                       (op.flags & SINKHORN_FLAG_EXACT_MAX) == 0, nullptr, device_status);
 }
@@ -2183,7 +2292,15 @@ int32_t sinkhorn_forward_warm_device_v1(const sinkhorn_problem_v1* prob,
   if (!mu || !nu || !out_cost || !out_log_u || !out_log_v ||
       (prob->cost_kind != SINKHORN_COST_GRID2D && !cost))
     return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
-  return forward_impl(*prob, *opt, mu, nu, cost, out_cost, out_log_u, out_log_v, out_iterations,
+  sinkhorn_problem_v1 pr = *prob;
+  if (pr.cost_kind == SINKHORN_COST_POINTS) {
+    if (int e = materialize_points(pr, cost, workspace, workspace_bytes,
+                                   static_cast<cudaStream_t>(stream), &cost, &workspace,
+                                   &workspace_bytes))
+      return e;
+    pr = as_shared(pr);
+  }
+  return forward_impl(pr, *opt, mu, nu, cost, out_cost, out_log_u, out_log_v, out_iterations,
                       out_residuals, workspace, workspace_bytes,
                       static_cast<cudaStream_t>(stream),
                       (opt->flags & SINKHORN_FLAG_EXACT_MAX) == 0, init_log_u);
@@ -2398,6 +2515,8 @@ int32_t sinkhorn_forward_f64_device_v1(const sinkhorn_problem_v1* prob,
                                        int32_t* out_iterations, double* out_residuals,
                                        void* workspace, size_t workspace_bytes, void* stream) {
   if (int e = check_problem(prob)) return e;
+  if (prob->cost_kind == SINKHORN_COST_POINTS)
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "the float64 mode takes stored or grid costs");
   if (prob->B == 0) {   // ffi.ts:107-109
     if (out_iterations) *out_iterations = 0;
     return 0;
@@ -2497,8 +2616,8 @@ int32_t sinkhorn_plan_grad_device_v1(const sinkhorn_problem_v1* prob, double lam
                                      const float* log_u, const float* log_v, const float* cost,
                                      const float* upstream, float* out_grad_cost, void* stream) {
   if (int e = check_problem(prob)) return e;
-  if (prob->cost_kind == SINKHORN_COST_GRID2D)
-    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "grid cost is not materialised");
+  if (prob->cost_kind == SINKHORN_COST_GRID2D || prob->cost_kind == SINKHORN_COST_POINTS)
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "grid / point costs are not materialised");
   if (!(std::isfinite(lambda) && lambda > 0))
     return fail(SINKHORN_STATUS_INVALID_CONFIG, "lam must be positive and finite");
   if (prob->d1 == 0 || prob->d2 == 0) return 0;

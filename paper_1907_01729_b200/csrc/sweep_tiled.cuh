@@ -316,7 +316,10 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
   const int n_local = int(chunk_of(a_end - 1) - g_first + 1);
 
   // Output tile tp_idx covers [p0, p0 + PT) but owns (writes) [tp_idx*PT, ...):
-  // the last tile is shifted left to end at Pv, so no tile is partial (a
+  // the last tile is shifted left to end at Pv -- its start rounded up to a
+  // float4 boundary (an unaligned start faulted for Pv % 4 != 0), so it may
+  // reach 3 columns into the padding, whose outputs are clamped to Pv - 1 --
+  // so no tile is partial (a
   // partial tile's few active warps are latency-bound and stretch the tail).
   auto atom_coords = [&](long long a, int& tile, int& qc, int& b0, int& p0) {
     tile = int((unsigned)a / (unsigned)nq);   // chunk indices fit in 32 bits
@@ -324,7 +327,7 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
     const int tb_idx = tile % p.ntile_b;     // lane tiles innermost: consecutive tiles share G
     const int tp_idx = tile / p.ntile_b;
     b0 = tb_idx * BT;
-    p0 = (tp_idx == p.ntile_p - 1) ? max(p.Pv - PT, 0) : tp_idx * PT;
+    p0 = (tp_idx == p.ntile_p - 1) ? max((p.Pv - PT + 3) & ~3, 0) : tp_idx * PT;
   };
 
   auto issue = [&](int l) {
@@ -345,7 +348,7 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
   auto est_fetch = [&](int tile_n) {
     const int tb_n = tile_n % p.ntile_b, tp_n = tile_n / p.ntile_b;
     const int b0n = tb_n * BT;
-    const int p0n = (tp_n == p.ntile_p - 1) ? max(p.Pv - PT, 0) : tp_n * PT;
+    const int p0n = (tp_n == p.ntile_p - 1) ? max((p.Pv - PT + 3) & ~3, 0) : tp_n * PT;
 #pragma unroll
     for (int rp = 0; rp < RP; ++rp) {
       const int pp = min(p0n + tp * RP + rp, p.Pv - 1);
@@ -383,7 +386,7 @@ __device__ __forceinline__ void sweep_phase(const CUtensorMap* tmap_g, const CUt
       ++tile;
       const int tb_idx = tile % p.ntile_b, tp_idx = tile / p.ntile_b;
       b0 = tb_idx * BT;
-      p0 = (tp_idx == p.ntile_p - 1) ? max(p.Pv - PT, 0) : tp_idx * PT;
+      p0 = (tp_idx == p.ntile_p - 1) ? max((p.Pv - PT + 3) & ~3, 0) : tp_idx * PT;
     }
     // this CTA's rows inside the chunk: [k_lo, k_hi) relative to the chunk start
     const long long row0 = (long long)tile * Qv + (long long)qc * QC;
@@ -682,7 +685,7 @@ __device__ __forceinline__ void merge_tile_groups(const TiledSweepParams& p, con
   // in an earlier tile); every later piece starts inside this tile
   const int sl0 = (atom_begin(p, c_lo) < t_first) ? 1 : 0;
   const int tb_idx = tile % p.ntile_b, tp_idx = tile / p.ntile_b;
-  const int p0 = (tp_idx == p.ntile_p - 1) ? max(p.Pv - PT, 0) : tp_idx * PT;
+  const int p0 = (tp_idx == p.ntile_p - 1) ? max((p.Pv - PT + 3) & ~3, 0) : tp_idx * PT;
   const int own_lo = tp_idx * PT;
   const bool want_res = p.res != nullptr && (kMode == kModeTail || d.res_kind != kResNone);
   for (int gb = g0; gb < g1; gb += NB) {

@@ -467,6 +467,53 @@ __global__ void umma_split_kernel(const float* __restrict__ x, int rows, int col
   }
 }
 
+// ---- point-cloud costs: c_ij = |x_i|^2 + |y_j|^2 - 2 x_i . y_j ---------------------
+// x: [d1][D], y: [d2][D] packed as one [(d1 + d2)][D]
+// fp32 array.  The dot products run on the tensor cores (umma_gemm_kernel with
+// A = y in the tiled layout, B = x's tf32 planes); these kernels prepare the
+// operands, the norms, and finish the cost.
+
+// Squared norms, accumulated in double (a non-finite point gives a non-finite norm).
+__global__ void points_norms_kernel(const float* __restrict__ pts, int n, int D,
+                                    float* __restrict__ norms) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < D; ++k) {
+      const float v = pts[(size_t)r * D + k];
+      s += (double)v * v;
+    }
+    norms[r] = (float)s;
+  }
+}
+
+// y -> the tiled A-operand layout (128-row tiles, kch chunks of kUmBK, zero padding).
+__global__ void points_tile_a_kernel(const float* __restrict__ y, int rows, int D, long long kch,
+                                     float* __restrict__ out) {
+  const long long mt = (rows + kUmBM - 1) / kUmBM;
+  const long long n = mt * kUmBM * kch * kUmBK;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long blk = e / (kUmBM * kUmBK);
+    const int within = (int)(e % (kUmBM * kUmBK));
+    const int sb = within / (kUmBM * 32), w2 = within % (kUmBM * 32);
+    const long long r = (blk / kch) * kUmBM + w2 / 32;
+    const long long k = (blk % kch) * kUmBK + sb * 32 + w2 % 32;
+    out[e] = (r < rows && k < D) ? y[r * D + k] : 0.f;
+  }
+}
+
+// c_ij = max(0, |x_i|^2 + |y_j|^2 - 2 dot_ij), in place over the [d1][d2] dot products.
+__global__ void points_cost_kernel(float* __restrict__ c, const float* __restrict__ nx,
+                                   const float* __restrict__ ny, int d1, int d2) {
+  const long long n = (long long)d1 * d2;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / d2), j = (int)(e - (long long)i * d2);
+    const float v = fmaf(-2.f, c[e], nx[i] + ny[j]);
+    c[e] = v < 0.f ? 0.f : v;   // rounding below 0 clamps; NaN (non-finite points) stays
+  }
+}
+
 // K = 2^(c * kscale) and K o C (E0) as tiled A operands over (d1 rows, d2
 // reduction), and K^T over (d2 rows, d1 reduction), from the caller's cost
 // (validated: finite, >= 0, status 15).  One block per 32 x 32 cost block

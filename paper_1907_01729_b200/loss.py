@@ -54,6 +54,36 @@ class GridCost:
         return (x[:, None] - x[None, :]) ** 2 + (y[:, None] - y[None, :]) ** 2
 
 
+@dataclass(frozen=True)
+class PointCloudCost:
+    """Squared Euclidean cost between point clouds: c_ij = |x_i - y_j|^2.
+
+    x (d1, D) and y (d2, D) are the histograms' support points.  The library
+    evaluates |x|^2 + |y|^2 - 2 x.y with the x.y contraction on the tensor
+    cores (3xTF32) and then solves with the materialised cost (PAPER.md:147,
+    SPEC.md:13).
+    """
+
+    x: torch.Tensor
+    y: torch.Tensor
+
+    @property
+    def dim(self) -> int:
+        return int(self.x.shape[1])
+
+    def packed(self, device) -> torch.Tensor:
+        """[x; y] as one contiguous float32 (d1 + d2, D) device tensor."""
+        x = torch.as_tensor(self.x).to(device=device, dtype=torch.float32)
+        y = torch.as_tensor(self.y).to(device=device, dtype=torch.float32)
+        return torch.cat([x, y], dim=0).contiguous()
+
+    def materialize(self, device=None, dtype=torch.float64) -> torch.Tensor:
+        """The (d1, d2) matrix this descriptor stands for (tests only)."""
+        x = torch.as_tensor(self.x).to(device=device, dtype=dtype)
+        y = torch.as_tensor(self.y).to(device=device, dtype=dtype)
+        return ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
+
+
 @dataclass
 class SolveResult:
     """Per-lane E0 costs plus the complete backward state (batch.py:237-253)."""
@@ -120,6 +150,9 @@ def _problem(B: int, d1: int, d2: int, cost) -> _lib.Problem:
         pr.cost_kind = _lib.COST_GRID2D
         pr.grid_nx, pr.grid_ny = cost.nx, cost.ny
         pr.grid_hx, pr.grid_hy = hx, hy
+    elif isinstance(cost, PointCloudCost):
+        pr.cost_kind = _lib.COST_POINTS
+        pr.grid_nx = cost.dim
     elif cost.dim() == 3:
         pr.cost_kind = _lib.COST_PER_SAMPLE
     else:
@@ -134,7 +167,13 @@ def _check_shapes(mu: torch.Tensor, nu: torch.Tensor, cost) -> tuple[int, int, i
     if nu.shape[0] != B:
         raise ShapeMismatch(f"batch sizes differ: mu has {B}, nu has {nu.shape[0]}")
     d2 = nu.shape[1]
-    if isinstance(cost, GridCost):
+    if isinstance(cost, PointCloudCost):
+        if cost.x.dim() != 2 or cost.y.dim() != 2 or cost.x.shape[1] != cost.y.shape[1]:
+            raise ShapeMismatch("point clouds must be (d1, D) and (d2, D)")
+        if cost.x.shape[0] != d1 or cost.y.shape[0] != d2:
+            raise ShapeMismatch(f"point clouds have {cost.x.shape[0]} and {cost.y.shape[0]} points "
+                                f"but histograms have d1={d1}, d2={d2}")
+    elif isinstance(cost, GridCost):
         if cost.d != d1 or cost.d != d2:
             raise ShapeMismatch(f"grid has {cost.d} points but histograms have d1={d1}, d2={d2}")
     elif cost.dim() == 2:
@@ -182,14 +221,18 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
     if fp64:
         return _solve_f64(mu, nu, cost, lam, max_iters, tolerance, check_interval, validate)
     mu, nu = torch.as_tensor(mu), torch.as_tensor(nu)
-    if not isinstance(cost, GridCost):
+    if not isinstance(cost, (GridCost, PointCloudCost)):
         cost = torch.as_tensor(cost)
     B, d1, d2 = _check_shapes(mu, nu, cost)   # host-side, before touching the device
     mu = _as_f32_cuda(mu)
     dev = mu.device
     nu = _as_f32_cuda(nu, dev)
-    if not isinstance(cost, GridCost):
-        cost = _as_f32_cuda(cost, dev)
+    if isinstance(cost, GridCost):
+        cost_buf = None                      # recomputed on the fly
+    elif isinstance(cost, PointCloudCost):
+        cost_buf = cost.packed(dev)          # [x; y]
+    else:
+        cost = cost_buf = _as_f32_cuda(cost, dev)
     lib = _lib.load()
     pr = _problem(B, d1, d2, cost)
     op = _lib.Options()
@@ -217,7 +260,7 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
             dstat = torch.empty(1, device=dev, dtype=torch.int32)
             st = lib.sinkhorn_forward_async_device_v1(
                 ctypes.byref(pr), ctypes.byref(op), _ptr(mu), _ptr(nu),
-                None if isinstance(cost, GridCost) else _ptr(cost), _ptr(out_cost), _ptr(log_u),
+                _ptr(cost_buf), _ptr(out_cost), _ptr(log_u),
                 _ptr(log_v), _ptr(residuals), _ptr(dstat), _ptr(ws), ws.numel(),
                 _stream_handle(dev))
             raise_for_status(st, "sinkhorn_forward_async_device_v1")
@@ -229,13 +272,13 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
                 raise ShapeMismatch(f"init_log_u must be ({B}, {d1}), got {tuple(init.shape)}")
             st = lib.sinkhorn_forward_warm_device_v1(
                 ctypes.byref(pr), ctypes.byref(op), _ptr(mu), _ptr(nu),
-                None if isinstance(cost, GridCost) else _ptr(cost), _ptr(init), _ptr(out_cost),
+                _ptr(cost_buf), _ptr(init), _ptr(out_cost),
                 _ptr(log_u), _ptr(log_v), ctypes.byref(iters), _ptr(residuals), _ptr(ws),
                 ws.numel(), _stream_handle(dev))
         else:
             st = lib.sinkhorn_forward_device_v1(
                 ctypes.byref(pr), ctypes.byref(op), _ptr(mu), _ptr(nu),
-                None if isinstance(cost, GridCost) else _ptr(cost), _ptr(out_cost), _ptr(log_u),
+                _ptr(cost_buf), _ptr(out_cost), _ptr(log_u),
                 _ptr(log_v), ctypes.byref(iters), _ptr(residuals), _ptr(ws), ws.numel(),
                 _stream_handle(dev))
     raise_for_status(st, "sinkhorn_forward_device_v1")
@@ -264,7 +307,7 @@ def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: f
     batch is one group.  Results are device tensors, as from ``solve``.
     """
     mu, nu = torch.as_tensor(mu), torch.as_tensor(nu)
-    grid = isinstance(cost, GridCost)
+    grid = isinstance(cost, (GridCost, PointCloudCost))   # small descriptors: passed through
     if not grid:
         cost = torch.as_tensor(cost)
     B, d1, d2 = _check_shapes(mu, nu, cost)
@@ -438,7 +481,7 @@ class SinkhornLossFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, mu, nu, cost, lam, max_iters, tolerance, check_interval):
-        grid = cost if isinstance(cost, GridCost) else None
+        grid = cost if isinstance(cost, (GridCost, PointCloudCost)) else None
         res = solve(mu.detach(), nu.detach(), grid if grid is not None else cost.detach(), lam,
                     max_iters, tolerance, check_interval)
         # the complete backward state: final potentials only (loss.ts:104)

@@ -520,3 +520,26 @@ def test_gemm_path_underflowing_rows_fall_back_exactly(cuda):
                     float(g["lam"]), int(g["max_iters"]), float(g["tol"]),
                     int(g["check_interval"]), tiled_only=True, gemm=True)
     _check_loss_and_grads(g, res)
+
+
+@pytest.mark.parametrize("d1,d2", [(190, 190), (257, 190), (190, 257), (255, 131)])
+def test_tiled_sweeps_with_ragged_extents(d1, d2, cuda):
+    """The stream-K tiled half-sweeps (also the exact-rerun path of every shared
+    cost) with output extents that are not multiples of 4 or 64: the last tile
+    is shifted to end at the extent on a float4 boundary (an unaligned shift
+    faulted in round 1).  Against the float64 oracle."""
+    from oracle import sinkhorn_oracle as orc
+
+    skb = pytest.importorskip("paper_1907_01729_b200")
+    rng = np.random.default_rng(d1 + d2)
+    mu = orc.fp32_exact(orc.random_histogram_batch(5, d1, rng))
+    nu = orc.fp32_exact(orc.random_histogram_batch(5, d2, rng))
+    c = orc.fp32_exact(rng.random((d1, d2)))
+    ref = orc.batch_forward(mu, nu, c, 0.1, 40, 0.0, workers=2)
+    res = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda),
+                    torch.tensor(c, dtype=torch.float32, device=cuda), 0.1, 40, 0.0,
+                    tiled_only=True, fused=False, gemm=False)
+    assert res.path == "tiled"
+    rel = np.abs(res.cost_e0.double().cpu().numpy() - ref.cost_e0) / ref.cost_e0
+    assert rel.max() <= LOSS_RTOL
+    assert np.abs(res.log_v.double().cpu().numpy() - ref.log_v).max() <= 1e-4

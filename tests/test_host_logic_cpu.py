@@ -93,3 +93,25 @@ def test_library_is_required_no_cpu_fallback(monkeypatch, tmp_path):
     with pytest.raises(ImportError, match="no CPU fallback"):
         _lib.load()
     assert _build.LIB_NAME == "libsinkhorn_b200.so"
+
+
+def test_point_cloud_cost_descriptor():
+    """PointCloudCost: the (d1, d2) matrix it stands for, and the host-side shape
+    checks solve() applies before touching the device."""
+    import torch
+
+    from paper_1907_01729_b200 import PointCloudCost, ShapeMismatch
+    from paper_1907_01729_b200.loss import _check_shapes
+
+    x = torch.tensor([[0.0, 0.0], [1.0, 0.0], [0.0, 2.0]])
+    y = torch.tensor([[1.0, 1.0], [0.0, 0.0]])
+    c = PointCloudCost(x, y).materialize()
+    assert torch.allclose(c, torch.tensor([[2.0, 0.0], [1.0, 1.0], [2.0, 4.0]], dtype=torch.float64))
+    assert PointCloudCost(x, y).dim == 2
+    assert PointCloudCost(x, y).packed("cpu").shape == (5, 2)
+    mu, nu = torch.full((4, 3), 1 / 3), torch.full((4, 2), 0.5)
+    assert _check_shapes(mu, nu, PointCloudCost(x, y)) == (4, 3, 2)
+    with pytest.raises(ShapeMismatch):
+        _check_shapes(mu, nu, PointCloudCost(x, y[:1]))
+    with pytest.raises(ShapeMismatch):
+        _check_shapes(mu, nu, PointCloudCost(x, torch.zeros(2, 3)))
