@@ -272,6 +272,17 @@ int32_t sinkhorn_plan_grad_device_v1(const sinkhorn_problem_v1* prob, double lam
                                      const float* log_u, const float* log_v, const float* cost,
                                      const float* upstream, float* out_grad_cost, void* stream);
 
+/* The same dC with a caller workspace: shared costs run it as a tensor-core
+ * contraction over the lanes, S = U^T V with U_bi = up_b 2^(log2 u_bi - max_b),
+ * V_bj = 2^(log2 v_bj - max_b) (3xTF32 on tcgen05), then dC_ij = S_ij *
+ * 2^(-c_ij/lambda log2e + the two shifts).  Other cost kinds fall back to
+ * sinkhorn_plan_grad_device_v1. */
+size_t sinkhorn_plan_grad_workspace_bytes_v1(const sinkhorn_problem_v1* prob);
+int32_t sinkhorn_plan_grad_ws_device_v1(const sinkhorn_problem_v1* prob, double lambda,
+                                        const float* log_u, const float* log_v, const float* cost,
+                                        const float* upstream, float* out_grad_cost,
+                                        void* workspace, size_t workspace_bytes, void* stream);
+
 /* Human-readable detail for the last non-zero status on this thread. */
 const char* sinkhorn_last_error(void);
 

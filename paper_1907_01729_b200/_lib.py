@@ -61,6 +61,8 @@ EXPORTED_SYMBOLS = (
     "sinkhorn_set_residual_reducer_v1",
     "sinkhorn_forward_rows_device_v1",
     "sinkhorn_forward_async_device_v1",
+    "sinkhorn_plan_grad_workspace_bytes_v1",
+    "sinkhorn_plan_grad_ws_device_v1",
     "sinkhorn_last_error",
     "sinkhorn_version",
     "sinkhorn_launch_count_v1",
@@ -142,6 +144,9 @@ def _declare(lib):
         "sinkhorn_half_sweep_workspace_bytes_v1": (sz, [i64, i64, i64]),
         "sinkhorn_half_sweep_device_v1": (i32, [i64, i64, i64, f64, P, P, P, P, P, P, P, sz, P]),
         "sinkhorn_plan_grad_device_v1": (i32, [ctypes.POINTER(Problem), f64, P, P, P, P, P, P]),
+        "sinkhorn_plan_grad_workspace_bytes_v1": (sz, [ctypes.POINTER(Problem)]),
+        "sinkhorn_plan_grad_ws_device_v1": (
+            i32, [ctypes.POINTER(Problem), f64, P, P, P, P, P, P, sz, P]),
         "sinkhorn_e0_partial_device_v1": (i32, [i64, i64, i64, f64, P, P, P, P, P, sz, P]),
         "sinkhorn_set_residual_reducer_v1": (None, [REDUCER, P]),
         "sinkhorn_forward_async_device_v1": (

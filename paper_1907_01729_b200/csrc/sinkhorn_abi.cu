@@ -2612,6 +2612,74 @@ int32_t sinkhorn_half_sweep_device_v1(int64_t B, int64_t d1, int64_t d2, double 
   return h == 0 ? 0 : fail(h, "device status " + std::to_string(h));
 }
 
+// ---- dC on the tensor cores (shared costs) -------------------------------------
+namespace {
+struct PlanLayout {
+  size_t va = 0, uh = 0, ul = 0, al = 0, be = 0, part = 0, total = 0;
+  long long kch = 0;
+};
+PlanLayout plan_layout(const sinkhorn_problem_v1& pr, int sms) {
+  PlanLayout P;
+  Carver c;
+  P.kch = (pr.B + kUmBK - 1) / kUmBK;
+  P.va = c.take((size_t)round_up(pr.d2, kUmBM) * P.kch * kUmBK * 4);
+  P.uh = c.take((size_t)round_up(pr.d1, kUmBN) * P.kch * kUmBK * 4);
+  P.ul = c.take((size_t)round_up(pr.d1, kUmBN) * P.kch * kUmBK * 4);
+  P.al = c.take((size_t)pr.d1 * 4);
+  P.be = c.take((size_t)pr.d2 * 4);
+  P.part = c.take((size_t)sms * 2 * kUmBN * kUmBM * 4);
+  P.total = c.take(256);
+  return P;
+}
+
+int plan_grad_umma(const sinkhorn_problem_v1& pr, double lambda, const float* log_u,
+                   const float* log_v, const float* cost, const float* up, float* dc, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
+  const DeviceInfo di = device_info();
+  const PlanLayout P = plan_layout(pr, di.sms);
+  if (ws == nullptr || ws_bytes < P.total) return fail(SINKHORN_STATUS_WORKSPACE, "workspace too small");
+  const int B = (int)pr.B, d1 = (int)pr.d1, d2 = (int)pr.d2;
+  float* al = at<float>(ws, P.al);
+  float* be = at<float>(ws, P.be);
+  g_launches += 3;
+  plan_lane_max_kernel<<<grid_for((size_t)d1), 256, 0, st>>>(log_u, B, d1, al);
+  plan_lane_max_kernel<<<grid_for((size_t)d2), 256, 0, st>>>(log_v, B, d2, be);
+  const size_t nop = (size_t)(round_up(d2, kUmBM) + round_up(d1, kUmBN)) * P.kch * kUmBK;
+  plan_operands_kernel<<<grid_for(nop), 256, 0, st>>>(log_u, log_v, up, al, be, B, d1, d2, P.kch,
+                                                      at<float>(ws, P.va), at<float>(ws, P.uh),
+                                                      at<float>(ws, P.ul));
+  CK(cudaGetLastError());
+  CUtensorMap ta, tbh, tbl;
+  const size_t mt = (size_t)round_up(d2, kUmBM) / kUmBM, nt = (size_t)round_up(d1, kUmBN) / kUmBN;
+  const size_t sub = (size_t)P.kch * kUmSub;
+  bool ok = make_tmap_sw128(&ta, at<float>(ws, P.va), mt * sub * kUmBM, 32, 32, kUmBM);
+  ok &= make_tmap_sw128(&tbh, at<float>(ws, P.uh), nt * sub * kUmBN, 32, 32, kUmBN);
+  ok &= make_tmap_sw128(&tbl, at<float>(ws, P.ul), nt * sub * kUmBN, 32, 32, kUmBN);
+  if (!ok) return fail(SINKHORN_STATUS_CUDA_ERROR, "cuTensorMapEncodeTiled failed (plan)");
+  UmmaParams p = {};   // S[i][j] = sum_b U_bi V_bj: M = d2 (A = V), N = d1 (lanes = U)
+  p.M = d2;
+  p.N = d1;
+  p.K = B;
+  p.MT = (int)mt;
+  p.NT = (int)nt;
+  p.KCH = (int)P.kch;
+  p.units = (long long)p.MT * p.NT * p.KCH;
+  p.G = (int)std::min<long long>(di.sms, p.units);
+  p.out = dc;
+  p.ldo = d2;
+  p.part = at<float>(ws, P.part);
+  p.status = nullptr;
+  if (int e = set_max_smem(reinterpret_cast<const void*>(&umma_gemm_kernel), kUmSmemBytes)) return e;
+  g_launches += 3;
+  CK(launch_pdl(umma_gemm_kernel, dim3(p.G), dim3(kUmThreads), kUmSmemBytes, st, ta, tbh, tbl, p));
+  CK(launch_pdl(umma_fixup_kernel, dim3((unsigned)p.G), dim3(256), 0, st, p));
+  plan_finish_kernel<<<grid_for((size_t)d1 * d2), 256, 0, st>>>(
+      dc, cost, al, be, d1, d2, (float)(-kLog2e / lambda));
+  CK(cudaGetLastError());
+  return 0;
+}
+}  // namespace
+
 int32_t sinkhorn_plan_grad_device_v1(const sinkhorn_problem_v1* prob, double lambda,
                                      const float* log_u, const float* log_v, const float* cost,
                                      const float* upstream, float* out_grad_cost, void* stream) {
@@ -2626,6 +2694,7 @@ int32_t sinkhorn_plan_grad_device_v1(const sinkhorn_problem_v1* prob, double lam
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const float k = (float)(-1.4426950408889634 / lambda);
   dim3 g((unsigned)((prob->d2 + 31) / 32), (unsigned)((prob->d1 + 7) / 8));
+  // (the workspace variant below runs the shared-cost case on the tensor cores)
   if (prob->cost_kind == SINKHORN_COST_SHARED) {
     ++g_launches;
     plan_grad_shared_kernel<<<g, 256, 0, st>>>(log_u, log_v, cost, upstream, (int)prob->B,
@@ -2639,6 +2708,28 @@ int32_t sinkhorn_plan_grad_device_v1(const sinkhorn_problem_v1* prob, double lam
   }
   CK(cudaGetLastError());
   return 0;
+}
+
+size_t sinkhorn_plan_grad_workspace_bytes_v1(const sinkhorn_problem_v1* prob) {
+  if (check_problem(prob) != 0) return 0;
+  if (prob->cost_kind != SINKHORN_COST_SHARED) return 256;
+  return plan_layout(*prob, device_info().sms).total;
+}
+
+int32_t sinkhorn_plan_grad_ws_device_v1(const sinkhorn_problem_v1* prob, double lambda,
+                                        const float* log_u, const float* log_v, const float* cost,
+                                        const float* upstream, float* out_grad_cost,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+  if (int e = check_problem(prob)) return e;
+  if (prob->cost_kind != SINKHORN_COST_SHARED || prob->B == 0 || prob->d1 == 0 || prob->d2 == 0)
+    return sinkhorn_plan_grad_device_v1(prob, lambda, log_u, log_v, cost, upstream, out_grad_cost,
+                                        stream);
+  if (!(std::isfinite(lambda) && lambda > 0))
+    return fail(SINKHORN_STATUS_INVALID_CONFIG, "lam must be positive and finite");
+  if (!log_u || !log_v || !cost || !upstream || !out_grad_cost)
+    return fail(SINKHORN_STATUS_BAD_ARGUMENT, "null pointer");
+  return plan_grad_umma(*prob, lambda, log_u, log_v, cost, upstream, out_grad_cost, workspace,
+                        workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
 void sinkhorn_set_residual_reducer_v1(sinkhorn_residual_reducer_v1 fn, void* user) {

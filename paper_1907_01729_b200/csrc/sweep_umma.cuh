@@ -514,6 +514,72 @@ __global__ void points_cost_kernel(float* __restrict__ c, const float* __restric
   }
 }
 
+// ---- dC = sum_b up_b P_b for a shared cost, as a tensor-core contraction -------
+// P_bij = 2^(u_bi + A2_ij + v_bj) (log2 units) = 2^(A2_ij + al_i + be_j) *
+// U_bi V_bj with al_i = max_b u_bi, be_j = max_b v_bj, U_bi = up_b 2^(u_bi - al_i),
+// V_bj = 2^(v_bj - be_j) <= 1: S = U^T V is a (d1 x B)(B x d2) contraction over
+// the lanes (core.py:363-368 per lane, the one dense
+// contraction of the path).  A operand: V over (d2 rows, B reduction); B
+// operand: U's tf32 planes over (d1 rows, B reduction); out[i * d2 + j].
+
+// al / be: the per-row maxima over the lanes (natural-log input -> log2);
+// -inf everywhere (zero mass in every lane) -> 0, its terms are all 0.
+__global__ void plan_lane_max_kernel(const float* __restrict__ lx, int B, int d,
+                                     float* __restrict__ mx) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x) {
+    float m = neg_inf();
+    for (int b = 0; b < B; ++b) m = fmaxf(m, lx[(size_t)b * d + i] * kLog2e);
+    mx[i] = m == neg_inf() ? 0.f : m;
+  }
+}
+
+// V -> the tiled A-operand layout (rows j, reduction b); U -> tf32 planes of
+// the lane operand (rows i, reduction b).  Grid-stride over the tiled index
+// space of each (zero padding).
+__global__ void plan_operands_kernel(const float* __restrict__ log_u, const float* __restrict__ log_v,
+                                     const float* __restrict__ up, const float* __restrict__ al,
+                                     const float* __restrict__ be, int B, int d1, int d2,
+                                     long long kch, float* __restrict__ va,
+                                     float* __restrict__ uh, float* __restrict__ ul) {
+  const long long nva = (long long)((d2 + kUmBM - 1) / kUmBM) * kUmBM * kch * kUmBK;
+  const long long nu = (long long)((d1 + kUmBN - 1) / kUmBN) * kUmBN * kch * kUmBK;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nva + nu;
+       e += (long long)gridDim.x * blockDim.x) {
+    const bool isv = e < nva;
+    const long long f = isv ? e : e - nva;
+    const int R = isv ? kUmBM : kUmBN;
+    const long long blk = f / (R * kUmBK);
+    const int within = (int)(f % (R * kUmBK));
+    const int sb = within / (R * 32), w2 = within % (R * 32);
+    const long long r = (blk / kch) * R + w2 / 32;          // j (V) or i (U)
+    const int b = (int)((blk % kch) * kUmBK + sb * 32 + w2 % 32);
+    if (isv) {
+      float v = 0.f;
+      if (r < d2 && b < B) v = exp2f(log_v[(size_t)b * d2 + r] * kLog2e - be[r]);
+      va[f] = v;
+    } else {
+      float x = 0.f;
+      if (r < d1 && b < B) x = up[b] * exp2f(log_u[(size_t)b * d1 + r] * kLog2e - al[r]);
+      const float h = tf32_hi(x);
+      uh[f] = h;
+      ul[f] = x - h;
+    }
+  }
+}
+
+// dC_ij = S_ij * 2^(c_ij * kscale + al_i + be_j), in place over S (row-major [d1][d2]).
+__global__ void plan_finish_kernel(float* __restrict__ dc, const float* __restrict__ c,
+                                   const float* __restrict__ al, const float* __restrict__ be,
+                                   int d1, int d2, float kscale) {
+  const long long n = (long long)d1 * d2;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / d2), j = (int)(e - (long long)i * d2);
+    const float s = dc[e];
+    dc[e] = s == 0.f ? 0.f : s * exp2f(fmaf(c[e], kscale, al[i] + be[j]));
+  }
+}
+
 // K = 2^(c * kscale) and K o C (E0) as tiled A operands over (d1 rows, d2
 // reduction), and K^T over (d2 rows, d1 reduction), from the caller's cost
 // (validated: finite, >= 0, status 15).  One block per 32 x 32 cost block

@@ -468,11 +468,14 @@ def plan_gradient(log_u: torch.Tensor, log_v: torch.Tensor, cost: torch.Tensor, 
     out = torch.empty_like(cost)
     lib = _lib.load()
     with torch.cuda.device(dev):
-        st = lib.sinkhorn_plan_grad_device_v1(ctypes.byref(pr), float(lam),
-                                              _ptr(log_u.float().contiguous()),
-                                              _ptr(log_v.float().contiguous()), _ptr(cost),
-                                              _ptr(up), _ptr(out), _stream_handle(dev))
-    raise_for_status(st, "sinkhorn_plan_grad_device_v1")
+        # shared costs: the tensor-core contraction over the lanes (workspace variant)
+        ws = _workspace(dev, lib.sinkhorn_plan_grad_workspace_bytes_v1(ctypes.byref(pr)))
+        st = lib.sinkhorn_plan_grad_ws_device_v1(ctypes.byref(pr), float(lam),
+                                                 _ptr(log_u.float().contiguous()),
+                                                 _ptr(log_v.float().contiguous()), _ptr(cost),
+                                                 _ptr(up), _ptr(out), _ptr(ws), ws.numel(),
+                                                 _stream_handle(dev))
+    raise_for_status(st, "sinkhorn_plan_grad_ws_device_v1")
     return out
 
 

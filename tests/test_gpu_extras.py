@@ -231,3 +231,38 @@ def test_config5_full_support_against_float64(nccl_world1, cuda):
         rel = float(((cost - want_cost).abs() / want_cost).max())
         assert rel <= 1e-5, (name, rel)
         assert float((log_u - want_u).abs().max()) <= 1e-3, name
+
+
+@pytest.mark.parametrize("B,d1,d2", [(256, 784, 784), (64, 300, 190), (5, 1000, 77)])
+def test_plan_gradient_tensor_core_path_matches_direct_sum(B, d1, d2, cuda):
+    """The shared-cost dC contraction on the tensor cores (sinkhorn_plan_grad_ws_device_v1)
+    against the direct per-cell sum over lanes (sinkhorn_plan_grad_device_v1), with
+    mixed-sign upstream and zero-mass rows (-inf potentials)."""
+    import ctypes
+
+    from paper_1907_01729_b200 import _lib
+
+    skb = _skb()
+    lib = _lib.load()
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(B + d1)
+    m = torch.rand(B, d1, generator=gen, device=cuda, dtype=torch.float64) + 0.5
+    mu = (m / m.sum(1, keepdim=True)).float()
+    mu[0, :5] = 0.0
+    mu[0] /= mu[0].sum()
+    m = torch.rand(B, d2, generator=gen, device=cuda, dtype=torch.float64) + 0.5
+    nu = (m / m.sum(1, keepdim=True)).float()
+    c = torch.rand(d1, d2, generator=gen, device=cuda)
+    res = skb.solve(mu, nu, c, 0.05, 30, 0.0)
+    up = torch.randn(B, generator=gen, device=cuda)
+    got = skb.plan_gradient(res.log_u, res.log_v, c, 0.05, up)
+    want = torch.empty_like(c)
+    pr = _lib.Problem()
+    pr.B, pr.d1, pr.d2, pr.cost_kind = B, d1, d2, _lib.COST_SHARED
+    st = lib.sinkhorn_plan_grad_device_v1(ctypes.byref(pr), 0.05, res.log_u.data_ptr(),
+                                          res.log_v.data_ptr(), c.data_ptr(), up.data_ptr(),
+                                          want.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert st == 0
+    torch.cuda.synchronize()
+    scale = float(want.abs().max())
+    assert float((got - want).abs().max()) <= 1e-5 * scale
