@@ -520,7 +520,7 @@ def init_dist():
     return world, rank, local
 
 
-def config_dict(cfg: dict, world: int, row: bool, path: str | None = None) -> dict:
+def config_dict(cfg: dict, world: int, row: bool) -> dict:
     """The `config` object both arms print (same keys, same values)."""
     jobs = 1 if row else world
     out = {"workload": cfg["workload"], "B_per_gpu": cfg["B"], "global_batch": cfg["B"] * jobs,
@@ -530,8 +530,6 @@ def config_dict(cfg: dict, world: int, row: bool, path: str | None = None) -> di
                            "column sums per iteration") if row else f"batch-sharded dp{world}",
            "l2": ("flushed between steps (256 MiB write outside the timed events); config-4 / "
                   "config-5 inputs (4.3 / 17.2 GB) also exceed L2")}
-    if path is not None:
-        out["solver_path"] = path
     return out
 
 
@@ -699,7 +697,8 @@ def run_ours(args, cfg, world, rank, local):
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong" if row else "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": config_dict(cfg, world, row, path),
+        "config": config_dict(cfg, world, row),
+        "solver_path": path,
         "roofline": roofline(cfg, kernel_ms, peaks, clocks, load_traffic(args.config, path), path,
                              share=(1.0 / world) if row else 1.0),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
