@@ -194,7 +194,7 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
           dense_grid: bool = False, init_log_u=None, fused: bool = True,
           fp64: bool = False, gemm: bool | None = None,
           time_kernel: bool = False, asynchronous: bool = False,
-          force_rerun: bool = False) -> SolveResult:
+          force_rerun: bool = False, out=None) -> SolveResult:
     """batch_forward (batch.py:264-349) on the GPU.
 
     mu (B, d1), nu (B, d2) histograms; cost a (d1, d2) tensor shared by all
@@ -217,6 +217,8 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
     estimate-guard rerun is decided on the device; device-detected errors are
     raised by ``result.check()`` (``iterations_run`` is ``max_iters``).
     ``force_rerun`` (diagnostics) exercises the exact-rerun machinery.
+    ``out``: optional preallocated (cost (B,), log_u (B, d1), log_v (B, d2),
+    residuals (B,)) float32 device tensors to write into.
     """
     if fp64:
         return _solve_f64(mu, nu, cost, lam, max_iters, tolerance, check_interval, validate)
@@ -246,10 +248,17 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
         (_lib.FLAG_FORCE_GEMM if gemm else 0) | (_lib.FLAG_NO_GEMM if gemm is False else 0) | \
         (_lib.FLAG_TIME_KERNEL if time_kernel else 0) | \
         (_lib.FLAG_FORCE_RERUN if force_rerun else 0)
-    out_cost = torch.empty(B, device=dev, dtype=torch.float32)
-    log_u = torch.empty(B, d1, device=dev, dtype=torch.float32)
-    log_v = torch.empty(B, d2, device=dev, dtype=torch.float32)
-    residuals = torch.empty(B, device=dev, dtype=torch.float32)
+    if out is not None:
+        out_cost, log_u, log_v, residuals = out
+        for t, shp in zip(out, ((B,), (B, d1), (B, d2), (B,))):
+            if tuple(t.shape) != shp or t.dtype != torch.float32 or not t.is_contiguous() \
+                    or t.device != dev:
+                raise ShapeMismatch(f"out tensor must be contiguous float32 {shp} on {dev}")
+    else:
+        out_cost = torch.empty(B, device=dev, dtype=torch.float32)
+        log_u = torch.empty(B, d1, device=dev, dtype=torch.float32)
+        log_v = torch.empty(B, d2, device=dev, dtype=torch.float32)
+        residuals = torch.empty(B, device=dev, dtype=torch.float32)
     with torch.cuda.device(dev):
         nbytes = lib.sinkhorn_workspace_bytes_v1(ctypes.byref(pr))
         ws = _workspace(dev, nbytes)
@@ -297,14 +306,15 @@ def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: f
                    validate: bool = True) -> SolveResult:
     """``solve`` from host tensors, overlapping the host->device upload with the solve.
 
-    mu (B, d1), nu (B, d2) and cost -- shared (d1, d2), per-sample (B, d1, d2)
-    or a GridCost -- in host memory (pin it for full PCIe bandwidth).  At
-    tolerance 0 the lanes are independent (test_batch.py:46-63), so the batch
-    is solved in ``chunks`` lane groups: while group k solves on the current
-    stream, group k+1's histograms and per-sample costs are copied on a
-    second stream into the other of two device buffers.  With tolerance > 0
-    the lockstep stopping rule couples every lane (batch.py:318-322), so the
-    batch is one group.  Results are device tensors, as from ``solve``.
+    mu (B, d1), nu (B, d2) and cost -- shared (d1, d2), per-sample (B, d1, d2),
+    a GridCost or a PointCloudCost -- in host memory (pin it for full PCIe
+    bandwidth).  At tolerance 0 the lanes are independent (test_batch.py:46-63),
+    so the batch is solved in ``chunks`` lane groups through three rotating
+    device buffers: group k+1 and k+2's histograms and per-sample costs are
+    copied on a second stream while group k solves, and the solves are
+    asynchronous (no host synchronisation until the end), so the copy engine
+    never waits for the host.  With tolerance > 0 the lockstep stopping rule
+    couples every lane (batch.py:318-322): one group, synchronous.
     """
     mu, nu = torch.as_tensor(mu), torch.as_tensor(nu)
     grid = isinstance(cost, (GridCost, PointCloudCost))   # small descriptors: passed through
@@ -314,19 +324,21 @@ def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: f
     dev = torch.device(device) if device is not None else \
         torch.device("cuda", torch.cuda.current_device())
     per_sample = (not grid) and cost.dim() == 3
-    if tolerance > 0 or B == 0:
+    asynchronous = tolerance == 0 and B > 0
+    if not asynchronous:
         chunks = 1
     chunks = max(1, min(int(chunks), B if B else 1))
+    nbuf = min(3, chunks)
     bounds = [(B * k // chunks, B * (k + 1) // chunks) for k in range(chunks)]
     gmax = max(hi - lo for lo, hi in bounds) if B else 0
     compute = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
     f32 = dict(device=dev, dtype=torch.float32)
     bufs = [(torch.empty(gmax, d1, **f32), torch.empty(gmax, d2, **f32),
-             torch.empty(gmax, d1, d2, **f32) if per_sample else None) for _ in range(2)]
+             torch.empty(gmax, d1, d2, **f32) if per_sample else None) for _ in range(nbuf)]
     shared = None if (grid or per_sample) else cost.to(**f32, non_blocking=True)
-    ready = [torch.cuda.Event() for _ in range(2)]
-    free = [torch.cuda.Event() for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(nbuf)]
+    free = [torch.cuda.Event() for _ in range(nbuf)]
     out_cost = torch.empty(B, **f32)
     log_u = torch.empty(B, d1, **f32)
     log_v = torch.empty(B, d2, **f32)
@@ -334,36 +346,36 @@ def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: f
 
     def upload(k):
         lo, hi = bounds[k]
-        m, n, c = bufs[k % 2]
+        m, n, c = bufs[k % nbuf]
         with torch.cuda.stream(copy):
-            if k >= 2:
-                copy.wait_event(free[k % 2])      # group k-2 has finished with the buffer
+            if k >= nbuf:
+                copy.wait_event(free[k % nbuf])   # group k - nbuf has finished with it
             m[: hi - lo].copy_(mu[lo:hi], non_blocking=True)
             n[: hi - lo].copy_(nu[lo:hi], non_blocking=True)
             if c is not None:
                 c[: hi - lo].copy_(cost[lo:hi], non_blocking=True)
-            ready[k % 2].record(copy)
+            ready[k % nbuf].record(copy)
 
-    iters = 0
+    iters, checks = 0, []
     with torch.cuda.device(dev):
-        upload(0)
-        if chunks > 1:
-            upload(1)
+        for k in range(min(nbuf, chunks)):
+            upload(k)
         for k, (lo, hi) in enumerate(bounds):
-            m, n, c = bufs[k % 2]
-            compute.wait_event(ready[k % 2])
+            m, n, c = bufs[k % nbuf]
+            compute.wait_event(ready[k % nbuf])
             g = hi - lo
             cg = cost if grid else (c[:g] if per_sample else shared)
+            # results straight into the slices of the outputs (contiguous lane ranges)
             r = solve(m[:g], n[:g], cg, lam, max_iters, tolerance, check_interval,
-                      validate=validate)
-            out_cost[lo:hi] = r.cost_e0
-            log_u[lo:hi] = r.log_u
-            log_v[lo:hi] = r.log_v
-            residuals[lo:hi] = r.residuals
+                      validate=validate, asynchronous=asynchronous,
+                      out=(out_cost[lo:hi], log_u[lo:hi], log_v[lo:hi], residuals[lo:hi]))
+            checks.append(r)
             iters = max(iters, r.iterations_run)
-            free[k % 2].record(compute)
-            if k + 2 < chunks:
-                upload(k + 2)
+            free[k % nbuf].record(compute)
+            if k + nbuf < chunks:
+                upload(k + nbuf)
+    for r in checks:
+        r.check()
     return SolveResult(out_cost, log_u, log_v, float(lam), iters, residuals, -1.0,
                        _lib.load().sinkhorn_last_path_v1().decode())
 
