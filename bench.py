@@ -743,6 +743,20 @@ def run_e2e_row(args, step_fn, mu_l, nu, dev):
             "path": "row_sharded_solve()+row_sharded_backward() from pinned host tensors"}
 
 
+def pinned_copy(t):
+    """A page-locked host copy of device tensor t, allocated pinned directly
+    (no pageable intermediate: config 5's cost is 17 GB); pageable if the host
+    cannot lock that much."""
+    import torch
+
+    try:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    except RuntimeError:
+        return t.cpu()
+    h.copy_(t)
+    return h
+
+
 def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
     """Host buffers in, host results out, copies inside the timed region."""
     import ctypes
@@ -796,8 +810,7 @@ def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
         h_mu = mu.cpu().pin_memory()
         h_nu = nu.cpu().pin_memory()
         grid = isinstance(cost, skb.GridCost)
-        big = (not grid) and cost.numel() * 4 > (8 << 30)   # > 8 GiB: pageable, not pinned
-        h_c = None if grid else (cost.cpu() if big else cost.cpu().pin_memory())
+        h_c = None if grid else pinned_copy(cost)
         h_loss = torch.empty(B).pin_memory()
         h_gm = torch.empty(B, d).pin_memory()
         h_gn = torch.empty(B, d).pin_memory()
@@ -817,7 +830,7 @@ def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
         h2d = 4 * (2 * B * d + (0 if grid else cost.numel()))
         d2h = 4 * (B + 2 * B * d)
         path = (f"torch API solve_streamed(chunks={chunks})+potentials_backward() from pinned "
-                "host tensors (uploads overlap the solve)")
+                "host tensors" + (" (uploads overlap the solve)" if chunks > 1 else ""))
     one()
     t0 = time.perf_counter()
     for _ in range(steps):

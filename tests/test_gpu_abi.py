@@ -194,3 +194,31 @@ def test_every_path_reports_invalid_inputs(path, cuda):
     c_bad[..., 2, 2] = -1.0
     with pytest.raises(skb.InvalidCost):
         skb.solve(t(mu), t(nu), t(c_bad), 0.1, 20, **kw)
+
+
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+def test_cost_validation_covers_every_element(offset, cuda):
+    """validate_cost_kernel reads float4s after a scalar head: a bad element in
+    the head, the vector body or the tail is found for every 16-byte
+    misalignment of the caller's pointer, and a valid cost passes."""
+    import torch
+
+    import paper_1907_01729_b200 as skb
+
+    B, d = 3, 13   # B*d*d = 507: head, body and tail all non-empty
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(offset)
+    m = torch.rand(B, d, generator=gen, device=cuda) + 0.5
+    mu = m / m.sum(1, keepdim=True)
+    nu = mu.flip(0).contiguous()
+    n = B * d * d
+    flat = torch.rand(n + 8, generator=gen, device=cuda)
+    cost = flat[offset:offset + n].view(B, d, d)
+    skb.solve(mu, nu, cost, 0.1, 5)
+    for k in (0, 1, 2, 3, 4, n // 2, n - 4, n - 3, n - 2, n - 1):
+        for v in (-1.0, float("nan"), float("inf")):
+            saved = float(flat[offset + k])
+            flat[offset + k] = v
+            with pytest.raises(skb.InvalidCost):
+                skb.solve(mu, nu, cost, 0.1, 5)
+            flat[offset + k] = saved
