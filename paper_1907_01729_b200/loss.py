@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from .errors import ShapeMismatch, raise_for_status
+from .errors import InvalidConfig, ShapeMismatch, raise_for_status
 
 
 @dataclass(frozen=True)
@@ -302,7 +302,7 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
 
 
 def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.0,
-                   check_interval: int = 10, chunks: int = 8, device=None,
+                   check_interval: int = 10, chunks=8, device=None,
                    validate: bool = True) -> SolveResult:
     """``solve`` from host tensors, overlapping the host->device upload with the solve.
 
@@ -315,6 +315,9 @@ def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: f
     asynchronous (no host synchronisation until the end), so the copy engine
     never waits for the host.  With tolerance > 0 the lockstep stopping rule
     couples every lane (batch.py:318-322): one group, synchronous.
+    ``chunks`` is a group count (equal groups) or a list of group sizes summing
+    to B -- the pipeline's exposed ends are the first group's upload and the
+    last group's solve, so short groups there shorten the step.
     """
     mu, nu = torch.as_tensor(mu), torch.as_tensor(nu)
     grid = isinstance(cost, (GridCost, PointCloudCost))   # small descriptors: passed through
@@ -327,9 +330,17 @@ def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: f
     asynchronous = tolerance == 0 and B > 0
     if not asynchronous:
         chunks = 1
-    chunks = max(1, min(int(chunks), B if B else 1))
+    if isinstance(chunks, int):
+        chunks = max(1, min(int(chunks), B if B else 1))
+        bounds = [(B * k // chunks, B * (k + 1) // chunks) for k in range(chunks)]
+    else:   # explicit lane-group sizes (e.g. a short first and last group)
+        sizes = [int(n) for n in chunks if int(n) > 0]
+        if sum(sizes) != B:
+            raise InvalidConfig("solve_streamed: lane-group sizes must sum to B")
+        edges = [sum(sizes[:k]) for k in range(len(sizes) + 1)]
+        bounds = list(zip(edges[:-1], edges[1:]))
+    chunks = len(bounds)
     nbuf = min(3, chunks)
-    bounds = [(B * k // chunks, B * (k + 1) // chunks) for k in range(chunks)]
     gmax = max(hi - lo for lo, hi in bounds) if B else 0
     compute = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
