@@ -543,3 +543,34 @@ def test_tiled_sweeps_with_ragged_extents(d1, d2, cuda):
     rel = np.abs(res.cost_e0.double().cpu().numpy() - ref.cost_e0) / ref.cost_e0
     assert rel.max() <= LOSS_RTOL
     assert np.abs(res.log_v.double().cpu().numpy() - ref.log_v).max() <= 1e-4
+
+
+@pytest.mark.parametrize("B,d1,d2", [(70, 1300, 2100), (130, 2049, 1031)])
+def test_gemm_path_ragged_tiles_match_tiled(B, d1, d2, cuda):
+    """The tcgen05 contractions with ragged M tiles (d not a multiple of 128),
+    a ragged reduction chunk (not a multiple of 64) and more than one 64-lane
+    N tile (the last one partial): equal to the log-domain tiled half-sweeps."""
+    skb = _skb()
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(B)
+
+    def hist(d):
+        m = torch.rand(B, d, generator=gen, device=cuda, dtype=torch.float64) + 0.5
+        return (m / m.sum(1, keepdim=True)).float()
+    mu, nu = hist(d1), hist(d2)
+    i = torch.arange(d1, device=cuda, dtype=torch.float64)[:, None] / (d1 - 1)
+    j = torch.arange(d2, device=cuda, dtype=torch.float64)[None, :] / (d2 - 1)
+    c = ((i - j) ** 2 + 0.1 * torch.rand(d1, d2, generator=gen, device=cuda,
+                                          dtype=torch.float64)).float()
+    args = (mu, nu, c, 0.05, 40, 0.0)
+    res = skb.solve(*args, tiled_only=True, gemm=True)
+    assert res.path == "gemm"
+    tiled = skb.solve(*args, tiled_only=True, fused=False, gemm=False)
+    rel = ((res.cost_e0.double() - tiled.cost_e0.double()).abs() / tiled.cost_e0.double()).max()
+    assert float(rel) <= 2e-6
+    assert float((res.log_u - tiled.log_u).abs().max()) <= 1e-4
+    assert float((res.log_v - tiled.log_v).abs().max()) <= 1e-4
+    gm, gn = skb.potentials_backward(res.log_u, res.log_v, 0.05, torch.ones(B, device=cuda))
+    tm, tn = skb.potentials_backward(tiled.log_u, tiled.log_v, 0.05, torch.ones(B, device=cuda))
+    assert float((gm - tm).abs().max()) <= GRAD_ATOL
+    assert float((gn - tn).abs().max()) <= GRAD_ATOL
