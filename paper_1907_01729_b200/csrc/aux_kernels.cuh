@@ -201,6 +201,43 @@ __global__ void __launch_bounds__(256) e0_finalize_kernel(const float* __restric
   }
 }
 
+// The same for lane-major E0 terms (sj == 1: lane b's terms contiguous):
+// one warp per lane reads them coalesced, the (max, sum) pairs merged by a
+// fixed xor butterfly (deterministic).  8 lanes per 256-thread block.
+__global__ void __launch_bounds__(256) e0_finalize_rows_kernel(const float* __restrict__ e0, int B,
+                                                               int d2, long long sb,
+                                                               float* __restrict__ out_cost,
+                                                               int* status, int out_log2) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (b >= B) return;
+  const float* row = e0 + (size_t)b * sb;
+  float m = kNegBig, s = 0.f;
+  for (int j = lane; j < d2; j += 32) {
+    const float v = __ldg(row + j);
+    if (v > m + kLazy) {
+      s *= ex2(m - v);
+      m = v;
+    }
+    s += ex2(v - m);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float mo = __shfl_xor_sync(0xffffffffu, m, off);
+    const float so = __shfl_xor_sync(0xffffffffu, s, off);
+    lse_merge(m, s, mo, so);
+  }
+  if (lane == 0) {
+    if (out_log2) {
+      out_cost[b] = lse_final(m, s);
+    } else {
+      const float cost = exp2f(lse_final(m, s));
+      out_cost[b] = cost;
+      if (!isfinite(cost)) set_status(status, 12);
+    }
+  }
+}
+
 // Solver layout (log2) -> caller layout (B, d) row-major natural log; NaN in
 // the state is status 12 (batch.py:326-327 NaNProduced, ffi.ts:124-128).
 __global__ void __launch_bounds__(256) export_potential_kernel(const float* __restrict__ x,

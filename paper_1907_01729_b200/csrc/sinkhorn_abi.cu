@@ -1837,7 +1837,10 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     } else if (L.fused)   // per-row E0 terms of the fused passes
       e0_rows_finalize_kernel<<<(unsigned)((pr.B + 7) / 8), 256, 0, st>>>(
           S.F(L.e0), (int)pr.B, (int)pr.d1, L.D1p, out_cost, status);
-    else           // per-column E0 terms of the tail pass
+    else if (sj == 1)   // per-column E0 terms of the tail pass, lane-major
+      e0_finalize_rows_kernel<<<(unsigned)((pr.B + 7) / 8), 256, 0, st>>>(
+          S.F(L.e0), (int)pr.B, (int)pr.d2, sb, out_cost, status, 0);
+    else
       e0_finalize_kernel<<<nb, 256, 0, st>>>(S.F(L.e0), (int)pr.B, (int)pr.d2, sb, sj, out_cost,
                                              status, 0);
     dim3 gu((unsigned)((pr.d1 + 31) / 32), (unsigned)((pr.B + 31) / 32));

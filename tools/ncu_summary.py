@@ -31,8 +31,12 @@ KEYS = [
 
 
 def raw(rep: str):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    """The raw page of a report, or an exported `ncu -i rep --page raw --csv` file."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     return [dict(zip(r[0], row)) for row in r[2:]], dict(zip(r[0], r[1]))
 
