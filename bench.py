@@ -565,7 +565,7 @@ def run_reference(args, cfg, world, rank):
                          "cpu": r["cpu"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(args, cfg, world, rank, local):
@@ -714,7 +714,7 @@ def run_ours(args, cfg, world, rank, local):
                                   light=cfg["cost"] != "per_sample" and d > 100)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu")}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist.is_initialized():
         dist.destroy_process_group()
 
@@ -839,6 +839,26 @@ def run_e2e(args, cfg, mu, nu, cost, lam, iters, dev):
     return {"seconds_per_step": dt, "h2d": h2d, "d2h": d2h, "path": path}
 
 
+_JSON_OUT = None   # the process's original stdout (see quiet_stdout)
+
+
+def quiet_stdout() -> None:
+    """stdout carries exactly one JSON line: from here on anything else that
+    writes to file descriptor 1 -- NCCL's version banner, library prints --
+    lands on stderr, and emit() writes to the saved original stdout."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(obj) -> None:
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(obj) + "\n")
+    out.flush()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -876,6 +896,7 @@ def main():
     if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}: "
                          "launch N ranks for --gpus N")
+    quiet_stdout()   # a worker (or the single process): the launcher above keeps its stdout
     if args.steps is None:
         # enough steps that a rare host-side stall (seen on the boxes: one
         # step in ~100 takes 5-100 ms longer, with or without our sampler)
@@ -890,8 +911,8 @@ def main():
         t = torch.ones(1)
         dist.all_reduce(t)
         if rank == 0:
-            print(json.dumps({"probe": "ranks", "world": world, "ranks_seen": int(t.item()),
-                              "gpus_arg": args.gpus}), flush=True)
+            emit({"probe": "ranks", "world": world, "ranks_seen": int(t.item()),
+                  "gpus_arg": args.gpus})
         dist.destroy_process_group()
         return
     if args.impl == "reference":
