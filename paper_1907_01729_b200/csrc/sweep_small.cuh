@@ -97,9 +97,9 @@ struct SmallSmem {
 
 // (max, sum 2^(row + x - max)[, sum of 2^(...) * row * cinv]) of one unit,
 // reduced over the S threads of its group.  All 32 lanes of the warp call it.
-template <bool kTail>
+template <int S, bool kTail>
 __device__ __forceinline__ void small_unit_lse(const float* __restrict__ row,
-                                               const float* __restrict__ x, int n, int S, int s,
+                                               const float* __restrict__ x, int n, int s,
                                                bool active, float cinv, float& m_out,
                                                float& s_out, float& w_out) {
   float m0 = neg_inf(), m1 = neg_inf(), m2 = neg_inf(), m3 = neg_inf();
@@ -114,6 +114,7 @@ __device__ __forceinline__ void small_unit_lse(const float* __restrict__ row,
     for (; i < n; i += S) m0 = fmaxf(m0, row[i] + x[i]);
   }
   float m = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+#pragma unroll
   for (int o = 1; o < S; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   const float mm = (m == neg_inf()) ? 0.f : m;   // all terms -inf: the sum is 0
   float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f;
@@ -143,6 +144,7 @@ __device__ __forceinline__ void small_unit_lse(const float* __restrict__ row,
   }
   float sum = (s0 + s1) + (s2 + s3);
   float w = w0 + w1;
+#pragma unroll
   for (int o = 1; o < S; o <<= 1) {
     sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (kTail) w += __shfl_xor_sync(0xffffffffu, w, o);
@@ -152,23 +154,53 @@ __device__ __forceinline__ void small_unit_lse(const float* __restrict__ row,
   w_out = w;
 }
 
+// Single pass shifted by an estimate of the result (the previous sweep's lse
+// at this output, est = target - previous output): sum 2^(row + x - est).
+// Accepted when the sum lies in [2^-60, 2^100] -- no term overflows and every
+// term within 2^-60 of the largest is represented -- as the tiled and
+// separable sweeps' estimate mode; the caller redoes the unit exactly
+// otherwise (first iteration: no estimate).
+template <int S>
+__device__ __forceinline__ float small_unit_est(const float* __restrict__ row,
+                                                const float* __restrict__ x, int n, int s,
+                                                bool active, float est) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (active) {
+    int i = s;
+    for (; i + 3 * S < n; i += 4 * S) {
+      s0 += ex2(row[i] + x[i] - est);
+      s1 += ex2(row[i + S] + x[i + S] - est);
+      s2 += ex2(row[i + 2 * S] + x[i + 2 * S] - est);
+      s3 += ex2(row[i + 3 * S] + x[i + 3 * S] - est);
+    }
+    for (; i < n; i += S) s0 += ex2(row[i] + x[i] - est);
+  }
+  float sum = (s0 + s1) + (s2 + s3);
+#pragma unroll
+  for (int o = 1; o < S; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  return sum;
+}
+
 // One half-sweep over the CTA's nl lanes and its output slice [o0, o1):
 // out[l][o] = target - LSE_k(M[o - o0][k] + x[l][k]), stored locally and into
 // every other CTA of the cluster (peer[r] = the same buffer in CTA r).
 //   kRes 0: plain update; 1: row residual |2^(out + lse) - marg|;
 //   2: column residual against `old` (the check sweep), 3: TAIL (residual
 //   against `old` + the E0 term written to `out`, batch.py:329-337).
-template <int NT, int kRes>
-__device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld, int nout, int o0,
-                                            int o1, int nin, int S, int nl,
-                                            const float* __restrict__ x,
-                                            const float* __restrict__ target,
-                                            const float* __restrict__ marg,
-                                            const float* __restrict__ old, float* out,
-                                            unsigned int* rres, float cinv, float* const* peers,
-                                            const float* local_base, int C, int self) {
+// prev: the previous potential of this orientation (the estimate source; may
+// alias out -- each output is read by its own group before it is written).
+template <int NT, int kRes, int S>
+__device__ __forceinline__ void small_sweep_s(const float* __restrict__ M, int ld, int nout, int o0,
+                                              int o1, int nin, int nl,
+                                              const float* __restrict__ x,
+                                              const float* __restrict__ target,
+                                              const float* __restrict__ marg,
+                                              const float* __restrict__ old, const float* prev,
+                                              float* out, unsigned int* rres, float cinv,
+                                              float* const* peers, const float* local_base, int C,
+                                              int self) {
   const int tid = threadIdx.x;
-  const int gpr = NT / S;   // groups per round
+  constexpr int gpr = NT / S;   // groups per round
   const int s = tid % S;
   const int ns = o1 - o0;
   const int U = nl * ns;
@@ -178,12 +210,29 @@ __device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld,
     const int l = active ? u / ns : 0;
     const int os = active ? u - l * ns : 0;
     const int o = o0 + os;
-    float m, sum, w;
-    small_unit_lse<kRes == 3>(M + (size_t)os * ld, x + (size_t)l * nin, nin, S, s, active, cinv,
-                              m, sum, w);
+    const int idx = l * nout + o;
+    const float* mrow = M + (size_t)os * ld;
+    const float* xl = x + (size_t)l * nin;
+    float m, sum, w = 0.f;
+    bool exact = true;
+    if constexpr (kRes != 3) {
+      const float tg = active ? target[idx] : 0.f;
+      const float est = active ? tg - prev[idx] : 0.f;
+      const bool have = active && est - est == 0.f;   // finite (no NaN / inf)
+      // zero-mass outputs stay -inf whatever the sum: no estimate needed
+      const bool skip = active && tg == neg_inf();
+      const bool any_est = __any_sync(0xffffffffu, have);
+      if (any_est) {
+        m = have ? est : 0.f;
+        sum = small_unit_est<S>(mrow, xl, nin, s, active && have, m);
+        const bool ok = !active || skip || (have && sum >= 0x1p-60f && sum <= 0x1p100f);
+        exact = __any_sync(0xffffffffu, !ok);
+      }
+    }
+    if (exact)
+      small_unit_lse<S, kRes == 3>(mrow, xl, nin, s, active, cinv, m, sum, w);
     if (active && s == 0) {
       const float lse = lse_final(m, sum);
-      const int idx = l * nout + o;
       float r = 0.f, v;
       if (kRes == 3) {
         const float ov = old[idx];
@@ -207,6 +256,36 @@ __device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld,
       }
     }
   }
+}
+
+// The group size S (threads per output, a power of two chosen on the host)
+// as a template argument: unrolled shuffles, shift/mask indexing.
+template <int NT, int kRes>
+__device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld, int nout, int o0,
+                                            int o1, int nin, int S, int nl,
+                                            const float* __restrict__ x,
+                                            const float* __restrict__ target,
+                                            const float* __restrict__ marg,
+                                            const float* __restrict__ old, const float* prev,
+                                            float* out, unsigned int* rres, float cinv,
+                                            float* const* peers, const float* local_base, int C,
+                                            int self) {
+#define SKB_SMALL_CASE(SS)                                                                      \
+  case SS:                                                                                      \
+    small_sweep_s<NT, kRes, SS>(M, ld, nout, o0, o1, nin, nl, x, target, marg, old, prev, out,  \
+                                rres, cinv, peers, local_base, C, self);                        \
+    break;
+  switch (S) {
+    SKB_SMALL_CASE(1)
+    SKB_SMALL_CASE(2)
+    SKB_SMALL_CASE(4)
+    SKB_SMALL_CASE(8)
+    SKB_SMALL_CASE(16)
+    default:
+      small_sweep_s<NT, kRes, 32>(M, ld, nout, o0, o1, nin, nl, x, target, marg, old, prev, out,
+                                  rres, cinv, peers, local_base, C, self);
+  }
+#undef SKB_SMALL_CASE
 }
 
 // End of a half-sweep: every CTA of the cluster has stored its slice everywhere.
@@ -271,6 +350,8 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
     const size_t gj = (size_t)(b0 + l) * p.sb2 + (size_t)j * p.si2;
     sm.lnu[e] = p.l2nu[gj];
     sm.nu[e] = p.nu[gj];
+    sm.g0[e] = neg_inf();   // log v0 (batch.py:296): no estimate for the first column sweep
+    sm.g1[e] = neg_inf();
   }
   small_sync(C);   // also publishes s_peer; every CTA of the cluster is running
   float* const* peers = s_peer;
@@ -285,7 +366,8 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
   for (int k = 1; k <= p.max_iters; ++k) {
     if (!have_next) {
       small_sweep<NT, 0>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, sm.lnu, nullptr,
-                         nullptr, sm.g(cur ^ 1), nullptr, 0.f, peers, small_smem, C, crank);
+                         nullptr, sm.g(cur), sm.g(cur ^ 1), nullptr, 0.f, peers, small_smem, C,
+                         crank);
       if (tl && k <= 8) p.dbg[4 * k] = globaltimer_ns();
       small_sync(C);
       if (tl && k <= 8) p.dbg[4 * k + 1] = globaltimer_ns();
@@ -298,10 +380,10 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
       for (int l = tid; l < nl; l += NT) sm.rres[l] = 0u;
       __syncthreads();
       small_sweep<NT, 1>(sm.A, p.ldr, p.d1, i0, i1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, sm.mu,
-                         nullptr, sm.f, sm.rres, 0.f, peers, small_smem, C, crank);
+                         nullptr, sm.f, sm.f, sm.rres, 0.f, peers, small_smem, C, crank);
     } else {
       small_sweep<NT, 0>(sm.A, p.ldr, p.d1, i0, i1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, nullptr,
-                         nullptr, sm.f, nullptr, 0.f, peers, small_smem, C, crank);
+                         nullptr, sm.f, sm.f, nullptr, 0.f, peers, small_smem, C, crank);
     }
     if (tl && k <= 8) p.dbg[4 * k + 2] = globaltimer_ns();
     small_sync(C);
@@ -310,7 +392,8 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
     if (check) {
       // column sweep k+1 doubles as the column residual of iteration k
       small_sweep<NT, 2>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, sm.lnu, sm.nu,
-                         sm.g(cur), sm.g(cur ^ 1), sm.rres, 0.f, peers, small_smem, C, crank);
+                         sm.g(cur), sm.g(cur), sm.g(cur ^ 1), sm.rres, 0.f, peers, small_smem, C,
+                         crank);
       small_sync(C);
       // every CTA publishes the max over its lanes and slices; all CTAs read
       // all of them behind a grid barrier and take the same decision
@@ -342,7 +425,7 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
   // ---- tail: column residual + E0 terms, then export (batch.py:323-337) -----
   float* e0t = sm.g(cur ^ 1);
   small_sweep<NT, 3>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, nullptr, sm.nu, sm.g(cur),
-                     e0t, sm.rres, p.cinv, peers, small_smem, C, crank);
+                     nullptr, e0t, sm.rres, p.cinv, peers, small_smem, C, crank);
   small_sync(C);
   // the lane residual is the max over the cluster's slices (peer reads)
   if (C > 1 && crank == 0) {
