@@ -1250,17 +1250,30 @@ struct Solve {
       if ((long long)Lc * d1 * d2 > kSmallMaxCells) continue;
       const int Gl = (int)((B + Lc - 1) / Lc);   // lane groups
       // spread a lane group over a cluster while SMs are left idle and every
-      // CTA keeps >= 16 outputs per half-sweep
+      // CTA keeps >= 16 outputs and >= 16k cells per half-sweep: a cluster
+      // barrier costs ~0.5 us per half-sweep, and below that size the sweep is
+      // bound by its serial chain, not its cell count (config 1, d = 100:
+      // C = 1 0.317 ms per loop, C = 4 0.328)
       int Cc = 1;
-      while (Cc < 8 && (long long)Gl * Cc * 2 <= di.sms && std::min(d1, d2) / (Cc * 2) >= 16)
+      while (Cc < 8 && (long long)Gl * Cc * 2 <= di.sms && std::min(d1, d2) / (Cc * 2) >= 16 &&
+             (long long)Lc * d1 * d2 / (Cc * 2) >= 16384)
         Cc *= 2;
       static const int force_c = getenv("SKB_SMALL_C") ? atoi(getenv("SKB_SMALL_C")) : 0;
       if (force_c > 0) Cc = force_c;   // diagnostics: cluster size A/B
-      const long long units_c = (long long)Lc * ((d2 + Cc - 1) / Cc);
-      const long long units_r = (long long)Lc * ((d1 + Cc - 1) / Cc);
-      const int Sc = pick_group(units_c, d1), Sr = pick_group(units_r, d2);
-      const int ldc = (int)round_up(d1, 32) + (Sc % 32), ldr = (int)round_up(d2, 32) + (Sr % 32);
-      const size_t bytes = SmallSmem::floats((int)d1, (int)d2, Lc, ldc, ldr, Cc) * 4;
+      int Sc = 1, Sr = 1, ldc = 0, ldr = 0;
+      size_t bytes = 0;
+      for (;; Cc *= 2) {   // a larger cluster when the cost slices do not fit one CTA
+        const long long units_c = (long long)Lc * ((d2 + Cc - 1) / Cc);
+        const long long units_r = (long long)Lc * ((d1 + Cc - 1) / Cc);
+        Sc = pick_group(units_c, d1);
+        Sr = pick_group(units_r, d2);
+        ldc = (int)round_up(d1, 32) + (Sc % 32);
+        ldr = (int)round_up(d2, 32) + (Sr % 32);
+        bytes = SmallSmem::floats((int)d1, (int)d2, Lc, ldc, ldr, Cc) * 4;
+        if (bytes <= (size_t)smem_optin / occ - 2048 || force_c > 0 || Cc >= 8 ||
+            (long long)Gl * Cc * 2 > di.sms || std::min(d1, d2) / (Cc * 2) < 16)
+          break;
+      }
       if (bytes > (size_t)smem_optin / occ - 2048) continue;
       int fit = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, kSmallNT, bytes));

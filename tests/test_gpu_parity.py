@@ -574,3 +574,29 @@ def test_gemm_path_ragged_tiles_match_tiled(B, d1, d2, cuda):
     tm, tn = skb.potentials_backward(tiled.log_u, tiled.log_v, 0.05, torch.ones(B, device=cuda))
     assert float((gm - tm).abs().max()) <= GRAD_ATOL
     assert float((gn - tn).abs().max()) <= GRAD_ATOL
+
+
+@pytest.mark.parametrize("B,d1,d2", [(8, 256, 256), (4, 300, 210), (6, 181, 333)])
+def test_small_solver_clusters_match_tiled(B, d1, d2, cuda):
+    """Problems large enough for the single-launch solver to spread each lane
+    over a thread-block cluster (slices exchanged through distributed shared
+    memory, ragged slices when C does not divide d): equal to the tiled
+    half-sweeps, including a lockstep tolerance stop."""
+    skb = _skb()
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(d1 + d2)
+
+    def hist(d):
+        m = torch.rand(B, d, generator=gen, device=cuda, dtype=torch.float64) + 0.5
+        return (m / m.sum(1, keepdim=True)).float()
+    mu, nu = hist(d1), hist(d2)
+    c = torch.rand(d1, d2, generator=gen, device=cuda)
+    for iters, tol in ((60, 0.0), (400, 1e-5)):
+        res = skb.solve(mu, nu, c, 0.05, iters, tol)
+        assert res.path == "small"
+        ref = skb.solve(mu, nu, c, 0.05, iters, tol, tiled_only=True, fused=False, gemm=False)
+        assert res.iterations_run == ref.iterations_run
+        rel = ((res.cost_e0.double() - ref.cost_e0.double()).abs() / ref.cost_e0.double()).max()
+        assert float(rel) <= 2e-6
+        assert float((res.log_u - ref.log_u).abs().max()) <= 1e-4
+        assert float((res.log_v - ref.log_v).abs().max()) <= 1e-4
