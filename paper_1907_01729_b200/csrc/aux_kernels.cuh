@@ -395,4 +395,34 @@ __global__ void __launch_bounds__(256) plan_grad_per_sample_kernel(
   dc[o] = up[b] * exp2f(t);
 }
 
+// The same, HBM-bound at config-4 size (4.3 GB read + 4.3 GB written): a warp
+// per (lane, row) -- grid-stride over the B * d1 rows -- streams the row as
+// float4 (d2 % 4 == 0, 16-byte aligned cost and output), evict-first.
+__global__ void __launch_bounds__(256) plan_grad_per_sample_vec4_kernel(
+    const float* __restrict__ log_u, const float* __restrict__ log_v,
+    const float* __restrict__ c, const float* __restrict__ up, int B, int d1, int d2, float k,
+    float* __restrict__ dc) {
+  const int lane = threadIdx.x & 31;
+  const long long rows = (long long)B * d1;
+  const int q4 = d2 / 4;
+  for (long long r = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); r < rows;
+       r += (long long)gridDim.x * 8) {
+    const int b = (int)(r / d1);
+    const float lu = log_u[r] * kLog2e, ub = up[b];
+    const float4* cr = reinterpret_cast<const float4*>(c + r * d2);
+    float4* dr = reinterpret_cast<float4*>(dc + r * d2);
+    const float4* lv = reinterpret_cast<const float4*>(log_v + (size_t)b * d2);
+    for (int j = lane; j < q4; j += 32) {
+      const float4 cv = __ldcs(cr + j);
+      const float4 v = __ldg(lv + j);
+      float4 o;
+      o.x = ub * exp2f(fmaf(v.x, kLog2e, lu) + cv.x * k);
+      o.y = ub * exp2f(fmaf(v.y, kLog2e, lu) + cv.y * k);
+      o.z = ub * exp2f(fmaf(v.z, kLog2e, lu) + cv.z * k);
+      o.w = ub * exp2f(fmaf(v.w, kLog2e, lu) + cv.w * k);
+      __stcs(dr + j, o);
+    }
+  }
+}
+
 }  // namespace skb

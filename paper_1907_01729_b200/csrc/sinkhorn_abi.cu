@@ -2729,8 +2729,24 @@ int32_t sinkhorn_plan_grad_device_v1(const sinkhorn_problem_v1* prob, double lam
     if (prob->B == 0) return 0;
     g.z = (unsigned)prob->B;
     ++g_launches;
-    plan_grad_per_sample_kernel<<<g, 256, 0, st>>>(log_u, log_v, cost, upstream, (int)prob->d1,
-                                                    (int)prob->d2, k, out_grad_cost);
+    const bool vec = prob->d2 % 4 == 0 && (reinterpret_cast<uintptr_t>(cost) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(out_grad_cost) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(log_v) & 15) == 0;
+    if (vec) {
+      int dev = 0;
+      CK(cudaGetDevice(&dev));
+      int sms = 148;
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const long long rows = prob->B * prob->d1;
+      const int grid = (int)std::min<long long>((rows + 7) / 8, (long long)sms * 8);
+      plan_grad_per_sample_vec4_kernel<<<grid, 256, 0, st>>>(log_u, log_v, cost, upstream,
+                                                              (int)prob->B, (int)prob->d1,
+                                                              (int)prob->d2, k, out_grad_cost);
+    } else {
+      plan_grad_per_sample_kernel<<<g, 256, 0, st>>>(log_u, log_v, cost, upstream,
+                                                      (int)prob->d1, (int)prob->d2, k,
+                                                      out_grad_cost);
+    }
   }
   CK(cudaGetLastError());
   return 0;
