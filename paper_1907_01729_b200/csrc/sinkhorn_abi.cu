@@ -1106,8 +1106,31 @@ struct Solve {
     return p;
   }
 
+  bool validate_cost_in_sweep = false;   // per-sample: the first column sweep checks the cost
+
   int lane_col(int mode, float* out, const float* old, int res_kind) {
     LaneSweepParams p = lane_params();
+    const bool validate = validate_cost_in_sweep && mode == kModeUpdate;
+    if (validate) {
+      validate_cost_in_sweep = false;
+      p.vstatus = at<int>(ws, L.status);
+      dim3 grid((unsigned)L.lane_nsplit, (unsigned)pr.B, (unsigned)L.lane_nj);
+      p.x = F(L.f2);
+      p.ldx = L.D1p;
+      p.ldo = L.D2p;
+      p.target = F(L.l2nu);
+      p.marg = F(L.nu);
+      p.out = out;
+      p.old = old;
+      p.res = F(L.res);
+      p.res_kind = res_kind;
+      p.e0 = F(L.e0);
+      if (L.lane_vec == 4)
+        CK(launch_pdl(&lane_col_kernel<4, kModeUpdate, true>, grid, dim3(256), 0, st, p));
+      else
+        CK(launch_pdl(&lane_col_kernel<1, kModeUpdate, true>, grid, dim3(256), 0, st, p));
+      return 0;
+    }
     p.x = F(L.f2);
     p.ldx = L.D1p;
     p.ldo = L.D2p;
@@ -1628,10 +1651,9 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
       CK(cudaGetLastError());
     }
   } else if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE && !(op.flags & SINKHORN_FLAG_SKIP_VALIDATION)) {
-    const size_t n = (size_t)pr.B * pr.d1 * pr.d2;
-    ++g_launches;
-    validate_cost_kernel<<<grid_for(n), 256, 0, st>>>(cost, n, status);
-    CK(cudaGetLastError());
+    // checked by the first column sweep, which reads every element once anyway
+    // (lane_col_kernel<..., kValidate>): no separate pass over the 4.3 GB
+    S.validate_cost_in_sweep = true;
   }
   if (L.sep) {   // the separable sweeps' factor tables (once per solve), log u transposed
     const int nblk = (int)((pr.grid_nx + 31) / 32);

@@ -37,6 +37,7 @@ struct LaneSweepParams {
   int nsplit;
   int res_kind;
   const int* status;     // abort early if an earlier stage failed validation
+  int* vstatus;          // kValidate: the cost check rides on this sweep (status 15)
 };
 
 // Streaming (evict-first, ld.global.cs) loads: each cost element is used once per sweep.
@@ -78,7 +79,11 @@ __device__ __forceinline__ void lane_consume(const float (&t)[KC], const float (
 // ---------------------------------------------------------------------------
 // column sweep: out[b, j] = target - log2 sum_i 2^(C_b[i,j]*k + x[b,i])
 // grid (nsplit, B, nj); block 256; thread owns VEC consecutive columns.
-template <int VEC, int kMode>
+// kValidate (the solve's first sweep): every cost element is read exactly
+// once here, so the CostMatrix check (finite, >= 0; core.py:53-63) is done on
+// the same loads instead of a separate 4.3 GB pass at config 4; status 15
+// stops every later kernel of the solve.
+template <int VEC, int kMode, bool kValidate = false>
 __global__ void __launch_bounds__(256) lane_col_kernel(const LaneSweepParams p) {
   constexpr int NT = 256;
   constexpr int KC = 8;
@@ -106,6 +111,10 @@ __global__ void __launch_bounds__(256) lane_col_kernel(const LaneSweepParams p) 
   float m[VEC], s[VEC], s2[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) { m[v] = kNegBig; s[v] = 0.f; s2[v] = 0.f; }
+  bool good = true;   // kValidate
+  auto check = [&](float c) {
+    if constexpr (kValidate) good &= (c >= 0.f) & (c != __int_as_float(0x7f800000));
+  };
 
   for (int ic = i_begin; ic < i_end; ic += XCH) {
     const int n = min(XCH, i_end - ic);
@@ -130,7 +139,10 @@ __global__ void __launch_bounds__(256) lane_col_kernel(const LaneSweepParams p) 
       for (int v = 0; v < VEC; ++v) {
         float t[KC];
 #pragma unroll
-        for (int k = 0; k < KC; ++k) t[k] = fmaf(cv[v][k], p.kscale, sx[i + k]);
+        for (int k = 0; k < KC; ++k) {
+          check(cv[v][k]);
+          t[k] = fmaf(cv[v][k], p.kscale, sx[i + k]);
+        }
         lane_consume<KC, kTail>(t, cv[v], m[v], s[v], s2[v]);
       }
     }
@@ -140,11 +152,14 @@ __global__ void __launch_bounds__(256) lane_col_kernel(const LaneSweepParams p) 
       for (int v = 0; v < VEC; ++v) {
         float t[1] = {fmaf(row[v], p.kscale, sx[i])};
         float cv1[1] = {row[v]};
+        check(row[v]);
         lane_consume<1, kTail>(t, cv1, m[v], s[v], s2[v]);
       }
     }
   }
 
+  if constexpr (kValidate)
+    if (__any_sync(0xffffffffu, !good) && (tid & 31) == 0) set_status(p.vstatus, 15);
   auto finish = [&]() {
     float rmax = 0.f;
     if (colok) {
