@@ -1631,11 +1631,18 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     CK(cudaGetLastError());
   }
   if (L.gemm) {
-    dim3 g((unsigned)(L.ldk2 / 32), (unsigned)(L.ldk1 / 32));
     ++g_launches;
-    umma_kernel_matrices<<<g, 256, 0, st>>>(cost, (int)pr.d1, (int)pr.d2,
-                                            (float)(-kLog2e / op.lambda), S.F(L.kmat),
-                                            S.F(L.kc), S.F(L.kmatT), status);
+    if (pr.d2 % 4 == 0 && (reinterpret_cast<uintptr_t>(cost) & 15) == 0) {
+      dim3 g((unsigned)(L.ldk2 / 128), (unsigned)(L.ldk1 / 32));
+      umma_kernel_matrices_vec4<<<g, 256, 0, st>>>(cost, (int)pr.d1, (int)pr.d2,
+                                                   (float)(-kLog2e / op.lambda), S.F(L.kmat),
+                                                   S.F(L.kc), S.F(L.kmatT), status);
+    } else {
+      dim3 g((unsigned)(L.ldk2 / 32), (unsigned)(L.ldk1 / 32));
+      umma_kernel_matrices<<<g, 256, 0, st>>>(cost, (int)pr.d1, (int)pr.d2,
+                                              (float)(-kLog2e / op.lambda), S.F(L.kmat),
+                                              S.F(L.kc), S.F(L.kmatT), status);
+    }
     CK(cudaGetLastError());
   } else if (pr.cost_kind == SINKHORN_COST_SHARED) {
     dim3 g((unsigned)((L.D2p + 31) / 32), (unsigned)((L.D1p + 31) / 32));
