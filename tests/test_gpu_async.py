@@ -168,3 +168,41 @@ def test_async_needs_tolerance_zero(cuda):
     mu, nu, c = _problem("shared", 100, 4, 16, cuda)
     with pytest.raises(skb.InvalidConfig):
         skb.solve(mu, nu, c, 0.05, 50, 1e-6, asynchronous=True)
+
+
+def test_host_threads_solve_concurrently(cuda):
+    """the calls are reentrant and thread-safe for disjoint
+    buffers.  Four host threads (ctypes drops the GIL inside the library), each
+    on its own stream and solver path, repeatedly; every result equals the same
+    solve run alone."""
+    import threading
+
+    skb = _skb()
+    jobs = [_problem("per_sample", 256, 24, 41, cuda) + ({},),
+            _problem("shared", 400, 24, 42, cuda) + ({"tiled_only": True},),
+            _problem("grid", 256, 24, 43, cuda) + ({},),
+            _problem("shared", 100, 24, 44, cuda) + ({},)]
+    want = [skb.solve(m, n, c, 0.05, 40, 0.0, **kw) for m, n, c, kw in jobs]
+    torch.cuda.synchronize()
+    errors, got = [], [None] * len(jobs)
+
+    def work(k):
+        try:
+            m, n, c, kw = jobs[k]
+            s = torch.cuda.Stream(cuda)
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    got[k] = skb.solve(m, n, c, 0.05, 40, 0.0, **kw)
+            s.synchronize()
+        except Exception as e:   # noqa: BLE001 -- reported below
+            errors.append((k, repr(e)))
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(len(jobs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for r, w in zip(got, want):
+        assert r.path == w.path
+        _same(r.cost_e0, w.cost_e0, 1e-6 * float(w.cost_e0.abs().max()))
+        _same(r.log_u, w.log_u, 1e-5)
