@@ -1,0 +1,81 @@
+"""Odd shapes on every solver path against the float64 oracle.
+
+Degenerate and ragged extents (1, 7, 129, 1023, 1025, 2049 -- not multiples
+of the tiles, vectors, chunks or lane groups the kernels use), B above one
+64-lane tensor-core tile, one-row and one-column problems.  A ragged-extent
+fault in the tiled sweeps went unnoticed through round 1; this sweep is the
+guard.  Tolerances are the north star's (conftest.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import GRAD_ATOL, LOSS_RTOL
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+SHAPES = [(1, 1, 1), (1, 1, 7), (3, 7, 1), (2, 5, 129), (5, 129, 5), (1, 1025, 3), (4, 63, 65),
+          (2, 257, 1023), (3, 1030, 70), (65, 33, 31), (2, 2049, 17)]
+SHARED_PATHS = {"auto": {}, "tiled": {"tiled_only": True, "fused": False, "gemm": False},
+                "fused": {"tiled_only": True}, "gemm": {"tiled_only": True, "gemm": True}}
+PER_SAMPLE_PATHS = {"auto": {}, "lane": {"fused": False}}
+
+
+def _inputs(B, d1, d2, seed, per_sample):
+    from oracle import sinkhorn_oracle as orc
+
+    rng = np.random.default_rng(seed)
+    mu = orc.fp32_exact(orc.random_histogram_batch(B, d1, rng))
+    nu = orc.fp32_exact(orc.random_histogram_batch(B, d2, rng))
+    shape = (B, d1, d2) if per_sample else (d1, d2)
+    c = orc.fp32_exact(rng.random(shape))
+    return mu, nu, c
+
+
+def _check(res, ref, lam, cuda):
+    import paper_1907_01729_b200 as skb
+
+    got = res.cost_e0.double().cpu().numpy()
+    rel = np.abs(got - ref.cost_e0) / np.abs(ref.cost_e0)
+    assert rel.max() <= LOSS_RTOL, (rel.max(), res.path)
+    B = got.shape[0]
+    gm, gn = skb.potentials_backward(res.log_u, res.log_v, lam, torch.ones(B, device=cuda))
+    from oracle import sinkhorn_oracle as orc
+
+    gm_ref, gn_ref = orc.batch_backward(ref.log_u, ref.log_v, lam, np.ones(B))
+    assert np.abs(gm.double().cpu().numpy() - gm_ref).max() <= GRAD_ATOL, res.path
+    assert np.abs(gn.double().cpu().numpy() - gn_ref).max() <= GRAD_ATOL, res.path
+
+
+@pytest.mark.parametrize("B,d1,d2", SHAPES)
+def test_shared_cost_shapes(B, d1, d2, cuda):
+    import paper_1907_01729_b200 as skb
+    from oracle import sinkhorn_oracle as orc
+
+    lam, iters = 0.1, 20
+    mu, nu, c = _inputs(B, d1, d2, d1 * 7 + d2, per_sample=False)
+    ref = orc.batch_forward(mu, nu, c, lam, iters, 0.0, workers=4)
+    t = lambda a: torch.tensor(a, dtype=torch.float32, device=cuda)   # noqa: E731
+    for name, kw in SHARED_PATHS.items():
+        res = skb.solve(t(mu), t(nu), t(c), lam, iters, 0.0, **kw)
+        assert res.iterations_run == iters, name
+        _check(res, ref, lam, cuda)
+
+
+@pytest.mark.parametrize("B,d1,d2", SHAPES)
+def test_per_sample_cost_shapes(B, d1, d2, cuda):
+    import paper_1907_01729_b200 as skb
+    from oracle import sinkhorn_oracle as orc
+
+    lam, iters = 0.1, 20
+    mu, nu, c = _inputs(B, d1, d2, d1 * 5 + d2, per_sample=True)
+    ref = orc.per_sample_forward(mu, nu, c, lam, iters, 0.0)
+    t = lambda a: torch.tensor(a, dtype=torch.float32, device=cuda)   # noqa: E731
+    for name, kw in PER_SAMPLE_PATHS.items():
+        res = skb.solve(t(mu), t(nu), t(c), lam, iters, 0.0, **kw)
+        assert res.iterations_run == iters, name
+        _check(res, ref, lam, cuda)
