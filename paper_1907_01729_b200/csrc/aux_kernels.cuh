@@ -384,15 +384,16 @@ __global__ void __launch_bounds__(256) plan_grad_shared_kernel(
 
 __global__ void __launch_bounds__(256) plan_grad_per_sample_kernel(
     const float* __restrict__ log_u, const float* __restrict__ log_v,
-    const float* __restrict__ c, const float* __restrict__ up, int d1, int d2, float k,
+    const float* __restrict__ c, const float* __restrict__ up, int B, int d1, int d2, float k,
     float* __restrict__ dc) {
-  const int b = blockIdx.z;
   const int j = blockIdx.x * 32 + (threadIdx.x & 31);
   const int i = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (i >= d1 || j >= d2) return;
-  const size_t o = ((size_t)b * d1 + i) * d2 + j;
-  const float t = (log_u[(size_t)b * d1 + i] + log_v[(size_t)b * d2 + j]) * kLog2e + c[o] * k;
-  dc[o] = up[b] * exp2f(t);
+  for (int b = blockIdx.z; b < B; b += gridDim.z) {   // gridDim.z <= 65535 lanes at a time
+    const size_t o = ((size_t)b * d1 + i) * d2 + j;
+    const float t = (log_u[(size_t)b * d1 + i] + log_v[(size_t)b * d2 + j]) * kLog2e + c[o] * k;
+    dc[o] = up[b] * exp2f(t);
+  }
 }
 
 // The same, HBM-bound at config-4 size (4.3 GB read + 4.3 GB written): a warp

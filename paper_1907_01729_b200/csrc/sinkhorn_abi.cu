@@ -197,6 +197,12 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
 }
 
 int grid_for(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 16); }
+// Kernels with one grid row per lane (grid.y = lane) launch at most this many
+// lanes at a time (the grid.y limit), with the first lane in their params.
+constexpr long long kMaxLanesPerLaunch = 65535;
+unsigned lanes_in_launch(long long B, long long b0) {
+  return (unsigned)std::min<long long>(kMaxLanesPerLaunch, B - b0);
+}
 
 // ---- workspace layout --------------------------------------------------------
 struct Carver {
@@ -715,7 +721,11 @@ struct Solve {
       p.dbg = tl_buf;
     }
     kt_mark(st);
-    CK(launch_pdl(kern, grid, dim3(SepS::NT), smem, st, p));
+    for (long long b0 = 0; b0 < pr.B; b0 += kMaxLanesPerLaunch) {
+      p.b0 = (int)b0;
+      grid.y = lanes_in_launch(pr.B, b0);
+      CK(launch_pdl(kern, grid, dim3(SepS::NT), smem, st, p));
+    }
     kt_mark(st);
     if (tl) {
       std::vector<unsigned long long> h(8 * 4096);
@@ -771,11 +781,14 @@ struct Solve {
     p.res = F(L.res);
     p.res_kind = res_kind;
     const int rows = 32;
-    dim3 grid((unsigned)((pr.d1 + rows - 1) / rows), (unsigned)pr.B);
-    if (L.lane_vec == 4)
-      CK(launch_pdl(&lane_row_kernel<4>, grid, dim3(256), 0, st, p, rows));
-    else
-      CK(launch_pdl(&lane_row_kernel<1>, grid, dim3(256), 0, st, p, rows));
+    for (long long b0 = 0; b0 < pr.B; b0 += kMaxLanesPerLaunch) {
+      p.b0 = (int)b0;
+      dim3 grid((unsigned)((pr.d1 + rows - 1) / rows), lanes_in_launch(pr.B, b0));
+      if (L.lane_vec == 4)
+        CK(launch_pdl(&lane_row_kernel<4>, grid, dim3(256), 0, st, p, rows));
+      else
+        CK(launch_pdl(&lane_row_kernel<1>, grid, dim3(256), 0, st, p, rows));
+    }
     return 0;
   }
 
@@ -945,9 +958,12 @@ struct Solve {
     mp.marg = F(L.nu);
     mp.res = res ? F(L.res) : nullptr;
     mp.est_fail = est_fail;
-    ++g_launches;
-    CK(launch_pdl(&fused_merge_kernel, dim3((unsigned)((L.D2p + 511) / 512), (unsigned)pr.B),
-                  dim3(256), 0, st, mp));
+    for (long long b0 = 0; b0 < pr.B; b0 += kMaxLanesPerLaunch) {
+      mp.b0 = (int)b0;
+      CK(launch_pdl(&fused_merge_kernel,
+                    dim3((unsigned)((L.D2p + 511) / 512), lanes_in_launch(pr.B, b0)), dim3(256), 0,
+                    st, mp));
+    }
     return 0;
   }
 
@@ -1022,7 +1038,12 @@ struct Solve {
     cp.est_fail = est_fail;
     cp.status = at<int>(ws, L.status);
     ++g_launches;
-    gemm_col_kernel<<<lane_grid(pr.d2), 256, 0, st>>>(cp);
+    for (long long b0 = 0; b0 < pr.B; b0 += kMaxLanesPerLaunch) {
+      cp.b0 = (int)b0;
+      dim3 g = lane_grid(pr.d2);
+      g.y = lanes_in_launch(pr.B, b0);
+      gemm_col_kernel<<<g, 256, 0, st>>>(cp);
+    }
     CK(cudaGetLastError());
     return 0;
   }
@@ -1062,7 +1083,12 @@ struct Solve {
     rp.res = res ? F(L.res) : nullptr;
     rp.status = at<int>(ws, L.status);
     ++g_launches;
-    gemm_row_kernel<<<lane_grid(pr.d1), 256, 0, st>>>(rp);
+    for (long long b0 = 0; b0 < pr.B; b0 += kMaxLanesPerLaunch) {
+      rp.b0 = (int)b0;
+      dim3 g = lane_grid(pr.d1);
+      g.y = lanes_in_launch(pr.B, b0);
+      gemm_row_kernel<<<g, 256, 0, st>>>(rp);
+    }
     ++g_launches;
     gemm_row_fallback_kernel<<<(unsigned)di.sms, 256, 0, st>>>(rp, cost, F(L.g2[cur]),
                                                                 -kLog2e / lam);
@@ -1125,10 +1151,14 @@ struct Solve {
       p.res = F(L.res);
       p.res_kind = res_kind;
       p.e0 = F(L.e0);
-      if (L.lane_vec == 4)
-        CK(launch_pdl(&lane_col_kernel<4, kModeUpdate, true>, grid, dim3(256), 0, st, p));
-      else
-        CK(launch_pdl(&lane_col_kernel<1, kModeUpdate, true>, grid, dim3(256), 0, st, p));
+      for (long long b0 = 0; b0 < pr.B; b0 += kMaxLanesPerLaunch) {
+        p.b0 = (int)b0;
+        grid.y = lanes_in_launch(pr.B, b0);
+        if (L.lane_vec == 4)
+          CK(launch_pdl(&lane_col_kernel<4, kModeUpdate, true>, grid, dim3(256), 0, st, p));
+        else
+          CK(launch_pdl(&lane_col_kernel<1, kModeUpdate, true>, grid, dim3(256), 0, st, p));
+      }
       return 0;
     }
     p.x = F(L.f2);
@@ -1142,12 +1172,16 @@ struct Solve {
     p.res_kind = res_kind;
     p.e0 = F(L.e0);
     dim3 grid((unsigned)L.lane_nsplit, (unsigned)pr.B, (unsigned)L.lane_nj);
-    if (mode == kModeTail) {
-      if (L.lane_vec == 4) CK(launch_pdl(&lane_col_kernel<4, kModeTail>, grid, dim3(256), 0, st, p));
-      else CK(launch_pdl(&lane_col_kernel<1, kModeTail>, grid, dim3(256), 0, st, p));
-    } else {
-      if (L.lane_vec == 4) CK(launch_pdl(&lane_col_kernel<4, kModeUpdate>, grid, dim3(256), 0, st, p));
-      else CK(launch_pdl(&lane_col_kernel<1, kModeUpdate>, grid, dim3(256), 0, st, p));
+    for (long long b0 = 0; b0 < pr.B; b0 += kMaxLanesPerLaunch) {
+      p.b0 = (int)b0;
+      grid.y = lanes_in_launch(pr.B, b0);
+      if (mode == kModeTail) {
+        if (L.lane_vec == 4) CK(launch_pdl(&lane_col_kernel<4, kModeTail>, grid, dim3(256), 0, st, p));
+        else CK(launch_pdl(&lane_col_kernel<1, kModeTail>, grid, dim3(256), 0, st, p));
+      } else {
+        if (L.lane_vec == 4) CK(launch_pdl(&lane_col_kernel<4, kModeUpdate>, grid, dim3(256), 0, st, p));
+        else CK(launch_pdl(&lane_col_kernel<1, kModeUpdate>, grid, dim3(256), 0, st, p));
+      }
     }
     return 0;
   }
@@ -2443,7 +2477,8 @@ int forward_f64_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& o
   f64_prep_kernel<<<grid_for((size_t)B * (d1 + d2)), 256, 0, st>>>(mu, nu, B, d1, d2, D(L.lmu),
                                                                     D(L.lnu), D(L.u), D(L.v));
   {
-    dim3 g((unsigned)((d2 + 31) / 32), (unsigned)((d1 + 31) / 32), per_sample ? (unsigned)B : 1u);
+    dim3 g((unsigned)((d2 + 31) / 32), (unsigned)((d1 + 31) / 32),
+           per_sample ? lanes_in_launch(B, 0) : 1u);   // the kernel strides over the rest
     ++g_launches;
     f64_cost_kernel<<<g, 256, 0, st>>>(pr.cost_kind == SINKHORN_COST_GRID2D ? nullptr : cost,
                                        per_sample ? B : 1, d1, d2, op.lambda, (int)pr.grid_nx,
@@ -2466,12 +2501,15 @@ int forward_f64_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& o
     p.marg = marg;
     p.lam = op.lambda;
     p.status = status;
-    dim3 g((unsigned)((p.P + 7) / 8), (unsigned)B);
-    ++g_launches;
-    if (mode == kF64Update) f64_sweep_kernel<kF64Update><<<g, 256, 0, st>>>(p);
-    else if (mode == kF64Residual) f64_sweep_kernel<kF64Residual><<<g, 256, 0, st>>>(p);
-    else f64_sweep_kernel<kF64E0><<<g, 256, 0, st>>>(p);
-    CK(cudaGetLastError());
+    for (long long b0 = 0; b0 < B; b0 += kMaxLanesPerLaunch) {
+      p.b0 = (int)b0;
+      dim3 g((unsigned)((p.P + 7) / 8), lanes_in_launch(B, b0));
+      ++g_launches;
+      if (mode == kF64Update) f64_sweep_kernel<kF64Update><<<g, 256, 0, st>>>(p);
+      else if (mode == kF64Residual) f64_sweep_kernel<kF64Residual><<<g, 256, 0, st>>>(p);
+      else f64_sweep_kernel<kF64E0><<<g, 256, 0, st>>>(p);
+      CK(cudaGetLastError());
+    }
     return 0;
   };
   // lane_residuals (batch.py:303-309): row term with A, column term with A^T
@@ -2756,7 +2794,7 @@ int32_t sinkhorn_plan_grad_device_v1(const sinkhorn_problem_v1* prob, double lam
                                                 (int)prob->d1, (int)prob->d2, k, out_grad_cost);
   } else {
     if (prob->B == 0) return 0;
-    g.z = (unsigned)prob->B;
+    g.z = lanes_in_launch(prob->B, 0);   // the kernel strides over the rest
     ++g_launches;
     const bool vec = prob->d2 % 4 == 0 && (reinterpret_cast<uintptr_t>(cost) & 15) == 0 &&
                      (reinterpret_cast<uintptr_t>(out_grad_cost) & 15) == 0 &&
@@ -2773,8 +2811,8 @@ int32_t sinkhorn_plan_grad_device_v1(const sinkhorn_problem_v1* prob, double lam
                                                               (int)prob->d2, k, out_grad_cost);
     } else {
       plan_grad_per_sample_kernel<<<g, 256, 0, st>>>(log_u, log_v, cost, upstream,
-                                                      (int)prob->d1, (int)prob->d2, k,
-                                                      out_grad_cost);
+                                                      (int)prob->B, (int)prob->d1, (int)prob->d2,
+                                                      k, out_grad_cost);
     }
   }
   CK(cudaGetLastError());

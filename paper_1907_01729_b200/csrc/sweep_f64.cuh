@@ -23,6 +23,7 @@ enum F64Mode : int { kF64Update = 0, kF64Residual = 1, kF64E0 = 2 };
 
 struct F64SweepParams {
   int B, P, Q;
+  int b0;                 // first lane of this launch (grid.y <= 65535 lanes per launch)
   const double* G;        // [P][Q] (shared) or lane b at G + b * P * Q (per-sample)
   long long g_lane;       // 0 for a shared operand, P * Q per-sample
   const double* x;        // [B][Q] reduced-side potentials
@@ -65,7 +66,7 @@ __device__ __forceinline__ double f64_lse(const double* __restrict__ g, const do
 template <int kMode>
 __global__ void __launch_bounds__(256) f64_sweep_kernel(const F64SweepParams p) {
   if (p.status != nullptr && *p.status != 0) return;
-  const int b = blockIdx.y;
+  const int b = p.b0 + blockIdx.y;
   const int o = blockIdx.x * 8 + warp_id();
   if (o >= p.P) return;
   const double* g = p.G + b * p.g_lane + (size_t)o * p.Q;
@@ -154,33 +155,36 @@ __global__ void __launch_bounds__(256) f64_cost_kernel(const double* __restrict_
                                                        double* __restrict__ a,
                                                        double* __restrict__ at, int* status) {
   __shared__ double tile[32][33];
-  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32, l = blockIdx.z;
+  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const size_t base = (size_t)l * d1 * d2;
   bool bad = false;
-  for (int r = ty; r < 32; r += 8) {
-    const int i = i0 + r, j = j0 + tx;
-    double v = 0.0;
-    if (i < d1 && j < d2) {
-      double cv;
-      if (c != nullptr) {
-        cv = c[base + (size_t)i * d2 + j];
-      } else {
-        const double dx = (double)(i % gnx - j % gnx), dy = (double)(i / gnx - j / gnx);
-        cv = ghx2 * dx * dx + ghy2 * dy * dy;
+  for (int l = blockIdx.z; l < lanes; l += gridDim.z) {   // gridDim.z <= 65535 lanes at a time
+    const size_t base = (size_t)l * d1 * d2;
+    for (int r = ty; r < 32; r += 8) {
+      const int i = i0 + r, j = j0 + tx;
+      double v = 0.0;
+      if (i < d1 && j < d2) {
+        double cv;
+        if (c != nullptr) {
+          cv = c[base + (size_t)i * d2 + j];
+        } else {
+          const double dx = (double)(i % gnx - j % gnx), dy = (double)(i / gnx - j / gnx);
+          cv = ghx2 * dx * dx + ghy2 * dy * dy;
+        }
+        if (!(cv >= 0.0) || isinf(cv)) bad = true;
+        v = -cv / lam;
+        a[base + (size_t)i * d2 + j] = v;
       }
-      if (!(cv >= 0.0) || isinf(cv)) bad = true;
-      v = -cv / lam;
-      a[base + (size_t)i * d2 + j] = v;
+      tile[r][tx] = v;
     }
-    tile[r][tx] = v;
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int j = j0 + r, i = i0 + tx;
+      if (j < d2 && i < d1) at[base + (size_t)j * d1 + i] = tile[tx][r];
+    }
+    __syncthreads();
   }
   if (bad) set_status(status, 15);
-  __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int j = j0 + r, i = i0 + tx;
-    if (j < d2 && i < d1) at[base + (size_t)j * d1 + i] = tile[tx][r];
-  }
 }
 
 // NaN anywhere in the potentials -> status 12 (batch.py:326-327).

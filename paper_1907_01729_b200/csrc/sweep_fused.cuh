@@ -90,6 +90,7 @@ struct FusedMergeParams {
   const float* marg;      // [B][rowlen] nu
   float* res;             // [B] column residual, atomic max (nullable)
   int* est_fail;          // set when a column's plan mass is below 2^-60
+  int b0;                 // first lane of this launch (grid.y <= 65535 lanes per launch)
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -1010,7 +1011,7 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
 __global__ void __launch_bounds__(256) fused_merge_kernel(const FusedMergeParams p) {
   __shared__ int s_off[256];  // partial rows of this lane (rowlen units), ascending CTA (nct <= 256)
   __shared__ int s_c0, s_n;
-  const int b = blockIdx.y;
+  const int b = p.b0 + blockIdx.y;
   const int g = b / p.nw, w = b % p.nw;
   if (threadIdx.x == 0) {
     const long long ua = (long long)g * p.nrows, ub = ua + p.nrows - 1;

@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(1024) gemm_scale_kernel(const float* __restric
 
 struct GemmRowParams {
   int B, d1, d2;
+  int b0;                // first lane of this launch (grid.y <= 65535 lanes per launch)
   const float* S;        // [B][d1] K X
   const float* vmax;     // [B]
   const float* l2mu;     // [B][d1]
@@ -68,7 +69,7 @@ struct GemmRowParams {
 // u_i and a_i from the GEMM row sums; grid (x: grid-stride over d1, y: lane b).
 __global__ void gemm_row_kernel(const GemmRowParams p) {
   if (p.status != nullptr && *p.status != 0) return;
-  const int b = blockIdx.y;
+  const int b = p.b0 + blockIdx.y;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.d1; i += gridDim.x * blockDim.x) {
     const size_t k = (size_t)b * p.d1 + i;
     const float S = p.S[k];
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(256) gemm_row_fallback_kernel(const GemmRowPar
 
 struct GemmColParams {
   int B, d2;
+  int b0;                // first lane of this launch (grid.y <= 65535 lanes per launch)
   const float* T;        // [B][d2] K^T a
   const float* vmax;     // [B] shift of the a's (the row pass's vmax, or 0 for the first sweep)
   const float* v_old;    // [B][d2] (residual), nullable on the first sweep
@@ -135,7 +137,7 @@ struct GemmColParams {
 // grid (x: grid-stride over d2, y: lane b).
 __global__ void gemm_col_kernel(const GemmColParams p) {
   if (p.status != nullptr && *p.status != 0) return;
-  const int b = blockIdx.y;
+  const int b = p.b0 + blockIdx.y;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.d2; j += gridDim.x * blockDim.x) {
     const size_t k = (size_t)b * p.d2 + j;
     const float T = p.T[k];

@@ -38,6 +38,7 @@ struct LaneSweepParams {
   int res_kind;
   const int* status;     // abort early if an earlier stage failed validation
   int* vstatus;          // kValidate: the cost check rides on this sweep (status 15)
+  int b0;                // first lane of this launch (grid.y <= 65535 lanes per launch)
 };
 
 // Streaming (evict-first, ld.global.cs) loads: each cost element is used once per sweep.
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(256) lane_col_kernel(const LaneSweepParams p) 
   if (p.status != nullptr && *p.status != 0) return;
 
   const int split = blockIdx.x;
-  const int b = blockIdx.y;
+  const int b = p.b0 + blockIdx.y;
   const int jb = blockIdx.z;
   const int tid = threadIdx.x;
   const int j0 = jb * NT * VEC + tid * VEC;
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(256) lane_row_kernel(const LaneSweepParams p, 
   pdl_wait();
   if (p.status != nullptr && *p.status != 0) return;
 
-  const int b = blockIdx.y;
+  const int b = p.b0 + blockIdx.y;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const float* C = p.cost + (size_t)b * p.d1 * p.d2;

@@ -43,6 +43,7 @@ struct SepParams {
   int B;
   int nblk;                // jx blocks per lane
   int use_poly;            // part of the exponentials on the FMA pipe
+  int b0;                  // first lane of this launch (grid.y <= 65535 lanes per launch)
   const float* est_src;    // previous potential of this orientation (estimate mode) or null
   unsigned int* redo;      // count of thread tiles redone exactly (statistics)
   unsigned long long* dbg; // optional per-CTA timeline (diagnostics), nullable
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(S::NT, 4) sep_sweep_kernel(const SepParams p) 
   float* R = T + (size_t)ny * NB;            // [ny][NB], tail only
   __shared__ unsigned int s_res;
   const int tid = threadIdx.x;
-  const int b = blockIdx.y;
+  const int b = p.b0 + blockIdx.y;
   const int jx0 = blockIdx.x * NB;
 
   if (tid == 0) s_res = 0u;

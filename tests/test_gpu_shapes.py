@@ -79,3 +79,40 @@ def test_per_sample_cost_shapes(B, d1, d2, cuda):
         res = skb.solve(t(mu), t(nu), t(c), lam, iters, 0.0, **kw)
         assert res.iterations_run == iters, name
         _check(res, ref, lam, cuda)
+
+
+BIG_B_PATHS = [pytest.param("shared", {}, id="fused"),
+               pytest.param("shared", {"tiled_only": True, "fused": False, "gemm": False},
+                            id="tiled"),
+               pytest.param("shared", {"tiled_only": True, "gemm": True}, id="gemm"),
+               pytest.param("per_sample", {}, id="per_sample_fused"),
+               pytest.param("per_sample", {"fused": False}, id="per_sample_lane"),
+               pytest.param("grid", {}, id="separable"),
+               pytest.param("shared", {"fp64": True}, id="fp64")]
+
+
+@pytest.mark.parametrize("kind,kw", BIG_B_PATHS)
+def test_batches_above_the_grid_y_limit(kind, kw, cuda):
+    """B = 70000 lanes (> 65535, the grid.y limit of the kernels with one grid
+    row per lane; they launch in lane slices): lanes at both ends and across
+    the slice boundary equal their single-lane solves."""
+    import paper_1907_01729_b200 as skb
+
+    B, d = 70000, 16
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(5)
+    m = torch.rand(B, d, generator=gen, device=cuda, dtype=torch.float64) + 0.5
+    mu = (m / m.sum(1, keepdim=True)).float()
+    nu = mu.flip(0).contiguous()
+    if kind == "shared":
+        c = torch.rand(d, d, generator=gen, device=cuda)
+    elif kind == "per_sample":
+        c = torch.rand(B, d, d, generator=gen, device=cuda)
+    else:
+        c = skb.GridCost(4, 4)
+    res = skb.solve(mu, nu, c, 0.1, 20, 0.0, **kw)
+    for b in (0, 65534, 65535, 65536, B - 1):
+        cb = c[b:b + 1] if kind == "per_sample" else c
+        one = skb.solve(mu[b:b + 1], nu[b:b + 1], cb, 0.1, 20, 0.0, **kw)
+        assert abs(float(one.cost_e0[0]) - float(res.cost_e0[b])) <= 1e-5 * float(one.cost_e0[0])
+        assert float((one.log_u[0] - res.log_u[b]).abs().max()) <= 1e-4
