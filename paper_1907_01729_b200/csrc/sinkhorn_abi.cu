@@ -249,8 +249,21 @@ bool fused_eligible(const sinkhorn_problem_v1& pr) {
          round_up(pr.d1, TILE_PAD) <= 64 * kFusedMaxNQ && round_up(pr.d2, TILE_PAD) <= 64 * kFusedMaxNQ;
 }
 
+#ifndef SKB_SEP_RN
+#define SKB_SEP_RN 2
+#endif
+using SepGridShape = SepShape<32, SKB_SEP_RN, (SKB_SEP_RN == 2) ? 256 : 128>;
+// The separable sweep stages a lane's whole nx x ny potential plus both factor
+// tables in shared memory; larger grids take the dense on-the-fly sweeps.
+constexpr size_t kSepSmemLimit = 227 * 1024;
+bool sep_fits(const sinkhorn_problem_v1& pr) {
+  return sep_smem_floats<SepGridShape>((int)pr.grid_nx, (int)pr.grid_ny, true) * 4 <=
+         kSepSmemLimit;
+}
+
 // Grid costs run the separable sweeps on lane-major buffers unless the dense
-// on-the-fly tiled sweeps are requested (SINKHORN_FLAG_DENSE_GRID).
+// on-the-fly tiled sweeps are requested (SINKHORN_FLAG_DENSE_GRID) or the grid
+// is too large for the separable sweep's shared memory.
 Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = false,
                    bool fused = false, bool gemm = false) {
   Layout L;
@@ -259,6 +272,7 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
   L.d2 = pr.d2;
   L.gemm = gemm && pr.cost_kind == SINKHORN_COST_SHARED;
   L.fused = !L.gemm && fused && fused_eligible(pr);
+  if (pr.cost_kind == SINKHORN_COST_GRID2D && !sep_fits(pr)) dense_grid = true;
   L.sep = pr.cost_kind == SINKHORN_COST_GRID2D && !dense_grid;
   L.tiled = !L.fused && !L.gemm && (pr.cost_kind == SINKHORN_COST_SHARED ||
                                     (pr.cost_kind == SINKHORN_COST_GRID2D && dense_grid));
@@ -677,10 +691,7 @@ struct Solve {
 
   // column half-sweep: g2[dst] = l2nu - LSE_i(A2 + f2)
   // ---- separable grid sweeps (sweep_sep.cuh) --------------------------------
-#ifndef SKB_SEP_RN
-#define SKB_SEP_RN 2
-#endif
-  using SepS = SepShape<32, SKB_SEP_RN, (SKB_SEP_RN == 2) ? 256 : 128>;
+  using SepS = SepGridShape;
   static constexpr int kSepNB = SepS::NB;
   int sep_sweep(int mode, const float* xT, const float* target, const float* marg,
                 const float* old, float* out, float* outT, int res_kind,
