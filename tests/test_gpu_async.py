@@ -206,3 +206,20 @@ def test_host_threads_solve_concurrently(cuda):
         assert r.path == w.path
         _same(r.cost_e0, w.cost_e0, 1e-6 * float(w.cost_e0.abs().max()))
         _same(r.log_u, w.log_u, 1e-5)
+
+
+def test_graph_cache_eviction_keeps_results_right(cuda):
+    """More distinct asynchronous problems than the instantiated-graph cache
+    holds (8, LRU): every solve -- fresh capture, replay, in-place update or
+    after eviction -- equals its synchronous result."""
+    skb = _skb()
+    probs = [_problem("per_sample", 64 + 4 * k, 8, 50 + k, cuda) for k in range(11)]
+    want = [skb.solve(m, n, c, 0.05, 30, 0.0, fused=True) for m, n, c in probs]
+    order = list(range(11)) + list(range(10, -1, -1)) + [0, 5, 10, 0]
+    for k in order:
+        m, n, c = probs[k]
+        res = skb.solve(m, n, c, 0.05, 30, 0.0, fused=True, asynchronous=True,
+                        force_rerun=(k % 3 == 0)).check()
+        ref = want[k] if k % 3 else skb.solve(m, n, c, 0.05, 30, 0.0, fused=True, force_rerun=True)
+        _same(res.cost_e0, ref.cost_e0, 1e-6 * float(ref.cost_e0.abs().max()))
+        _same(res.log_v, ref.log_v, 1e-5)
