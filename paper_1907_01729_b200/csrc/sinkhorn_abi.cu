@@ -239,12 +239,12 @@ struct Layout {
 // Fused passes (sweep_fused.cuh): shared stored cost, both padded extents
 // within the register-resident row (NQ <= kFusedMaxNQ 64-column chunks).
 constexpr int kFusedMaxNQ = kFusedMaxChunks;
-// Per-sample costs (sweep_fused.cuh fused_ps_kernel): rows of d2 <= 1024
+// Per-sample costs (sweep_fused.cuh fused_ps_kernel): rows of d2 <= 2048
 // floats, d2 % 4 == 0 so every row is a whole number of 16-byte units.
 bool fused_eligible(const sinkhorn_problem_v1& pr) {
   if (pr.B < 1) return false;
   if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE)
-    return pr.d2 % 4 == 0 && round_up(pr.d2, TILE_PAD) <= 64 * kFusedMaxNQ;
+    return pr.d2 % 4 == 0 && round_up(pr.d2, TILE_PAD) <= 64 * kPsMaxChunks;
   return pr.cost_kind == SINKHORN_COST_SHARED &&
          round_up(pr.d1, TILE_PAD) <= 64 * kFusedMaxNQ && round_up(pr.d2, TILE_PAD) <= 64 * kFusedMaxNQ;
 }
@@ -856,7 +856,7 @@ struct Solve {
   }
   template <int NQ>
   int launch_fused_ps(const FusedParams& fp) {
-    if constexpr (NQ > kFusedMaxChunks) {
+    if constexpr (NQ > kPsMaxChunks) {
       return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
     } else {
       if (fp.nq != NQ) return launch_fused_ps<NQ + 1>(fp);

@@ -48,7 +48,8 @@ constexpr int kFusedWarps = 16;    // max lanes per group = warps per CTA
 // Lanes per group for a row of nq chunks: 16 warps while the row's registers
 // (potentials, plan partials, exponentials: 6 per chunk) fit in 128, else 12
 // warps with up to 168 registers.
-__host__ __device__ constexpr int fused_warps(int nq) { return nq <= 13 ? 16 : 12; }
+// Per-sample rows up to 2048 columns (fused_ps_kernel only): 8 warps.
+__host__ __device__ constexpr int fused_warps(int nq) { return nq <= 13 ? 16 : nq <= 16 ? 12 : 8; }
 constexpr int kFusedStages = 8;    // cost rows in flight per CTA
 constexpr int kFusedMaxChunks = 16;  // row length <= 1024 columns
 constexpr float kFusedMinColsum = 8.673617379884035e-19f;   // 2^-60
@@ -516,10 +517,13 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_pass_kernel(const FusedParam
 // are reduced in the log domain, t_j = c_ij * (-log2e / lambda) + v_j, with
 // the previous-lse shift and the exact fallback of the shared-cost pass.
 constexpr int kPsStages = 4;
+constexpr int kPsMaxChunks = 32;   // per-sample rows <= 2048 columns
+// ring slots per warp: 4 for rows <= 1024 columns, 3 above (192 KB either way)
+__host__ __device__ constexpr int ps_stages(int nq) { return nq <= 16 ? kPsStages : 3; }
 
 template <int NQ>
 __host__ __device__ constexpr size_t fused_ps_smem_bytes() {
-  return (size_t)fused_warps(NQ) * kPsStages * (NQ * 64 * 4 + 8);
+  return (size_t)fused_warps(NQ) * ps_stages(NQ) * (NQ * 64 * 4 + 8);
 }
 
 template <int NQ, bool kTail, int NW = fused_warps(NQ)>
@@ -527,6 +531,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
                                                               int d2, float kscale) {
   extern __shared__ __align__(128) unsigned char fsm[];
   constexpr int rowlen = NQ * 64;
+  constexpr int kPsStages = ps_stages(NQ);
   const int warp = warp_id(), lane = lane_id();
   float* ring = reinterpret_cast<float*>(fsm) + (size_t)warp * kPsStages * rowlen;
   uint64_t* full = reinterpret_cast<uint64_t*>(fsm + (size_t)NW * kPsStages * rowlen * 4) +
