@@ -144,6 +144,20 @@ __global__ void validate_cost_kernel(const float* __restrict__ c, size_t n, int*
   if (__any_sync(0xffffffffu, !good) && (threadIdx.x & 31) == 0) set_status(status, 15);
 }
 
+// Rows of n floats -> rows of ld floats (ld >= n), the tail zero: the fused
+// per-sample pass's bulk copies need rows of whole 16-byte units.  A warp per
+// row, grid-stride.
+__global__ void __launch_bounds__(256) pad_rows_kernel(const float* __restrict__ src, long long rows,
+                                                       int n, int ld, float* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = (blockIdx.x * 256LL + threadIdx.x) >> 5; r < rows;
+       r += (long long)gridDim.x * 8) {
+    const float* s = src + r * n;
+    float* d = dst + r * ld;
+    for (int j = lane; j < ld; j += 32) d[j] = j < n ? __ldcs(s + j) : 0.f;
+  }
+}
+
 // Max over lanes of the residual vector (NaN wins), for the host's stopping test
 // (batch.py:318-322).
 __global__ void reduce_max_kernel(const float* __restrict__ res, int B, float* out) {

@@ -229,6 +229,9 @@ struct Layout {
   int lane_nsplit = 1, lane_nj = 1, lane_vec = 4;
   bool fused = false;             // shared cost, one fused row->column pass per iteration
   int fused_nct = 0, fused_maxseg = 0;
+  size_t cpad = 0;   // per-sample fused pass, d2 % 4 != 0: zero-padded copy of the costs
+  int ldc = 0;       // its row stride (floats)
+  bool padded = false;
   int fg_nct = 0, fg_maxseg = 0;  // the two-GEMM block pass (units: 16 lanes x 16 rows)
   bool gemm = false;              // large shared cost: two fp32 GEMMs per iteration
   size_t kc = 0, gx = 0, gs = 0, gt = 0, ga = 0, gvmax = 0, gvmax0 = 0, gfall = 0;
@@ -240,11 +243,12 @@ struct Layout {
 // within the register-resident row (NQ <= kFusedMaxNQ 64-column chunks).
 constexpr int kFusedMaxNQ = kFusedMaxChunks;
 // Per-sample costs (sweep_fused.cuh fused_ps_kernel): rows of d2 <= 2048
-// floats, d2 % 4 == 0 so every row is a whole number of 16-byte units.
+// floats; the bulk copies move whole 16-byte units, so d2 % 4 != 0 runs on a
+// zero-padded copy of the costs made once per solve (Layout::cpad).
 bool fused_eligible(const sinkhorn_problem_v1& pr) {
   if (pr.B < 1) return false;
-  if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE)
-    return pr.d2 % 4 == 0 && round_up(pr.d2, TILE_PAD) <= 64 * kPsMaxChunks;
+  if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE)   // d2 % 4 != 0: through a padded copy
+    return round_up(pr.d2, TILE_PAD) <= 64 * kPsMaxChunks;
   return pr.cost_kind == SINKHORN_COST_SHARED &&
          round_up(pr.d1, TILE_PAD) <= 64 * kFusedMaxNQ && round_up(pr.d2, TILE_PAD) <= 64 * kFusedMaxNQ;
 }
@@ -334,6 +338,9 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
       L.a2t = c.take((size_t)L.D2p * L.D1p * 4);
       L.kmat = c.take((size_t)L.D1p * L.D2p * 4);
     } else {   // the first column sweep runs lane_col_kernel (one split per column block)
+      L.ldc = (int)round_up(pr.d2, 4);
+      L.padded = L.ldc != pr.d2;   // rows of whole 16-byte units for the bulk copies
+      if (L.padded) L.cpad = c.take((size_t)pr.B * pr.d1 * L.ldc * 4);
       L.lane_vec = (pr.d2 % 4 == 0 && pr.d1 % 4 == 0) ? 4 : 1;
       L.lane_nj = (int)((pr.d2 + 256 * L.lane_vec - 1) / (256 * L.lane_vec));
       L.lane_nsplit = 1;
@@ -849,8 +856,9 @@ struct Solve {
     if (int e = set_max_smem(reinterpret_cast<const void*>(kern), smem)) return e;
     ++g_launches;
     kt_mark(st);
-    CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(fused_warps(NQ) * 32), smem, st, fp, cost,
-                  (int)pr.d2, (float)(-kLog2e / lam)));
+    const float* rows = L.padded ? F(L.cpad) : cost;
+    CK(launch_pdl(kern, dim3((unsigned)fp.nct), dim3(fused_warps(NQ) * 32), smem, st, fp, rows,
+                  (int)pr.d2, L.ldc, (float)(-kLog2e / lam)));
     kt_mark(st);
     return 0;
   }
@@ -1706,6 +1714,12 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
     // checked by the first column sweep, which reads every element once anyway
     // (lane_col_kernel<..., kValidate>): no separate pass over the 4.3 GB
     S.validate_cost_in_sweep = true;
+  }
+  if (L.padded) {   // fused per-sample pass with d2 % 4 != 0: rows padded to 16-byte units
+    ++g_launches;
+    pad_rows_kernel<<<grid_for((size_t)pr.B * pr.d1 * 32), 256, 0, st>>>(
+        cost, (long long)pr.B * pr.d1, (int)pr.d2, L.ldc, S.F(L.cpad));
+    CK(cudaGetLastError());
   }
   if (L.sep) {   // the separable sweeps' factor tables (once per solve), log u transposed
     const int nblk = (int)((pr.grid_nx + 31) / 32);

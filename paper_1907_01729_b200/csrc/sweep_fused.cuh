@@ -528,7 +528,7 @@ __host__ __device__ constexpr size_t fused_ps_smem_bytes() {
 
 template <int NQ, bool kTail, int NW = fused_warps(NQ)>
 __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams p, const float* cost,
-                                                              int d2, float kscale) {
+                                                              int d2, int ldc, float kscale) {
   extern __shared__ __align__(128) unsigned char fsm[];
   constexpr int rowlen = NQ * 64;
   constexpr int kPsStages = ps_stages(NQ);
@@ -540,13 +540,15 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
   const long long u1 = fused_seg_start(p.U, p.nct, blockIdx.x + 1);
   const int n = (int)(u1 - u0);
   const int nrows = p.nrows;
-  const uint32_t row_bytes = (uint32_t)d2 * 4u;
-  const size_t lane_cells = (size_t)nrows * d2;
+  // cost rows of ldc floats (ldc = d2, or d2 rounded up to 4 in the solver's
+  // zero-padded copy when d2 % 4 != 0: bulk copies move whole 16-byte units)
+  const uint32_t row_bytes = (uint32_t)ldc * 4u;
+  const size_t lane_cells = (size_t)nrows * ldc;
 
   // columns past d2 are never written by the copies: zero them once so the
   // -inf potentials there meet a finite cost
   for (int k = lane; k < kPsStages * rowlen; k += 32)
-    if ((k % rowlen) >= d2) ring[k] = 0.f;
+    if ((k % rowlen) >= ldc) ring[k] = 0.f;
   if (lane == 0) {
     for (int st = 0; st < kPsStages; ++st) mbar_init(&full[st], 1);
     fence_barrier_init();
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
     const int b = pg * NW + warp;
     if (b < p.B) {
       mbar_arrive_expect_tx(&full[st], row_bytes);
-      bulk_g2s(ring + st * rowlen, cost + b * lane_cells + (size_t)pi * d2, row_bytes, &full[st]);
+      bulk_g2s(ring + st * rowlen, cost + b * lane_cells + (size_t)pi * ldc, row_bytes, &full[st]);
     } else {
       mbar_arrive(&full[st]);   // idle lane: complete the phase without data
     }

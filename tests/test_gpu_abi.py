@@ -182,9 +182,10 @@ def test_every_path_reports_invalid_inputs(path, cuda):
     dt = torch.float64 if path == "fp64" else torch.float32
     t = lambda a: torch.tensor(a, dtype=dt, device=cuda)   # noqa: E731
     kw = {"tiled_only": True, "gemm": path == "gemm", "fp64": path == "fp64"}
+    if path == "per_sample":
+        kw["fused"] = False   # the lane half-sweeps
     cost = np.repeat(c[None], B, axis=0) if path.startswith("per_sample") else c
     res = skb.solve(t(mu), t(nu), t(cost), 0.1, 20, **kw)
-    # (d2 = 9 is not a multiple of 4: per-sample costs take the lane kernels here)
     assert res.path == {"per_sample": "lane", "per_sample_fused": "fused"}.get(path, path)
     bad = mu.copy()
     bad[1, 3] += 1e-3
