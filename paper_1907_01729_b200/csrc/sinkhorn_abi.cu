@@ -1534,9 +1534,10 @@ struct FusedGraphKey {
   double lambda;
   int32_t max_iters;
   int dev;
+  int path;   // 1 fused passes, 2 GEMM iteration (the same problem can take either)
   bool operator==(const FusedGraphKey& o) const {
     return ws == o.ws && cost == o.cost && B == o.B && d1 == o.d1 && d2 == o.d2 && kind == o.kind &&
-           lambda == o.lambda && max_iters == o.max_iters && dev == o.dev;
+           lambda == o.lambda && max_iters == o.max_iters && dev == o.dev && path == o.path;
   }
 };
 struct FusedGraph {
@@ -1775,6 +1776,49 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
                 : L.tiled ? "tiled"
                 : L.sep   ? "separable"
                           : "lane";
+  // Without a stopping test the loop has no host decision: a repeated solve
+  // (same workspace, cost and shape) replays it as one CUDA graph, so its
+  // launches (2 per iteration fused, 8 on the GEMM iteration) cannot stall
+  // behind the host.
+  auto run_loop = [&](auto&& loop, bool graphable) -> int {
+    FusedGraph* fg = nullptr;
+    if (graphable && !checks && g_reducer == nullptr && !g_no_graph && !g_kt.on && !capturing)
+      fg = fused_graph_slot(FusedGraphKey{ws, cost, pr.B, pr.d1, pr.d2, pr.cost_kind, op.lambda,
+                                          op.max_iters, S.di.dev, L.gemm ? 2 : 1});
+    if (fg != nullptr && fg->seen && fg->exec == nullptr) {   // second sighting: capture
+      // a capture stream per (thread, device): a stream belongs to the device
+      // that was current when it was created
+      static thread_local cudaStream_t cs_dev[64] = {};
+      if (S.di.dev < 0 || S.di.dev >= 64) return fail(SINKHORN_STATUS_CUDA_ERROR, "device ordinal");
+      cudaStream_t& cs = cs_dev[S.di.dev];
+      if (cs == nullptr) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      const unsigned long long l0 = g_launches;
+      S.st = cs;
+      CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      const int e = loop();
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+      S.st = st;
+      if (e) return e;
+      CK(ce);
+      CK(cudaGraphInstantiate(&fg->exec, graph, 0));
+      CK(cudaGraphDestroy(graph));
+      fg->launches = g_launches - l0;
+      fg->iters = iters;
+      fg->cur = cur;
+      g_launches = l0;
+    }
+    if (fg != nullptr && fg->exec != nullptr) {
+      CK(cudaGraphLaunch(fg->exec, st));
+      g_launches += fg->launches;
+      iters = fg->iters;
+      cur = fg->cur;
+    } else {
+      if (fg != nullptr) fg->seen = true;
+      if (int e = loop()) return e;
+    }
+    return 0;
+  };
   if (L.fused && !small) {
     // v_1 from u_0, then one fused pass (+ column merge) per iteration
     auto fused_loop = [&]() -> int {
@@ -1813,74 +1857,41 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
       }
       return 0;
     };
-    // Without a stopping test the loop has no host decision: a repeated solve
-    // (same workspace, cost and shape) replays it as one CUDA graph, so its
-    // ~2 launches per iteration cannot stall behind the host.
-    FusedGraph* fg = nullptr;
-    if (!checks && g_reducer == nullptr && !g_no_graph && !g_kt.on && !capturing)
-      fg = fused_graph_slot(FusedGraphKey{ws, cost, pr.B, pr.d1, pr.d2, pr.cost_kind, op.lambda,
-                                          op.max_iters, S.di.dev});
-    if (fg != nullptr && fg->seen && fg->exec == nullptr) {   // second sighting: capture
-      // a capture stream per (thread, device): a stream belongs to the device
-      // that was current when it was created
-      static thread_local cudaStream_t cs_dev[64] = {};
-      if (S.di.dev < 0 || S.di.dev >= 64) return fail(SINKHORN_STATUS_CUDA_ERROR, "device ordinal");
-      cudaStream_t& cs = cs_dev[S.di.dev];
-      if (cs == nullptr) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-      const unsigned long long l0 = g_launches;
-      S.st = cs;
-      CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      const int e = fused_loop();
-      cudaGraph_t graph = nullptr;
-      const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
-      S.st = st;
-      if (e) return e;
-      CK(ce);
-      CK(cudaGraphInstantiate(&fg->exec, graph, 0));
-      CK(cudaGraphDestroy(graph));
-      fg->launches = g_launches - l0;
-      fg->iters = iters;
-      fg->cur = cur;
-      g_launches = l0;
-    }
-    if (fg != nullptr && fg->exec != nullptr) {
-      CK(cudaGraphLaunch(fg->exec, st));
-      g_launches += fg->launches;
-      iters = fg->iters;
-      cur = fg->cur;
-    } else {
-      if (fg != nullptr) fg->seen = true;
-      if (int e = fused_loop()) return e;
-    }
+    if (int e = run_loop(fused_loop, true)) return e;
   }
   if (L.gemm && !small) {
-    if (int e = S.gemm_first()) return e;
-    cur = 1;
-    for (int k = 1; k <= op.max_iters; ++k) {
-      const bool last = (k == op.max_iters);
-      const bool check = checks && (k % op.check_interval == 0) && !last;
-      if (check || last) {
-        if (int e = S.zero_res()) return e;
+    auto gemm_loop = [&]() -> int {
+      if (int e = S.gemm_first()) return e;
+      cur = 1;
+      for (int k = 1; k <= op.max_iters; ++k) {
+        const bool last = (k == op.max_iters);
+        const bool check = checks && (k % op.check_interval == 0) && !last;
+        if (check || last) {
+          if (int e = S.zero_res()) return e;
+        }
+        if (int e = S.gemm_iteration(cur, check || last)) return e;
+        iters = k;
+        if (last) break;
+        if (check) {
+          ++g_launches;
+          reduce_max_kernel<<<1, 256, 0, S.st>>>(S.F(L.res), (int)pr.B, S.F(L.scratch));
+          CK(cudaGetLastError());
+          float hmax = 0.f;
+          int hstatus = 0;
+          CK(cudaMemcpyAsync(&hmax, S.F(L.scratch), 4, cudaMemcpyDeviceToHost, S.st));
+          CK(cudaMemcpyAsync(&hstatus, status, 4, cudaMemcpyDeviceToHost, S.st));
+          CK(cudaStreamSynchronize(S.st));
+          double gmax = (hstatus != 0) ? NAN : (double)hmax;
+          if (g_reducer) gmax = g_reducer(gmax, g_reducer_user);
+          if (hstatus != 0) break;
+          if (gmax <= op.tolerance) break;   // converged: g2[cur] = log_v_k, X and a of iteration k
+        }
+        cur ^= 1;
       }
-      if (int e = S.gemm_iteration(cur, check || last)) return e;
-      iters = k;
-      if (last) break;
-      if (check) {
-        ++g_launches;
-        reduce_max_kernel<<<1, 256, 0, st>>>(S.F(L.res), (int)pr.B, S.F(L.scratch));
-        CK(cudaGetLastError());
-        float hmax = 0.f;
-        int hstatus = 0;
-        CK(cudaMemcpyAsync(&hmax, S.F(L.scratch), 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&hstatus, status, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        double gmax = (hstatus != 0) ? NAN : (double)hmax;
-        if (g_reducer) gmax = g_reducer(gmax, g_reducer_user);
-        if (hstatus != 0) break;
-        if (gmax <= op.tolerance) break;   // converged: g2[cur] = log_v_k, X and a of iteration k
-      }
-      cur ^= 1;
-    }
+      return 0;
+    };
+    // (row shards call the all-reduce between contractions: not captured)
+    if (int e = run_loop(gemm_loop, g_allreduce == nullptr)) return e;
   }
   for (int k = 1; !persist && !small && !L.fused && !L.gemm && k <= op.max_iters; ++k) {
     // estimate mode once the potentials have settled past the first sweeps
