@@ -245,10 +245,16 @@ constexpr int kFusedMaxNQ = kFusedMaxChunks;
 // Per-sample costs (sweep_fused.cuh fused_ps_kernel): rows of d2 <= 2048
 // floats; the bulk copies move whole 16-byte units, so d2 % 4 != 0 runs on a
 // zero-padded copy of the costs made once per solve (Layout::cpad).
+// Lanes per group of the per-sample pass: rows above 2048 columns take two
+// warps per lane (fused_ps_kernel<..., kHalves = 2>, 8 warps = 4 lanes).
+int ps_group_lanes(int d2p) {
+  const int nq = d2p / 64;
+  return nq <= kPsMaxChunks ? fused_warps(nq) : 4;
+}
 bool fused_eligible(const sinkhorn_problem_v1& pr) {
   if (pr.B < 1) return false;
   if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE)   // d2 % 4 != 0: through a padded copy
-    return round_up(pr.d2, TILE_PAD) <= 64 * kPsMaxChunks;
+    return round_up(pr.d2, TILE_PAD) <= 2 * 64 * kPsMaxChunks;   // > 2048: two warps per lane
   return pr.cost_kind == SINKHORN_COST_SHARED &&
          round_up(pr.d1, TILE_PAD) <= 64 * kFusedMaxNQ && round_up(pr.d2, TILE_PAD) <= 64 * kFusedMaxNQ;
 }
@@ -354,7 +360,8 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     L.mu = c.take(n1);
     L.nu = c.take(n2);
     L.e0 = c.take(std::max(n1, n2));
-    const int nw = fused_warps(L.D2p / 64);
+    const int nw = pr.cost_kind == SINKHORN_COST_PER_SAMPLE ? ps_group_lanes(L.D2p)
+                                                            : fused_warps(L.D2p / 64);
     const long long groups = (pr.B + nw - 1) / nw;
     const long long U = groups * pr.d1;
     L.fused_nct = (int)std::max<long long>(1, std::min<long long>(sms, U));
@@ -849,9 +856,9 @@ struct Solve {
                               : launch_fused_t<NQ, false, false, true>(fp);
     }
   }
-  template <int NQ, bool kTail>
+  template <int NQ, bool kTail, int kHalves = 1>
   int launch_fused_ps_t(const FusedParams& fp) {
-    auto kern = &fused_ps_kernel<NQ, kTail>;
+    auto kern = &fused_ps_kernel<NQ, kTail, fused_warps(NQ), kHalves>;
     const size_t smem = fused_ps_smem_bytes<NQ>();
     if (int e = set_max_smem(reinterpret_cast<const void*>(kern), smem)) return e;
     ++g_launches;
@@ -865,10 +872,21 @@ struct Solve {
   template <int NQ>
   int launch_fused_ps(const FusedParams& fp) {
     if constexpr (NQ > kPsMaxChunks) {
-      return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
+      return launch_fused_ps2<kPsMaxChunks / 2 + 1>(fp);   // rows above 2048 columns
     } else {
       if (fp.nq != NQ) return launch_fused_ps<NQ + 1>(fp);
       return fp.e0 != nullptr ? launch_fused_ps_t<NQ, true>(fp) : launch_fused_ps_t<NQ, false>(fp);
+    }
+  }
+  // two warps per lane, NQ chunks each (NQ = ceil(nq / 2) in 17..32)
+  template <int NQ>
+  int launch_fused_ps2(const FusedParams& fp) {
+    if constexpr (NQ > kPsMaxChunks) {
+      return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
+    } else {
+      if ((fp.nq + 1) / 2 != NQ) return launch_fused_ps2<NQ + 1>(fp);
+      return fp.e0 != nullptr ? launch_fused_ps_t<NQ, true, 2>(fp)
+                              : launch_fused_ps_t<NQ, false, 2>(fp);
     }
   }
   template <int NQ>
@@ -923,7 +941,8 @@ struct Solve {
   // g2[cur ^ 1] from the plan's column marginal; residuals / E0 row terms on request
   int fused_iteration(int cur, bool res, bool e0, bool first = false) {
     FusedParams fp = fused_common();
-    const int nw = fused_warps(L.D2p / 64);
+    const int nw = pr.cost_kind == SINKHORN_COST_PER_SAMPLE ? ps_group_lanes(L.D2p)
+                                                            : fused_warps(L.D2p / 64);
     const long long groups = (pr.B + nw - 1) / nw;
     fp.nrows = (int)pr.d1;
     fp.rowlen = L.D2p;

@@ -526,13 +526,43 @@ __host__ __device__ constexpr size_t fused_ps_smem_bytes() {
   return (size_t)fused_warps(NQ) * ps_stages(NQ) * (NQ * 64 * 4 + 8);
 }
 
-template <int NQ, bool kTail, int NW = fused_warps(NQ)>
+// kHalves = 2 (rows of 2049-4096 columns): two warps per lane, each streaming
+// and holding one half of every row; the row's sums and maxima are combined
+// through shared memory behind a 64-thread named barrier per exchange.
+template <int NQ, bool kTail, int NW = fused_warps(NQ), int kHalves = 1>
 __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams p, const float* cost,
                                                               int d2, int ldc, float kscale) {
   extern __shared__ __align__(128) unsigned char fsm[];
-  constexpr int rowlen = NQ * 64;
+  constexpr int rowlen = NQ * 64;          // columns held by one warp
   constexpr int kPsStages = ps_stages(NQ);
+  constexpr int LPG = NW / kHalves;        // lanes per group
   const int warp = warp_id(), lane = lane_id();
+  const int lw = warp % LPG, half = warp / LPG;
+  const int col0 = half * rowlen;          // this warp's first column
+  __shared__ float xch[kHalves == 2 ? LPG : 1][2][2];   // [lane][parity][half]
+  int xc = 0;
+  auto pair_sum = [&](float v) -> float {
+    if constexpr (kHalves == 1) {
+      return v;
+    } else {
+      const int par = xc & 1;
+      ++xc;
+      if (lane == 0) xch[lw][par][half] = v;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + lw) : "memory");
+      return xch[lw][par][0] + xch[lw][par][1];
+    }
+  };
+  auto pair_max = [&](float v) -> float {
+    if constexpr (kHalves == 1) {
+      return v;
+    } else {
+      const int par = xc & 1;
+      ++xc;
+      if (lane == 0) xch[lw][par][half] = v;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + lw) : "memory");
+      return fmaxf(xch[lw][par][0], xch[lw][par][1]);
+    }
+  };
   float* ring = reinterpret_cast<float*>(fsm) + (size_t)warp * kPsStages * rowlen;
   uint64_t* full = reinterpret_cast<uint64_t*>(fsm + (size_t)NW * kPsStages * rowlen * 4) +
                    warp * kPsStages;
@@ -542,13 +572,14 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
   const int nrows = p.nrows;
   // cost rows of ldc floats (ldc = d2, or d2 rounded up to 4 in the solver's
   // zero-padded copy when d2 % 4 != 0: bulk copies move whole 16-byte units)
-  const uint32_t row_bytes = (uint32_t)ldc * 4u;
+  const int ncopy = ldc - col0 < rowlen ? (ldc - col0 > 0 ? ldc - col0 : 0) : rowlen;
+  const uint32_t row_bytes = (uint32_t)ncopy * 4u;   // this warp's part of a row
   const size_t lane_cells = (size_t)nrows * ldc;
 
   // columns past d2 are never written by the copies: zero them once so the
   // -inf potentials there meet a finite cost
   for (int k = lane; k < kPsStages * rowlen; k += 32)
-    if ((k % rowlen) >= ldc) ring[k] = 0.f;
+    if ((k % rowlen) >= ncopy) ring[k] = 0.f;
   if (lane == 0) {
     for (int st = 0; st < kPsStages; ++st) mbar_init(&full[st], 1);
     fence_barrier_init();
@@ -558,10 +589,11 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
   int pp = 0, pg = (int)(u0 / nrows), pi = (int)(u0 % nrows);
   auto produce = [&]() {   // lane 0: position pp into slot pp % kPsStages
     const int st = pp % kPsStages;
-    const int b = pg * NW + warp;
-    if (b < p.B) {
+    const int b = pg * LPG + lw;
+    if (b < p.B && row_bytes > 0) {
       mbar_arrive_expect_tx(&full[st], row_bytes);
-      bulk_g2s(ring + st * rowlen, cost + b * lane_cells + (size_t)pi * ldc, row_bytes, &full[st]);
+      bulk_g2s(ring + st * rowlen, cost + b * lane_cells + (size_t)pi * ldc + col0, row_bytes,
+               &full[st]);
     } else {
       mbar_arrive(&full[st]);   // idle lane: complete the phase without data
     }
@@ -586,15 +618,16 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
     const int i_begin = (int)(u - (long long)g * nrows);
     const long long seg_end = (long long)(g + 1) * nrows < u1 ? (long long)(g + 1) * nrows : u1;
     const int i_end = (int)(seg_end - (long long)g * nrows);
-    const int b = g * NW + warp;
+    const int b = g * LPG + lw;
     const bool act = b < p.B && !dead;
 
     uint64_t xv[NQ], acc[NQ];
-    const float* x_b = p.x + (size_t)b * p.rowlen + 2 * lane;
+    const float* x_b = p.x + (size_t)b * p.rowlen + col0 + 2 * lane;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       float2 v2 = make_float2(neg_inf(), neg_inf());
-      if (act && 2 * lane + 64 * q < d2) v2 = __ldg(reinterpret_cast<const float2*>(x_b + 64 * q));
+      if (act && col0 + 2 * lane + 64 * q < d2)
+        v2 = __ldg(reinterpret_cast<const float2*>(x_b + 64 * q));
       xv[q] = pk2(v2.x, v2.y);
       acc[q] = 0ull;
     }
@@ -651,6 +684,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
         S = lo2(s01) + hi2(s01);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+        S = pair_sum(S);
         exact = act && !(S >= kFusedEstLo && S <= kFusedEstHi);
       }
       if (exact) {   // warp-uniform; the first iteration and rare rows after it
@@ -665,6 +699,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
         float m = fmaxf(m0, m1);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+        m = pair_max(m);
         ms = fmaxf(m, kNegBig);
         const uint64_t nm = pk2(-ms, -ms);
         uint64_t s0 = 0ull, s1 = 0ull;
@@ -679,6 +714,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
         S = lo2(s01) + hi2(s01);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(0xffffffffu, S, off);
+        S = pair_sum(S);
       }
       const float lse = S > 0.f ? ms + lg2(S) : neg_inf();
       const float o = sweep_out(tgt, lse);
@@ -698,10 +734,12 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, off);
-        if (act && lane == 0) e0_b[i] = (a > 0.f && qs > 0.f) ? log2f(a) + log2f(qs) : neg_inf();
+        qs = pair_sum(qs);
+        if (act && half == 0 && lane == 0)
+          e0_b[i] = (a > 0.f && qs > 0.f) ? log2f(a) + log2f(qs) : neg_inf();
       }
       if (wi == 31 || i + 1 == i_end) {   // this window's u_i, one coalesced store
-        if (act && lane <= wi) out_b[i - wi + lane] = ob;
+        if (act && half == 0 && lane <= wi) out_b[i - wi + lane] = ob;
       }
       // refill the slot just consumed with the position kPsStages ahead
       __syncwarp();
@@ -711,11 +749,11 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
       }
     }
     if (act) {
-      float* dst = p.part + (((size_t)blockIdx.x * p.maxseg + (g - g_first)) * NW + warp) *
-                                (size_t)p.rowlen;
+      float* dst = p.part + (((size_t)blockIdx.x * p.maxseg + (g - g_first)) * LPG + lw) *
+                                (size_t)p.rowlen + col0;
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
-        if (2 * lane + 64 * q < p.rowlen)
+        if (col0 + 2 * lane + 64 * q < p.rowlen)
           *reinterpret_cast<float2*>(dst + 2 * lane + 64 * q) = make_float2(lo2(acc[q]), hi2(acc[q]));
     }
     if constexpr (kTail) {
