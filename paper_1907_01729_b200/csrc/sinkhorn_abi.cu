@@ -245,16 +245,16 @@ constexpr int kFusedMaxNQ = kFusedMaxChunks;
 // Per-sample costs (sweep_fused.cuh fused_ps_kernel): rows of d2 <= 2048
 // floats; the bulk copies move whole 16-byte units, so d2 % 4 != 0 runs on a
 // zero-padded copy of the costs made once per solve (Layout::cpad).
-// Lanes per group of the per-sample pass: rows above 2048 columns take two
-// warps per lane (fused_ps_kernel<..., kHalves = 2>, 8 warps = 4 lanes).
+// Lanes per group of the per-sample pass: rows above 2048 (4096) columns take
+// two (four) warps per lane (fused_ps_kernel<..., kHalves>, 8 warps).
 int ps_group_lanes(int d2p) {
   const int nq = d2p / 64;
-  return nq <= kPsMaxChunks ? fused_warps(nq) : 4;
+  return nq <= kPsMaxChunks ? fused_warps(nq) : nq <= 2 * kPsMaxChunks ? 4 : 2;
 }
 bool fused_eligible(const sinkhorn_problem_v1& pr) {
   if (pr.B < 1) return false;
   if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE)   // d2 % 4 != 0: through a padded copy
-    return round_up(pr.d2, TILE_PAD) <= 2 * 64 * kPsMaxChunks;   // > 2048: two warps per lane
+    return round_up(pr.d2, TILE_PAD) <= 4 * 64 * kPsMaxChunks;   // > 2048: 2 or 4 warps per lane
   return pr.cost_kind == SINKHORN_COST_SHARED &&
          round_up(pr.d1, TILE_PAD) <= 64 * kFusedMaxNQ && round_up(pr.d2, TILE_PAD) <= 64 * kFusedMaxNQ;
 }
@@ -872,21 +872,32 @@ struct Solve {
   template <int NQ>
   int launch_fused_ps(const FusedParams& fp) {
     if constexpr (NQ > kPsMaxChunks) {
-      return launch_fused_ps2<kPsMaxChunks / 2 + 1>(fp);   // rows above 2048 columns
+      return launch_fused_ps2<kPsMaxChunks / 2 + 2>(fp);   // rows above 2048 columns
     } else {
       if (fp.nq != NQ) return launch_fused_ps<NQ + 1>(fp);
       return fp.e0 != nullptr ? launch_fused_ps_t<NQ, true>(fp) : launch_fused_ps_t<NQ, false>(fp);
     }
   }
-  // two warps per lane, NQ chunks each (NQ = ceil(nq / 2) in 17..32)
+  // two warps per lane, NQ chunks each (ceil(nq / 2) rounded up to even, 18..32:
+  // half the instantiations; the extra columns are zero-filled), then four
   template <int NQ>
   int launch_fused_ps2(const FusedParams& fp) {
     if constexpr (NQ > kPsMaxChunks) {
-      return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
+      return launch_fused_ps4<kPsMaxChunks / 2 + 2>(fp);
     } else {
-      if ((fp.nq + 1) / 2 != NQ) return launch_fused_ps2<NQ + 1>(fp);
+      if ((((fp.nq + 1) / 2) + 1) / 2 * 2 != NQ) return launch_fused_ps2<NQ + 2>(fp);
       return fp.e0 != nullptr ? launch_fused_ps_t<NQ, true, 2>(fp)
                               : launch_fused_ps_t<NQ, false, 2>(fp);
+    }
+  }
+  template <int NQ>
+  int launch_fused_ps4(const FusedParams& fp) {
+    if constexpr (NQ > kPsMaxChunks) {
+      return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
+    } else {
+      if ((((fp.nq + 3) / 4) + 1) / 2 * 2 != NQ) return launch_fused_ps4<NQ + 2>(fp);
+      return fp.e0 != nullptr ? launch_fused_ps_t<NQ, true, 4>(fp)
+                              : launch_fused_ps_t<NQ, false, 4>(fp);
     }
   }
   template <int NQ>

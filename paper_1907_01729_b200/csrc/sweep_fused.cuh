@@ -526,9 +526,10 @@ __host__ __device__ constexpr size_t fused_ps_smem_bytes() {
   return (size_t)fused_warps(NQ) * ps_stages(NQ) * (NQ * 64 * 4 + 8);
 }
 
-// kHalves = 2 (rows of 2049-4096 columns): two warps per lane, each streaming
-// and holding one half of every row; the row's sums and maxima are combined
-// through shared memory behind a 64-thread named barrier per exchange.
+// kHalves = 2 or 4 (rows of 2049-4096 / 4097-8192 columns): that many warps
+// per lane, each streaming and holding one slice of every row; the row's sums
+// and maxima are combined through shared memory (fixed slice order, so every
+// warp of the lane gets the same value) behind a named barrier per exchange.
 template <int NQ, bool kTail, int NW = fused_warps(NQ), int kHalves = 1>
 __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams p, const float* cost,
                                                               int d2, int ldc, float kscale) {
@@ -539,28 +540,38 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams 
   const int warp = warp_id(), lane = lane_id();
   const int lw = warp % LPG, half = warp / LPG;
   const int col0 = half * rowlen;          // this warp's first column
-  __shared__ float xch[kHalves == 2 ? LPG : 1][2][2];   // [lane][parity][half]
+  __shared__ float xch[kHalves > 1 ? LPG : 1][2][kHalves];   // [lane][parity][slice]
   int xc = 0;
+  // exchange v among the lane's warps: parity double-buffering makes one
+  // barrier per exchange enough (a warp cannot pass the next barrier before
+  // every partner has read this one's values)
+  auto exchange = [&](float v) -> int {
+    const int par = xc & 1;
+    ++xc;
+    if (lane == 0) xch[lw][par][half] = v;
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + lw), "r"(32 * kHalves) : "memory");
+    return par;
+  };
   auto pair_sum = [&](float v) -> float {
     if constexpr (kHalves == 1) {
       return v;
     } else {
-      const int par = xc & 1;
-      ++xc;
-      if (lane == 0) xch[lw][par][half] = v;
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + lw) : "memory");
-      return xch[lw][par][0] + xch[lw][par][1];
+      const int par = exchange(v);
+      float t = xch[lw][par][0];
+#pragma unroll
+      for (int h = 1; h < kHalves; ++h) t += xch[lw][par][h];
+      return t;
     }
   };
   auto pair_max = [&](float v) -> float {
     if constexpr (kHalves == 1) {
       return v;
     } else {
-      const int par = xc & 1;
-      ++xc;
-      if (lane == 0) xch[lw][par][half] = v;
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + lw) : "memory");
-      return fmaxf(xch[lw][par][0], xch[lw][par][1]);
+      const int par = exchange(v);
+      float t = xch[lw][par][0];
+#pragma unroll
+      for (int h = 1; h < kHalves; ++h) t = fmaxf(t, xch[lw][par][h]);
+      return t;
     }
   };
   float* ring = reinterpret_cast<float*>(fsm) + (size_t)warp * kPsStages * rowlen;
