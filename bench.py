@@ -877,7 +877,7 @@ def main():
     ap.add_argument("--probe-ranks", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--reference-budget-s", type=float, default=150.0,
                     help="--impl reference: stop sampling after this many seconds of CPU work")
-    ap.add_argument("--e2e-chunks", type=int, default=8,
+    ap.add_argument("--e2e-chunks", type=int, default=16,
                     help="e2e leg, per-sample costs: lane groups whose upload overlaps the solve")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]

@@ -131,6 +131,17 @@ def _workspace(dev: torch.device, nbytes: int) -> torch.Tensor:
     return ws
 
 
+_AUX_STREAMS: dict = {}
+
+
+def _aux_stream(dev: torch.device, k: int) -> torch.cuda.Stream:
+    """Long-lived extra compute streams (their workspaces are cached per stream)."""
+    key = (dev, k)
+    if key not in _AUX_STREAMS:
+        _AUX_STREAMS[key] = torch.cuda.Stream(dev)
+    return _AUX_STREAMS[key]
+
+
 def _as_f32_cuda(x, device=None) -> torch.Tensor:
     t = torch.as_tensor(x)
     if device is None:
@@ -303,7 +314,7 @@ def solve(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.
 
 def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: float = 0.0,
                    check_interval: int = 10, chunks=8, device=None,
-                   validate: bool = True) -> SolveResult:
+                   validate: bool = True, compute_streams: int = 2) -> SolveResult:
     """``solve`` from host tensors, overlapping the host->device upload with the solve.
 
     mu (B, d1), nu (B, d2) and cost -- shared (d1, d2), per-sample (B, d1, d2),
@@ -317,7 +328,9 @@ def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: f
     couples every lane (batch.py:318-322): one group, synchronous.
     ``chunks`` is a group count (equal groups) or a list of group sizes summing
     to B -- the pipeline's exposed ends are the first group's upload and the
-    last group's solve, so short groups there shorten the step.
+    last group's solve, so short groups there shorten the step.  Consecutive
+    groups alternate over ``compute_streams`` streams (each with its own
+    workspace), so one group's kernel tails overlap the next one's.
     """
     mu, nu = torch.as_tensor(mu), torch.as_tensor(nu)
     grid = isinstance(cost, (GridCost, PointCloudCost))   # small descriptors: passed through
@@ -343,6 +356,8 @@ def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: f
     nbuf = min(3, chunks)
     gmax = max(hi - lo for lo, hi in bounds) if B else 0
     compute = torch.cuda.current_stream(dev)
+    streams = [compute] + [_aux_stream(dev, k) for k in range(
+        max(0, min(int(compute_streams), chunks) - 1) if asynchronous else 0)]
     copy = torch.cuda.Stream(dev)
     f32 = dict(device=dev, dtype=torch.float32)
     bufs = [(torch.empty(gmax, d1, **f32), torch.empty(gmax, d2, **f32),
@@ -371,20 +386,35 @@ def solve_streamed(mu, nu, cost, lam: float, max_iters: int = 1000, tolerance: f
     with torch.cuda.device(dev):
         for k in range(min(nbuf, chunks)):
             upload(k)
+        start = torch.cuda.Event()
+        start.record(compute)   # the caller's prior work on its stream comes first
+        for s_ in streams[1:]:
+            s_.wait_event(start)
+        if shared is not None:
+            shared_ready = torch.cuda.Event()
+            shared_ready.record(compute)
         for k, (lo, hi) in enumerate(bounds):
             m, n, c = bufs[k % nbuf]
-            compute.wait_event(ready[k % nbuf])
+            st = streams[k % len(streams)]
+            st.wait_event(ready[k % nbuf])
+            if shared is not None and st is not compute:
+                st.wait_event(shared_ready)
             g = hi - lo
             cg = cost if grid else (c[:g] if per_sample else shared)
             # results straight into the slices of the outputs (contiguous lane ranges)
-            r = solve(m[:g], n[:g], cg, lam, max_iters, tolerance, check_interval,
-                      validate=validate, asynchronous=asynchronous,
-                      out=(out_cost[lo:hi], log_u[lo:hi], log_v[lo:hi], residuals[lo:hi]))
+            with torch.cuda.stream(st):
+                r = solve(m[:g], n[:g], cg, lam, max_iters, tolerance, check_interval,
+                          validate=validate, asynchronous=asynchronous,
+                          out=(out_cost[lo:hi], log_u[lo:hi], log_v[lo:hi], residuals[lo:hi]))
             checks.append(r)
             iters = max(iters, r.iterations_run)
-            free[k % nbuf].record(compute)
+            free[k % nbuf].record(st)
             if k + nbuf < chunks:
                 upload(k + nbuf)
+        for s_ in streams[1:]:   # the outputs are complete on the caller's stream
+            done = torch.cuda.Event()
+            done.record(s_)
+            compute.wait_event(done)
     for r in checks:
         r.check()
     return SolveResult(out_cost, log_u, log_v, float(lam), iters, residuals, -1.0,

@@ -42,36 +42,29 @@ def main():
     h_gm = torch.empty(B, cfg["d"]).pin_memory()
     h_gn = torch.empty(B, cfg["d"]).pin_memory()
 
-    def step(chunks):
-        res = skb.solve_streamed(h_mu, h_nu, h_c, lam, iters, 0.0, chunks=chunks, device=dev)
+    def step(chunks, ns=2):
+        res = skb.solve_streamed(h_mu, h_nu, h_c, lam, iters, 0.0, chunks=chunks, device=dev,
+                                 compute_streams=ns)
         gm, gn = skb.potentials_backward(res.log_u, res.log_v, lam, torch.ones(B, device=dev))
         h_loss.copy_(res.cost_e0, non_blocking=True)
         h_gm.copy_(gm, non_blocking=True)
         h_gn.copy_(gn, non_blocking=True)
         torch.cuda.synchronize()
 
-    schedules = {
-        "equal8": 8,
-        "ramp_a": [32, 64] + [128] * 6 + [96, 48, 16],
-        "ramp_b": [32, 96] + [128] * 6 + [96, 32],
-        "ramp_c": [64] + [128] * 6 + [96, 64, 32],
-        "ramp_d": [16, 48, 96] + [128] * 6 + [64, 24, 8],
-        "ramp_e": [48, 112] + [128] * 6 + [64, 32],
-        "big_mid": [64, 192, 192, 192, 192, 128, 64],
-    }
+    schedules = {"equal8_1stream": (8, 1), "equal8_2streams": (8, 2), "equal16_2streams": (16, 2),
+                 "equal16_3streams": (16, 3), "equal24_2streams": (24, 2),
+                 "equal32_2streams": (32, 2), "equal32_3streams": (32, 3)}
     out = {}
-    for name, ch in schedules.items():
-        if not isinstance(ch, int):
-            assert sum(ch) == B, (name, sum(ch))
-        step(ch)
+    for name, (ch, ns) in schedules.items():
+        step(ch, ns)
         ts = []
         for _ in range(5):
             t0 = time.perf_counter()
-            step(ch)
+            step(ch, ns)
             ts.append((time.perf_counter() - t0) * 1e3)
         ts.sort()
         out[name] = {"ms_median": ts[2], "ms_min": ts[0]}
-        print(name, ch, f"{ts[2]:.2f} ms (min {ts[0]:.2f})", flush=True)
+        print(name, f"{ts[2]:.2f} ms (min {ts[0]:.2f})", flush=True)
     print(json.dumps(out))
 
 
