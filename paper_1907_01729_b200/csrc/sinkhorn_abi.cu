@@ -303,7 +303,6 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     L.ldk1 = (int)round_up(pr.d1, 128);   // padded row / reduction extents
     L.ldk2 = (int)round_up(pr.d2, 128);
     L.kmat = c.take((size_t)L.ldk1 * L.ldk2 * 4);
-    L.kc = c.take((size_t)L.ldk1 * L.ldk2 * 4);
     L.kmatT = c.take((size_t)L.ldk2 * L.ldk1 * 4);
     const size_t n1 = (size_t)L.B * L.D1p * 4, n2 = (size_t)L.B * L.D2p * 4;
     // tf32 hi / lo planes of X (reduction d2) and a (reduction d1): the MMAs'
@@ -1019,7 +1018,7 @@ struct Solve {
   // ---- GEMM path (sweep_gemm.cuh, contractions in sweep_umma.cuh) -------------
   // rows: S[b][i] = sum_j K[i][j] X[b][j]  (A = K or K o C, B operand = X)
   // cols: T[b][j] = sum_i K^T[j][i] a[b][i] (A = K^T, B operand = a)
-  CUtensorMap tm_k, tm_kt, tm_kc, tm_xh, tm_xl, tm_ah, tm_al;
+  CUtensorMap tm_k, tm_kt, tm_xh, tm_xl, tm_ah, tm_al;
   int setup_umma_maps() {
     if (!L.gemm) return 0;
     // tiled operands: 2-D [tiles * chunks * sub-blocks * rows][32] maps, pitch 128 B
@@ -1028,7 +1027,6 @@ struct Solve {
     const size_t mt1 = (size_t)L.ldk1 / kUmBM, mt2 = (size_t)L.ldk2 / kUmBM;
     const size_t nt = (size_t)(pr.B + kUmBN - 1) / kUmBN;
     bool ok = make_tmap_sw128(&tm_k, F(L.kmat), mt1 * k2 * kUmBM, 32, 32, kUmBM);
-    ok &= make_tmap_sw128(&tm_kc, F(L.kc), mt1 * k2 * kUmBM, 32, 32, kUmBM);
     ok &= make_tmap_sw128(&tm_kt, F(L.kmatT), mt2 * k1 * kUmBM, 32, 32, kUmBM);
     ok &= make_tmap_sw128(&tm_xh, F(L.gxh), nt * k2 * kUmBN, 32, 32, kUmBN);
     ok &= make_tmap_sw128(&tm_xl, F(L.gxl), nt * k2 * kUmBN, 32, 32, kUmBN);
@@ -1050,7 +1048,7 @@ struct Solve {
     CK(cudaGetLastError());
     return 0;
   }
-  int gemm(bool rows, const CUtensorMap& tA, float* C) {
+  int gemm(bool rows, const CUtensorMap& tA, float* C, bool kc = false) {
     UmmaParams p = {};
     p.M = (int)(rows ? pr.d1 : pr.d2);
     p.K = (int)(rows ? pr.d2 : pr.d1);
@@ -1064,10 +1062,11 @@ struct Solve {
     p.ldo = p.M;
     p.part = F(L.um_part);
     p.status = at<int>(ws, L.status);
-    if (int e = set_max_smem(reinterpret_cast<const void*>(&umma_gemm_kernel), kUmSmemBytes))
-      return e;
+    p.kc_scale = (float)(lam * kLn2);
+    auto kern = kc ? &umma_gemm_kernel<true> : &umma_gemm_kernel<false>;
+    if (int e = set_max_smem(reinterpret_cast<const void*>(kern), kUmSmemBytes)) return e;
     kt_mark(st);
-    CK(launch_pdl(umma_gemm_kernel, dim3(p.G), dim3(kUmThreads), kUmSmemBytes, st, tA,
+    CK(launch_pdl(kern, dim3(p.G), dim3(kUmThreads), kUmSmemBytes, st, tA,
                   rows ? tm_xh : tm_ah, rows ? tm_xl : tm_al, p));
     kt_mark(st);
     CK(launch_pdl(umma_fixup_kernel, dim3((unsigned)p.G), dim3(256), 0, st, p));
@@ -1149,7 +1148,7 @@ struct Solve {
   }
   // E0 from the last iteration's X and a: sum_i a_i ((K o C) X)_i
   int gemm_e0(float* out_cost) {
-    if (int e = gemm(true, tm_kc, F(L.gs))) return e;
+    if (int e = gemm(true, tm_k, F(L.gs), true)) return e;   // (K o C) X from K
     ++g_launches;
     gemm_e0_kernel<<<(unsigned)pr.B, 256, 0, st>>>(F(L.ga), F(L.gs), (int)pr.d1, out_cost,
                                                    at<int>(ws, L.status));
@@ -1720,12 +1719,12 @@ int forward_impl(const sinkhorn_problem_v1& pr, const sinkhorn_options_v1& op, c
       dim3 g((unsigned)(L.ldk2 / 128), (unsigned)(L.ldk1 / 32));
       umma_kernel_matrices_vec4<<<g, 256, 0, st>>>(cost, (int)pr.d1, (int)pr.d2,
                                                    (float)(-kLog2e / op.lambda), S.F(L.kmat),
-                                                   S.F(L.kc), S.F(L.kmatT), status);
+                                                   S.F(L.kmatT), status);
     } else {
       dim3 g((unsigned)(L.ldk2 / 32), (unsigned)(L.ldk1 / 32));
       umma_kernel_matrices<<<g, 256, 0, st>>>(cost, (int)pr.d1, (int)pr.d2,
                                               (float)(-kLog2e / op.lambda), S.F(L.kmat),
-                                              S.F(L.kc), S.F(L.kmatT), status);
+                                              S.F(L.kmatT), status);
     }
     CK(cudaGetLastError());
   } else if (pr.cost_kind == SINKHORN_COST_SHARED) {
@@ -2125,9 +2124,9 @@ int materialize_points(const sinkhorn_problem_v1& pr, const float* pts, void* ws
   p.ldo = d2;
   p.part = at<float>(ws, P.part);
   p.status = nullptr;
-  if (int e = set_max_smem(reinterpret_cast<const void*>(&umma_gemm_kernel), kUmSmemBytes)) return e;
+  if (int e = set_max_smem(reinterpret_cast<const void*>(&umma_gemm_kernel<false>), kUmSmemBytes)) return e;
   g_launches += 2;
-  CK(launch_pdl(umma_gemm_kernel, dim3(p.G), dim3(kUmThreads), kUmSmemBytes, st, ta, tbh, tbl, p));
+  CK(launch_pdl(umma_gemm_kernel<false>, dim3(p.G), dim3(kUmThreads), kUmSmemBytes, st, ta, tbh, tbl, p));
   CK(launch_pdl(umma_fixup_kernel, dim3((unsigned)p.G), dim3(256), 0, st, p));
   ++g_launches;
   points_cost_kernel<<<grid_for((size_t)d1 * d2), 256, 0, st>>>(C, nrm, nrm + d1, d1, d2);
@@ -2828,9 +2827,9 @@ int plan_grad_umma(const sinkhorn_problem_v1& pr, double lambda, const float* lo
   p.ldo = d2;
   p.part = at<float>(ws, P.part);
   p.status = nullptr;
-  if (int e = set_max_smem(reinterpret_cast<const void*>(&umma_gemm_kernel), kUmSmemBytes)) return e;
+  if (int e = set_max_smem(reinterpret_cast<const void*>(&umma_gemm_kernel<false>), kUmSmemBytes)) return e;
   g_launches += 3;
-  CK(launch_pdl(umma_gemm_kernel, dim3(p.G), dim3(kUmThreads), kUmSmemBytes, st, ta, tbh, tbl, p));
+  CK(launch_pdl(umma_gemm_kernel<false>, dim3(p.G), dim3(kUmThreads), kUmSmemBytes, st, ta, tbh, tbl, p));
   CK(launch_pdl(umma_fixup_kernel, dim3((unsigned)p.G), dim3(256), 0, st, p));
   plan_finish_kernel<<<grid_for((size_t)d1 * d2), 256, 0, st>>>(
       dc, cost, al, be, d1, d2, (float)(-kLog2e / lambda));

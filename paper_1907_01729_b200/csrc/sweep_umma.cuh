@@ -85,6 +85,8 @@ struct UmmaParams {
   long long ldo;
   float* part;          // [G][2][kUmBN][kUmBM] split-tile partials
   const int* status;    // skip the work when an earlier kernel failed (nullable)
+  float kc_scale;       // kKC: A is K o C, C recovered from K = 2^(-C log2e / lambda) as
+                        // -log2(K) * kc_scale (kc_scale = lambda ln 2)
 };
 
 // First unit of CTA c's stream-K range (U units over G CTAs; U * G < 2^62).
@@ -100,6 +102,10 @@ __device__ __forceinline__ int um_owner(long long U, int G, long long u) {
   return c;
 }
 
+// kKC (the E0 contraction): the splitters turn each K element into
+// K * C = -K log2(K) * kc_scale before the hi / lo split, so K o C needs no
+// stored copy (17 GB at config 5).
+template <bool kKC = false>
 __global__ void __launch_bounds__(kUmThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
                      const __grid_constant__ CUtensorMap tmBl, const UmmaParams p) {
@@ -266,7 +272,11 @@ __global__ void __launch_bounds__(kUmThreads, 1)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float4 v = rowp[q ^ (row & 7)];
-          const float x[4] = {v.x, v.y, v.z, v.w};
+          float x[4] = {v.x, v.y, v.z, v.w};
+          if constexpr (kKC) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] = x[e] > 0.f ? -x[e] * lg2(x[e]) * p.kc_scale : 0.f;
+          }
 #pragma unroll
           for (int e = 0; e < 4; e += 2) {   // lo = x - hi on packed pairs (FADD2)
             const int c = 32 * sb + 4 * q + e;
@@ -589,29 +599,24 @@ __global__ void plan_finish_kernel(float* __restrict__ dc, const float* __restri
 // extents rounded up to 128; block 256.
 __global__ void __launch_bounds__(256) umma_kernel_matrices(const float* __restrict__ c, int d1,
                                                             int d2, float kscale,
-                                                            float* __restrict__ K, float* __restrict__ KC,
+                                                            float* __restrict__ K,
                                                             float* __restrict__ KT, int* status) {
   __shared__ float tile[32][33];
   const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
   const long long kch1 = (d1 + kUmBK - 1) / kUmBK, kch2 = (d2 + kUmBK - 1) / kUmBK;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const bool in_k = i0 < ((d1 + kUmBM - 1) / kUmBM) * kUmBM && j0 < kch2 * kUmBK;    // K / KC rows
+  const bool in_k = i0 < ((d1 + kUmBM - 1) / kUmBM) * kUmBM && j0 < kch2 * kUmBK;    // K rows
   const bool in_kt = j0 < ((d2 + kUmBM - 1) / kUmBM) * kUmBM && i0 < kch1 * kUmBK;   // K^T rows
   bool bad = false;
   for (int r = ty; r < 32; r += 8) {
     const int i = i0 + r, j = j0 + tx;
-    float k = 0.f, kc = 0.f;
+    float k = 0.f;
     if (i < d1 && j < d2) {
       const float cv = c[(size_t)i * d2 + j];
       if (!(cv >= 0.f) || isinf(cv)) bad = true;
       k = ex2(cv * kscale);
-      kc = k * cv;
     }
-    if (in_k) {
-      const long long o = um_tiled_index(i, j, kUmBM, kch2);
-      K[o] = k;
-      KC[o] = kc;
-    }
+    if (in_k) K[um_tiled_index(i, j, kUmBM, kch2)] = k;
     tile[r][tx] = k;
   }
   __syncthreads();
@@ -621,11 +626,11 @@ __global__ void __launch_bounds__(256) umma_kernel_matrices(const float* __restr
 }
 
 // The same on 32 x 128 strips with float4 loads and stores (d2 % 4 == 0 and a
-// 16-byte aligned cost): HBM-bound, 4 B read and 12 B written per element
-// (K, K o C, K^T).  grid (ldk2 / 128, ldk1 / 32); block 256 = 8 warps.
+// 16-byte aligned cost): HBM-bound, 4 B read and 8 B written per element
+// (K, K^T).  grid (ldk2 / 128, ldk1 / 32); block 256 = 8 warps.
 __global__ void __launch_bounds__(256) umma_kernel_matrices_vec4(
     const float* __restrict__ c, int d1, int d2, float kscale, float* __restrict__ K,
-    float* __restrict__ KC, float* __restrict__ KT, int* status) {
+    float* __restrict__ KT, int* status) {
   __shared__ float tile[32][128 + 4];
   const int j0 = blockIdx.x * 128, i0 = blockIdx.y * 32;
   const long long kch1 = (d1 + kUmBK - 1) / kUmBK, kch2 = (d2 + kUmBK - 1) / kUmBK;
@@ -635,25 +640,20 @@ __global__ void __launch_bounds__(256) umma_kernel_matrices_vec4(
   bool bad = false;
   for (int r = ty; r < 32; r += 8) {
     const int i = i0 + r;
-    float4 k4 = make_float4(0.f, 0.f, 0.f, 0.f), kc4 = k4;
+    float4 k4 = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i < d1 && j < d2) {   // d2 % 4 == 0: the four columns are all inside
       const float4 cv = __ldcs(reinterpret_cast<const float4*>(c + (size_t)i * d2 + j));
       const float cc[4] = {cv.x, cv.y, cv.z, cv.w};
-      float kk[4], kcv[4];
+      float kk[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         if (!(cc[e] >= 0.f) || isinf(cc[e])) bad = true;
         kk[e] = ex2(cc[e] * kscale);
-        kcv[e] = kk[e] * cc[e];
       }
       k4 = make_float4(kk[0], kk[1], kk[2], kk[3]);
-      kc4 = make_float4(kcv[0], kcv[1], kcv[2], kcv[3]);
     }
-    if (i < mrows1 && j < kch2 * kUmBK) {
-      const long long o = um_tiled_index(i, j, kUmBM, kch2);   // 4 consecutive floats
-      *reinterpret_cast<float4*>(K + o) = k4;
-      *reinterpret_cast<float4*>(KC + o) = kc4;
-    }
+    if (i < mrows1 && j < kch2 * kUmBK)   // 4 consecutive floats of the tiled layout
+      *reinterpret_cast<float4*>(K + um_tiled_index(i, j, kUmBM, kch2)) = k4;
     *reinterpret_cast<float4*>(&tile[r][4 * tx]) = k4;
   }
   __syncthreads();

@@ -81,11 +81,11 @@ int main(int argc, char** argv) {
   make_map(&ta, A, na / 32, kUmBM);
   make_map(&tbh, Bh, nb / 32, kUmBN);
   make_map(&tbl, Bl, nb / 32, kUmBN);
-  cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUmSmemBytes);
+  cudaFuncSetAttribute(umma_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kUmSmemBytes);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int w = 0; w < 2; ++w) {
-    umma_gemm_kernel<<<p.G, kUmThreads, kUmSmemBytes>>>(ta, tbh, tbl, p);
+    umma_gemm_kernel<false><<<p.G, kUmThreads, kUmSmemBytes>>>(ta, tbh, tbl, p);
     umma_fixup_kernel<<<p.G, 256>>>(p);
   }
   cudaError_t err = cudaDeviceSynchronize();
@@ -93,7 +93,7 @@ int main(int argc, char** argv) {
   unsigned long long zero2[2] = {0, 0};
   cudaMemcpyToSymbol(g_um_dbg_cycles, zero2, 16);
   cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r) umma_gemm_kernel<<<p.G, kUmThreads, kUmSmemBytes>>>(ta, tbh, tbl, p);
+  for (int r = 0; r < reps; ++r) umma_gemm_kernel<false><<<p.G, kUmThreads, kUmSmemBytes>>>(ta, tbh, tbl, p);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
