@@ -163,7 +163,8 @@ def test_per_sample_cost(fused, cuda):
 
 @pytest.mark.parametrize("B,d1,d2,tol", [(37, 50, 68, 1e-5), (16, 64, 64, 0.0), (5, 300, 1024, 0.0),
                                          (20, 1000, 36, 1e-4), (9, 40, 67, 1e-5),
-                                         (7, 33, 1999, 0.0), (3, 100, 1537, 1e-5)])
+                                         (7, 33, 1999, 0.0), (3, 100, 1537, 1e-5),
+                                         (3, 20, 3001, 1e-5), (5, 12, 5000, 0.0)])
 def test_fused_per_sample_ragged_shapes_against_oracle(B, d1, d2, tol, cuda):
     """Per-sample costs through the fused pass: ragged lane groups, d2 not a
     multiple of 64 (zeroed ring tails) nor of 4 (the zero-padded copy), rows
