@@ -224,6 +224,8 @@ struct Layout {
   size_t res = 0, scratch = 0, part = 0, counters = 0, status = 0, badrow = 0, total = 0;
   size_t kmat = 0;                // fused: K = 2^A2 [D1p][D2p]
   size_t sep_ax = 0, sep_ay = 0;   // separable grid: Ax [nx][nblk*32], Ay [ny][sep_ld(ny)]
+  bool sep_split = false;          // large grids: the two-kernel separable sweep
+  size_t sep_tg = 0, sep_rg = 0;   // its T (and tail R) [B][nblk][ny][32]
   size_t f2T = 0, g2T[2] = {0, 0}; // separable grid: the potentials transposed per lane
   size_t part_bytes = 0, counter_count = 0;
   int lane_nsplit = 1, lane_nj = 1, lane_vec = 4;
@@ -270,6 +272,11 @@ bool sep_fits(const sinkhorn_problem_v1& pr) {
   return sep_smem_floats<SepGridShape>((int)pr.grid_nx, (int)pr.grid_ny, true) * 4 <=
          kSepSmemLimit;
 }
+// the two-kernel split (sweep_sep.cuh sep_step1/2_kernel): O(n * 96) floats
+bool sep_split_fits(const sinkhorn_problem_v1& pr) {
+  return sep_split1_floats<SepGridShape>((int)pr.grid_nx) * 4 <= kSepSmemLimit &&
+         sep_split2_floats<SepGridShape>((int)pr.grid_ny, true) * 4 <= kSepSmemLimit;
+}
 
 // Grid costs run the separable sweeps on lane-major buffers unless the dense
 // on-the-fly tiled sweeps are requested (SINKHORN_FLAG_DENSE_GRID) or the grid
@@ -282,8 +289,16 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
   L.d2 = pr.d2;
   L.gemm = gemm && pr.cost_kind == SINKHORN_COST_SHARED;
   L.fused = !L.gemm && fused && fused_eligible(pr);
-  if (pr.cost_kind == SINKHORN_COST_GRID2D && !sep_fits(pr)) dense_grid = true;
+  static const bool force_split = getenv("SKB_SEP_SPLIT") != nullptr;   // diagnostics / tests
+  if (pr.cost_kind == SINKHORN_COST_GRID2D && !dense_grid) {
+    L.sep_split = force_split || !sep_fits(pr);
+    // degenerate aspect (nx*ny/(nx+ny) < 8: the separable saving is below 8x)
+    // or too large even for the split kernels: the dense on-the-fly sweeps
+    const double gain = (double)pr.grid_nx * pr.grid_ny / (double)(pr.grid_nx + pr.grid_ny);
+    if (L.sep_split && (!sep_split_fits(pr) || (!force_split && gain < 8.0))) dense_grid = true;
+  }
   L.sep = pr.cost_kind == SINKHORN_COST_GRID2D && !dense_grid;
+  if (!L.sep) L.sep_split = false;
   L.tiled = !L.fused && !L.gemm && (pr.cost_kind == SINKHORN_COST_SHARED ||
                                     (pr.cost_kind == SINKHORN_COST_GRID2D && dense_grid));
   Carver c;
@@ -436,6 +451,11 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     L.f2T = c.take((size_t)L.B * L.D1p * 4);
     L.g2T[0] = c.take((size_t)L.B * L.D2p * 4);
     L.g2T[1] = c.take((size_t)L.B * L.D2p * 4);
+    if (L.sep_split) {
+      const size_t tsz = (size_t)pr.B * nblk * pr.grid_ny * 32 * 4;
+      L.sep_tg = c.take(tsz);
+      L.sep_rg = c.take(tsz);
+    }
   }
   L.scratch = c.take(64);
   L.counters = c.take(std::max<size_t>(L.counter_count, 1) * 4);
@@ -730,6 +750,26 @@ struct Solve {
     p.est_src = est_src;
     p.redo = at<unsigned int>(ws, L.scratch + 48);
     const bool tail = mode == kModeTail;
+    if (L.sep_split) {   // large grid: step 1 -> T in global -> step 2
+      p.tg = F(L.sep_tg);
+      p.rg = F(L.sep_rg);
+      const size_t sm1 = sep_split1_floats<SepS>(p.nx) * 4;
+      const size_t sm2 = sep_split2_floats<SepS>(p.ny, tail) * 4;
+      auto k1 = tail ? &sep_step1_kernel<SepS, kModeTail> : &sep_step1_kernel<SepS, kModeUpdate>;
+      auto k2 = tail ? &sep_step2_kernel<SepS, kModeTail> : &sep_step2_kernel<SepS, kModeUpdate>;
+      if (int e = set_max_smem(reinterpret_cast<const void*>(k1), sm1)) return e;
+      if (int e = set_max_smem(reinterpret_cast<const void*>(k2), sm2)) return e;
+      const unsigned mblk = (unsigned)((p.ny + SepS::MT - 1) / SepS::MT);
+      kt_mark(st);
+      for (long long b0 = 0; b0 < pr.B; b0 += kMaxLanesPerLaunch) {
+        p.b0 = (int)b0;
+        const dim3 grid((unsigned)p.nblk, mblk, lanes_in_launch(pr.B, b0));
+        CK(launch_pdl(k1, grid, dim3(SepS::NT), sm1, st, p));
+        CK(launch_pdl(k2, grid, dim3(SepS::NT), sm2, st, p));
+      }
+      kt_mark(st);
+      return 0;
+    }
     const size_t smem = sep_smem_floats<SepS>(p.nx, p.ny, tail) * 4;
     auto kern = tail ? &sep_sweep_kernel<SepS, kModeTail> : &sep_sweep_kernel<SepS, kModeUpdate>;
     if (int e = set_max_smem(reinterpret_cast<const void*>(kern), smem)) return e;

@@ -47,6 +47,8 @@ struct SepParams {
   const float* est_src;    // previous potential of this orientation (estimate mode) or null
   unsigned int* redo;      // count of thread tiles redone exactly (statistics)
   unsigned long long* dbg; // optional per-CTA timeline (diagnostics), nullable
+  float* tg;               // split sweeps: T per (lane, jx block) [B][nblk][ny][NB]
+  float* rg;               // split sweeps, tail: the E0 weights R, same layout
 };
 
 // Estimate mode: the shifted sum must stay inside [2^kSepLo, 2^kSepHi] so no
@@ -427,6 +429,145 @@ __global__ void __launch_bounds__(S::NT, 4) sep_sweep_kernel(const SepParams p) 
   if (p.dbg) {
     __syncthreads();
     if (tid == 0) p.dbg[4 * cta + 2] = globaltimer_ns();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Split separable sweep for grids whose lane potential and Ay table do not fit
+// one CTA's shared memory (the fused kernel above stages 2 n^2 floats): the
+// two nested LSE-GEMMs become two kernels with T in global memory, each CTA
+// owning one 64-row m block (kSepBlk = S::MT) of its step --
+//   step 1 (lane, jx block, iy block):  T(iy, n) = LSE_ix(x(iy, ix) + Ax(ix, n))
+//   step 2 (lane, jx block, jy block):  lse(jy, n) = LSE_iy(Ay(iy, jy) + T(iy, n))
+// -- so shared memory is O(n * 96) floats: grids up to ~590 x 450.  Same
+// arithmetic, estimate mode and tail weights as the fused kernel.
+template <class S>
+__host__ __device__ inline size_t sep_split1_floats(int nx) {
+  return (size_t)nx * S::MT + (size_t)nx * S::NB + S::MT;     // XT block [ix][64], Ax block
+}
+template <class S>
+__host__ __device__ inline size_t sep_split2_floats(int ny, bool tail) {
+  return (size_t)ny * S::MT + (size_t)ny * S::NB * (tail ? 2 : 1) + S::MT;   // Ay block, T (, R)
+}
+
+template <class S, int kMode>
+__global__ void __launch_bounds__(S::NT, 2) sep_step1_kernel(const SepParams p) {
+  constexpr bool kTail = (kMode == kModeTail);
+  constexpr int NB = S::NB, RN = S::RN, NT = S::NT, MB = S::MT;
+  extern __shared__ __align__(16) float sep_smem[];
+  const int nx = p.nx, ny = p.ny;
+  float* XT = sep_smem;                 // [nx][MB]: x(iy0 + m, ix) transposed
+  float* AX = XT + (size_t)nx * MB;     // [nx][NB]
+  const int b = p.b0 + blockIdx.z;
+  const int jx0 = blockIdx.x * NB, iy0 = blockIdx.y * MB;
+  const int niy = min(MB, ny - iy0);
+  const int tid = threadIdx.x, tn = tid % S::TN, tm = tid / S::TN;
+  sep_stage_rows<NT>(AX, NB, p.ax_tab + jx0, (size_t)p.nblk * NB, nx, NB);
+  cp_async_commit();
+  pdl_wait();   // x is the previous sweep's output
+  sep_stage_rows<NT>(XT, MB, p.xT + (size_t)b * p.ld + iy0, (size_t)ny, nx, niy);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  pdl_launch_dependents();
+  float mx[S::OUT], sm[S::OUT], w[S::OUT];
+  bool done = false;
+  if (!kTail && p.est_src != nullptr) {
+    done = sep_estimate<S>(p, b, iy0, jx0, mx) &&
+           (p.use_poly ? sep_lse_gemm<S, 0, true, true>(XT, MB, AX, nullptr, nx, 0, p.cinv, mx, sm, w)
+                       : sep_lse_gemm<S, 0, false, true>(XT, MB, AX, nullptr, nx, 0, p.cinv, mx, sm, w));
+    if (!done && p.redo) atomicAdd(p.redo, 1u);
+  }
+  if (done) {
+  } else if (!kTail && p.use_poly)
+    sep_lse_gemm<S, 0, true>(XT, MB, AX, nullptr, nx, 0, p.cinv, mx, sm, w);
+  else
+    sep_lse_gemm<S, kTail ? 1 : 0, false>(XT, MB, AX, nullptr, nx, 0, p.cinv, mx, sm, w);
+  float* T = p.tg + ((size_t)b * p.nblk + blockIdx.x) * ny * NB;
+  float* R = kTail ? p.rg + ((size_t)b * p.nblk + blockIdx.x) * ny * NB : nullptr;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int m = tm * 4 + a;
+    if (m >= niy) continue;
+#pragma unroll
+    for (int c = 0; c < RN; ++c) {
+      const int e = a * RN + c;
+      T[(size_t)(iy0 + m) * NB + tn * RN + c] = lse_final(mx[e], sm[e]);
+      if (kTail) R[(size_t)(iy0 + m) * NB + tn * RN + c] = (sm[e] > 0.f) ? w[e] / sm[e] : 0.f;
+    }
+  }
+}
+
+template <class S, int kMode>
+__global__ void __launch_bounds__(S::NT, 2) sep_step2_kernel(const SepParams p) {
+  constexpr bool kTail = (kMode == kModeTail);
+  constexpr int NB = S::NB, RN = S::RN, NT = S::NT, MB = S::MT;
+  extern __shared__ __align__(16) float sep_smem[];
+  const int nx = p.nx, ny = p.ny, ldm = sep_ld(ny);
+  float* AY = sep_smem;                 // [ny][MB]: Ay(iy, jy0 + m)
+  float* T = AY + (size_t)ny * MB;      // [ny][NB]
+  float* R = T + (size_t)ny * NB;       // [ny][NB], tail only
+  __shared__ unsigned int s_res;
+  const int b = p.b0 + blockIdx.z;
+  const int jx0 = blockIdx.x * NB, jy0 = blockIdx.y * MB;
+  const int njy = min(MB, ny - jy0);
+  const int tid = threadIdx.x, tn = tid % S::TN, tm = tid / S::TN;
+  if (tid == 0) s_res = 0u;
+  sep_stage_rows<NT>(AY, MB, p.ay_tab + jy0, (size_t)ldm, ny, njy);
+  cp_async_commit();
+  pdl_wait();   // T is step 1's output
+  const size_t tb = ((size_t)b * p.nblk + blockIdx.x) * ny * NB;
+  sep_stage_rows<NT>(T, NB, p.tg + tb, (size_t)NB, ny, NB);
+  if (kTail) sep_stage_rows<NT>(R, NB, p.rg + tb, (size_t)NB, ny, NB);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  pdl_launch_dependents();
+  float mx[S::OUT], sm[S::OUT], w[S::OUT];
+  bool done = false;
+  if (!kTail && p.est_src != nullptr) {
+    done = sep_estimate<S>(p, b, jy0, jx0, mx) &&
+           (p.use_poly ? sep_lse_gemm<S, 0, true, true>(AY, MB, T, R, ny, 0, p.cinv, mx, sm, w)
+                       : sep_lse_gemm<S, 0, false, true>(AY, MB, T, R, ny, 0, p.cinv, mx, sm, w));
+    if (!done && p.redo) atomicAdd(p.redo, 1u);
+  }
+  if (done) {
+  } else if (!kTail && p.use_poly)
+    sep_lse_gemm<S, 0, true>(AY, MB, T, R, ny, 0, p.cinv, mx, sm, w);
+  else
+    sep_lse_gemm<S, kTail ? 2 : 0, false>(AY, MB, T, R, ny, 0, p.cinv, mx, sm, w);
+  float rmax = 0.f;
+  const int jxb = jx0 + tn * RN;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int m = tm * 4 + a;
+    if (m >= njy) continue;
+    const int jy = jy0 + m;
+#pragma unroll
+    for (int c = 0; c < RN; ++c) {
+      const int jx = jxb + c;
+      if (jx >= nx) continue;
+      const int e = a * RN + c;
+      const size_t k = (size_t)b * p.ld + (size_t)jy * nx + jx;
+      const float lse = lse_final(mx[e], sm[e]);
+      if (kTail) {
+        const float ov = p.old[k];
+        p.out[k] = (w[e] > 0.f) ? (mx[e] + log2f(w[e]) + ov) : neg_inf();
+        rmax = fmaxf(rmax, fabsf(exp2f(ov + lse) - p.marg[k]));
+      } else {
+        const float nv = sweep_out(p.target[k], lse);
+        p.out[k] = nv;
+        p.outT[(size_t)b * p.ld + (size_t)jx * ny + jy] = nv;   // the next sweep's layout
+        if (p.res_kind == kResRow) rmax = fmaxf(rmax, fabsf(exp2f(nv + lse) - p.marg[k]));
+        if (p.res_kind == kResCol) rmax = fmaxf(rmax, fabsf(exp2f(p.old[k] + lse) - p.marg[k]));
+      }
+    }
+  }
+  if (kTail || p.res_kind != kResNone) {
+    if (rmax != rmax) rmax = __int_as_float(0x7fc00000);
+    atomicMax(&s_res, __float_as_uint(rmax));
+    __syncthreads();
+    if (tid == 0) atomic_max_nonneg(&p.res[b], __uint_as_float(s_res));
   }
 }
 

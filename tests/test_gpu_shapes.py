@@ -141,3 +141,27 @@ def test_grid_costs_of_any_aspect(nx, ny, cuda):
     rel = ((res.cost_e0.double() - ref.cost_e0.double()).abs() / ref.cost_e0.double()).max()
     assert float(rel) <= 2e-6
     assert float((res.log_u - ref.log_u).abs().max()) <= 1e-4
+
+
+@pytest.mark.parametrize("nx,ny", [(150, 160), (200, 96), (64, 420)])
+def test_large_grids_take_the_split_separable_sweeps(nx, ny, cuda):
+    """Grids too large for the one-kernel separable sweep run the two-kernel
+    split (T through global memory) instead of the dense sweeps: equal to the
+    dense on-the-fly path, with a lockstep stop."""
+    import paper_1907_01729_b200 as skb
+
+    B, d = 3, nx * ny
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(nx + ny)
+    m = torch.rand(B, d, generator=gen, device=cuda, dtype=torch.float64) + 0.5
+    mu = (m / m.sum(1, keepdim=True)).float()
+    nu = mu.flip(0).contiguous()
+    gc = skb.GridCost(nx, ny)
+    for iters, tol in ((12, 0.0), (300, 1e-4)):
+        res = skb.solve(mu, nu, gc, 0.01, iters, tol)
+        assert res.path == "separable"
+        ref = skb.solve(mu, nu, gc, 0.01, iters, tol, dense_grid=True)
+        assert res.iterations_run == ref.iterations_run
+        rel = ((res.cost_e0.double() - ref.cost_e0.double()).abs() / ref.cost_e0.double()).max()
+        assert float(rel) <= 2e-6
+        assert float((res.log_u - ref.log_u).abs().max()) <= 1e-4
