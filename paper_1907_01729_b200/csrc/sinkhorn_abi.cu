@@ -247,16 +247,17 @@ constexpr int kFusedMaxNQ = kFusedMaxChunks;
 // Per-sample costs (sweep_fused.cuh fused_ps_kernel): rows of d2 <= 2048
 // floats; the bulk copies move whole 16-byte units, so d2 % 4 != 0 runs on a
 // zero-padded copy of the costs made once per solve (Layout::cpad).
-// Lanes per group of the per-sample pass: rows above 2048 (4096) columns take
-// two (four) warps per lane (fused_ps_kernel<..., kHalves>, 8 warps).
+// Lanes per group of the per-sample pass: rows above 2048 (4096, 8192) columns
+// take two (four, eight) warps per lane (fused_ps_kernel<..., kHalves>, 8 warps).
 int ps_group_lanes(int d2p) {
   const int nq = d2p / 64;
-  return nq <= kPsMaxChunks ? fused_warps(nq) : nq <= 2 * kPsMaxChunks ? 4 : 2;
+  return nq <= kPsMaxChunks ? fused_warps(nq) : nq <= 2 * kPsMaxChunks ? 4
+                                             : nq <= 4 * kPsMaxChunks ? 2 : 1;
 }
 bool fused_eligible(const sinkhorn_problem_v1& pr) {
   if (pr.B < 1) return false;
   if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE)   // d2 % 4 != 0: through a padded copy
-    return round_up(pr.d2, TILE_PAD) <= 4 * 64 * kPsMaxChunks;   // > 2048: 2 or 4 warps per lane
+    return round_up(pr.d2, TILE_PAD) <= 8 * 64 * kPsMaxChunks;   // > 2048: 2, 4 or 8 warps per lane
   return pr.cost_kind == SINKHORN_COST_SHARED &&
          round_up(pr.d1, TILE_PAD) <= 64 * kFusedMaxNQ && round_up(pr.d2, TILE_PAD) <= 64 * kFusedMaxNQ;
 }
@@ -932,11 +933,21 @@ struct Solve {
   template <int NQ>
   int launch_fused_ps4(const FusedParams& fp) {
     if constexpr (NQ > kPsMaxChunks) {
-      return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
+      return launch_fused_ps8<kPsMaxChunks / 2 + 2>(fp);
     } else {
       if ((((fp.nq + 3) / 4) + 1) / 2 * 2 != NQ) return launch_fused_ps4<NQ + 2>(fp);
       return fp.e0 != nullptr ? launch_fused_ps_t<NQ, true, 4>(fp)
                               : launch_fused_ps_t<NQ, false, 4>(fp);
+    }
+  }
+  template <int NQ>
+  int launch_fused_ps8(const FusedParams& fp) {
+    if constexpr (NQ > kPsMaxChunks) {
+      return fail(SINKHORN_STATUS_BAD_ARGUMENT, "fused pass: row too long");
+    } else {
+      if ((((fp.nq + 7) / 8) + 1) / 2 * 2 != NQ) return launch_fused_ps8<NQ + 2>(fp);
+      return fp.e0 != nullptr ? launch_fused_ps_t<NQ, true, 8>(fp)
+                              : launch_fused_ps_t<NQ, false, 8>(fp);
     }
   }
   template <int NQ>

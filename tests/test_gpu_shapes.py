@@ -21,7 +21,7 @@ torch = pytest.importorskip("torch")
 SHAPES = [(1, 1, 1), (1, 1, 7), (3, 7, 1), (2, 5, 129), (5, 129, 5), (1, 1025, 3), (4, 63, 65),
           (2, 257, 1023), (3, 1030, 70), (65, 33, 31), (2, 2049, 17), (3, 300, 1500),
           (2, 130, 2048), (2, 64, 2052), (5, 40, 3001), (2, 33, 4096), (1, 20, 4097),
-          (2, 9, 8192), (1, 5, 8193)]
+          (2, 9, 8192), (1, 5, 8193), (2, 6, 12000), (1, 4, 16384), (1, 3, 16385)]
 SHARED_PATHS = {"auto": {}, "tiled": {"tiled_only": True, "fused": False, "gemm": False},
                 "fused": {"tiled_only": True}, "gemm": {"tiled_only": True, "gemm": True}}
 PER_SAMPLE_PATHS = {"auto": {}, "lane": {"fused": False}}

@@ -13,7 +13,7 @@ g = torch.Generator(device=dev)
 g.manual_seed(0)
 for B, d in [(1024, 1024), (448, 1536), (256, 2048), (300, 1800), (1024, 1023), (256, 2047),
              (110, 3100), (64, 4096), (64, 4095), (180, 2500), (42, 5000), (16, 8192),
-             (20, 7001)]:
+             (20, 7001), (8, 12000), (4, 16384)]:
     m = torch.rand(B, d, generator=g, device=dev, dtype=torch.float64) + 0.5
     mu = (m / m.sum(1, keepdim=True)).float()
     nu = mu.flip(0).contiguous()
