@@ -77,7 +77,8 @@ struct SepShape {
 __host__ __device__ inline int sep_ld(int n) { return (n + 3) & ~3; }
 template <class S>
 __host__ __device__ inline size_t sep_smem_floats(int nx, int ny, bool tail) {
-  return std::max((size_t)nx * sep_ld(ny), (size_t)S::NB * (ny + 1))   // XT [ix][iy] / OT [n][jy]
+  const size_t xt = (size_t)nx * sep_ld(ny), ot = (size_t)S::NB * (ny + 1);
+  return (xt > ot ? xt : ot)        // XT [ix][iy] / OT [n][jy]
          + (size_t)nx * S::NB      // Ax block [ix][n]
          + (size_t)ny * sep_ld(ny) // Ay [iy][jy]
          + (size_t)ny * S::NB      // T  [iy][n]
