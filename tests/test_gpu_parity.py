@@ -603,3 +603,32 @@ def test_small_solver_clusters_match_tiled(B, d1, d2, cuda):
         assert float(rel) <= 2e-6
         assert float((res.log_u - ref.log_u).abs().max()) <= 1e-4
         assert float((res.log_v - ref.log_v).abs().max()) <= 1e-4
+
+
+@pytest.mark.parametrize("kind,d,kw", [("shared", 300, {"tiled_only": True}),
+                                       ("shared", 1100, {"tiled_only": True, "gemm": True}),
+                                       ("per_sample", 256, {}),
+                                       ("per_sample", 3000, {})])
+def test_graph_replay_equals_eager(kind, d, kw, cuda):
+    """Tolerance-0 solves repeated on the same workspace and cost are captured
+    as one CUDA graph on the second call and replayed from the third (fused
+    passes and the GEMM iteration): every call returns the same numbers."""
+    skb = _skb()
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(d)
+    B = 6
+
+    def hist():
+        m = torch.rand(B, d, generator=gen, device=cuda, dtype=torch.float64) + 0.5
+        return (m / m.sum(1, keepdim=True)).float()
+    mu, nu = hist(), hist()
+    if kind == "shared":
+        c = torch.rand(d, d, generator=gen, device=cuda)
+    else:
+        c = torch.rand(B, d, d, generator=gen, device=cuda)
+    runs = [skb.solve(mu, nu, c, 0.05, 30, 0.0, **kw) for _ in range(4)]
+    for r in runs[1:]:
+        assert r.path == runs[0].path
+        assert torch.equal(r.cost_e0, runs[0].cost_e0)
+        assert torch.equal(r.log_u, runs[0].log_u)
+        assert torch.equal(r.log_v, runs[0].log_v)
