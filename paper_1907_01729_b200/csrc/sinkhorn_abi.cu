@@ -379,7 +379,9 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
                                                             : fused_warps(L.D2p / 64);
     const long long groups = (pr.B + nw - 1) / nw;
     const long long U = groups * pr.d1;
-    L.fused_nct = (int)std::max<long long>(1, std::min<long long>(sms, U));
+    const int occ = pr.cost_kind == SINKHORN_COST_PER_SAMPLE ? ps_ctas_per_sm(L.D2p / 64) : 1;
+    L.fused_nct = (int)std::max<long long>(
+        1, std::min<long long>(std::min<long long>((long long)sms * occ, kFusedMaxCtas), U));
     const long long per = (U + L.fused_nct - 1) / L.fused_nct;
     L.fused_maxseg = (int)((per - 1) / pr.d1 + 2);
     L.part_bytes = (size_t)L.fused_nct * L.fused_maxseg * nw * L.D2p * 4;

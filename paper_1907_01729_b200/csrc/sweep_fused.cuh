@@ -52,6 +52,7 @@ constexpr int kFusedWarps = 16;    // max lanes per group = warps per CTA
 __host__ __device__ constexpr int fused_warps(int nq) { return nq <= 13 ? 16 : nq <= 16 ? 12 : 8; }
 constexpr int kFusedStages = 8;    // cost rows in flight per CTA
 constexpr int kFusedMaxChunks = 16;  // row length <= 1024 columns
+constexpr int kFusedMaxCtas = 1024;   // CTAs of one fused launch (sms x CTAs per SM)
 constexpr float kFusedMinColsum = 8.673617379884035e-19f;   // 2^-60
 
 struct FusedParams {
@@ -518,8 +519,20 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_pass_kernel(const FusedParam
 // the previous-lse shift and the exact fallback of the shared-cost pass.
 constexpr int kPsStages = 4;
 constexpr int kPsMaxChunks = 32;   // per-sample rows <= 2048 columns
-// ring slots per warp: 4 for rows <= 1024 columns, 3 above (192 KB either way)
-__host__ __device__ constexpr int ps_stages(int nq) { return nq <= 16 ? kPsStages : 3; }
+// CTAs per SM of the per-sample pass: short rows (<= 256 columns) are bound by
+// each warp's serial per-row chain, so two CTAs (32 warps) share an SM
+__host__ __device__ constexpr int ps_ctas_per_sm(int nq) { return nq <= 4 ? 2 : 1; }
+// ring slots per warp: ~192 KB of rows in flight per SM whatever the row
+// length, capped at 32 (4 for 1024-column rows, 3 above)
+__host__ __device__ constexpr int ps_stages(int nq) {
+  return nq <= 16 ? (196608 / ps_ctas_per_sm(nq) / ((nq <= 13 ? 16 : 12) * nq * 256) > 32
+                         ? 32
+                         : (196608 / ps_ctas_per_sm(nq) / ((nq <= 13 ? 16 : 12) * nq * 256) <
+                                    kPsStages
+                                ? kPsStages
+                                : 196608 / ps_ctas_per_sm(nq) / ((nq <= 13 ? 16 : 12) * nq * 256)))
+                  : 3;
+}
 
 template <int NQ>
 __host__ __device__ constexpr size_t fused_ps_smem_bytes() {
@@ -531,7 +544,7 @@ __host__ __device__ constexpr size_t fused_ps_smem_bytes() {
 // and maxima are combined through shared memory (fixed slice order, so every
 // warp of the lane gets the same value) behind a named barrier per exchange.
 template <int NQ, bool kTail, int NW = fused_warps(NQ), int kHalves = 1>
-__global__ void __launch_bounds__(NW * 32, 1) fused_ps_kernel(const FusedParams p, const float* cost,
+__global__ void __launch_bounds__(NW * 32, ps_ctas_per_sm(NQ)) fused_ps_kernel(const FusedParams p, const float* cost,
                                                               int d2, int ldc, float kscale) {
   extern __shared__ __align__(128) unsigned char fsm[];
   constexpr int rowlen = NQ * 64;          // columns held by one warp
@@ -1065,7 +1078,7 @@ __global__ void __launch_bounds__(kFgThreads, 1) fgemm_pass_kernel(const FusedPa
 // covered lane b's group (ascending), v'_j = v_j + l2nu_j - log2(colsum_j),
 // column residual |colsum_j - nu_j|.  grid (ceil(rowlen / 256), B).
 __global__ void __launch_bounds__(256) fused_merge_kernel(const FusedMergeParams p) {
-  __shared__ int s_off[256];  // partial rows of this lane (rowlen units), ascending CTA (nct <= 256)
+  __shared__ int s_off[kFusedMaxCtas];   // partial rows of this lane, ascending CTA
   __shared__ int s_c0, s_n;
   const int b = p.b0 + blockIdx.y;
   const int g = b / p.nw, w = b % p.nw;
@@ -1075,10 +1088,10 @@ __global__ void __launch_bounds__(256) fused_merge_kernel(const FusedMergeParams
     s_n = (int)(((ub + 1) * p.nct - 1) / p.U) - s_c0 + 1;
   }
   __syncthreads();
-  if ((int)threadIdx.x < s_n) {   // every covering CTA has >= 1 unit (U >= nct)
-    const int c = s_c0 + threadIdx.x;
+  for (int t = threadIdx.x; t < s_n; t += blockDim.x) {   // every covering CTA has >= 1 unit
+    const int c = s_c0 + t;
     const long long s0 = fused_seg_start(p.U, p.nct, c);
-    s_off[threadIdx.x] = (int)(((long long)c * p.maxseg + (g - (int)(s0 / p.nrows))) * p.nw + w);
+    s_off[t] = (int)(((long long)c * p.maxseg + (g - (int)(s0 / p.nrows))) * p.nw + w);
   }
   __syncthreads();
   pdl_wait();
