@@ -94,6 +94,18 @@ __device__ __forceinline__ long long um_start(long long U, int G, int c) {
   return U * c / G;
 }
 
+// Tiles are numbered nt-major (tile = nt * MT + mt): the CTAs a quarter (for
+// NT = 4) of the grid apart work on the same rows of A with different lane
+// tiles at about the same time, so A streams from HBM once and the other N
+// tiles' reads hit L2 (mt-major, one CTA walked the N tiles of an A block in
+// turn and re-streamed it from HBM for each).
+__device__ __forceinline__ int um_tile_mt(const UmmaParams& p, long long tile) {
+  return (int)(tile % p.MT);
+}
+__device__ __forceinline__ int um_tile_nt(const UmmaParams& p, long long tile) {
+  return (int)(tile / p.MT);
+}
+
 // The CTA whose unit range holds unit u.
 __device__ __forceinline__ int um_owner(long long U, int G, long long u) {
   int c = (int)(u * G / U);
@@ -168,7 +180,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       for (long long u = u0; u < u1; ++u) {
         const long long tile = u / p.KCH;
         const int kc = (int)(u % p.KCH);
-        const int mt = (int)(tile / p.NT);
+        const int mt = um_tile_mt(p, tile);
         mbar_wait(&afree_sm[s], ph ^ 1);
         mbar_arrive_expect_tx(&afull_sm[s], kUmATileBytes);
         const int arow = (int)(((long long)mt * p.KCH + kc) * kUmSub * kUmBM);
@@ -188,7 +200,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       for (long long u = u0; u < u1; ++u) {
         const long long tile = u / p.KCH;
         const int kc = (int)(u % p.KCH);
-        const int nt = (int)(tile % p.NT);
+        const int nt = um_tile_nt(p, tile);
         mbar_wait(&bfree_sm[s], ph ^ 1);
         uint8_t* st = smB + (size_t)s * kUmBStageBytes;
         mbar_arrive_expect_tx(&bfull_sm[s], kUmBStageBytes);
@@ -352,7 +364,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         acc[2 * n] = lo2(acc2[n]);
         acc[2 * n + 1] = hi2(acc2[n]);
       }
-      const int nt = (int)(tile % p.NT), mt = (int)(tile / p.NT);
+      const int nt = um_tile_nt(p, tile), mt = um_tile_mt(p, tile);
       const int m = mt * kUmBM + row;
       if (k0 == 0 && k1 == p.KCH) {
         if (m < p.M) {
@@ -422,7 +434,7 @@ __global__ void __launch_bounds__(256) umma_fixup_kernel(const UmmaParams p) {
   __syncthreads();
   const int np = s_n;
   if (np == 0) return;
-  const int nt = (int)(t % p.NT), mt = (int)(t / p.NT);
+  const int nt = um_tile_nt(p, t), mt = um_tile_mt(p, t);
   const int nmax = min(kUmBN, p.N - nt * kUmBN);
   for (int e = threadIdx.x; e < kUmBM * kUmBN / 4; e += 256) {
     const int n = e / (kUmBM / 4), row = 4 * (e % (kUmBM / 4));
