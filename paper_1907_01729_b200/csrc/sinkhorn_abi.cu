@@ -1387,9 +1387,15 @@ struct Solve {
 
   int plan_small(SmallParams& sp, int& G, size_t& smem, bool* ok) {
     *ok = false;
-    if (!(L.tiled || L.sep) || g_reducer != nullptr || (op.flags & SINKHORN_FLAG_TILED_ONLY))
+    // per-sample costs: the small solver reads each lane's cost once per solve
+    // instead of once per iteration, which pays below ~64 x 64 cells per lane
+    // (tools/ps_small_bench.py: d = 32 3.3x, 64 1.15x, 128 0.97x the fused pass)
+    const bool ps = pr.cost_kind == SINKHORN_COST_PER_SAMPLE && pr.d1 * pr.d2 <= 4096;
+    if (pr.cost_kind == SINKHORN_COST_PER_SAMPLE && !ps) return 0;
+    if (!(L.tiled || L.sep || ps) || g_reducer != nullptr || (op.flags & SINKHORN_FLAG_TILED_ONLY))
       return 0;
-    if (pr.cost_kind != SINKHORN_COST_SHARED && pr.cost_kind != SINKHORN_COST_GRID2D) return 0;
+    if (pr.cost_kind != SINKHORN_COST_SHARED && pr.cost_kind != SINKHORN_COST_GRID2D && !ps)
+      return 0;
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, di.dev);
     const long long d1 = pr.d1, d2 = pr.d2, B = pr.B;
@@ -1404,7 +1410,17 @@ struct Solve {
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     }
     for (int occ = 4; occ >= 1; --occ) {
-      const int Lc = (int)((B + (long long)di.sms * occ - 1) / ((long long)di.sms * occ));
+      int Lc = (int)((B + (long long)di.sms * occ - 1) / ((long long)di.sms * occ));
+      if (ps) {   // per-sample: each lane stages its own cost; as many lanes as fit (no clusters)
+        const int S0c = pick_group((long long)d2, d1), S0r = pick_group((long long)d1, d2);
+        const int ldc0 = (int)round_up(d1, 32) + (S0c % 32), ldr0 = (int)round_up(d2, 32) + (S0r % 32);
+        Lc = 0;
+        while (Lc < 16 && Lc < B &&
+               SmallSmem::floats((int)d1, (int)d2, Lc + 1, ldc0, ldr0, 1, true) * 4 <=
+                   (size_t)smem_optin / occ - 2048)
+          ++Lc;
+        if (Lc == 0) continue;
+      }
       if ((long long)Lc * d1 * d2 > kSmallMaxCells) continue;
       const int Gl = (int)((B + Lc - 1) / Lc);   // lane groups
       // spread a lane group over a cluster while SMs are left idle and every
@@ -1413,11 +1429,11 @@ struct Solve {
       // bound by its serial chain, not its cell count (config 1, d = 100:
       // C = 1 0.317 ms per loop, C = 4 0.328)
       int Cc = 1;
-      while (Cc < 8 && (long long)Gl * Cc * 2 <= di.sms && std::min(d1, d2) / (Cc * 2) >= 16 &&
+      while (!ps && Cc < 8 && (long long)Gl * Cc * 2 <= di.sms && std::min(d1, d2) / (Cc * 2) >= 16 &&
              (long long)Lc * d1 * d2 / (Cc * 2) >= 16384)
         Cc *= 2;
       static const int force_c = getenv("SKB_SMALL_C") ? atoi(getenv("SKB_SMALL_C")) : 0;
-      if (force_c > 0) Cc = force_c;   // diagnostics: cluster size A/B
+      if (force_c > 0 && !ps) Cc = force_c;   // diagnostics: cluster size A/B
       int Sc = 1, Sr = 1, ldc = 0, ldr = 0;
       size_t bytes = 0;
       for (;; Cc *= 2) {   // a larger cluster when the cost slices do not fit one CTA
@@ -1427,8 +1443,8 @@ struct Solve {
         Sr = pick_group(units_r, d2);
         ldc = (int)round_up(d1, 32) + (Sc % 32);
         ldr = (int)round_up(d2, 32) + (Sr % 32);
-        bytes = SmallSmem::floats((int)d1, (int)d2, Lc, ldc, ldr, Cc) * 4;
-        if (bytes <= (size_t)smem_optin / occ - 2048 || force_c > 0 || Cc >= 8 ||
+        bytes = SmallSmem::floats((int)d1, (int)d2, Lc, ldc, ldr, Cc, ps) * 4;
+        if (bytes <= (size_t)smem_optin / occ - 2048 || force_c > 0 || Cc >= 8 || ps ||
             (long long)Gl * Cc * 2 > di.sms || std::min(d1, d2) / (Cc * 2) < 16)
           break;
       }
@@ -1458,6 +1474,8 @@ struct Solve {
       }
       smem = bytes;
       sp = SmallParams{};
+      sp.cps = ps ? cost : nullptr;
+      sp.kscale = (float)(-kLog2e / lam);
       sp.a2 = (pr.cost_kind == SINKHORN_COST_SHARED) ? F(L.a2) : nullptr;
       sp.a2t = (pr.cost_kind == SINKHORN_COST_SHARED) ? F(L.a2t) : nullptr;
       sp.D1p = L.D1p;

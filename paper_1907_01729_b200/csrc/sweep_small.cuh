@@ -60,6 +60,8 @@ struct SmallParams {
   int* result;        // [0] iterations_run
   int* status;
   unsigned long long* dbg;   // optional timeline of CTA 0 (diagnostics), nullable
+  const float* cps;   // per-sample costs (B, d1, d2) staged per lane (C = 1), else null
+  float kscale;       // per-sample: A2 = c * kscale (-log2 e / lambda)
 };
 
 __host__ __device__ inline int small_slice(int n, int C, int r) { return (int)((long long)n * r / C); }
@@ -76,14 +78,16 @@ struct SmallSmem {
   float* mu;   // [L][d1]
   float* nu;   // [L][d2]
   unsigned int* rres;   // [L] residual maxima (non-negative float bits)
-  __host__ __device__ static size_t floats(int d1, int d2, int L, int ldc, int ldr, int C) {
-    return (size_t)small_rows(d1, C) * ldr + (size_t)small_rows(d2, C) * ldc +
+  __host__ __device__ static size_t floats(int d1, int d2, int L, int ldc, int ldr, int C,
+                                           bool ps = false) {
+    return ((size_t)small_rows(d1, C) * ldr + (size_t)small_rows(d2, C) * ldc) * (ps ? L : 1) +
            (size_t)L * (3 * d1 + 5 * d2) + L + 8;
   }
   __device__ SmallSmem(float* base, const SmallParams& p) {
+    const size_t nl = p.cps != nullptr ? (size_t)p.L : 1;   // per-sample: a cost per lane
     A = base;
-    AT = A + (size_t)small_rows(p.d1, p.C) * p.ldr;
-    f = AT + (size_t)small_rows(p.d2, p.C) * p.ldc;
+    AT = A + (size_t)small_rows(p.d1, p.C) * p.ldr * nl;
+    f = AT + (size_t)small_rows(p.d2, p.C) * p.ldc * nl;
     g0 = f + (size_t)p.L * p.d1;
     g1 = g0 + (size_t)p.L * p.d2;
     lmu = g1 + (size_t)p.L * p.d2;
@@ -198,7 +202,7 @@ __device__ __forceinline__ void small_sweep_s(const float* __restrict__ M, int l
                                               const float* __restrict__ old, const float* prev,
                                               float* out, unsigned int* rres, float cinv,
                                               float* const* peers, const float* local_base, int C,
-                                              int self) {
+                                              int self, long long mls) {
   const int tid = threadIdx.x;
   constexpr int gpr = NT / S;   // groups per round
   const int s = tid % S;
@@ -211,7 +215,7 @@ __device__ __forceinline__ void small_sweep_s(const float* __restrict__ M, int l
     const int os = active ? u - l * ns : 0;
     const int o = o0 + os;
     const int idx = l * nout + o;
-    const float* mrow = M + (size_t)os * ld;
+    const float* mrow = M + (size_t)l * mls + (size_t)os * ld;   // mls: per-lane costs
     const float* xl = x + (size_t)l * nin;
     float m, sum, w = 0.f;
     bool exact = true;
@@ -269,11 +273,11 @@ __device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld,
                                             const float* __restrict__ old, const float* prev,
                                             float* out, unsigned int* rres, float cinv,
                                             float* const* peers, const float* local_base, int C,
-                                            int self) {
+                                            int self, long long mls = 0) {
 #define SKB_SMALL_CASE(SS)                                                                      \
   case SS:                                                                                      \
     small_sweep_s<NT, kRes, SS>(M, ld, nout, o0, o1, nin, nl, x, target, marg, old, prev, out,  \
-                                rres, cinv, peers, local_base, C, self);                        \
+                                rres, cinv, peers, local_base, C, self, mls);                   \
     break;
   switch (S) {
     SKB_SMALL_CASE(1)
@@ -283,7 +287,7 @@ __device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld,
     SKB_SMALL_CASE(16)
     default:
       small_sweep_s<NT, kRes, 32>(M, ld, nout, o0, o1, nin, nl, x, target, marg, old, prev, out,
-                                  rres, cinv, peers, local_base, C, self);
+                                  rres, cinv, peers, local_base, C, self, mls);
   }
 #undef SKB_SMALL_CASE
 }
@@ -328,6 +332,20 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
       const float dx = float(xi) - float(xj), dy = float(yi) - float(yj);
       sm.AT[(size_t)jl * p.ldc + i] = p.gk * fmaf(p.ghx2, dx * dx, p.ghy2 * dy * dy);
     }
+  } else if (p.cps != nullptr) {   // per-sample: each lane's own cost (C = 1), validated here
+    bool bad = false;
+    const size_t lc = (size_t)p.d1 * p.d2;
+    for (long long e = tid; e < (long long)nl * lc; e += NT) {
+      const int l = (int)(e / lc);
+      const int k = (int)(e - (long long)l * lc);
+      const int i = k / p.d2, j = k - i * p.d2;
+      const float cv = p.cps[(size_t)(b0 + l) * lc + k];
+      if (!(cv >= 0.f) || isinf(cv)) bad = true;
+      const float a = cv * p.kscale;
+      sm.A[(size_t)l * p.d1 * p.ldr + (size_t)i * p.ldr + j] = a;
+      sm.AT[(size_t)l * p.d2 * p.ldc + (size_t)j * p.ldc + i] = a;
+    }
+    if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) set_status(p.status, 15);
   } else {
     for (int e = tid; e < ni * p.d2; e += NT) {
       const int il = e / p.d2, j = e - il * p.d2;
@@ -367,7 +385,8 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
     if (!have_next) {
       small_sweep<NT, 0>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, sm.lnu, nullptr,
                          nullptr, sm.g(cur), sm.g(cur ^ 1), nullptr, 0.f, peers, small_smem, C,
-                         crank);
+                         crank,
+                         p.cps ? (long long)p.d2 * p.ldc : 0);
       if (tl && k <= 8) p.dbg[4 * k] = globaltimer_ns();
       small_sync(C);
       if (tl && k <= 8) p.dbg[4 * k + 1] = globaltimer_ns();
@@ -380,10 +399,12 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
       for (int l = tid; l < nl; l += NT) sm.rres[l] = 0u;
       __syncthreads();
       small_sweep<NT, 1>(sm.A, p.ldr, p.d1, i0, i1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, sm.mu,
-                         nullptr, sm.f, sm.f, sm.rres, 0.f, peers, small_smem, C, crank);
+                         nullptr, sm.f, sm.f, sm.rres, 0.f, peers, small_smem, C, crank,
+                         p.cps ? (long long)p.d1 * p.ldr : 0);
     } else {
       small_sweep<NT, 0>(sm.A, p.ldr, p.d1, i0, i1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, nullptr,
-                         nullptr, sm.f, sm.f, nullptr, 0.f, peers, small_smem, C, crank);
+                         nullptr, sm.f, sm.f, nullptr, 0.f, peers, small_smem, C, crank,
+                         p.cps ? (long long)p.d1 * p.ldr : 0);
     }
     if (tl && k <= 8) p.dbg[4 * k + 2] = globaltimer_ns();
     small_sync(C);
@@ -393,7 +414,8 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
       // column sweep k+1 doubles as the column residual of iteration k
       small_sweep<NT, 2>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, sm.lnu, sm.nu,
                          sm.g(cur), sm.g(cur), sm.g(cur ^ 1), sm.rres, 0.f, peers, small_smem, C,
-                         crank);
+                         crank,
+                         p.cps ? (long long)p.d2 * p.ldc : 0);
       small_sync(C);
       // every CTA publishes the max over its lanes and slices; all CTAs read
       // all of them behind a grid barrier and take the same decision
@@ -425,7 +447,8 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
   // ---- tail: column residual + E0 terms, then export (batch.py:323-337) -----
   float* e0t = sm.g(cur ^ 1);
   small_sweep<NT, 3>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, nullptr, sm.nu, sm.g(cur),
-                     nullptr, e0t, sm.rres, p.cinv, peers, small_smem, C, crank);
+                     nullptr, e0t, sm.rres, p.cinv, peers, small_smem, C, crank,
+                     p.cps ? (long long)p.d2 * p.ldc : 0);
   small_sync(C);
   // the lane residual is the max over the cluster's slices (peer reads)
   if (C > 1 && crank == 0) {

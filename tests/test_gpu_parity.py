@@ -184,7 +184,8 @@ def test_fused_per_sample_ragged_shapes_against_oracle(B, d1, d2, tol, cuda):
     refs = [orc.batch_forward(mu[b:b + 1], nu[b:b + 1], c[b], lam, max_iters=iters,
                               tolerance=0.0, check_interval=10) for b in range(B)]
     res = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda),
-                    torch.tensor(c, dtype=torch.float32, device=cuda), lam, iters, 0.0, 10)
+                    torch.tensor(c, dtype=torch.float32, device=cuda), lam, iters, 0.0, 10,
+                    tiled_only=True)   # (small lanes would take the single-launch solver)
     assert res.path == "fused"
     want = np.array([r.cost_e0[0] for r in refs])
     rel = np.abs(res.cost_e0.double().cpu().numpy() - want) / want
@@ -196,10 +197,11 @@ def test_fused_per_sample_ragged_shapes_against_oracle(B, d1, d2, tol, cuda):
     assert np.abs(lu[fu] - ref_lu[fu]).max() <= 1e-3 * max(1.0, np.abs(ref_lu[fu]).max())
     if tol > 0:   # lockstep stop: the same iteration count as the unfused lane kernels
         a = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda),
-                      torch.tensor(c, dtype=torch.float32, device=cuda), lam, 400, tol, 10)
+                      torch.tensor(c, dtype=torch.float32, device=cuda), lam, 400, tol, 10,
+                      tiled_only=True)
         b_ = skb.solve(torch.tensor(mu, device=cuda), torch.tensor(nu, device=cuda),
                        torch.tensor(c, dtype=torch.float32, device=cuda), lam, 400, tol, 10,
-                       fused=False)
+                       fused=False, tiled_only=True)
         assert a.path == "fused" and b_.path == "lane"
         assert a.iterations_run == b_.iterations_run
 
@@ -632,3 +634,35 @@ def test_graph_replay_equals_eager(kind, d, kw, cuda):
         assert torch.equal(r.cost_e0, runs[0].cost_e0)
         assert torch.equal(r.log_u, runs[0].log_u)
         assert torch.equal(r.log_v, runs[0].log_v)
+
+
+
+@pytest.mark.parametrize("B,d1,d2,tol", [(37, 50, 68, 0.0), (300, 16, 20, 1e-5), (5, 64, 64, 0.0),
+                                         (2000, 7, 9, 0.0)])
+def test_small_solver_per_sample_against_oracle(B, d1, d2, tol, cuda):
+    """Per-sample costs of <= 64 x 64 cells per lane take the single-launch
+    solver (each lane's cost staged once, validated there): against the
+    reference lane by lane, zero-mass bins and lockstep stops included."""
+    skb = _skb()
+    from oracle import sinkhorn_oracle as orc
+
+    rng = np.random.default_rng(B + d1 * 3 + d2)
+    mu = orc.fp32_exact(orc.random_histogram_batch(B, d1, rng))
+    nu = orc.fp32_exact(orc.random_histogram_batch(B, d2, rng))
+    mu[1 % B, 3 % d1] = 0.0
+    mu[1 % B] = orc.fp32_exact(mu[1 % B] / mu[1 % B].sum())
+    c = orc.fp32_exact(rng.random((B, d1, d2)) * 2.0)
+    lam, iters = 0.1, 400 if tol > 0 else 40
+    t = lambda a: torch.tensor(a, dtype=torch.float32, device=cuda)   # noqa: E731
+    res = skb.solve(t(mu), t(nu), t(c), lam, iters, tol, 10)
+    assert res.path == "small"
+    ref = orc.per_sample_forward(mu, nu, c, lam, iters, tol, 10)
+    assert res.iterations_run == ref.iterations_run
+    rel = np.abs(res.cost_e0.double().cpu().numpy() - ref.cost_e0) / ref.cost_e0
+    assert rel.max() <= LOSS_RTOL
+    fused = skb.solve(t(mu), t(nu), t(c), lam, iters, tol, 10, tiled_only=True)
+    assert fused.iterations_run == res.iterations_run
+    bad = c.copy()
+    bad[B - 1, d1 - 1, d2 - 1] = -1.0
+    with pytest.raises(skb.InvalidCost):
+        skb.solve(t(mu), t(nu), t(bad), lam, iters, tol, 10)
