@@ -1399,7 +1399,7 @@ struct Solve {
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, di.dev);
     const long long d1 = pr.d1, d2 = pr.d2, B = pr.B;
-    auto kern = &small_solve_kernel<kSmallNT>;
+    auto kern = ps ? &small_solve_kernel<kSmallNT, true> : &small_solve_kernel<kSmallNT, false>;
     {
       cudaFuncAttributes fa = {};
       CK(cudaFuncGetAttributes(&fa, kern));
@@ -1553,7 +1553,9 @@ struct Solve {
     }
     ++g_launches;
     kt_mark(st);
-    CK(cudaLaunchKernelEx(&cfg, &small_solve_kernel<kSmallNT>, sp));
+    CK(cudaLaunchKernelEx(&cfg, sp.cps != nullptr ? &small_solve_kernel<kSmallNT, true>
+                                                 : &small_solve_kernel<kSmallNT, false>,
+                          sp));
     kt_mark(st);
     if (tl) {
       unsigned long long h[64];

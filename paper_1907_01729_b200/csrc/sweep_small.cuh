@@ -83,8 +83,8 @@ struct SmallSmem {
     return ((size_t)small_rows(d1, C) * ldr + (size_t)small_rows(d2, C) * ldc) * (ps ? L : 1) +
            (size_t)L * (3 * d1 + 5 * d2) + L + 8;
   }
-  __device__ SmallSmem(float* base, const SmallParams& p) {
-    const size_t nl = p.cps != nullptr ? (size_t)p.L : 1;   // per-sample: a cost per lane
+  __device__ SmallSmem(float* base, const SmallParams& p, bool ps) {
+    const size_t nl = ps ? (size_t)p.L : 1;   // per-sample: a cost per lane
     A = base;
     AT = A + (size_t)small_rows(p.d1, p.C) * p.ldr * nl;
     f = AT + (size_t)small_rows(p.d2, p.C) * p.ldc * nl;
@@ -193,7 +193,7 @@ __device__ __forceinline__ float small_unit_est(const float* __restrict__ row,
 //   against `old` + the E0 term written to `out`, batch.py:329-337).
 // prev: the previous potential of this orientation (the estimate source; may
 // alias out -- each output is read by its own group before it is written).
-template <int NT, int kRes, int S>
+template <int NT, int kRes, int S, bool kPS>
 __device__ __forceinline__ void small_sweep_s(const float* __restrict__ M, int ld, int nout, int o0,
                                               int o1, int nin, int nl,
                                               const float* __restrict__ x,
@@ -215,7 +215,8 @@ __device__ __forceinline__ void small_sweep_s(const float* __restrict__ M, int l
     const int os = active ? u - l * ns : 0;
     const int o = o0 + os;
     const int idx = l * nout + o;
-    const float* mrow = M + (size_t)l * mls + (size_t)os * ld;   // mls: per-lane costs
+    const float* mrow = kPS ? M + (size_t)l * mls + (size_t)os * ld   // per-lane costs
+                            : M + (size_t)os * ld;
     const float* xl = x + (size_t)l * nin;
     float m, sum, w = 0.f;
     bool exact = true;
@@ -264,7 +265,7 @@ __device__ __forceinline__ void small_sweep_s(const float* __restrict__ M, int l
 
 // The group size S (threads per output, a power of two chosen on the host)
 // as a template argument: unrolled shuffles, shift/mask indexing.
-template <int NT, int kRes>
+template <int NT, int kRes, bool kPS = false>
 __device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld, int nout, int o0,
                                             int o1, int nin, int S, int nl,
                                             const float* __restrict__ x,
@@ -276,7 +277,7 @@ __device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld,
                                             int self, long long mls = 0) {
 #define SKB_SMALL_CASE(SS)                                                                      \
   case SS:                                                                                      \
-    small_sweep_s<NT, kRes, SS>(M, ld, nout, o0, o1, nin, nl, x, target, marg, old, prev, out,  \
+    small_sweep_s<NT, kRes, SS, kPS>(M, ld, nout, o0, o1, nin, nl, x, target, marg, old, prev, out,  \
                                 rres, cinv, peers, local_base, C, self, mls);                   \
     break;
   switch (S) {
@@ -286,7 +287,7 @@ __device__ __forceinline__ void small_sweep(const float* __restrict__ M, int ld,
     SKB_SMALL_CASE(8)
     SKB_SMALL_CASE(16)
     default:
-      small_sweep_s<NT, kRes, 32>(M, ld, nout, o0, o1, nin, nl, x, target, marg, old, prev, out,
+      small_sweep_s<NT, kRes, 32, kPS>(M, ld, nout, o0, o1, nin, nl, x, target, marg, old, prev, out,
                                   rres, cinv, peers, local_base, C, self, mls);
   }
 #undef SKB_SMALL_CASE
@@ -298,10 +299,12 @@ __device__ __forceinline__ void small_sync(int C) {
   else __syncthreads();
 }
 
-template <int NT>
+// kPS: per-sample costs (a cost per lane in shared memory); a separate
+// instantiation so the shared-cost solver's code and registers are unchanged.
+template <int NT, bool kPS = false>
 __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p) {
   extern __shared__ __align__(16) float small_smem[];
-  const SmallSmem sm(small_smem, p);
+  const SmallSmem sm(small_smem, p, kPS);
   const int tid = threadIdx.x;
   const int C = p.C;
   const int crank = (C > 1) ? (int)cooperative_groups::this_cluster().block_rank() : 0;
@@ -332,7 +335,7 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
       const float dx = float(xi) - float(xj), dy = float(yi) - float(yj);
       sm.AT[(size_t)jl * p.ldc + i] = p.gk * fmaf(p.ghx2, dx * dx, p.ghy2 * dy * dy);
     }
-  } else if (p.cps != nullptr) {   // per-sample: each lane's own cost (C = 1), validated here
+  } else if (kPS) {   // per-sample: each lane's own cost (C = 1), validated here
     bool bad = false;
     const size_t lc = (size_t)p.d1 * p.d2;
     for (long long e = tid; e < (long long)nl * lc; e += NT) {
@@ -383,10 +386,10 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
   if (tl) p.dbg[0] = globaltimer_ns();
   for (int k = 1; k <= p.max_iters; ++k) {
     if (!have_next) {
-      small_sweep<NT, 0>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, sm.lnu, nullptr,
+      small_sweep<NT, 0, kPS>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, sm.lnu, nullptr,
                          nullptr, sm.g(cur), sm.g(cur ^ 1), nullptr, 0.f, peers, small_smem, C,
                          crank,
-                         p.cps ? (long long)p.d2 * p.ldc : 0);
+                         kPS ? (long long)p.d2 * p.ldc : 0);
       if (tl && k <= 8) p.dbg[4 * k] = globaltimer_ns();
       small_sync(C);
       if (tl && k <= 8) p.dbg[4 * k + 1] = globaltimer_ns();
@@ -398,13 +401,13 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
     if (check || last) {
       for (int l = tid; l < nl; l += NT) sm.rres[l] = 0u;
       __syncthreads();
-      small_sweep<NT, 1>(sm.A, p.ldr, p.d1, i0, i1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, sm.mu,
+      small_sweep<NT, 1, kPS>(sm.A, p.ldr, p.d1, i0, i1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, sm.mu,
                          nullptr, sm.f, sm.f, sm.rres, 0.f, peers, small_smem, C, crank,
-                         p.cps ? (long long)p.d1 * p.ldr : 0);
+                         kPS ? (long long)p.d1 * p.ldr : 0);
     } else {
-      small_sweep<NT, 0>(sm.A, p.ldr, p.d1, i0, i1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, nullptr,
+      small_sweep<NT, 0, kPS>(sm.A, p.ldr, p.d1, i0, i1, p.d2, p.Sr, nl, sm.g(cur), sm.lmu, nullptr,
                          nullptr, sm.f, sm.f, nullptr, 0.f, peers, small_smem, C, crank,
-                         p.cps ? (long long)p.d1 * p.ldr : 0);
+                         kPS ? (long long)p.d1 * p.ldr : 0);
     }
     if (tl && k <= 8) p.dbg[4 * k + 2] = globaltimer_ns();
     small_sync(C);
@@ -412,10 +415,10 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
     iters = k;
     if (check) {
       // column sweep k+1 doubles as the column residual of iteration k
-      small_sweep<NT, 2>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, sm.lnu, sm.nu,
+      small_sweep<NT, 2, kPS>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, sm.lnu, sm.nu,
                          sm.g(cur), sm.g(cur), sm.g(cur ^ 1), sm.rres, 0.f, peers, small_smem, C,
                          crank,
-                         p.cps ? (long long)p.d2 * p.ldc : 0);
+                         kPS ? (long long)p.d2 * p.ldc : 0);
       small_sync(C);
       // every CTA publishes the max over its lanes and slices; all CTAs read
       // all of them behind a grid barrier and take the same decision
@@ -446,9 +449,9 @@ __global__ void __launch_bounds__(NT, 2) small_solve_kernel(const SmallParams p)
 
   // ---- tail: column residual + E0 terms, then export (batch.py:323-337) -----
   float* e0t = sm.g(cur ^ 1);
-  small_sweep<NT, 3>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, nullptr, sm.nu, sm.g(cur),
+  small_sweep<NT, 3, kPS>(sm.AT, p.ldc, p.d2, j0, j1, p.d1, p.Sc, nl, sm.f, nullptr, sm.nu, sm.g(cur),
                      nullptr, e0t, sm.rres, p.cinv, peers, small_smem, C, crank,
-                     p.cps ? (long long)p.d2 * p.ldc : 0);
+                     kPS ? (long long)p.d2 * p.ldc : 0);
   small_sync(C);
   // the lane residual is the max over the cluster's slices (peer reads)
   if (C > 1 && crank == 0) {
