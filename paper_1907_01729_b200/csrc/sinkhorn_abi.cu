@@ -228,6 +228,7 @@ struct Layout {
   size_t sep_tg = 0, sep_rg = 0;   // its T (and tail R) [B][nblk][ny][32]
   size_t f2T = 0, g2T[2] = {0, 0}; // separable grid: the potentials transposed per lane
   size_t part_bytes = 0, counter_count = 0;
+  size_t part_cap = 0;   // bytes actually reserved at `part`
   int lane_nsplit = 1, lane_nj = 1, lane_vec = 4;
   bool fused = false;             // shared cost, one fused row->column pass per iteration
   int fused_nct = 0, fused_maxseg = 0;
@@ -393,7 +394,8 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
       L.part_bytes = std::max(L.part_bytes,
                               (size_t)L.fg_nct * L.fg_maxseg * kFgLanes * L.D2p * 4);
     }
-    L.part = c.take(L.part_bytes);
+    L.part_cap = L.part_bytes;
+    L.part = c.take(L.part_cap);
     L.counter_count = 1;
   } else if (L.tiled) {
     L.Bp = (int)round_up(pr.B, pick_bt(pr.B));
@@ -415,7 +417,8 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     L.nu = c.take(n2);
     L.e0 = c.take(n2);
     L.part_bytes = (size_t)sms * MAX_OCC * 2 * 3 * 64 * PT_MAX * 4;   // G*BT is constant
-    L.part = c.take(L.part_bytes);
+    L.part_cap = L.part_bytes;
+    L.part = c.take(L.part_cap);
     L.counter_count = (size_t)(L.Bp / 64) * (std::max(L.D1p, L.D2p) / 32 + 1);
   } else {
     L.lane_vec = (pr.d2 % 4 == 0 && pr.d1 % 4 == 0) ? 4 : 1;
@@ -442,12 +445,15 @@ Layout make_layout(const sinkhorn_problem_v1& pr, int sms, bool dense_grid = fal
     ns = (int)std::min<long long>(ns, std::max<long long>(1, pr.d1 / 64));
     L.lane_nsplit = ns;
     L.part_bytes = ns > 1 ? (size_t)pr.B * L.lane_nj * ns * 3 * 256 * L.lane_vec * 4 : 256;
-    L.part = c.take(L.part_bytes);
+    // (also the small solver's per-check CTA maxima, [2][grid], for per-sample costs)
+    L.part_cap = std::max<size_t>(L.part_bytes, (size_t)sms * 8 * 2 * 4);
+    L.part = c.take(L.part_cap);
     L.counter_count = (size_t)pr.B * L.lane_nj;
   }
   L.res = c.take((size_t)std::max(L.Bp, 1) * 4);
   if (L.sep) {
-    L.part = c.take(std::max<size_t>(L.part_bytes, (size_t)sms * 8 * 2 * 4));
+    L.part_cap = std::max<size_t>(L.part_bytes, (size_t)sms * 8 * 2 * 4);
+    L.part = c.take(L.part_cap);
     const size_t nblk = (size_t)(pr.grid_nx + 31) / 32;
     L.sep_ax = c.take((size_t)pr.grid_nx * nblk * 32 * 4);
     L.sep_ay = c.take((size_t)pr.grid_ny * sep_ld((int)pr.grid_ny) * 4);
@@ -1453,6 +1459,8 @@ struct Solve {
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, kSmallNT, bytes));
       if (fit < 1) return 0;
       G = Gl * Cc;
+      // per-check CTA maxima [2][G] live in the layout's `part` region
+      if (op.tolerance > 0 && (size_t)2 * G * 4 > L.part_cap) continue;
       if (op.tolerance > 0) {   // the grid barrier needs every CTA (cluster) co-resident
         if (G > fit * di.sms) continue;
         if (Cc > 1) {
